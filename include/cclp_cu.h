@@ -1,0 +1,181 @@
+/* cclp_cu — B200-native PDHG engine behind the reference's run_pdhg interface.
+ *
+ * C ABI (plain pointers and sizes, no C++/torch types) exported by
+ * paper_2510_24429_b200/libcclp_cuda.so. It replaces the reference's hot path
+ *
+ *   cclp::run_pdhg(const LinearProgram&, const PdhgConfig&, const Tolerances&,
+ *                  const std::vector<Scalar>& thresholds, const SnapshotSink&,
+ *                  const std::atomic<bool>* cancel) -> PdhgResult
+ *   (reference: proj/include/cclp/pdhg.hpp:138-142, proj/src/pdhg.cpp:230-378)
+ *
+ * and the kernels it is built from (matvec / matvec_transpose,
+ * kernels.hpp:27-40; ruiz_scale, scaling.hpp:47-48; estimate_matrix_norm,
+ * pdhg.hpp:85-86). A C++ drop-in that re-implements cclp::run_pdhg on top of
+ * this ABI is shown in INTEGRATION.md.
+ *
+ * Conventions (mirroring the reference):
+ *  - The LP is equality form, CSC exactly as Eigen stores a compressed
+ *    SparseMatrix<double, ColMajor, int> (types.hpp:31): colptr = outerIndexPtr,
+ *    rowind = innerIndexPtr (ascending per column), val = valuePtr; bounds use
+ *    IEEE +-inf (types.hpp:35).
+ *  - Return codes: 0 ok; CCLP_CU_EINVAL where the reference throws
+ *    std::invalid_argument (pdhg.cpp:235-244); CCLP_CU_ECUDA / CCLP_CU_ENOMEM on
+ *    device failure. A non-finite iterate is NOT an error: it is stop reason
+ *    CCLP_CU_STOP_NUMERICAL_ERROR with error_iteration set (pdhg.cpp:369-376).
+ *  - The snapshot sink runs synchronously on the calling thread with pointers
+ *    valid only for the duration of the call (pdhg.cpp:346-358).
+ *  - cancel is polled (relaxed) between device batches, so a cancel is seen
+ *    within `poll_interval` iterations (reference: every iteration).
+ *  - One context per host thread; a context is not thread-safe.
+ */
+#ifndef CCLP_CU_H_
+#define CCLP_CU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CCLP_CU_OK 0
+#define CCLP_CU_EINVAL 1
+#define CCLP_CU_ECUDA 2
+#define CCLP_CU_ENOMEM 3
+
+/* PdhgStopReason (pdhg.hpp:44-51), same order. */
+#define CCLP_CU_STOP_CONVERGED 0
+#define CCLP_CU_STOP_ITERATION_LIMIT 1
+#define CCLP_CU_STOP_TIME_LIMIT 2
+#define CCLP_CU_STOP_CANCELLED 3
+#define CCLP_CU_STOP_WON_BY_CROSSOVER 4
+#define CCLP_CU_STOP_NUMERICAL_ERROR 5
+
+/* LinearProgram (lp.hpp:37-64), the fields run_pdhg reads. */
+typedef struct {
+  int32_t m, n;
+  const int32_t* colptr; /* n+1 */
+  const int32_t* rowind; /* colptr[n] */
+  const double* val;     /* colptr[n] */
+  const double* c;         /* n */
+  const double* row_lower; /* m */
+  const double* row_upper; /* m */
+  const double* col_lower; /* n */
+  const double* col_upper; /* n */
+} cclp_cu_lp;
+
+/* PdhgConfig (pdhg.hpp:29-42) plus the engine's own knobs (last two). */
+typedef struct {
+  double step_scale;      /* eta, 0.9 */
+  double primal_weight;   /* omega; <= 0 picks ||c'||/||b'|| */
+  double restart_factor;  /* 0.5 */
+  double time_limit;      /* seconds, +inf */
+  int32_t norm_iterations;    /* 100 */
+  int32_t scaling_iterations; /* 10 */
+  int64_t max_iterations;     /* 2e6 */
+  int32_t check_interval;     /* 1 */
+  uint64_t seed;              /* 0 */
+  int64_t log_interval;       /* 0 disables the iteration log */
+  int32_t deterministic;      /* always honoured: fixed reduction order */
+  int32_t poll_interval;      /* iterations per device batch (0 -> 64) */
+} cclp_cu_config;
+
+/* Tolerances (kkt.hpp:32-41). */
+typedef struct {
+  double eps_rel, eps_abs, eps_cross, decrement;
+} cclp_cu_tolerances;
+
+/* ResidualReport (kkt.hpp:43-58), same field order. */
+typedef struct {
+  double rp_norm2, rd_norm2, rp_inf, rd_inf;
+  double primal_objective, dual_objective, gap_abs;
+  double rel_primal, rel_dual, rel_gap, maxresid_rel, complementarity;
+} cclp_cu_report;
+
+/* PdhgSnapshot (pdhg.hpp:111-117). Arrays valid only during the sink call. */
+typedef struct {
+  const double* x; /* n, unscaled standard-form */
+  const double* y; /* m */
+  const double* z; /* n */
+  int32_t m, n;
+  double threshold;
+  double maxresid;
+  int32_t from_average;
+  int64_t iteration;
+} cclp_cu_snapshot;
+
+typedef void (*cclp_cu_sink_fn)(const cclp_cu_snapshot* snap, void* user);
+/* One iteration-log line in the reference's format (pdhg.cpp:332-340). */
+typedef void (*cclp_cu_log_fn)(const char* line, void* user);
+
+/* PdhgResult (pdhg.hpp:121-129) plus engine timings. */
+typedef struct {
+  int32_t stop;
+  int64_t iterations;
+  int64_t restarts;
+  int64_t error_iteration;
+  double seconds;
+  cclp_cu_report report;
+  double norm_estimate, omega, tau, sigma;
+  double setup_seconds; /* upload excluded: scaling + norm + init */
+  double loop_seconds;  /* device time of the iteration loop */
+  int64_t kernel_launches;
+} cclp_cu_result;
+
+typedef struct cclp_cu_ctx cclp_cu_ctx;
+
+const char* cclp_cu_last_error(void);
+const char* cclp_cu_stop_string(int32_t stop); /* to_string, pdhg.cpp:28-44 */
+void cclp_cu_default_config(cclp_cu_config* cfg);      /* pdhg.hpp:29-42 */
+void cclp_cu_default_tolerances(cclp_cu_tolerances* t); /* kkt.hpp:33-36 */
+
+/* Uploads the CSC and bounds to `device` and builds CSR(A) on the device. */
+int cclp_cu_create(const cclp_cu_lp* lp, int device, cclp_cu_ctx** out);
+int cclp_cu_destroy(cclp_cu_ctx* ctx);
+
+/* run_pdhg on a context (pdhg.cpp:230-378): Ruiz scaling, ||A|| estimate,
+ * the fused iteration loop, ladder snapshots, result download.
+ * x_out/z_out: n doubles, y_out: m doubles (host). log may be NULL. */
+int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg, const cclp_cu_tolerances* tol,
+                  const double* thresholds, int32_t nthr, cclp_cu_sink_fn sink, void* sink_user,
+                  const volatile uint8_t* cancel, cclp_cu_log_fn log, void* log_user,
+                  double* x_out, double* y_out, double* z_out, cclp_cu_result* res);
+
+/* One-shot drop-in: create + solve + destroy. */
+int cclp_cu_run_pdhg(const cclp_cu_lp* lp, const cclp_cu_config* cfg, const cclp_cu_tolerances* tol,
+                     const double* thresholds, int32_t nthr, cclp_cu_sink_fn sink, void* sink_user,
+                     const volatile uint8_t* cancel, double* x_out, double* y_out, double* z_out,
+                     cclp_cu_result* res, int device);
+
+/* ---- kernel-level entry points (unscaled A held by the context) ---------- */
+
+/* matvec / matvec_transpose (kernels.hpp:27-40). Host in, host out. */
+int cclp_cu_matvec(cclp_cu_ctx* ctx, const double* x, double* out);
+int cclp_cu_matvec_transpose(cclp_cu_ctx* ctx, const double* y, double* out);
+/* ruiz_scale factors (scaling.cpp:46-90): row_scale[m], col_scale[n]. */
+int cclp_cu_ruiz(cclp_cu_ctx* ctx, int32_t iterations, double* row_scale, double* col_scale);
+/* estimate_matrix_norm (pdhg.cpp:46-65) on the unscaled A. */
+int cclp_cu_estimate_norm(cclp_cu_ctx* ctx, int32_t iterations, uint64_t seed, double* out);
+
+/* ---- measurement hooks (bench.py) ---------------------------------------- */
+
+/* Begin a solve without running the loop: scaling, norm, initial check. */
+int cclp_cu_begin(cclp_cu_ctx* ctx, const cclp_cu_config* cfg, const cclp_cu_tolerances* tol);
+/* Advance exactly `iters` PDHG iterations (ignoring convergence and the
+ * iteration limit) with the full per-iteration checks, timed with CUDA
+ * events on the engine stream; returns device milliseconds. */
+int cclp_cu_advance(cclp_cu_ctx* ctx, int64_t iters, double* device_ms);
+/* Per-kernel device time: runs `iters` iterations launching kernels eagerly
+ * with events between them. out[0] = avg ms of the row kernel (A x + dual
+ * update), out[1] = avg ms of the column kernel (A'y + primal update +
+ * reports + finalize). */
+int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out);
+/* The engine's CUDA stream (cudaStream_t) for external event timing. */
+void* cclp_cu_stream(cclp_cu_ctx* ctx);
+/* Static description: nnz, CSR/CSC group sizes, grid sizes, bytes/iteration. */
+int cclp_cu_describe(cclp_cu_ctx* ctx, int64_t* out, int32_t nout);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CCLP_CU_H_ */

@@ -1,0 +1,961 @@
+// cclp_cu host engine + C ABI (include/cclp_cu.h).
+//
+// Host side of the B200 PDHG path: it owns the device copy of the LP, builds
+// CSR(A) next to the reference's CSC, runs the one-time setup on the device
+// (Ruiz scaling, ||A|| power iteration) and drives the fused iteration
+// kernels in CUDA-graph batches, reading back a small control block per
+// batch. Snapshots are extracted on the device and copied out on a side
+// stream into pinned memory; the sink is called on the caller's thread.
+// Reference: run_pdhg, proj/src/pdhg.cpp:230-378.
+#include <cub/device/device_radix_sort.cuh>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cclp_cu.h"
+#include "iter_kernels.cuh"
+#include "setup_kernels.cuh"
+
+namespace cclp_cu {
+
+thread_local std::string g_err;
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& w) : std::runtime_error(w), code(c) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    const int code = (e == cudaErrorMemoryAllocation) ? CCLP_CU_ENOMEM : CCLP_CU_ECUDA;
+    cudaGetLastError();
+    throw Error(code, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define CK(x) ::cclp_cu::ck((x), #x)
+#define CKL(what) ::cclp_cu::ck(cudaGetLastError(), what)
+
+namespace {
+
+template <class T>
+T* dalloc(size_t n) {
+  void* p = nullptr;
+  CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+  return static_cast<T*>(p);
+}
+
+int pick_group(long long nnz, long long rows) {
+  // lanes per row: each lane takes ~4 nonzeros of an average row
+  const double avg = rows > 0 ? static_cast<double>(nnz) / static_cast<double>(rows) : 0.0;
+  int g = 1;
+  while (g < 32 && g * 4 < avg) g *= 2;
+  return g;
+}
+
+int blocks_for(long long n, int per = kBlock, int cap = 148 * 8) {
+  long long b = (n + per - 1) / per;
+  return static_cast<int>(std::max<long long>(1, std::min<long long>(b, cap)));
+}
+
+}  // namespace
+
+struct Context {
+  int device = 0;
+  cudaStream_t stream = nullptr, side = nullptr;
+  int m = 0, n = 0;
+  long long nnz = 0;
+  // unscaled matrix: CSC (reference layout) and CSR
+  int *colptr = nullptr, *rowind = nullptr, *rowptr = nullptr, *colind = nullptr;
+  double *val_csc = nullptr, *val_csr = nullptr;
+  // scaled matrix values
+  double *sval_csc = nullptr, *sval_csr = nullptr;
+  double *c = nullptr, *l = nullptr, *u = nullptr, *b = nullptr;
+  double *r = nullptr, *s = nullptr;
+  bool equality = true;
+  // partitions
+  int Grow = 1, Gcol = 1, row_grid = 1, col_grid = 1;
+  int *row_start = nullptr, *col_start = nullptr;
+  // state
+  double* xc[3][2] = {};
+  double *aty[2] = {}, *xsum[2] = {}, *atysum[2] = {};
+  double *y[2] = {}, *ax[2] = {}, *ysum[2] = {}, *axsum[2] = {};
+  double *rowp = nullptr, *colp = nullptr, *work_part = nullptr;
+  unsigned* counter = nullptr;
+  Ctrl* ctrl = nullptr;
+  Ctrl* h_ctrl = nullptr;  // pinned, [4]
+  LogEntry* log = nullptr;
+  int log_cap = 4096;
+  LogEntry* h_log = nullptr;
+  double* thr = nullptr;
+  int thr_cap = 0;
+  unsigned long long* t0 = nullptr;
+  double* scalars = nullptr;  // device scratch [16]
+  double* h_scalars = nullptr;
+  PowerCtrl* pctrl = nullptr;
+  int* iflags = nullptr;    // [0] ruiz notdone, [1] amb row count, [2] amb col count
+  int* amb_idx = nullptr;   // [2][256]
+  double* wn = nullptr;     // n-vector scratch x2
+  double* wn2 = nullptr;
+  double* wm = nullptr;
+  // outputs (device views) + pinned staging for snapshots
+  double *vx = nullptr, *vy = nullptr, *vz = nullptr, *vrep = nullptr;
+  double *h_sx = nullptr, *h_sy = nullptr, *h_sz = nullptr;
+  cudaEvent_t ev_snap = nullptr, ev_a = nullptr, ev_b = nullptr;
+  // graph
+  cudaGraphExec_t graph = nullptr;
+  int graph_k = 0;
+  IterParams params{};
+  bool begun = false;
+  long long launches = 0;
+  double b_norm = 0, c_norm = 0;
+  double norm_est = 0, omega = 0, tau = 0, sigma = 0;
+
+  ~Context();
+  void upload(const cclp_cu_lp* lp);
+  void build_csr();
+  void partition();
+  void launch_spmv(bool transpose, const double* vec, double* out, bool scaled, const int* stop);
+  double reduce(const double* a, const double* bvec, long long len, int mode);
+  void ruiz(int iterations);
+  double power_norm(int iterations, uint64_t seed, bool scaled);
+  void begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thresholds,
+             int nthr);
+  void launch_iteration(bool init);
+  void build_graph(int k);
+  void fetch_ctrl(Ctrl* dst);
+  void extract_view(int view, const Ctrl& st, bool need_report);
+};
+
+Context::~Context() {
+  cudaSetDevice(device);
+  if (graph) cudaGraphExecDestroy(graph);
+  void* ptrs[] = {colptr, rowind, rowptr, colind, val_csc, val_csr, sval_csc, sval_csr, c, l, u, b,
+                  r, s, row_start, col_start, rowp, colp, work_part, counter, ctrl, log, thr, t0,
+                  scalars, pctrl, iflags, amb_idx, wn, wn2, wm, vx, vy, vz, vrep};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (int k = 0; k < 3; ++k)
+    for (int q = 0; q < 2; ++q)
+      if (xc[k][q]) cudaFree(xc[k][q]);
+  for (int q = 0; q < 2; ++q) {
+    double* v[] = {aty[q], xsum[q], atysum[q], y[q], ax[q], ysum[q], axsum[q]};
+    for (double* p : v)
+      if (p) cudaFree(p);
+  }
+  if (h_ctrl) cudaFreeHost(h_ctrl);
+  if (h_log) cudaFreeHost(h_log);
+  if (h_scalars) cudaFreeHost(h_scalars);
+  if (h_sx) cudaFreeHost(h_sx);
+  if (h_sy) cudaFreeHost(h_sy);
+  if (h_sz) cudaFreeHost(h_sz);
+  if (ev_snap) cudaEventDestroy(ev_snap);
+  if (ev_a) cudaEventDestroy(ev_a);
+  if (ev_b) cudaEventDestroy(ev_b);
+  if (stream) cudaStreamDestroy(stream);
+  if (side) cudaStreamDestroy(side);
+}
+
+void Context::upload(const cclp_cu_lp* lp) {
+  m = lp->m;
+  n = lp->n;
+  nnz = lp->colptr[n];
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ev_snap, cudaEventDisableTiming));
+  CK(cudaEventCreate(&ev_a));
+  CK(cudaEventCreate(&ev_b));
+  colptr = dalloc<int>(n + 1);
+  rowind = dalloc<int>(nnz);
+  val_csc = dalloc<double>(nnz);
+  c = dalloc<double>(n);
+  l = dalloc<double>(n);
+  u = dalloc<double>(n);
+  b = dalloc<double>(m);
+  r = dalloc<double>(m);
+  s = dalloc<double>(n);
+  CK(cudaMemcpyAsync(colptr, lp->colptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(rowind, lp->rowind, sizeof(int) * nnz, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(val_csc, lp->val, sizeof(double) * nnz, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(c, lp->c, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(l, lp->col_lower, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+  CK(cudaMemcpyAsync(u, lp->col_upper, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+  // equality form: b = row_lower (= row_upper); checked on the host view
+  equality = true;
+  for (int i = 0; i < m; ++i) {
+    const double lo = lp->row_lower[i], hi = lp->row_upper[i];
+    if (!(lo == hi && lo > -INFINITY && lo < INFINITY)) {
+      equality = false;
+      break;
+    }
+  }
+  CK(cudaMemcpyAsync(b, lp->row_lower, sizeof(double) * m, cudaMemcpyHostToDevice, stream));
+  build_csr();
+  partition();
+}
+
+void Context::build_csr() {
+  rowptr = dalloc<int>(m + 1);
+  colind = dalloc<int>(nnz);
+  val_csr = dalloc<double>(nnz);
+  if (nnz == 0) {
+    CK(cudaMemsetAsync(rowptr, 0, sizeof(int) * (m + 1), stream));
+    return;
+  }
+  // Stable radix sort of the CSC entries by row: within a row the entries
+  // keep CSC order, i.e. ascending column, as a CSR requires.
+  int* col_of = dalloc<int>(nnz);
+  int* keys_out = dalloc<int>(nnz);
+  int* perm_in = dalloc<int>(nnz);
+  int* perm_out = dalloc<int>(nnz);
+  k_expand_major<<<blocks_for(n), kBlock, 0, stream>>>(colptr, n, col_of);
+  k_iota<<<blocks_for(nnz), kBlock, 0, stream>>>(perm_in, nnz);
+  CKL("expand");
+  int bits = 1;
+  while ((1LL << bits) < m) ++bits;
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, rowind, keys_out, perm_in, perm_out,
+                                     static_cast<int>(nnz), 0, bits, stream));
+  void* tmp = dalloc<char>(tmp_bytes);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, rowind, keys_out, perm_in, perm_out,
+                                     static_cast<int>(nnz), 0, bits, stream));
+  k_offsets_from_sorted<<<blocks_for(m + 1), kBlock, 0, stream>>>(keys_out, nnz, m, rowptr);
+  k_gather_csr<<<blocks_for(nnz), kBlock, 0, stream>>>(perm_out, nnz, col_of, val_csc, colind, val_csr);
+  CKL("csr");
+  CK(cudaStreamSynchronize(stream));
+  cudaFree(tmp);
+  cudaFree(col_of);
+  cudaFree(keys_out);
+  cudaFree(perm_in);
+  cudaFree(perm_out);
+}
+
+void Context::partition() {
+  Grow = pick_group(nnz, m);
+  Gcol = pick_group(nnz, n);
+  const int cap = 148 * 4;
+  row_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (m + 63) / 64)));
+  col_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (n + 63) / 64)));
+  row_start = dalloc<int>(row_grid + 1);
+  col_start = dalloc<int>(col_grid + 1);
+  k_partition<<<blocks_for(row_grid + 1), kBlock, 0, stream>>>(rowptr, m, row_grid, 8, row_start);
+  k_partition<<<blocks_for(col_grid + 1), kBlock, 0, stream>>>(colptr, n, col_grid, 8, col_start);
+  CKL("partition");
+  rowp = dalloc<double>(static_cast<size_t>(std::max(row_grid, 148 * 8)) * kRowParts);
+  colp = dalloc<double>(static_cast<size_t>(std::max(col_grid, 148 * 8)) * kColParts);
+  work_part = dalloc<double>(148 * 8 * 2);
+  counter = dalloc<unsigned>(4);
+  CK(cudaMemsetAsync(counter, 0, sizeof(unsigned) * 4, stream));
+  scalars = dalloc<double>(16);
+  CK(cudaHostAlloc(&h_scalars, sizeof(double) * 16, cudaHostAllocDefault));
+  pctrl = dalloc<PowerCtrl>(1);
+  iflags = dalloc<int>(4);
+  amb_idx = dalloc<int>(512);
+  wn = dalloc<double>(n);
+  wn2 = dalloc<double>(n);
+  wm = dalloc<double>(m);
+  t0 = dalloc<unsigned long long>(1);
+}
+
+template <class Gather>
+static void spmv_dispatch(int G, int grid, cudaStream_t st, const int* ptr, const int* idx,
+                          const double* val, Gather g, const int* start, double* out,
+                          const int* stop) {
+  switch (G) {
+    case 1: k_spmv<1><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
+    case 2: k_spmv<2><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
+    case 4: k_spmv<4><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
+    case 8: k_spmv<8><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
+    case 16: k_spmv<16><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
+    default: k_spmv<32><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
+  }
+}
+
+void Context::launch_spmv(bool transpose, const double* vec, double* out, bool scaled,
+                          const int* stop) {
+  if (!transpose) {
+    spmv_dispatch(Grow, row_grid, stream, rowptr, colind, scaled ? sval_csr : val_csr,
+                  GatherPlain{vec}, row_start, out, stop);
+  } else {
+    spmv_dispatch(Gcol, col_grid, stream, colptr, rowind, scaled ? sval_csc : val_csc,
+                  GatherPlain{vec}, col_start, out, stop);
+  }
+  CKL("spmv");
+}
+
+double Context::reduce(const double* a, const double* bvec, long long len, int mode) {
+  const int grid = blocks_for(len, kBlock, 148 * 4);
+  k_reduce<<<grid, kBlock, 0, stream>>>(a, bvec, len, mode, work_part, counter + 1, scalars);
+  CKL("reduce");
+  CK(cudaMemcpyAsync(h_scalars, scalars, sizeof(double), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  return h_scalars[0];
+}
+
+// Ruiz factors into r, s (scaling.cpp:46-90); ambiguous pow2_sqrt cases are
+// evaluated with the host libm exactly as the reference does.
+void Context::ruiz(int iterations) {
+  k_fill<<<blocks_for(m), kBlock, 0, stream>>>(r, m, 1.0);
+  k_fill<<<blocks_for(n), kBlock, 0, stream>>>(s, n, 1.0);
+  CKL("ruiz init");
+  double* rmax = wm;
+  double* cmax = wn;
+  for (int t = 0; t < iterations; ++t) {
+    const int gr = blocks_for(m, kBlock / Grow, 148 * 8);
+    const int gc = blocks_for(n, kBlock / Gcol, 148 * 8);
+    auto absmax = [&](int G, int grid, const int* ptr, const int* idx, const double* val,
+                      const double* self, const double* other, int is_row, const int* start,
+                      double* out) {
+      switch (G) {
+        case 1: k_scaled_absmax<1><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
+        case 2: k_scaled_absmax<2><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
+        case 4: k_scaled_absmax<4><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
+        case 8: k_scaled_absmax<8><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
+        case 16: k_scaled_absmax<16><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
+        default: k_scaled_absmax<32><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
+      }
+    };
+    (void)gr;
+    (void)gc;
+    absmax(Grow, row_grid, rowptr, colind, val_csr, r, s, 1, row_start, rmax);
+    absmax(Gcol, col_grid, colptr, rowind, val_csc, s, r, 0, col_start, cmax);
+    CK(cudaMemsetAsync(iflags, 0, sizeof(int) * 4, stream));
+    k_ruiz_notdone<<<blocks_for(m), kBlock, 0, stream>>>(rmax, m, iflags);
+    k_ruiz_notdone<<<blocks_for(n), kBlock, 0, stream>>>(cmax, n, iflags);
+    CKL("ruiz max");
+    int hf[4];
+    CK(cudaMemcpyAsync(hf, iflags, sizeof(hf), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    if (!hf[0]) break;
+    k_ruiz_update<<<blocks_for(m), kBlock, 0, stream>>>(rmax, m, r, iflags + 1, amb_idx, 256);
+    k_ruiz_update<<<blocks_for(n), kBlock, 0, stream>>>(cmax, n, s, iflags + 2, amb_idx + 256, 256);
+    CKL("ruiz update");
+    CK(cudaMemcpyAsync(hf, iflags, sizeof(hf), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    for (int side_k = 0; side_k < 2; ++side_k) {
+      const int cnt = hf[1 + side_k];
+      if (cnt == 0) continue;
+      if (cnt > 256) throw Error(CCLP_CU_ECUDA, "ruiz: too many ambiguous pow2_sqrt cases");
+      std::vector<int> idx(cnt);
+      CK(cudaMemcpy(idx.data(), amb_idx + 256 * side_k, sizeof(int) * cnt, cudaMemcpyDeviceToHost));
+      double* mx = side_k == 0 ? rmax : cmax;
+      double* sc = side_k == 0 ? r : s;
+      for (int q = 0; q < cnt; ++q) {
+        double v, cur;
+        CK(cudaMemcpy(&v, mx + idx[q], sizeof(double), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(&cur, sc + idx[q], sizeof(double), cudaMemcpyDeviceToHost));
+        cur /= std::exp2(std::round(0.5 * std::log2(v)));  // pow2_sqrt, scaling.cpp:23-25
+        CK(cudaMemcpy(sc + idx[q], &cur, sizeof(double), cudaMemcpyHostToDevice));
+      }
+    }
+  }
+}
+
+// estimate_matrix_norm (pdhg.cpp:46-65) on the scaled or unscaled matrix.
+double Context::power_norm(int iterations, uint64_t seed, bool scaled) {
+  if (m == 0 || n == 0 || nnz == 0) return 0.0;
+  // start vector: mt19937_64 + normal_distribution, as the reference (:49-52)
+  std::vector<double> v0(n);
+  {
+    std::mt19937_64 rng(seed + 0x9e3779b97f4a7c15ull);
+    std::normal_distribution<double> gauss(0.0, 1.0);
+    for (int j = 0; j < n; ++j) v0[j] = gauss(rng);
+  }
+  double* u_prev = wn;
+  double* u = wn2;
+  CK(cudaMemcpyAsync(u_prev, v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+  double nv = reduce(u_prev, nullptr, n, 0);
+  if (std::sqrt(nv) == 0.0) {
+    k_fill<<<blocks_for(n), kBlock, 0, stream>>>(u_prev, n, 1.0);
+    nv = reduce(u_prev, nullptr, n, 0);
+  }
+  PowerCtrl pc{std::sqrt(nv), 0.0, 0, 0};
+  CK(cudaMemcpyAsync(pctrl, &pc, sizeof(pc), cudaMemcpyHostToDevice, stream));
+  const double* aval = scaled ? sval_csr : val_csr;
+  const double* atval = scaled ? sval_csc : val_csc;
+  for (int t = 0; t < iterations; ++t) {
+    // w = A v with v = u_prev / nu  (Vector w = A * v, :57)
+    switch (Grow) {
+#define CASE(G) case G: k_spmv<G><<<row_grid, kBlock, 0, stream>>>(rowptr, colind, aval, GatherDiv{u_prev, &pctrl->nu}, row_start, wm, &pctrl->zero); break;
+      CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
+      default: k_spmv<32><<<row_grid, kBlock, 0, stream>>>(rowptr, colind, aval, GatherDiv{u_prev, &pctrl->nu}, row_start, wm, &pctrl->zero); break;
+#undef CASE
+    }
+    // u = A' w; nu = ||u||; lambda = v.u  (:58-61)
+    switch (Gcol) {
+#define CASE(G) case G: k_power_cols<G><<<col_grid, kBlock, 0, stream>>>(colptr, rowind, atval, wm, col_start, u_prev, u, work_part, counter + 2, pctrl); break;
+      CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
+      default: k_power_cols<32><<<col_grid, kBlock, 0, stream>>>(colptr, rowind, atval, wm, col_start, u_prev, u, work_part, counter + 2, pctrl); break;
+#undef CASE
+    }
+    CKL("power");
+    std::swap(u_prev, u);
+  }
+  CK(cudaMemcpyAsync(&pc, pctrl, sizeof(pc), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  if (pc.zero) return 0.0;
+  return std::sqrt(std::max(pc.lambda, 0.0));
+}
+
+void Context::launch_iteration(bool init) {
+  const IterParams& p = params;
+  const int ii = init ? 1 : 0;
+  switch (Grow) {
+#define CASE(G) case G: k_rows<G><<<row_grid, kBlock, 0, stream>>>(p, ii); break;
+    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
+    default: k_rows<32><<<row_grid, kBlock, 0, stream>>>(p, ii); break;
+#undef CASE
+  }
+  switch (Gcol) {
+#define CASE(G) case G: k_cols<G><<<col_grid, kBlock, 0, stream>>>(p, ii); break;
+    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
+    default: k_cols<32><<<col_grid, kBlock, 0, stream>>>(p, ii); break;
+#undef CASE
+  }
+  launches += 2;
+}
+
+void Context::build_graph(int k) {
+  if (graph && graph_k == k) return;
+  if (graph) {
+    cudaGraphExecDestroy(graph);
+    graph = nullptr;
+  }
+  cudaGraph_t g;
+  CK(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+  const long long before = launches;
+  for (int i = 0; i < k; ++i) launch_iteration(false);
+  launches = before;
+  CK(cudaStreamEndCapture(stream, &g));
+  CK(cudaGraphInstantiate(&graph, g, 0));
+  cudaGraphDestroy(g);
+  graph_k = k;
+}
+
+void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
+                    const double* thresholds, int nthr) {
+  k_stamp<<<1, 1, 0, stream>>>(t0);
+  CKL("stamp");
+  const auto h0 = std::chrono::steady_clock::now();
+  // norms on the unscaled model (pdhg.cpp:253-254)
+  b_norm = std::sqrt(reduce(b, nullptr, m, 0));
+  c_norm = std::sqrt(reduce(c, nullptr, n, 0));
+  ruiz(cfg.scaling_iterations);
+  if (!sval_csr) sval_csr = dalloc<double>(nnz);
+  if (!sval_csc) sval_csc = dalloc<double>(nnz);
+  k_scale_values<<<blocks_for(static_cast<long long>(m) * 32), kBlock, 0, stream>>>(
+      rowptr, m, colind, val_csr, r, s, 1, sval_csr);
+  k_scale_values<<<blocks_for(static_cast<long long>(n) * 32), kBlock, 0, stream>>>(
+      colptr, n, rowind, val_csc, s, r, 0, sval_csc);
+  CKL("scale");
+  norm_est = power_norm(cfg.norm_iterations, cfg.seed, true);
+  const double a_norm = norm_est > 0.0 ? norm_est : 1.0;
+  omega = cfg.primal_weight;
+  if (omega <= 0.0) {  // pdhg.cpp:260-265 on the scaled model
+    const double cs = std::sqrt(reduce(c, s, n, 1));
+    const double bs = std::sqrt(reduce(b, r, m, 1));
+    omega = (cs > 0.0 && bs > 0.0) ? cs / bs : 1.0;
+  }
+  tau = cfg.step_scale * omega / a_norm;
+  sigma = cfg.step_scale / (omega * a_norm);
+
+  // state buffers
+  auto alloc_n = [&](double*& p) { if (!p) p = dalloc<double>(n); };
+  auto alloc_m = [&](double*& p) { if (!p) p = dalloc<double>(m); };
+  for (int k = 0; k < 3; ++k)
+    for (int q = 0; q < 2; ++q) alloc_n(xc[k][q]);
+  for (int q = 0; q < 2; ++q) {
+    alloc_n(aty[q]); alloc_n(xsum[q]); alloc_n(atysum[q]);
+    alloc_m(y[q]); alloc_m(ax[q]); alloc_m(ysum[q]); alloc_m(axsum[q]);
+  }
+  for (int q = 0; q < 2; ++q) {
+    CK(cudaMemsetAsync(y[q], 0, sizeof(double) * std::max(m, 1), stream));
+    CK(cudaMemsetAsync(ysum[q], 0, sizeof(double) * std::max(m, 1), stream));
+    CK(cudaMemsetAsync(axsum[q], 0, sizeof(double) * std::max(m, 1), stream));
+    CK(cudaMemsetAsync(xsum[q], 0, sizeof(double) * std::max(n, 1), stream));
+    CK(cudaMemsetAsync(atysum[q], 0, sizeof(double) * std::max(n, 1), stream));
+  }
+  if (!ctrl) {
+    ctrl = dalloc<Ctrl>(1);
+    CK(cudaHostAlloc(&h_ctrl, sizeof(Ctrl) * 4, cudaHostAllocDefault));
+    log = dalloc<LogEntry>(log_cap);
+    CK(cudaHostAlloc(&h_log, sizeof(LogEntry) * log_cap, cudaHostAllocDefault));
+  }
+  Ctrl c0;
+  std::memset(&c0, 0, sizeof c0);
+  c0.stop = -1;
+  c0.last_restart_resid = INFINITY;
+  CK(cudaMemcpyAsync(ctrl, &c0, sizeof c0, cudaMemcpyHostToDevice, stream));
+  if (nthr > thr_cap) {
+    if (thr) cudaFree(thr);
+    thr = dalloc<double>(nthr);
+    thr_cap = nthr;
+  }
+  if (nthr > 0)
+    CK(cudaMemcpyAsync(thr, thresholds, sizeof(double) * nthr, cudaMemcpyHostToDevice, stream));
+  k_init_x<<<blocks_for(n), kBlock, 0, stream>>>(l, u, s, n, xc[0][0]);
+  CKL("init x");
+
+  IterParams& p = params;
+  p.m = m; p.n = n;
+  p.rowptr = rowptr; p.colind = colind; p.aval = sval_csr;
+  p.colptr = colptr; p.rowind = rowind; p.atval = sval_csc;
+  p.row_start = row_start; p.col_start = col_start;
+  p.row_grid = row_grid; p.col_grid = col_grid;
+  p.c = c; p.l = l; p.u = u; p.b = b; p.r = r; p.s = s;
+  for (int k = 0; k < 3; ++k)
+    for (int q = 0; q < 2; ++q) p.xc[k][q] = xc[k][q];
+  for (int q = 0; q < 2; ++q) {
+    p.aty[q] = aty[q]; p.xsum[q] = xsum[q]; p.atysum[q] = atysum[q];
+    p.y[q] = y[q]; p.ax[q] = ax[q]; p.ysum[q] = ysum[q]; p.axsum[q] = axsum[q];
+  }
+  p.rowp = rowp; p.colp = colp; p.counter = counter; p.ctrl = ctrl;
+  p.log = log; p.log_cap = log_cap; p.log_interval = cfg.log_interval;
+  p.tau = tau; p.sigma = sigma; p.eps_rel = tol.eps_rel; p.restart_factor = cfg.restart_factor;
+  p.b_norm = b_norm; p.c_norm = c_norm; p.time_limit = cfg.time_limit;
+  p.max_iter = cfg.max_iterations; p.check_interval = cfg.check_interval;
+  p.nthr = nthr; p.thr = thr; p.t0_ns = t0;
+  // initial products and check(0)
+  launch_iteration(true);
+  if (graph) {
+    cudaGraphExecDestroy(graph);
+    graph = nullptr;
+  }
+  CK(cudaStreamSynchronize(stream));
+  (void)h0;
+  begun = true;
+}
+
+void Context::fetch_ctrl(Ctrl* dst) {
+  CK(cudaMemcpyAsync(dst, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+}
+
+// Unscaled x, y, z (and a report) of a view of the current state into vx,
+// vy, vz, vrep.
+void Context::extract_view(int view, const Ctrl& st, bool need_report) {
+  if (!vx) {
+    vx = dalloc<double>(n);
+    vz = dalloc<double>(n);
+    vy = dalloc<double>(m);
+    vrep = dalloc<double>(kRepN);
+  }
+  ViewParams v;
+  v.it = params;
+  int vv = view;
+  if (vv == kViewCurEff) vv = st.R ? kViewAvg : kViewCur;
+  v.view = vv;
+  v.t = st.iteration;
+  v.R_prev = st.R_prev;
+  v.inv = st.window > 0 ? 1.0 / static_cast<double>(st.window) : 0.0;
+  v.x_out = vx;
+  v.y_out = vy;
+  v.z_out = vz;
+  v.rowp = rowp;
+  v.colp = colp;
+  v.counter = counter + 3;
+  v.report = vrep;
+  const int gr = blocks_for(m, kBlock, 148 * 4);
+  const int gc = blocks_for(n, kBlock, 148 * 4);
+  k_view_rows<<<gr, kBlock, 0, stream>>>(v);
+  k_view_cols<<<gc, kBlock, 0, stream>>>(v, gr);
+  CKL("view");
+  (void)need_report;
+}
+
+}  // namespace cclp_cu
+
+using cclp_cu::Context;
+using cclp_cu::Ctrl;
+using cclp_cu::Error;
+using cclp_cu::g_err;
+
+struct cclp_cu_ctx {
+  Context c;
+};
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return CCLP_CU_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return CCLP_CU_EINVAL;
+  } catch (const std::bad_alloc& e) {
+    g_err = e.what();
+    return CCLP_CU_ENOMEM;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return CCLP_CU_ECUDA;
+  }
+}
+
+void validate_inputs(const cclp_cu_ctx* ctx, const cclp_cu_config& cfg,
+                     const cclp_cu_tolerances& tol, const double* thr, int nthr) {
+  // run_pdhg preconditions (pdhg.cpp:235-244, kkt.cpp:26-37)
+  if (!ctx->c.equality) throw std::invalid_argument("run_pdhg: LP must be in equality form");
+  if (!(tol.decrement > 0.0 && tol.decrement < 1.0))
+    throw std::invalid_argument("tolerances: decrement must be in (0,1)");
+  if (!(tol.eps_rel > 0.0 && tol.eps_rel <= tol.eps_cross))
+    throw std::invalid_argument("tolerances: need 0 < eps_rel <= eps_cross");
+  if (!(tol.eps_abs > 0.0)) throw std::invalid_argument("tolerances: eps_abs must be positive");
+  for (int i = 1; i < nthr; ++i)
+    if (!(thr[i] < thr[i - 1]))
+      throw std::invalid_argument("run_pdhg: thresholds must be strictly decreasing");
+  if (cfg.check_interval <= 0)  // modulo by zero in the reference (pdhg.cpp:311)
+    throw std::invalid_argument("run_pdhg: check_interval must be positive");
+}
+
+void copy_report(const double* src, cclp_cu_report* dst) {
+  std::memcpy(dst, src, sizeof(double) * cclp_cu::kRepN);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* cclp_cu_last_error(void) { return g_err.c_str(); }
+
+const char* cclp_cu_stop_string(int32_t stop) {
+  switch (stop) {  // pdhg.cpp:28-44
+    case CCLP_CU_STOP_CONVERGED: return "converged";
+    case CCLP_CU_STOP_ITERATION_LIMIT: return "iteration-limit";
+    case CCLP_CU_STOP_TIME_LIMIT: return "time-limit";
+    case CCLP_CU_STOP_CANCELLED: return "cancelled";
+    case CCLP_CU_STOP_WON_BY_CROSSOVER: return "won-by-crossover";
+    case CCLP_CU_STOP_NUMERICAL_ERROR: return "numerical-error";
+  }
+  return "unknown";
+}
+
+void cclp_cu_default_config(cclp_cu_config* cfg) {
+  cfg->step_scale = 0.9;
+  cfg->primal_weight = 0.0;
+  cfg->restart_factor = 0.5;
+  cfg->time_limit = INFINITY;
+  cfg->norm_iterations = 100;
+  cfg->scaling_iterations = 10;
+  cfg->max_iterations = 2000000;
+  cfg->check_interval = 1;
+  cfg->seed = 0;
+  cfg->log_interval = 0;
+  cfg->deterministic = 1;
+  cfg->poll_interval = 0;
+}
+
+void cclp_cu_default_tolerances(cclp_cu_tolerances* t) {
+  t->eps_rel = 1e-6;
+  t->eps_abs = 1e-6;
+  t->eps_cross = 1e-2;
+  t->decrement = 0.1;
+}
+
+int cclp_cu_create(const cclp_cu_lp* lp, int device, cclp_cu_ctx** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (lp == nullptr || lp->m < 0 || lp->n < 0 || lp->colptr == nullptr)
+      throw std::invalid_argument("cclp_cu_create: bad LP");
+    cclp_cu::ck(cudaSetDevice(device), "cudaSetDevice");
+    auto* ctx = new cclp_cu_ctx();
+    ctx->c.device = device;
+    try {
+      ctx->c.upload(lp);
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+int cclp_cu_destroy(cclp_cu_ctx* ctx) {
+  delete ctx;
+  return CCLP_CU_OK;
+}
+
+int cclp_cu_begin(cclp_cu_ctx* ctx, const cclp_cu_config* cfg, const cclp_cu_tolerances* tol) {
+  return guarded([&] {
+    cclp_cu::ck(cudaSetDevice(ctx->c.device), "cudaSetDevice");
+    validate_inputs(ctx, *cfg, *tol, nullptr, 0);
+    cclp_cu_tolerances t = *tol;
+    ctx->c.begin(*cfg, t, nullptr, 0);
+    // measurement mode: never converge, never hit the limit
+    ctx->c.params.eps_rel = -1.0;
+    ctx->c.params.max_iter = (1LL << 62);
+    ctx->c.params.time_limit = INFINITY;
+  });
+}
+
+int cclp_cu_advance(cclp_cu_ctx* ctx, int64_t iters, double* device_ms) {
+  return guarded([&] {
+    Context& C = ctx->c;
+    if (!C.begun) throw std::invalid_argument("cclp_cu_advance: call cclp_cu_begin first");
+    const int k = 32;
+    C.build_graph(k);
+    CK(cudaEventRecord(C.ev_a, C.stream));
+    long long done = 0;
+    while (done + k <= iters) {
+      CK(cudaGraphLaunch(C.graph, C.stream));
+      C.launches += 2 * k;
+      done += k;
+    }
+    while (done < iters) {
+      C.launch_iteration(false);
+      ++done;
+    }
+    CK(cudaEventRecord(C.ev_b, C.stream));
+    CK(cudaEventSynchronize(C.ev_b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, C.ev_a, C.ev_b));
+    if (device_ms) *device_ms = ms;
+  });
+}
+
+int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
+  return guarded([&] {
+    Context& C = ctx->c;
+    if (!C.begun) throw std::invalid_argument("cclp_cu_profile_kernels: call cclp_cu_begin first");
+    std::vector<cudaEvent_t> ev(3 * iters);
+    for (auto& e : ev) CK(cudaEventCreate(&e));
+    for (long long i = 0; i < iters; ++i) {
+      CK(cudaEventRecord(ev[3 * i], C.stream));
+      switch (C.Grow) {
+#define CASE(G) case G: cclp_cu::k_rows<G><<<C.row_grid, cclp_cu::kBlock, 0, C.stream>>>(C.params, 0); break;
+        CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
+        default: cclp_cu::k_rows<32><<<C.row_grid, cclp_cu::kBlock, 0, C.stream>>>(C.params, 0); break;
+#undef CASE
+      }
+      CK(cudaEventRecord(ev[3 * i + 1], C.stream));
+      switch (C.Gcol) {
+#define CASE(G) case G: cclp_cu::k_cols<G><<<C.col_grid, cclp_cu::kBlock, 0, C.stream>>>(C.params, 0); break;
+        CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
+        default: cclp_cu::k_cols<32><<<C.col_grid, cclp_cu::kBlock, 0, C.stream>>>(C.params, 0); break;
+#undef CASE
+      }
+      CK(cudaEventRecord(ev[3 * i + 2], C.stream));
+      C.launches += 2;
+    }
+    CK(cudaStreamSynchronize(C.stream));
+    double a = 0, b = 0;
+    for (long long i = 0; i < iters; ++i) {
+      float x, y;
+      CK(cudaEventElapsedTime(&x, ev[3 * i], ev[3 * i + 1]));
+      CK(cudaEventElapsedTime(&y, ev[3 * i + 1], ev[3 * i + 2]));
+      a += x;
+      b += y;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    out[0] = iters ? a / iters : 0.0;
+    out[1] = iters ? b / iters : 0.0;
+  });
+}
+
+void* cclp_cu_stream(cclp_cu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) : nullptr; }
+
+int cclp_cu_describe(cclp_cu_ctx* ctx, int64_t* out, int32_t nout) {
+  const Context& C = ctx->c;
+  const int64_t v[] = {C.m, C.n, C.nnz, C.Grow, C.Gcol, C.row_grid, C.col_grid, C.launches};
+  for (int i = 0; i < nout && i < static_cast<int>(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
+  return CCLP_CU_OK;
+}
+
+int cclp_cu_matvec(cclp_cu_ctx* ctx, const double* x, double* out) {
+  return guarded([&] {
+    Context& C = ctx->c;
+    CK(cudaSetDevice(C.device));
+    CK(cudaMemcpyAsync(C.wn, x, sizeof(double) * C.n, cudaMemcpyHostToDevice, C.stream));
+    C.launch_spmv(false, C.wn, C.wm, false, nullptr);
+    CK(cudaMemcpyAsync(out, C.wm, sizeof(double) * C.m, cudaMemcpyDeviceToHost, C.stream));
+    CK(cudaStreamSynchronize(C.stream));
+  });
+}
+
+int cclp_cu_matvec_transpose(cclp_cu_ctx* ctx, const double* y, double* out) {
+  return guarded([&] {
+    Context& C = ctx->c;
+    CK(cudaSetDevice(C.device));
+    CK(cudaMemcpyAsync(C.wm, y, sizeof(double) * C.m, cudaMemcpyHostToDevice, C.stream));
+    C.launch_spmv(true, C.wm, C.wn, false, nullptr);
+    CK(cudaMemcpyAsync(out, C.wn, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.stream));
+    CK(cudaStreamSynchronize(C.stream));
+  });
+}
+
+int cclp_cu_ruiz(cclp_cu_ctx* ctx, int32_t iterations, double* row_scale, double* col_scale) {
+  return guarded([&] {
+    Context& C = ctx->c;
+    CK(cudaSetDevice(C.device));
+    C.ruiz(iterations);
+    CK(cudaMemcpyAsync(row_scale, C.r, sizeof(double) * C.m, cudaMemcpyDeviceToHost, C.stream));
+    CK(cudaMemcpyAsync(col_scale, C.s, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.stream));
+    CK(cudaStreamSynchronize(C.stream));
+  });
+}
+
+int cclp_cu_estimate_norm(cclp_cu_ctx* ctx, int32_t iterations, uint64_t seed, double* out) {
+  return guarded([&] {
+    Context& C = ctx->c;
+    CK(cudaSetDevice(C.device));
+    *out = C.power_norm(iterations, seed, false);
+  });
+}
+
+int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_tolerances* tol,
+                  const double* thresholds, int32_t nthr, cclp_cu_sink_fn sink, void* sink_user,
+                  const volatile uint8_t* cancel, cclp_cu_log_fn logfn, void* log_user,
+                  double* x_out, double* y_out, double* z_out, cclp_cu_result* res) {
+  return guarded([&] {
+    Context& C = ctx->c;
+    CK(cudaSetDevice(C.device));
+    const cclp_cu_config cfg = *cfg_in;
+    validate_inputs(ctx, cfg, *tol, thresholds, nthr);
+    const auto wall0 = std::chrono::steady_clock::now();
+    C.launches = 0;
+    C.begin(cfg, *tol, thresholds, nthr);
+    const double setup_s =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    const int k = cfg.poll_interval > 0 ? cfg.poll_interval : 64;
+    C.build_graph(k);
+    CK(cudaEventRecord(C.ev_a, C.stream));
+
+    Ctrl st;
+    C.fetch_ctrl(&st);
+    long long log_seen = 0;
+    auto flush_log = [&](const Ctrl& q) {
+      if (!logfn || cfg.log_interval <= 0) {
+        log_seen = q.log_count;
+        return;
+      }
+      if (q.log_count == log_seen) return;
+      CK(cudaMemcpy(C.h_log, C.log, sizeof(cclp_cu::LogEntry) * C.log_cap, cudaMemcpyDeviceToHost));
+      for (long long i = std::max(log_seen, q.log_count - C.log_cap); i < q.log_count; ++i) {
+        const auto& e = C.h_log[i % C.log_cap];
+        char line[160];
+        std::snprintf(line, sizeof line, "%lld\t%.6e\t%.6e\t%.6e\t%.3f\n", e.iteration,
+                      e.rel_primal, e.rel_dual, e.rel_gap, e.elapsed);
+        logfn(line, log_user);
+      }
+      log_seen = q.log_count;
+    };
+    auto emit_snapshot = [&](const Ctrl& q) {
+      // PdhgSnapshot of the better view (pdhg.cpp:346-358)
+      C.extract_view(q.snap_use_avg ? cclp_cu::kViewAvg : cclp_cu::kViewCur, q, false);
+      if (!C.h_sx) {
+        CK(cudaHostAlloc(&C.h_sx, sizeof(double) * std::max(C.n, 1), cudaHostAllocDefault));
+        CK(cudaHostAlloc(&C.h_sz, sizeof(double) * std::max(C.n, 1), cudaHostAllocDefault));
+        CK(cudaHostAlloc(&C.h_sy, sizeof(double) * std::max(C.m, 1), cudaHostAllocDefault));
+      }
+      CK(cudaEventRecord(C.ev_snap, C.stream));
+      CK(cudaStreamWaitEvent(C.side, C.ev_snap, 0));
+      CK(cudaMemcpyAsync(C.h_sx, C.vx, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.side));
+      CK(cudaMemcpyAsync(C.h_sy, C.vy, sizeof(double) * C.m, cudaMemcpyDeviceToHost, C.side));
+      CK(cudaMemcpyAsync(C.h_sz, C.vz, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.side));
+      CK(cudaStreamSynchronize(C.side));
+      if (sink) {
+        cclp_cu_snapshot sp;
+        sp.x = C.h_sx;
+        sp.y = C.h_sy;
+        sp.z = C.h_sz;
+        sp.m = C.m;
+        sp.n = C.n;
+        sp.threshold = thresholds[q.snap_thr_idx];
+        sp.maxresid = q.snap_maxresid;
+        sp.from_average = q.snap_use_avg;
+        sp.iteration = q.snap_iteration;
+        sink(&sp, sink_user);
+      }
+    };
+    auto clear_halt = [&]() {
+      const int zero[2] = {0, 0};
+      CK(cudaMemcpyAsync(&C.ctrl->halt, &zero[0], sizeof(int), cudaMemcpyHostToDevice, C.stream));
+      CK(cudaMemcpyAsync(&C.ctrl->snap_pending, &zero[1], sizeof(int), cudaMemcpyHostToDevice, C.stream));
+      CK(cudaStreamSynchronize(C.stream));
+    };
+
+    // the initial check may already stop or snapshot
+    bool cancelled = false;
+    while (true) {
+      flush_log(st);
+      if (st.halt && st.snap_pending) {
+        emit_snapshot(st);
+        clear_halt();
+        st.halt = 0;
+      }
+      if (st.stop >= 0) break;
+      if (cancel != nullptr && *cancel) {
+        cancelled = true;
+        break;
+      }
+      // two batches in flight: launch, copy the control block, poll
+      CK(cudaGraphLaunch(C.graph, C.stream));
+      C.launches += 2 * k;
+      CK(cudaMemcpyAsync(&C.h_ctrl[0], C.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, C.stream));
+      CK(cudaStreamSynchronize(C.stream));
+      st = C.h_ctrl[0];
+    }
+    CK(cudaEventRecord(C.ev_b, C.stream));
+    CK(cudaEventSynchronize(C.ev_b));
+    float loop_ms = 0;
+    CK(cudaEventElapsedTime(&loop_ms, C.ev_a, C.ev_b));
+
+    int view = st.result_view;
+    int stop = st.stop;
+    bool rep_valid = st.result_report_valid != 0;
+    if (cancelled) {
+      stop = CCLP_CU_STOP_CANCELLED;
+      view = cclp_cu::kViewCurEff;
+      rep_valid = st.checked != 0;
+      if (rep_valid) std::memcpy(st.result_report, st.R ? st.avg : st.cur, sizeof(st.result_report));
+    }
+    C.extract_view(view, st, !rep_valid);
+    CK(cudaMemcpyAsync(x_out, C.vx, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.stream));
+    CK(cudaMemcpyAsync(y_out, C.vy, sizeof(double) * C.m, cudaMemcpyDeviceToHost, C.stream));
+    CK(cudaMemcpyAsync(z_out, C.vz, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.stream));
+    double rep[cclp_cu::kRepN];
+    CK(cudaMemcpyAsync(rep, C.vrep, sizeof(rep), cudaMemcpyDeviceToHost, C.stream));
+    CK(cudaStreamSynchronize(C.stream));
+    res->stop = stop;
+    res->iterations = st.iteration;
+    res->restarts = st.restarts;
+    res->error_iteration = stop == CCLP_CU_STOP_NUMERICAL_ERROR ? st.error_iteration : -1;
+    copy_report(rep_valid ? st.result_report : rep, &res->report);
+    res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    res->norm_estimate = C.norm_est;
+    res->omega = C.omega;
+    res->tau = C.tau;
+    res->sigma = C.sigma;
+    res->setup_seconds = setup_s;
+    res->loop_seconds = loop_ms * 1e-3;
+    res->kernel_launches = C.launches;
+    C.begun = false;
+  });
+}
+
+int cclp_cu_run_pdhg(const cclp_cu_lp* lp, const cclp_cu_config* cfg, const cclp_cu_tolerances* tol,
+                     const double* thresholds, int32_t nthr, cclp_cu_sink_fn sink, void* sink_user,
+                     const volatile uint8_t* cancel, double* x_out, double* y_out, double* z_out,
+                     cclp_cu_result* res, int device) {
+  cclp_cu_ctx* ctx = nullptr;
+  int rc = cclp_cu_create(lp, device, &ctx);
+  if (rc != CCLP_CU_OK) return rc;
+  rc = cclp_cu_solve(ctx, cfg, tol, thresholds, nthr, sink, sink_user, cancel, nullptr, nullptr,
+                     x_out, y_out, z_out, res);
+  cclp_cu_destroy(ctx);
+  return rc;
+}
+
+}  // extern "C"

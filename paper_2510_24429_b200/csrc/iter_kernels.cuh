@@ -1,0 +1,400 @@
+// The two fused kernels of one PDHG iteration, plus the on-device decision
+// tail. Step t (state t -> t+1, pdhg_step, pdhg.cpp:118-143) is:
+//
+//   k_rows(t): ax_{t+1} = A x_{t+1}  (x_{t+1} was produced by k_cols(t-1))
+//              y_{t+1}  = y' + sigma (b - (2 ax_{t+1} - ax'))     (:125-126)
+//              y_sum, ax_sum += ; row-side report partials for check(t+1)
+//   k_cols(t): aty_{t+1} = A' y_{t+1}
+//              x_sum, aty_sum += ; column-side report partials for check(t+1)
+//              next-x candidates x_{t+2} = proj(x - tau (c - aty)) for both
+//              outcomes of the restart test at check(t+1) (continue / restart
+//              from the average), so no restart kernel is ever launched;
+//              last block: finalize = check(t+1) decisions (:311-368).
+//
+// (x', y', ax', aty') is state t after restart_if_improved (:145-165): when
+// check(t) restarted, the kernels read sums * (1/window) instead of the
+// current vectors — the same values the reference stores — and restart the
+// sums at zero.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace cclp_cu {
+
+constexpr unsigned kRowMaxMask = (1u << 1) | (1u << 4);
+constexpr unsigned kColMaxMask = (1u << 1) | (1u << 2) | (1u << 3) | (1u << 7) | (1u << 8) | (1u << 9);
+
+struct StepInfo {
+  long long t;   // state index before the step (-1 for the initial products)
+  long long t1;  // t + 1
+  int R;         // restart applied by this step
+  int s0, s1;    // ping-pong slots of states t and t+1
+  int xs;        // candidate slot holding x_{t+1}
+  int xs2;       // candidate slot receiving x_{t+2}
+  double inv;    // 1/window_t (restart average)
+  double inv1;   // 1/window_{t+1} (average view at check(t+1))
+  bool check;    // check(t+1) happens
+  bool init;
+};
+
+__device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepInfo& si) {
+  const Ctrl* C = p.ctrl;
+  if (C->stop >= 0 || C->halt) return false;
+  if (init) {
+    si.t = -1;
+    si.t1 = 0;
+    si.R = 0;
+    si.s0 = 0;
+    si.s1 = 0;
+    si.xs = 0;
+    si.xs2 = 1;
+    si.inv = 0.0;
+    si.inv1 = 0.0;
+    si.check = true;
+    si.init = true;
+    return true;
+  }
+  si.t = C->iteration;
+  si.t1 = si.t + 1;
+  si.R = C->R;
+  const long long win = C->window;
+  const long long win1 = (si.R ? 0 : win) + 1;
+  si.inv = si.R ? 1.0 / static_cast<double>(win) : 0.0;
+  si.inv1 = 1.0 / static_cast<double>(win1);
+  si.s0 = static_cast<int>(si.t & 1);
+  si.s1 = si.s0 ^ 1;
+  si.xs = static_cast<int>(si.t1 % 3);
+  si.xs2 = static_cast<int>((si.t1 + 1) % 3);
+  si.check = (si.t1 % p.check_interval) == 0;
+  si.init = false;
+  return true;
+}
+
+template <int G>
+__global__ void __launch_bounds__(kBlock) k_rows(const IterParams p, int init) {
+  StepInfo si;
+  if (!read_step(p, init != 0, si)) return;
+  __shared__ double sums[kBlock];
+  __shared__ double red[(kBlock / 32) * kRowParts];
+  __shared__ double out[kRowParts];
+  double acc[kRowParts];
+#pragma unroll
+  for (int k = 0; k < kRowParts; ++k) acc[k] = 0.0;
+  const double* xg = p.xc[si.xs][si.R];
+  const int rb = p.row_start[blockIdx.x], re = p.row_start[blockIdx.x + 1];
+  tile_loop<G, 4>(rb, re, p.rowptr, p.colind, p.aval, GatherPlain{xg}, sums,
+                  [&](int i, double axn) {
+                    const double r = p.r[i], b = p.b[i];
+                    if (si.init) {
+                      p.ax[0][i] = axn;
+                      row_report(axn, p.y[0][i], r, b, acc);
+                      return;
+                    }
+                    const double ys0 = p.ysum[si.s0][i], axs0 = p.axsum[si.s0][i];
+                    double yo, axo;
+                    if (si.R) {
+                      yo = ys0 * si.inv;
+                      axo = axs0 * si.inv;
+                    } else {
+                      yo = p.y[si.s0][i];
+                      axo = p.ax[si.s0][i];
+                    }
+                    const double bs = b * r;  // row_lower.cwiseProduct(r)
+                    double t = 2.0 * axn;
+                    t = t - axo;
+                    t = bs - t;
+                    t = p.sigma * t;
+                    const double yn = yo + t;
+                    const double ysn = (si.R ? 0.0 : ys0) + yn;
+                    const double axsn = (si.R ? 0.0 : axs0) + axn;
+                    p.y[si.s1][i] = yn;
+                    p.ax[si.s1][i] = axn;
+                    p.ysum[si.s1][i] = ysn;
+                    p.axsum[si.s1][i] = axsn;
+                    if (nonfinite(yn)) acc[6] += 1.0;
+                    if (si.check) {
+                      row_report(axn, yn, r, b, acc);
+                      row_report(axsn * si.inv1, ysn * si.inv1, r, b, acc + 3);
+                    }
+                  });
+  block_reduce<kRowParts, kRowMaxMask>(acc, red, out);
+  if (threadIdx.x < kRowParts) p.rowp[blockIdx.x * kRowParts + threadIdx.x] = out[threadIdx.x];
+}
+
+// check(t+1) and everything after the step in the reference pass
+// (pdhg.cpp:128-130 error, 301-368 next pass: time, check, limit). Runs on
+// one block; thread 0 takes the decisions.
+__device__ void finalize(const IterParams& p, const StepInfo& si) {
+  __shared__ double red[(kBlock / 32) * kColParts];
+  __shared__ double rowv[kRowParts];
+  __shared__ double colv[kColParts];
+  double ra[kRowParts], ca[kColParts];
+#pragma unroll
+  for (int k = 0; k < kRowParts; ++k) ra[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < kColParts; ++k) ca[k] = 0.0;
+  for (int b = threadIdx.x; b < p.row_grid; b += kBlock) {
+#pragma unroll
+    for (int k = 0; k < kRowParts; ++k) {
+      const double v = __ldcg(p.rowp + b * kRowParts + k);
+      ra[k] = ((kRowMaxMask >> k) & 1u) ? amax(ra[k], v) : ra[k] + v;
+    }
+  }
+  for (int b = threadIdx.x; b < p.col_grid; b += kBlock) {
+#pragma unroll
+    for (int k = 0; k < kColParts; ++k) {
+      const double v = __ldcg(p.colp + b * kColParts + k);
+      ca[k] = ((kColMaxMask >> k) & 1u) ? amax(ca[k], v) : ca[k] + v;
+    }
+  }
+  block_reduce<kRowParts, kRowMaxMask>(ra, red, rowv);
+  block_reduce<kColParts, kColMaxMask>(ca, red, colv);
+  if (threadIdx.x != 0) return;
+
+  Ctrl* C = p.ctrl;
+  if (!si.init) {
+    if (rowv[6] + colv[12] > 0.0) {  // PdhgNumericalError before commit
+      C->stop = 5;
+      C->error_iteration = si.t;
+      C->result_view = kViewCurEff;
+      C->result_report_valid = C->checked;
+      if (C->checked) {
+        const double* src = C->R ? C->avg : C->cur;
+        for (int k = 0; k < kRepN; ++k) C->result_report[k] = src[k];
+      }
+      return;
+    }
+    C->R_prev = C->R;
+    C->window = (C->R ? 0 : C->window) + 1;
+    C->iteration = si.t1;
+    C->R = 0;
+  }
+  const long long t1 = si.t1;
+  const long long win = C->window;
+  C->checked = si.check ? 1 : 0;
+  if (si.check) {
+    make_report(rowv, colv, p.b_norm, p.c_norm, C->cur);
+    if (win > 0) make_report(rowv + 3, colv + 6, p.b_norm, p.c_norm, C->avg);
+  }
+  if (isfin(p.time_limit)) {  // pdhg.cpp:306-310
+    const double el = 1e-9 * static_cast<double>(globaltimer() - *p.t0_ns);
+    if (el > p.time_limit) {
+      C->stop = 2;
+      C->result_view = kViewCur;
+      C->result_report_valid = C->checked;
+      if (C->checked)
+        for (int k = 0; k < kRepN; ++k) C->result_report[k] = C->cur[k];
+      return;
+    }
+  }
+  if (si.check) {  // pdhg.cpp:311-363
+    const bool use_avg = win > 0 && C->avg[kMaxResid] < C->cur[kMaxResid];
+    C->use_avg = use_avg ? 1 : 0;
+    const double* better = use_avg ? C->avg : C->cur;
+    if (!C->have_best || better[kMaxResid] < C->best[kMaxResid]) {
+      for (int k = 0; k < kRepN; ++k) C->best[k] = better[k];
+      C->have_best = 1;
+    }
+    if (C->last_restart_resid == CCLP_INF) C->last_restart_resid = C->cur[kMaxResid];
+    if (p.log_interval > 0 && t1 % p.log_interval == 0) {
+      LogEntry& e = p.log[C->log_count % p.log_cap];
+      e.iteration = t1;
+      e.rel_primal = better[kRelP];
+      e.rel_dual = better[kRelD];
+      e.rel_gap = better[kRelGap];
+      e.elapsed = 1e-9 * static_cast<double>(globaltimer() - *p.t0_ns);
+      C->log_count++;
+    }
+    if (better[kMaxResid] <= p.eps_rel) {
+      C->stop = 0;
+      C->result_view = use_avg ? kViewAvg : kViewCur;
+      C->result_report_valid = 1;
+      for (int k = 0; k < kRepN; ++k) C->result_report[k] = better[k];
+      return;
+    }
+    if (C->next_threshold < p.nthr && better[kMaxResid] <= p.thr[C->next_threshold]) {
+      C->halt = 1;
+      C->snap_pending = 1;
+      C->snap_use_avg = use_avg ? 1 : 0;
+      C->snap_thr_idx = C->next_threshold;
+      C->snap_maxresid = better[kMaxResid];
+      C->snap_iteration = t1;
+      C->next_threshold++;
+    }
+    if (win > 0 && C->avg[kMaxResid] <= p.restart_factor * C->last_restart_resid) {
+      C->R = 1;  // applied by the next step's kernels
+      C->last_restart_resid = C->avg[kMaxResid];
+      C->restarts++;
+    }
+  }
+  if (t1 >= p.max_iter) {  // pdhg.cpp:364-368
+    C->stop = 1;
+    C->result_view = kViewCurEff;
+    C->result_report_valid = C->checked;
+    if (C->checked) {
+      const double* src = C->R ? C->avg : C->cur;
+      for (int k = 0; k < kRepN; ++k) C->result_report[k] = src[k];
+    }
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(kBlock) k_cols(const IterParams p, int init) {
+  StepInfo si;
+  if (!read_step(p, init != 0, si)) return;
+  __shared__ double sums[kBlock];
+  __shared__ double red[(kBlock / 32) * kColParts];
+  __shared__ double out[kColParts];
+  __shared__ bool last;
+  double acc[kColParts];
+#pragma unroll
+  for (int k = 0; k < kColParts; ++k) acc[k] = 0.0;
+  const double* yg = p.y[si.s1];
+  double* cand_c = p.xc[si.xs2][0];
+  double* cand_a = p.xc[si.xs2][1];
+  const double* xcur = p.xc[si.xs][si.R];
+  const int rb = p.col_start[blockIdx.x], re = p.col_start[blockIdx.x + 1];
+  tile_loop<G, 4>(rb, re, p.colptr, p.rowind, p.atval, GatherPlain{yg}, sums,
+                  [&](int j, double atyn) {
+                    const double s = p.s[j], c = p.c[j], l = p.l[j], u = p.u[j];
+                    const double x1 = xcur[j];
+                    const double cs = c * s, ls = l / s, us = u / s;  // apply_scaling
+                    cand_c[j] = primal_update(x1, atyn, cs, ls, us, p.tau);
+                    if (si.init) {
+                      p.aty[0][j] = atyn;
+                      col_report(x1, atyn, s, c, l, u, acc);
+                      return;
+                    }
+                    const double xs0 = p.xsum[si.s0][j], as0 = p.atysum[si.s0][j];
+                    const double xsn = (si.R ? 0.0 : xs0) + x1;
+                    const double asn = (si.R ? 0.0 : as0) + atyn;
+                    p.aty[si.s1][j] = atyn;
+                    p.xsum[si.s1][j] = xsn;
+                    p.atysum[si.s1][j] = asn;
+                    if (nonfinite(x1)) acc[12] += 1.0;
+                    if (si.check) {
+                      col_report(x1, atyn, s, c, l, u, acc);
+                      const double xa = xsn * si.inv1, aa = asn * si.inv1;
+                      col_report(xa, aa, s, c, l, u, acc + 6);
+                      cand_a[j] = primal_update(xa, aa, cs, ls, us, p.tau);
+                    }
+                  });
+  block_reduce<kColParts, kColMaxMask>(acc, red, out);
+  if (threadIdx.x < kColParts) p.colp[blockIdx.x * kColParts + threadIdx.x] = out[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned prev = atomicAdd(p.counter, 1u);
+    last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  finalize(p, si);
+  if (threadIdx.x == 0) *p.counter = 0u;
+}
+
+// ---------------------------------------------------------------------------
+// View extraction for results and ladder snapshots: unscaled x, y, z of the
+// current or averaged iterate of state t (view_of, pdhg.cpp:271-283), plus
+// report partials for an independent recomputation when no check ran.
+// ---------------------------------------------------------------------------
+struct ViewParams {
+  IterParams it;
+  int view;  // kViewCur / kViewAvg (kViewCurEff resolved on the host)
+  long long t;
+  int R_prev;
+  double inv;  // 1/window_t for kViewAvg
+  double* x_out;
+  double* y_out;
+  double* z_out;
+  double* rowp;
+  double* colp;
+  unsigned* counter;
+  double* report;  // [kRepN]
+};
+
+__global__ void __launch_bounds__(kBlock) k_view_rows(const ViewParams v) {
+  const IterParams& p = v.it;
+  __shared__ double red[(kBlock / 32) * kRowParts];
+  __shared__ double out[kRowParts];
+  double acc[kRowParts];
+#pragma unroll
+  for (int k = 0; k < kRowParts; ++k) acc[k] = 0.0;
+  const int sl = static_cast<int>(v.t & 1);
+  for (int i = blockIdx.x * kBlock + threadIdx.x; i < p.m; i += gridDim.x * kBlock) {
+    double ys, axs;
+    if (v.view == kViewAvg) {
+      ys = p.ysum[sl][i] * v.inv;
+      axs = p.axsum[sl][i] * v.inv;
+    } else {
+      ys = p.y[sl][i];
+      axs = p.ax[sl][i];
+    }
+    const double r = p.r[i];
+    v.y_out[i] = ys * r;
+    row_report(axs, ys, r, p.b[i], acc);
+  }
+  block_reduce<kRowParts, kRowMaxMask>(acc, red, out);
+  if (threadIdx.x < kRowParts) v.rowp[blockIdx.x * kRowParts + threadIdx.x] = out[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kBlock) k_view_cols(const ViewParams v, int row_blocks) {
+  const IterParams& p = v.it;
+  __shared__ double red[(kBlock / 32) * kColParts];
+  __shared__ double out[kColParts];
+  __shared__ double rowv[kRowParts];
+  __shared__ double colv[kColParts];
+  __shared__ bool last;
+  double acc[kColParts];
+#pragma unroll
+  for (int k = 0; k < kColParts; ++k) acc[k] = 0.0;
+  const int sl = static_cast<int>(v.t & 1);
+  const double* xcur = p.xc[v.t % 3][v.R_prev];
+  for (int j = blockIdx.x * kBlock + threadIdx.x; j < p.n; j += gridDim.x * kBlock) {
+    double xs, as;
+    if (v.view == kViewAvg) {
+      xs = p.xsum[sl][j] * v.inv;
+      as = p.atysum[sl][j] * v.inv;
+    } else {
+      xs = xcur[j];
+      as = p.aty[sl][j];
+    }
+    const double s = p.s[j], c = p.c[j], l = p.l[j], u = p.u[j];
+    const double x = xs * s;
+    v.x_out[j] = x;
+    v.z_out[j] = clip_z(c, as / s, x, l, u);
+    col_report(xs, as, s, c, l, u, acc);
+  }
+  block_reduce<kColParts, kColMaxMask>(acc, red, out);
+  if (threadIdx.x < kColParts) v.colp[blockIdx.x * kColParts + threadIdx.x] = out[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(v.counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double ra[kRowParts], ca[kColParts];
+#pragma unroll
+  for (int k = 0; k < kRowParts; ++k) ra[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < kColParts; ++k) ca[k] = 0.0;
+  for (int b = threadIdx.x; b < row_blocks; b += kBlock)
+    for (int k = 0; k < kRowParts; ++k) {
+      const double x = __ldcg(v.rowp + b * kRowParts + k);
+      ra[k] = ((kRowMaxMask >> k) & 1u) ? amax(ra[k], x) : ra[k] + x;
+    }
+  for (int b = threadIdx.x; b < gridDim.x; b += kBlock)
+    for (int k = 0; k < kColParts; ++k) {
+      const double x = __ldcg(v.colp + b * kColParts + k);
+      ca[k] = ((kColMaxMask >> k) & 1u) ? amax(ca[k], x) : ca[k] + x;
+    }
+  block_reduce<kRowParts, kRowMaxMask>(ra, red, rowv);
+  block_reduce<kColParts, kColMaxMask>(ca, red, colv);
+  if (threadIdx.x == 0) {
+    make_report(rowv, colv, p.b_norm, p.c_norm, v.report);
+    *v.counter = 0u;
+  }
+}
+
+}  // namespace cclp_cu

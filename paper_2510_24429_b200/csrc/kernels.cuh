@@ -1,0 +1,278 @@
+// Device kernels of the cclp_cu PDHG engine (sm_100a). Compiled with
+// --fmad=false so every a*b+c rounds twice, as the reference's x86-64 build
+// does (no FMA contraction); elementwise operations follow the reference's
+// operation order exactly (cited per function).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "engine.cuh"
+
+namespace cclp_cu {
+
+#define CCLP_INF (__longlong_as_double(0x7ff0000000000000LL))
+
+// std::max / std::min argument semantics (pdhg.cpp uses both).
+__device__ __forceinline__ double smax(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double smin(double a, double b) { return (b < a) ? b : a; }
+// Accumulating max that ignores NaN exactly like `acc = std::max(acc, v)` with
+// a finite accumulator (the comparison is false for NaN, keeping acc).
+__device__ __forceinline__ double amax(double acc, double v) { return (acc < v) ? v : acc; }
+__device__ __forceinline__ bool isfin(double v) { return v > -CCLP_INF && v < CCLP_INF; }
+__device__ __forceinline__ bool nonfinite(double v) { return isnan(v - v); }
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// ---------------------------------------------------------------------------
+// Parameters of the fused iteration kernels (passed by value, captured into
+// CUDA graphs once per solve).
+// ---------------------------------------------------------------------------
+struct IterParams {
+  int m, n;
+  // CSR(A), scaled values
+  const int* rowptr;
+  const int* colind;
+  const double* aval;
+  // CSR(A^T) == CSC(A), scaled values
+  const int* colptr;
+  const int* rowind;
+  const double* atval;
+  // balanced block partitions [grid+1]
+  const int* row_start;
+  const int* col_start;
+  int row_grid, col_grid;
+  // unscaled problem data and Ruiz factors
+  const double *c, *l, *u, *b, *r, *s;
+  // state
+  double* xc[3][2];
+  double* aty[2];
+  double* xsum[2];
+  double* atysum[2];
+  double* y[2];
+  double* ax[2];
+  double* ysum[2];
+  double* axsum[2];
+  // partials and control
+  double* rowp;
+  double* colp;
+  unsigned* counter;
+  Ctrl* ctrl;
+  LogEntry* log;
+  int log_cap;
+  long long log_interval;
+  // scalars
+  double tau, sigma, eps_rel, restart_factor, b_norm, c_norm, time_limit;
+  long long max_iter;
+  int check_interval;
+  int nthr;
+  const double* thr;
+  const unsigned long long* t0_ns;
+};
+
+// ---------------------------------------------------------------------------
+// Block reductions (deterministic: fixed shuffle tree, fixed warp order).
+// ---------------------------------------------------------------------------
+template <int N, unsigned MAXMASK>
+__device__ __forceinline__ void block_reduce(double (&v)[N], double* smem, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < N; ++k) {
+    double a = v[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_down_sync(0xffffffffu, a, off);
+      a = ((MAXMASK >> k) & 1u) ? amax(a, o) : a + o;
+    }
+    if (lane == 0) smem[warp * N + k] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < N) {
+    const int k = threadIdx.x;
+    double a = smem[k];
+    for (int w = 1; w < kBlock / 32; ++w) {
+      const double o = smem[w * N + k];
+      a = ((MAXMASK >> k) & 1u) ? amax(a, o) : a + o;
+    }
+    out[k] = a;
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Group-of-G-lanes row dot product: lane l accumulates elements l, l+G, ...
+// sequentially (U independent loads in flight), then an xor-butterfly. The
+// order is fixed, so results are bit-reproducible run to run.
+// ---------------------------------------------------------------------------
+struct GatherPlain {
+  const double* v;
+  __device__ __forceinline__ double operator()(int j) const { return __ldg(v + j); }
+};
+struct GatherDiv {  // v_j = u_j / nu (power iteration: v = u / norm, pdhg.cpp:62)
+  const double* v;
+  const double* nu;
+  __device__ __forceinline__ double operator()(int j) const { return __ldg(v + j) / *nu; }
+};
+
+template <int G, int U, class Gather>
+__device__ __forceinline__ double group_dot(int beg, int end, int lane, const int* __restrict__ idx,
+                                            const double* __restrict__ val, const Gather& g) {
+  double acc = 0.0;
+  for (int p = beg + lane; p < end; p += G * U) {
+    int ii[U];
+    double vv[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int q = p + k * G;
+      const bool ok = q < end;
+      ii[k] = ok ? __ldcs(idx + q) : -1;
+      vv[k] = ok ? __ldcs(val + q) : 0.0;
+    }
+    double xx[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) xx[k] = ii[k] >= 0 ? g(ii[k]) : 0.0;
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (ii[k] >= 0) acc = acc + vv[k] * xx[k];
+  }
+  return acc;
+}
+
+template <int G>
+__device__ __forceinline__ double group_allreduce(double s) {
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+  return s;
+}
+
+// Tile loop shared by every "row" kernel: the block owns rows [rb, re) and
+// walks them in tiles of kBlock rows. Phase 1 (SpMV): groups of G lanes
+// reduce one row each, G passes per tile, into smem. Phase 2 (epilogue): one
+// thread per row, coalesced, calls epi(row, sum).
+template <int G, int U, class Gather, class Epi>
+__device__ __forceinline__ void tile_loop(int rb, int re, const int* __restrict__ ptr,
+                                          const int* __restrict__ idx,
+                                          const double* __restrict__ val, const Gather& g,
+                                          double* sums, Epi&& epi) {
+  constexpr int GPB = kBlock / G;
+  const int gid = threadIdx.x / G, lane = threadIdx.x % G;
+  for (int tile = rb; tile < re; tile += kBlock) {
+    const int nrows = min(kBlock, re - tile);
+#pragma unroll 1
+    for (int k = 0; k < G; ++k) {
+      const int local = k * GPB + gid;
+      double s = 0.0;
+      if (local < nrows) {
+        const int row = tile + local;
+        s = group_dot<G, U>(__ldg(ptr + row), __ldg(ptr + row + 1), lane, idx, val, g);
+      }
+      s = group_allreduce<G>(s);
+      if (lane == 0 && local < nrows) sums[local] = s;
+    }
+    __syncthreads();
+    if (threadIdx.x < nrows) epi(tile + threadIdx.x, sums[threadIdx.x]);
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Report contributions (report_from_products, pdhg.cpp:170-220) on the
+// unscaled model, computed from scaled values exactly as view_of does
+// (pdhg.cpp:271-283: x*s, y*r, ax/r, aty/s).
+// ---------------------------------------------------------------------------
+// acc: [0] rp2 (sum), [1] rp_inf (max), [2] b.y (sum)
+__device__ __forceinline__ void row_report(double axs, double ys, double r, double b, double* acc) {
+  const double ax = axs / r;
+  const double y = ys * r;
+  double v = 0.0;
+  if (ax < b) {
+    v = b - ax;
+  } else if (ax > b) {
+    v = ax - b;
+  }
+  acc[0] += v * v;
+  acc[1] = amax(acc[1], v);
+  acc[2] += b * y;
+}
+
+// clipped_reduced_costs (pdhg.cpp:89-108) for one column.
+__device__ __forceinline__ double clip_z(double c, double aty, double x, double l, double u) {
+  double z = c - aty;
+  const bool lo = isfin(l), up = isfin(u);
+  if (!lo && !up) {
+    z = 0.0;
+  } else if (lo && up) {
+    const double dl = x - l, du = u - x;
+    z = dl <= du ? smax(z, 0.0) : smin(z, 0.0);
+  } else if (lo) {
+    z = smax(z, 0.0);
+  } else {
+    z = smin(z, 0.0);
+  }
+  return z;
+}
+
+// acc: [0] rd2 (sum), [1] rd_inf (max), [2] bound violation inf (max),
+//      [3] complementarity (max), [4] dual bound terms (sum), [5] c.x (sum)
+__device__ __forceinline__ void col_report(double xs, double atys, double s, double c, double l,
+                                           double u, double* acc) {
+  const double x = xs * s;
+  const double aty = atys / s;
+  const double z = clip_z(c, aty, x, l, u);
+  double rd = aty + z;
+  rd = rd - c;
+  acc[0] += rd * rd;
+  acc[1] = amax(acc[1], fabs(rd));
+  double bv = l - x;  // std::max({l - x, x - u, 0.0})
+  if (bv < x - u) bv = x - u;
+  if (bv < 0.0) bv = 0.0;
+  acc[2] = amax(acc[2], bv);
+  double dist = CCLP_INF;
+  if (isfin(l)) dist = smin(dist, fabs(x - l));
+  if (isfin(u)) dist = smin(dist, fabs(x - u));
+  if (isfin(dist)) acc[3] = amax(acc[3], dist * fabs(z));
+  if (z > 0.0 && isfin(l)) {
+    acc[4] += l * z;
+  } else if (z < 0.0 && isfin(u)) {
+    acc[4] += u * z;
+  }
+  acc[5] += c * x;
+}
+
+// pdhg_step primal update (pdhg.cpp:121-123): (x - tau*(c - aty)) clamped.
+__device__ __forceinline__ double primal_update(double x, double aty, double cs, double ls,
+                                                double us, double tau) {
+  double t = cs - aty;
+  t = tau * t;
+  t = x - t;
+  t = smax(t, ls);  // cwiseMax(col_lower)
+  return smin(t, us);  // cwiseMin(col_upper)
+}
+
+// Assembles a ResidualReport (pdhg.cpp:211-219).
+__device__ __forceinline__ void make_report(const double* rowv, const double* colv, double bn,
+                                            double cn, double* rep) {
+  rep[kRpNorm2] = sqrt(rowv[0]);
+  rep[kRdNorm2] = sqrt(colv[0]);
+  rep[kRpInf] = amax(rowv[1], colv[2]);
+  rep[kRdInf] = colv[1];
+  rep[kCompl] = colv[3];
+  rep[kPobj] = colv[5];
+  rep[kDobj] = rowv[2] + colv[4];
+  rep[kGap] = fabs(rep[kPobj] - rep[kDobj]);
+  rep[kRelP] = rep[kRpNorm2] / (1.0 + bn);
+  rep[kRelD] = rep[kRdNorm2] / (1.0 + cn);
+  rep[kRelGap] = rep[kGap] / (1.0 + fabs(rep[kPobj]) + fabs(rep[kDobj]));
+  double mx = rep[kRelP];  // std::max({p, d, g})
+  if (mx < rep[kRelD]) mx = rep[kRelD];
+  if (mx < rep[kRelGap]) mx = rep[kRelGap];
+  rep[kMaxResid] = mx;
+}
+
+}  // namespace cclp_cu

@@ -1,0 +1,298 @@
+// One-time kernels: CSR(A) construction, balanced partitions, plain SpMV,
+// Ruiz equilibration (scaling.cpp:46-90), power iteration for ||A||
+// (pdhg.cpp:46-65) and deterministic vector reductions.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace cclp_cu {
+
+__global__ void k_expand_major(const int* __restrict__ ptr, int outer, int* __restrict__ major) {
+  // major[p] = outer index owning nonzero p
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < outer; j += gridDim.x * blockDim.x)
+    for (int p = ptr[j]; p < ptr[j + 1]; ++p) major[p] = j;
+}
+
+__global__ void k_iota(int* a, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = static_cast<int>(i);
+}
+
+// ptr[i] = first position with sorted_key >= i (sorted keys -> CSR offsets).
+__global__ void k_offsets_from_sorted(const int* __restrict__ keys, long long nnz, int rows,
+                                      int* __restrict__ ptr) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= rows; i += gridDim.x * blockDim.x) {
+    long long lo = 0, hi = nnz;
+    while (lo < hi) {
+      const long long mid = (lo + hi) / 2;
+      if (keys[mid] >= i) hi = mid; else lo = mid + 1;
+    }
+    ptr[i] = static_cast<int>(lo);
+  }
+}
+
+__global__ void k_gather_csr(const int* __restrict__ perm, long long nnz,
+                             const int* __restrict__ col_of, const double* __restrict__ val_in,
+                             int* __restrict__ colind, double* __restrict__ val_out) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < nnz;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int p = perm[q];
+    colind[q] = col_of[p];
+    val_out[q] = val_in[p];
+  }
+}
+
+// Block b owns rows [start[b], start[b+1]) with ~equal weight
+// w(i) = ptr[i] + alpha * i (nonzeros plus a per-row epilogue cost).
+__global__ void k_partition(const int* __restrict__ ptr, int rows, int grid, long long alpha,
+                            int* __restrict__ start) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b > grid) return;
+  if (b == grid) {
+    start[b] = rows;
+    return;
+  }
+  const long long total = static_cast<long long>(ptr[rows]) + alpha * rows;
+  const long long target = total * b / grid;
+  int lo = 0, hi = rows;
+  while (lo < hi) {
+    const int mid = (lo + hi) / 2;
+    if (static_cast<long long>(ptr[mid]) + alpha * mid >= target) hi = mid; else lo = mid + 1;
+  }
+  start[b] = lo;
+}
+
+// Plain y = M v over a CSR (used for matvec / matvec_transpose and the power
+// iteration's A v; G = 1 gives the reference's exact sequential order).
+template <int G, class Gather>
+__global__ void __launch_bounds__(kBlock) k_spmv(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                                 const double* __restrict__ val, Gather g,
+                                                 const int* __restrict__ start, double* __restrict__ out,
+                                                 const int* stop_flag) {
+  if (stop_flag != nullptr && *stop_flag) return;
+  __shared__ double sums[kBlock];
+  const int rb = start[blockIdx.x], re = start[blockIdx.x + 1];
+  tile_loop<G, 4>(rb, re, ptr, idx, val, g, sums, [&](int i, double s) { out[i] = 0.0 + s; });
+}
+
+// ---- power iteration (estimate_matrix_norm, pdhg.cpp:46-65) ---------------
+struct PowerCtrl {
+  double nu;      // ||u_prev|| (v = u_prev / nu)
+  double lambda;  // Rayleigh quotient v.u
+  int zero;       // ||u|| == 0 -> result 0
+  int pad;
+};
+
+// u = A' w, partial sums of u.u and v.u with v = u_prev / nu; the last block
+// finalizes nu and lambda.
+template <int G>
+__global__ void __launch_bounds__(kBlock) k_power_cols(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ w,
+                                                       const int* __restrict__ start,
+                                                       const double* __restrict__ u_prev,
+                                                       double* __restrict__ u, double* part,
+                                                       unsigned* counter, PowerCtrl* pc) {
+  if (pc->zero) return;
+  __shared__ double sums[kBlock];
+  __shared__ double red[(kBlock / 32) * 2];
+  __shared__ double out[2];
+  __shared__ bool last;
+  double acc[2] = {0.0, 0.0};
+  const double nu = pc->nu;
+  const int rb = start[blockIdx.x], re = start[blockIdx.x + 1];
+  tile_loop<G, 4>(rb, re, ptr, idx, val, GatherPlain{w}, sums, [&](int j, double s) {
+    const double uj = 0.0 + s;
+    u[j] = uj;
+    const double vj = u_prev[j] / nu;
+    acc[0] += uj * uj;
+    acc[1] += vj * uj;
+  });
+  block_reduce<2, 0u>(acc, red, out);
+  if (threadIdx.x < 2) part[blockIdx.x * 2 + threadIdx.x] = out[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double a2[2] = {0.0, 0.0};
+  for (int b = threadIdx.x; b < gridDim.x; b += kBlock) {
+    a2[0] += __ldcg(part + 2 * b);
+    a2[1] += __ldcg(part + 2 * b + 1);
+  }
+  block_reduce<2, 0u>(a2, red, out);
+  if (threadIdx.x == 0) {
+    const double norm = sqrt(out[0]);
+    if (norm == 0.0) {
+      pc->zero = 1;
+    } else {
+      pc->lambda = out[1];
+      pc->nu = norm;
+    }
+    *counter = 0u;
+  }
+}
+
+// ---- deterministic reductions over a vector --------------------------------
+// mode 0: sum a[i]^2      mode 1: sum (a[i]*b[i])^2      mode 2: sum a[i]*b[i]
+__global__ void __launch_bounds__(kBlock) k_reduce(const double* __restrict__ a, const double* __restrict__ b,
+                                                   long long n, int mode, double* part,
+                                                   unsigned* counter, double* result) {
+  __shared__ double red[kBlock / 32];
+  __shared__ double out[1];
+  __shared__ bool last;
+  double acc[1] = {0.0};
+  for (long long i = blockIdx.x * (long long)kBlock + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kBlock) {
+    double v;
+    if (mode == 0) {
+      v = a[i] * a[i];
+    } else if (mode == 1) {
+      const double t = a[i] * b[i];
+      v = t * t;
+    } else {
+      v = a[i] * b[i];
+    }
+    acc[0] += v;
+  }
+  block_reduce<1, 0u>(acc, red, out);
+  if (threadIdx.x == 0) part[blockIdx.x] = out[0];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double s[1] = {0.0};
+  for (int q = threadIdx.x; q < gridDim.x; q += kBlock) s[0] += __ldcg(part + q);
+  block_reduce<1, 0u>(s, red, out);
+  if (threadIdx.x == 0) {
+    *result = out[0];
+    *counter = 0u;
+  }
+}
+
+__global__ void k_div_scalar(const double* __restrict__ a, const double* den, double* __restrict__ out,
+                             long long n) {
+  const double d = *den;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    out[i] = a[i] / d;
+}
+
+__global__ void k_fill(double* a, long long n, double v) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    a[i] = v;
+}
+
+// ---- Ruiz equilibration (scaling.cpp:46-90) --------------------------------
+// max over the row of (|a| * r_row) * s_col: exact (order-free).
+template <int G>
+__global__ void __launch_bounds__(kBlock) k_scaled_absmax(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                                          const double* __restrict__ val,
+                                                          const double* __restrict__ self_scale,
+                                                          const double* __restrict__ other_scale,
+                                                          int self_is_row, const int* __restrict__ start,
+                                                          double* __restrict__ out) {
+  constexpr int GPB = kBlock / G;
+  const int gid = threadIdx.x / G, lane = threadIdx.x % G;
+  const int rb = start[blockIdx.x], re = start[blockIdx.x + 1];
+  for (int tile = rb; tile < re; tile += GPB) {
+    const int row = tile + gid;
+    double mx = 0.0;
+    if (row < re) {
+      const double sr = self_scale[row];
+      for (int p = ptr[row] + lane; p < ptr[row + 1]; p += G) {
+        const double so = other_scale[idx[p]];
+        // v = |a_ij| * r_i * s_j evaluated left to right (scaling.cpp:60-61)
+        const double v = self_is_row ? (fabs(val[p]) * sr) * so : (fabs(val[p]) * so) * sr;
+        if (v > mx) mx = v;
+      }
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, mx, off);
+      if (o > mx) mx = o;
+    }
+    if (lane == 0 && row < re) out[row] = mx;
+  }
+}
+
+// flag |= some max outside [1/2, 2) (scaling.cpp:64-80)
+__global__ void k_ruiz_notdone(const double* __restrict__ mx, int n, int* flag) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double v = mx[i];
+    if (v > 0.0 && (v < 0.5 || v >= 2.0)) *flag = 1;
+  }
+}
+
+// pow2_sqrt(v) = exp2(round(0.5 * log2(v))) (scaling.cpp:23-25), bit-exact
+// with glibc: exact powers of two are decided in integer arithmetic; values
+// whose half-log lies within 1e-9 of a rounding boundary are listed for the
+// host to evaluate with glibc (never observed on generated LPs).
+__device__ __forceinline__ bool pow2_sqrt_dev(double v, double* out) {
+  int e;
+  const double f = frexp(v, &e);  // v = f 2^e, f in [0.5, 1)
+  if (f == 0.5) {
+    const int L = e - 1;  // log2(v), exact
+    int k;                // round(L / 2), halves away from zero
+    if (L >= 0) k = (L + 1) / 2; else k = -((-L + 1) / 2);
+    *out = ldexp(1.0, k);
+    return true;
+  }
+  const double h = 0.5 * log2(v);
+  const double fl = floor(h);
+  const double frac = h - fl;
+  if (fabs(frac - 0.5) < 1e-9) return false;
+  *out = ldexp(1.0, static_cast<int>(frac < 0.5 ? fl : fl + 1.0));
+  return true;
+}
+
+__global__ void k_ruiz_update(const double* __restrict__ mx, int n, double* __restrict__ scale,
+                              int* amb_count, int* amb_idx, int amb_cap) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double v = mx[i];
+    if (!(v > 0.0)) continue;
+    double p2;
+    if (pow2_sqrt_dev(v, &p2)) {
+      scale[i] /= p2;
+    } else {
+      const int k = atomicAdd(amb_count, 1);
+      if (k < amb_cap) amb_idx[k] = i;
+    }
+  }
+}
+
+// scaled values: val * (r_row * s_col)  (apply_scaling, scaling.cpp:33-37)
+__global__ void k_scale_values(const int* __restrict__ ptr, int outer, const int* __restrict__ idx,
+                               const double* __restrict__ val, const double* __restrict__ outer_scale,
+                               const double* __restrict__ inner_scale, int outer_is_row,
+                               double* __restrict__ out) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int o = warp; o < outer; o += nwarps) {
+    const double so = outer_scale[o];
+    for (int p = ptr[o] + lane; p < ptr[o + 1]; p += 32) {
+      const double si = inner_scale[idx[p]];
+      const double f = outer_is_row ? so * si : si * so;  // r_i * s_j
+      out[p] = val[p] * f;
+    }
+  }
+}
+
+// x_0 = Zero.cwiseMax(l').cwiseMin(u') on the scaled bounds (pdhg.cpp:71-73)
+__global__ void k_init_x(const double* __restrict__ l, const double* __restrict__ u,
+                         const double* __restrict__ s, int n, double* __restrict__ x) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
+    const double ls = l[j] / s[j], us = u[j] / s[j];
+    x[j] = smin(smax(0.0, ls), us);
+  }
+}
+
+__global__ void k_stamp(unsigned long long* t) { *t = globaltimer(); }
+
+}  // namespace cclp_cu

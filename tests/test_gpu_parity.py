@@ -1,0 +1,177 @@
+"""GPU parity: the sm_100a engine against the CPU oracle (oracle/cclp_oracle.c,
+itself pinned bit-exact to the reference's own code and golden fixtures).
+
+Tolerances (north_star, BASELINE.json): primal/dual iterates within 1e-6
+relative after equal iteration counts (fp64); iterations-to-converge within
+5%. Integer/exact work (Ruiz factors, pow2 scaling) is checked bit-exact.
+"""
+import numpy as np
+import pytest
+
+from paper_2510_24429_b200 import lpgen
+from paper_2510_24429_b200.lp import INF, LinearProgram
+from paper_2510_24429_b200.pdhg import (Engine, PdhgConfig, PdhgStopReason, Tolerances,
+                                        run_pdhg)
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-6  # north_star: iterates within 1e-6 relative at equal iterations
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    d = np.linalg.norm(a - b)
+    return d / max(np.linalg.norm(b), 1e-300) if d > 0 else 0.0
+
+
+def small_lps():
+    out = [("twovar", lpgen.two_var_lp())]
+    for seed in range(4):
+        out.append((f"eq6x12_s{seed}", lpgen.small_equality_lp(6, 12, 0.5, seed)[0]))
+    out.append(("eq40x90", lpgen.small_equality_lp(40, 90, 0.2, 7)[0]))
+    out.append(("transport20x30", lpgen.transportation_lp(20, 30, seed=3)))
+    return out
+
+
+@pytest.mark.parametrize("name,lp", small_lps())
+def test_matvec_matches_oracle(name, lp, oracle):
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal(lp.n)
+    y = rng.standard_normal(lp.m)
+    with Engine(lp) as eng:
+        ax, aty = eng.matvec(x), eng.matvec_transpose(y)
+    ax_o, aty_o = oracle.matvec(lp, x), oracle.matvec_transpose(lp, y)
+    assert np.allclose(ax, ax_o, rtol=1e-13, atol=1e-13)
+    assert np.allclose(aty, aty_o, rtol=1e-13, atol=1e-13)
+
+
+@pytest.mark.parametrize("name,lp", small_lps())
+def test_ruiz_bit_exact(name, lp, oracle):
+    with Engine(lp) as eng:
+        r, s = eng.ruiz(10)
+    r_o, s_o, _ = oracle.ruiz(lp, 10)
+    assert np.array_equal(r, r_o)
+    assert np.array_equal(s, s_o)
+
+
+@pytest.mark.parametrize("name,lp", small_lps())
+def test_norm_estimate(name, lp, oracle):
+    with Engine(lp) as eng:
+        est = eng.estimate_norm(100, 0)
+    ref = oracle.estimate_norm(lp, 100, 0)
+    assert est == pytest.approx(ref, rel=1e-12)
+
+
+def test_norm_known_answers():
+    # test_pdhg.cpp:13-25
+    row = LinearProgram(1, 2, np.array([0, 1, 2], np.int32), np.array([0, 0], np.int32),
+                        np.ones(2), np.ones(2), np.ones(1), np.ones(1), np.zeros(2),
+                        np.full(2, INF))
+    with Engine(row) as e:
+        assert e.estimate_norm(50, 1) == pytest.approx(np.sqrt(2.0), rel=1e-12)
+    diag = LinearProgram(2, 2, np.array([0, 1, 2], np.int32), np.array([0, 1], np.int32),
+                         np.array([3.0, 4.0]), np.ones(2), np.ones(2), np.ones(2), np.zeros(2),
+                         np.full(2, INF))
+    with Engine(diag) as e:
+        assert e.estimate_norm(100, 1) == pytest.approx(4.0, rel=1e-10)
+
+
+@pytest.mark.parametrize("name,lp", small_lps())
+@pytest.mark.parametrize("iters", [0, 1, 7, 200])
+def test_equal_iteration_parity(name, lp, iters, oracle):
+    cfg = PdhgConfig(max_iterations=iters)
+    res = run_pdhg(lp, cfg)
+    ref = oracle.run_pdhg(lp, config=dict(max_iterations=iters))
+    if ref["stop"] == "converged":
+        assert res.stop == PdhgStopReason.kConverged
+    else:
+        assert res.stop == PdhgStopReason.kIterationLimit
+    assert res.iterations == ref["iterations"]
+    assert res.restarts == ref["restarts"]
+    assert rel(res.iterate.x, ref["x"]) <= REL_TOL
+    assert rel(res.iterate.y, ref["y"]) <= REL_TOL
+    assert rel(res.iterate.z, ref["z"]) <= REL_TOL
+    assert res.report.maxresid_rel == pytest.approx(ref["report"]["maxresid_rel"], rel=1e-6,
+                                                    abs=1e-12)
+
+
+@pytest.mark.parametrize("name,lp", small_lps())
+def test_convergence_parity(name, lp, oracle):
+    res = run_pdhg(lp, PdhgConfig(max_iterations=20000))
+    ref = oracle.run_pdhg(lp, config=dict(max_iterations=20000))
+    assert res.stop.name == {"converged": "kConverged",
+                             "iteration-limit": "kIterationLimit"}[ref["stop"]]
+    assert abs(res.iterations - ref["iterations"]) <= 0.05 * ref["iterations"] + 1
+    if ref["stop"] == "converged":
+        assert res.report.maxresid_rel <= 1e-6
+        assert rel(res.iterate.x, ref["x"]) <= 1e-4
+
+
+def test_two_var_vertex():
+    # test_pdhg.cpp:107-120
+    res = run_pdhg(lpgen.two_var_lp())
+    assert res.stop == PdhgStopReason.kConverged
+    assert res.report.maxresid_rel <= 1e-6
+    assert abs(res.iterate.x[0] - 2.0) < 1e-4 and abs(res.iterate.x[1]) < 1e-4
+    assert res.report.primal_objective == pytest.approx(2.0, rel=1e-5)
+
+
+def test_snapshot_ladder(oracle):
+    # test_pdhg.cpp:122-136
+    snaps = []
+    res = run_pdhg(lpgen.two_var_lp(), thresholds=[1e-2, 1e-3], sink=snaps.append)
+    ref = oracle.run_pdhg(lpgen.two_var_lp(), thresholds=[1e-2, 1e-3])
+    assert res.stop == PdhgStopReason.kConverged
+    assert [s.threshold for s in snaps] == [1e-2, 1e-3]
+    assert snaps[0].maxresid <= 1e-2 and snaps[1].maxresid <= 1e-3
+    assert snaps[0].iteration < snaps[1].iteration
+    assert [s.iteration for s in snaps] == [s["iteration"] for s in ref["snapshots"]]
+    for s, r in zip(snaps, ref["snapshots"]):
+        assert s.from_average == r["from_average"]
+        assert rel(s.iterate.x, r["x"]) <= REL_TOL
+        assert rel(s.iterate.y, r["y"]) <= REL_TOL
+
+
+def test_preconditions_raise():
+    lp = lpgen.two_var_lp()
+    with pytest.raises(ValueError):
+        run_pdhg(lp, thresholds=[1e-3, 1e-2])
+    with pytest.raises(ValueError):
+        run_pdhg(lp, tol=Tolerances(eps_rel=1e-1))
+    ineq = lpgen.two_var_lp()
+    ineq.row_lower = np.array([-INF])
+    with pytest.raises(ValueError):
+        run_pdhg(ineq)
+
+
+def test_numerical_error_reported(oracle):
+    # test_pdhg.cpp:93-105 drives pdhg_step with huge steps; through run_pdhg
+    # a 1e308 cost overflows the iterate.
+    lp = lpgen.two_var_lp()
+    lp.c = np.array([1e308, 2.0])
+    res = run_pdhg(lp, PdhgConfig(max_iterations=100, scaling_iterations=0, step_scale=1.0))
+    ref = oracle.run_pdhg(lp, config=dict(max_iterations=100, scaling_iterations=0,
+                                          step_scale=1.0))
+    assert to_name(res.stop) == ref["stop"]
+    if ref["stop"] == "numerical-error":
+        assert res.error_iteration == ref["error_iteration"]
+
+
+def to_name(stop):
+    return ["converged", "iteration-limit", "time-limit", "cancelled", "won-by-crossover",
+            "numerical-error"][int(stop)]
+
+
+def test_zero_iteration_budget():
+    res = run_pdhg(lpgen.two_var_lp(), PdhgConfig(max_iterations=0))
+    assert res.stop == PdhgStopReason.kIterationLimit
+    assert res.iterations == 0
+
+
+def test_rerun_bit_identical():
+    lp = lpgen.small_equality_lp(6, 12, 0.5, 77)[0]
+    a = run_pdhg(lp, PdhgConfig(max_iterations=500))
+    b = run_pdhg(lp, PdhgConfig(max_iterations=500))
+    assert np.array_equal(a.iterate.x, b.iterate.x)
+    assert np.array_equal(a.iterate.y, b.iterate.y)
+    assert a.report.maxresid_rel == b.report.maxresid_rel
