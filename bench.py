@@ -1,0 +1,363 @@
+"""Benchmark: PDHG iterations/s of the B200 engine on BASELINE.json configs[1]
+(C2: synthetic random sparse equality LP, m=100k, n=500k, 5M nnz, fp64).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one batch of `--iters-per-step` PDHG iterations (reference loop
+body, check_interval = 1: both residual reports, restart and stop decisions
+every iteration) on device-resident state. `value` = total iterations / max
+over ranks of the device time of the K timed steps (CUDA events on the engine
+stream). `e2e` = the same metric through the public C-ABI call
+(cclp_cu_run_pdhg via paper_2510_24429_b200.pdhg.run_pdhg) from pinned host
+buffers: LP upload, CSR build, Ruiz, ||A||, the loop and the result download
+are all inside the timed region. The working set (~180 MB) exceeds the
+126 MB L2, so no flush is needed between steps.
+
+Multi-GPU (torchrun, N>1): C2 fits one GPU, so ranks run independent
+replicas ("replicas only" for C1-C3); value sums iterations over
+ranks, time is the max over ranks.
+
+`--impl reference` times the reference's own run_pdhg (oracle/_ref, built
+from /root/reference's sources) on the host cores of rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PDHG iterations/s (C2 random LP 100k x 500k, 5M nnz, fp64, check every iteration)"
+UNIT = "iter/s"
+CONFIG_NAME = "C2"
+
+
+def algorithmic_bytes(m: int, n: int, nnz: int) -> dict:
+    """B_iter = 24 nnz + 20 (m+n) + 8, split per kernel:
+    row kernel (A x): 12 nnz + 4(m+1) + 8n (x) + 8m (ax);
+    column kernel (A'y): 12 nnz + 4(n+1) + 8m (y) + 8n (aty)."""
+    return dict(iteration=24 * nnz + 20 * (m + n) + 8,
+                rows=12 * nnz + 4 * (m + 1) + 8 * n + 8 * m,
+                cols=12 * nnz + 4 * (n + 1) + 8 * m + 8 * n)
+
+
+def measured_peak_gbs():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1 and args.impl != "reference":
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group(backend="nccl")
+        pg = dist
+    return world, rank, local, pg
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def allreduce_max(pg, v: float, device) -> float:
+    if pg is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(pg, v: float, device) -> float:
+    if pg is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    pg.all_reduce(t, op=pg.ReduceOp.SUM)
+    return float(t.item())
+
+
+def pinned_copy(lp):
+    """The LP's arrays in pinned host memory (the e2e input buffers)."""
+    import torch
+    from paper_2510_24429_b200.lp import LinearProgram
+
+    def pin(a, dt):
+        t = torch.empty(a.shape, dtype=dt, pin_memory=True)
+        t.numpy()[...] = a
+        return t
+
+    keep = [pin(lp.colptr, torch.int32), pin(lp.rowind, torch.int32), pin(lp.val, torch.float64),
+            pin(lp.c, torch.float64), pin(lp.row_lower, torch.float64),
+            pin(lp.row_upper, torch.float64), pin(lp.col_lower, torch.float64),
+            pin(lp.col_upper, torch.float64)]
+    arrs = [k.numpy() for k in keep]
+    return LinearProgram(lp.m, lp.n, *arrs, name=lp.name), keep
+
+
+def cpu_reference_rate(lp, iters: int, use_ref: bool = True):
+    """Loop-only iterations/s of the reference run_pdhg: (T(S) - T(0)) / S."""
+    from oracle.pyoracle import Reference, Restatement, reference_available
+    kind = "reference" if (use_ref and reference_available()) else "port"
+    impl = Reference() if kind == "reference" else Restatement()
+    t = time.perf_counter()
+    impl.run_pdhg(lp, config=dict(max_iterations=0))
+    t0 = time.perf_counter() - t
+    t = time.perf_counter()
+    r = impl.run_pdhg(lp, config=dict(max_iterations=iters))
+    ts = time.perf_counter() - t
+    return dict(value=r["iterations"] / max(ts - t0, 1e-9), setup_s=t0, total_s=ts,
+                iterations=r["iterations"], kind=kind)
+
+
+def run_reference_arm(args, world, rank, pg):
+    from paper_2510_24429_b200 import lpgen
+    if rank != 0:  # the reference is a single-process CPU code: rank 0 only
+        return
+    lp = lpgen.make_config(CONFIG_NAME)
+    from oracle.pyoracle import Reference, Restatement, reference_available
+    kind = "reference" if reference_available() else "port"
+    impl = Reference() if kind == "reference" else Restatement()
+    S = args.ref_iters
+    t = time.perf_counter()
+    impl.run_pdhg(lp, config=dict(max_iterations=0))  # setup only: Ruiz + ||A|| + check(0)
+    t_setup = time.perf_counter() - t
+    for _ in range(max(args.warmup - 1, 0)):
+        impl.run_pdhg(lp, config=dict(max_iterations=1))
+    loop_s, iters = 0.0, 0
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        r = impl.run_pdhg(lp, config=dict(max_iterations=S))
+        loop_s += max(time.perf_counter() - t - t_setup, 1e-9)
+        iters += r["iterations"]
+    v = iters / loop_s
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * loop_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded generator, paper_2510_24429_b200/lpgen.py)",
+        "config": {"workload": CONFIG_NAME, "m": lp.m, "n": lp.n, "nnz": lp.nnz,
+                   "iters_per_step": S, "check_interval": 1},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": kind,
+                         "sample": f"C2, {args.steps} x run_pdhg(max_iterations={S}) minus its "
+                                   f"setup ({t_setup:.2f} s: Ruiz + power iteration), "
+                                   "single-threaded (reference has no threading)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--iters-per-step", type=int, default=100)
+    ap.add_argument("--e2e-iters", type=int, default=2000)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--ref-iters", type=int, default=20)
+    ap.add_argument("--cpu-iters", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local, pg = dist_setup(args)
+    if args.impl == "reference":
+        run_reference_arm(args, world, rank, pg)
+        return
+
+    import torch
+    from paper_2510_24429_b200 import lpgen
+    from paper_2510_24429_b200.pdhg import Engine, PdhgConfig, Tolerances, run_pdhg
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lp = lpgen.make_config(CONFIG_NAME)
+    eng = Engine(lp, device=local)
+    eng.begin(PdhgConfig())
+    stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
+    K, W, I = args.steps, args.warmup, args.iters_per_step
+    for _ in range(W):
+        eng.advance(I)
+    launches0 = eng.describe()["launches"]
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    barrier(pg)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        ev0.record(stream)
+        lib_ms = 0.0
+        for _ in range(K):
+            lib_ms += eng.advance(I)
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier(pg)
+    dev_ms = ev0.elapsed_time(ev1)
+    launches = eng.describe()["launches"] - launches0
+    t_max = allreduce_max(pg, dev_ms, dev)
+    total_iters = allreduce_sum(pg, float(K * I), dev)
+    value = total_iters / (t_max * 1e-3)
+
+    # per-kernel device time for the roofline (eager launches, events between)
+    rows_ms, cols_ms = eng.profile_kernels(100)
+    ab = algorithmic_bytes(lp.m, lp.n, lp.nnz)
+    dom = "cols" if cols_ms >= rows_ms else "rows"
+    dom_ms = max(rows_ms, cols_ms)
+    achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
+    peak, peak_kind = measured_peak_gbs()
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            tr = json.load(f).get(CONFIG_NAME, {})
+            traffic = tr.get("k_cols" if dom == "cols" else "k_rows")
+    except Exception:
+        pass
+    iter_us = dev_ms * 1e3 / (K * I)
+    eng.close()
+
+    # e2e: public API from pinned host buffers, upload..download timed
+    plp, _keep = pinned_copy(lp)
+    h2d = sum(a.nbytes for a in (plp.colptr, plp.rowind, plp.val, plp.c, plp.row_lower,
+                                 plp.row_upper, plp.col_lower, plp.col_upper))
+    d2h = 8 * (2 * lp.n + lp.m)
+    cfg = PdhgConfig(max_iterations=args.e2e_iters)
+    run_pdhg(plp, PdhgConfig(max_iterations=10), device=local)  # warm
+    barrier(pg)
+    e2e_t, e2e_it = 0.0, 0
+    for _ in range(args.e2e_steps):
+        t = time.perf_counter()
+        res = run_pdhg(plp, cfg, device=local)
+        e2e_t += time.perf_counter() - t
+        e2e_it += res.iterations
+    e2e_t = allreduce_max(pg, e2e_t, dev)
+    e2e_total = allreduce_sum(pg, float(e2e_it), dev)
+    e2e_value = e2e_total / e2e_t
+
+    # time to tolerance (one solve, rank 0)
+    ttt = None
+    if rank == 0:
+        t = time.perf_counter()
+        r4 = run_pdhg(plp, PdhgConfig(max_iterations=200000),
+                      tol=Tolerances(eps_rel=1e-4),
+                      device=local)
+        ttt = {"eps_rel": 1e-4, "seconds": time.perf_counter() - t, "iterations": r4.iterations,
+               "stop": r4.stop.name, "restarts": r4.restarts}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cb = cpu_reference_rate(lp, args.cpu_iters)
+        cpu = {"value": cb["value"], "unit": UNIT, "cores": 1, "kind": cb["kind"],
+               "sample": f"C2, run_pdhg(max_iterations={args.cpu_iters}) minus "
+                         f"run_pdhg(max_iterations=0) ({cb['setup_s']:.2f} s setup), 1 thread "
+                         "(the reference loop is single-threaded)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": t_max / K, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, paper_2510_24429_b200/lpgen.py)",
+            "config": {"workload": CONFIG_NAME, "m": lp.m, "n": lp.n, "nnz": lp.nnz,
+                       "iters_per_step": I, "check_interval": 1,
+                       "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "working set ~180 MB > 126 MB L2, no flush"},
+            "us_per_iteration": iter_us,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": f"k_{dom}",
+                         "kernel_us": dom_ms * 1e3, "bytes_per_launch": ab[dom],
+                         "peak_kind": peak_kind,
+                         "iteration": {"bytes": ab["iteration"],
+                                       "achieved": ab["iteration"] / (iter_us * 1e-6) / 1e9,
+                                       "frac": ab["iteration"] / (iter_us * 1e-6) / 1e9 / peak},
+                         "rows_kernel_us": rows_ms * 1e3, "cols_kernel_us": cols_ms * 1e3},
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "iters_per_step": args.e2e_iters,
+                    "includes": "upload, CSR build, Ruiz, ||A|| power iteration, loop, download"},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+            "time_to_tolerance": ttt,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -77,6 +77,10 @@ typedef struct {
   int64_t log_interval;       /* 0 disables the iteration log */
   int32_t deterministic;      /* always honoured: fixed reduction order */
   int32_t poll_interval;      /* iterations per device batch (0 -> 64) */
+  int32_t exact_spmv;         /* 1: every SpMV row sum in the reference's own
+                                 sequential order (bit-identical products;
+                                 slower on long rows). 0: G lanes per row with
+                                 a fixed butterfly (deterministic). */
 } cclp_cu_config;
 
 /* Tolerances (kkt.hpp:32-41). */

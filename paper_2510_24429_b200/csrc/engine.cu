@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <type_traits>
 #include <random>
 #include <stdexcept>
 #include <string>
@@ -66,6 +67,19 @@ int blocks_for(long long n, int per = kBlock, int cap = 148 * 8) {
   return static_cast<int>(std::max<long long>(1, std::min<long long>(b, cap)));
 }
 
+// Calls f(std::integral_constant<int, G>) for the runtime group size G.
+template <class F>
+void with_group(int G, F&& f) {
+  switch (G) {
+    case 1: f(std::integral_constant<int, 1>{}); break;
+    case 2: f(std::integral_constant<int, 2>{}); break;
+    case 4: f(std::integral_constant<int, 4>{}); break;
+    case 8: f(std::integral_constant<int, 8>{}); break;
+    case 16: f(std::integral_constant<int, 16>{}); break;
+    default: f(std::integral_constant<int, 32>{}); break;
+  }
+}
+
 }  // namespace
 
 struct Context {
@@ -84,6 +98,7 @@ struct Context {
   // partitions
   int Grow = 1, Gcol = 1, row_grid = 1, col_grid = 1;
   int *row_start = nullptr, *col_start = nullptr;
+  bool exact = false;  // G = 1: reference-order (bit-identical) SpMV sums
   // state
   double* xc[3][2] = {};
   double *aty[2] = {}, *xsum[2] = {}, *atysum[2] = {};
@@ -123,6 +138,8 @@ struct Context {
   void upload(const cclp_cu_lp* lp);
   void build_csr();
   void partition();
+  int grow() const { return exact ? 1 : Grow; }
+  int gcol() const { return exact ? 1 : Gcol; }
   void launch_spmv(bool transpose, const double* vec, double* out, bool scaled, const int* stop);
   double reduce(const double* a, const double* bvec, long long len, int mode);
   void ruiz(int iterations);
@@ -241,9 +258,20 @@ void Context::build_csr() {
 void Context::partition() {
   Grow = pick_group(nnz, m);
   Gcol = pick_group(nnz, n);
-  const int cap = 148 * 4;
-  row_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (m + 63) / 64)));
-  col_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (n + 63) / 64)));
+  // Persistent-style grids: exactly the resident blocks of the whole GPU
+  // (148 SMs x occupancy), each owning a contiguous, nnz-balanced row range.
+  int sms = 148, occ_r = 1, occ_c = 1;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  with_group(Grow, [&](auto g) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, k_rows<decltype(g)::value>, kRowsBlock, 0));
+  });
+  with_group(Gcol, [&](auto g) {
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_cols<decltype(g)::value>, kColsBlock, 0));
+  });
+  const long long cap_r = static_cast<long long>(sms) * std::max(occ_r, 1);
+  const long long cap_c = static_cast<long long>(sms) * std::max(occ_c, 1);
+  row_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap_r, (m + 31) / 32 + nnz / 1024)));
+  col_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap_c, (n + 31) / 32 + nnz / 1024)));
   row_start = dalloc<int>(row_grid + 1);
   col_start = dalloc<int>(col_grid + 1);
   k_partition<<<blocks_for(row_grid + 1), kBlock, 0, stream>>>(rowptr, m, row_grid, 8, row_start);
@@ -251,6 +279,7 @@ void Context::partition() {
   CKL("partition");
   rowp = dalloc<double>(static_cast<size_t>(std::max(row_grid, 148 * 8)) * kRowParts);
   colp = dalloc<double>(static_cast<size_t>(std::max(col_grid, 148 * 8)) * kColParts);
+  // view kernels reuse rowp/colp with up to 148*4 blocks
   work_part = dalloc<double>(148 * 8 * 2);
   counter = dalloc<unsigned>(4);
   CK(cudaMemsetAsync(counter, 0, sizeof(unsigned) * 4, stream));
@@ -265,28 +294,15 @@ void Context::partition() {
   t0 = dalloc<unsigned long long>(1);
 }
 
-template <class Gather>
-static void spmv_dispatch(int G, int grid, cudaStream_t st, const int* ptr, const int* idx,
-                          const double* val, Gather g, const int* start, double* out,
-                          const int* stop) {
-  switch (G) {
-    case 1: k_spmv<1><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
-    case 2: k_spmv<2><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
-    case 4: k_spmv<4><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
-    case 8: k_spmv<8><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
-    case 16: k_spmv<16><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
-    default: k_spmv<32><<<grid, kBlock, 0, st>>>(ptr, idx, val, g, start, out, stop); break;
-  }
-}
-
 void Context::launch_spmv(bool transpose, const double* vec, double* out, bool scaled,
                           const int* stop) {
+  // kernel-level matvec (kernels.hpp:27-40): reference-order sums (G = 1)
   if (!transpose) {
-    spmv_dispatch(Grow, row_grid, stream, rowptr, colind, scaled ? sval_csr : val_csr,
-                  GatherPlain{vec}, row_start, out, stop);
+    k_spmv<1><<<row_grid, kBlock, 0, stream>>>(rowptr, colind, scaled ? sval_csr : val_csr,
+                                               GatherPlain{vec}, row_start, out, stop);
   } else {
-    spmv_dispatch(Gcol, col_grid, stream, colptr, rowind, scaled ? sval_csc : val_csc,
-                  GatherPlain{vec}, col_start, out, stop);
+    k_spmv<1><<<col_grid, kBlock, 0, stream>>>(colptr, rowind, scaled ? sval_csc : val_csc,
+                                               GatherPlain{vec}, col_start, out, stop);
   }
   CKL("spmv");
 }
@@ -383,19 +399,15 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled) {
   const double* atval = scaled ? sval_csc : val_csc;
   for (int t = 0; t < iterations; ++t) {
     // w = A v with v = u_prev / nu  (Vector w = A * v, :57)
-    switch (Grow) {
-#define CASE(G) case G: k_spmv<G><<<row_grid, kBlock, 0, stream>>>(rowptr, colind, aval, GatherDiv{u_prev, &pctrl->nu}, row_start, wm, &pctrl->zero); break;
-      CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
-      default: k_spmv<32><<<row_grid, kBlock, 0, stream>>>(rowptr, colind, aval, GatherDiv{u_prev, &pctrl->nu}, row_start, wm, &pctrl->zero); break;
-#undef CASE
-    }
+    with_group(grow(), [&](auto g) {
+      k_spmv<decltype(g)::value><<<row_grid, kBlock, 0, stream>>>(
+          rowptr, colind, aval, GatherDiv{u_prev, &pctrl->nu}, row_start, wm, &pctrl->zero);
+    });
     // u = A' w; nu = ||u||; lambda = v.u  (:58-61)
-    switch (Gcol) {
-#define CASE(G) case G: k_power_cols<G><<<col_grid, kBlock, 0, stream>>>(colptr, rowind, atval, wm, col_start, u_prev, u, work_part, counter + 2, pctrl); break;
-      CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
-      default: k_power_cols<32><<<col_grid, kBlock, 0, stream>>>(colptr, rowind, atval, wm, col_start, u_prev, u, work_part, counter + 2, pctrl); break;
-#undef CASE
-    }
+    with_group(gcol(), [&](auto g) {
+      k_power_cols<decltype(g)::value><<<col_grid, kBlock, 0, stream>>>(
+          colptr, rowind, atval, wm, col_start, u_prev, u, work_part, counter + 2, pctrl);
+    });
     CKL("power");
     std::swap(u_prev, u);
   }
@@ -408,18 +420,8 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled) {
 void Context::launch_iteration(bool init) {
   const IterParams& p = params;
   const int ii = init ? 1 : 0;
-  switch (Grow) {
-#define CASE(G) case G: k_rows<G><<<row_grid, kBlock, 0, stream>>>(p, ii); break;
-    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
-    default: k_rows<32><<<row_grid, kBlock, 0, stream>>>(p, ii); break;
-#undef CASE
-  }
-  switch (Gcol) {
-#define CASE(G) case G: k_cols<G><<<col_grid, kBlock, 0, stream>>>(p, ii); break;
-    CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
-    default: k_cols<32><<<col_grid, kBlock, 0, stream>>>(p, ii); break;
-#undef CASE
-  }
+  with_group(grow(), [&](auto g) { k_rows<decltype(g)::value><<<row_grid, kRowsBlock, 0, stream>>>(p, ii); });
+  with_group(gcol(), [&](auto g) { k_cols<decltype(g)::value><<<col_grid, kColsBlock, 0, stream>>>(p, ii); });
   launches += 2;
 }
 
@@ -442,6 +444,11 @@ void Context::build_graph(int k) {
 
 void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
                     const double* thresholds, int nthr) {
+  exact = cfg.exact_spmv != 0;
+  if (graph) {
+    cudaGraphExecDestroy(graph);
+    graph = nullptr;
+  }
   k_stamp<<<1, 1, 0, stream>>>(t0);
   CKL("stamp");
   const auto h0 = std::chrono::steady_clock::now();
@@ -655,6 +662,7 @@ void cclp_cu_default_config(cclp_cu_config* cfg) {
   cfg->log_interval = 0;
   cfg->deterministic = 1;
   cfg->poll_interval = 0;
+  cfg->exact_spmv = 0;
 }
 
 void cclp_cu_default_tolerances(cclp_cu_tolerances* t) {
@@ -733,19 +741,13 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
     for (auto& e : ev) CK(cudaEventCreate(&e));
     for (long long i = 0; i < iters; ++i) {
       CK(cudaEventRecord(ev[3 * i], C.stream));
-      switch (C.Grow) {
-#define CASE(G) case G: cclp_cu::k_rows<G><<<C.row_grid, cclp_cu::kBlock, 0, C.stream>>>(C.params, 0); break;
-        CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
-        default: cclp_cu::k_rows<32><<<C.row_grid, cclp_cu::kBlock, 0, C.stream>>>(C.params, 0); break;
-#undef CASE
-      }
+      cclp_cu::with_group(C.grow(), [&](auto g) {
+        cclp_cu::k_rows<decltype(g)::value><<<C.row_grid, cclp_cu::kRowsBlock, 0, C.stream>>>(C.params, 0);
+      });
       CK(cudaEventRecord(ev[3 * i + 1], C.stream));
-      switch (C.Gcol) {
-#define CASE(G) case G: cclp_cu::k_cols<G><<<C.col_grid, cclp_cu::kBlock, 0, C.stream>>>(C.params, 0); break;
-        CASE(1) CASE(2) CASE(4) CASE(8) CASE(16)
-        default: cclp_cu::k_cols<32><<<C.col_grid, cclp_cu::kBlock, 0, C.stream>>>(C.params, 0); break;
-#undef CASE
-      }
+      cclp_cu::with_group(C.gcol(), [&](auto g) {
+        cclp_cu::k_cols<decltype(g)::value><<<C.col_grid, cclp_cu::kColsBlock, 0, C.stream>>>(C.params, 0);
+      });
       CK(cudaEventRecord(ev[3 * i + 2], C.stream));
       C.launches += 2;
     }
@@ -768,7 +770,13 @@ void* cclp_cu_stream(cclp_cu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.
 
 int cclp_cu_describe(cclp_cu_ctx* ctx, int64_t* out, int32_t nout) {
   const Context& C = ctx->c;
-  const int64_t v[] = {C.m, C.n, C.nnz, C.Grow, C.Gcol, C.row_grid, C.col_grid, C.launches};
+  Ctrl st;
+  std::memset(&st, 0, sizeof st);
+  if (C.ctrl != nullptr && cudaMemcpy(&st, C.ctrl, sizeof st, cudaMemcpyDeviceToHost) != cudaSuccess)
+    cudaGetLastError();
+  const int64_t v[] = {C.m, C.n, C.nnz, C.grow(), C.gcol(), C.row_grid, C.col_grid, C.launches,
+                       static_cast<int64_t>(st.t_fin_start - st.t_cols_start),
+                       static_cast<int64_t>(st.t_fin_end - st.t_fin_start)};
   for (int i = 0; i < nout && i < static_cast<int>(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
   return CCLP_CU_OK;
 }

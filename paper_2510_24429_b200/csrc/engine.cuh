@@ -17,7 +17,9 @@
 
 namespace cclp_cu {
 
-constexpr int kBlock = 256;
+constexpr int kBlock = 256;       // setup / view kernels
+constexpr int kRowsBlock = 256;
+constexpr int kColsBlock = 256;
 constexpr int kRowParts = 8;   // per-block partials of the row kernel
 constexpr int kColParts = 14;  // per-block partials of the column kernel
 
@@ -58,6 +60,9 @@ struct Ctrl {
   int pad;
   double last_restart_resid;
   double snap_maxresid;
+  // timing probes (globaltimer ns) of the last step: column-kernel start
+  // (block 0), finalize start and end
+  unsigned long long t_cols_start, t_fin_start, t_fin_end;
   double cur[kRepN], avg[kRepN], best[kRepN], result_report[kRepN];
 };
 

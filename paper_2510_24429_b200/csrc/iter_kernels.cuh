@@ -71,87 +71,75 @@ __device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepIn
 }
 
 template <int G>
-__global__ void __launch_bounds__(kBlock) k_rows(const IterParams p, int init) {
+__global__ void __launch_bounds__(kRowsBlock) k_rows(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
-  __shared__ double sums[kBlock];
-  __shared__ double red[(kBlock / 32) * kRowParts];
+  __shared__ double wsum[kRowsBlock];
+  __shared__ double red[(kRowsBlock / 32) * kRowParts];
   __shared__ double out[kRowParts];
   double acc[kRowParts];
 #pragma unroll
   for (int k = 0; k < kRowParts; ++k) acc[k] = 0.0;
   const double* xg = p.xc[si.xs][si.R];
   const int rb = p.row_start[blockIdx.x], re = p.row_start[blockIdx.x + 1];
-  tile_loop<G, 4>(rb, re, p.rowptr, p.colind, p.aval, GatherPlain{xg}, sums,
-                  [&](int i, double axn) {
-                    const double r = p.r[i], b = p.b[i];
-                    if (si.init) {
-                      p.ax[0][i] = axn;
-                      row_report(axn, p.y[0][i], r, b, acc);
-                      return;
-                    }
-                    const double ys0 = p.ysum[si.s0][i], axs0 = p.axsum[si.s0][i];
-                    double yo, axo;
-                    if (si.R) {
-                      yo = ys0 * si.inv;
-                      axo = axs0 * si.inv;
-                    } else {
-                      yo = p.y[si.s0][i];
-                      axo = p.ax[si.s0][i];
-                    }
-                    const double bs = b * r;  // row_lower.cwiseProduct(r)
-                    double t = 2.0 * axn;
-                    t = t - axo;
-                    t = bs - t;
-                    t = p.sigma * t;
-                    const double yn = yo + t;
-                    const double ysn = (si.R ? 0.0 : ys0) + yn;
-                    const double axsn = (si.R ? 0.0 : axs0) + axn;
-                    p.y[si.s1][i] = yn;
-                    p.ax[si.s1][i] = axn;
-                    p.ysum[si.s1][i] = ysn;
-                    p.axsum[si.s1][i] = axsn;
-                    if (nonfinite(yn)) acc[6] += 1.0;
-                    if (si.check) {
-                      row_report(axn, yn, r, b, acc);
-                      row_report(axsn * si.inv1, ysn * si.inv1, r, b, acc + 3);
-                    }
-                  });
-  block_reduce<kRowParts, kRowMaxMask>(acc, red, out);
+  struct RowOps {
+    double r, b, y, ax, ys, axs;
+  };
+  warp_tiles<G>(rb, re, p.rowptr, p.colind, p.aval, GatherPlain{xg}, wsum + (threadIdx.x & ~31),
+                [&](int i) {
+                  RowOps o;
+                  o.r = p.r[i];
+                  o.b = p.b[i];
+                  o.y = p.y[si.s0][i];
+                  o.ax = si.init ? 0.0 : p.ax[si.s0][i];
+                  o.ys = si.init ? 0.0 : p.ysum[si.s0][i];
+                  o.axs = si.init ? 0.0 : p.axsum[si.s0][i];
+                  return o;
+                },
+                [&](int i, double axn, const RowOps& o) {
+                  const double r = o.r, b = o.b;
+                  const double rinv = pow2_recip(r);
+                  if (si.init) {
+                    p.ax[0][i] = axn;
+                    row_report(axn, o.y, r, rinv, b, acc);
+                    return;
+                  }
+                  const double ys0 = o.ys, axs0 = o.axs;
+                  double yo, axo;
+                  if (si.R) {
+                    yo = ys0 * si.inv;
+                    axo = axs0 * si.inv;
+                  } else {
+                    yo = o.y;
+                    axo = o.ax;
+                  }
+                  const double bs = b * r;  // row_lower.cwiseProduct(r)
+                  double t = 2.0 * axn;
+                  t = t - axo;
+                  t = bs - t;
+                  t = p.sigma * t;
+                  const double yn = yo + t;
+                  const double ysn = (si.R ? 0.0 : ys0) + yn;
+                  const double axsn = (si.R ? 0.0 : axs0) + axn;
+                  p.y[si.s1][i] = yn;
+                  p.ax[si.s1][i] = axn;
+                  p.ysum[si.s1][i] = ysn;
+                  p.axsum[si.s1][i] = axsn;
+                  if (nonfinite(yn)) acc[6] += 1.0;
+                  if (si.check) {
+                    row_report(axn, yn, r, rinv, b, acc);
+                    row_report(axsn * si.inv1, ysn * si.inv1, r, rinv, b, acc + 3);
+                  }
+                });
+  block_reduce<kRowParts, kRowMaxMask, kRowsBlock>(acc, red, out);
   if (threadIdx.x < kRowParts) p.rowp[blockIdx.x * kRowParts + threadIdx.x] = out[threadIdx.x];
 }
 
 // check(t+1) and everything after the step in the reference pass
-// (pdhg.cpp:128-130 error, 301-368 next pass: time, check, limit). Runs on
-// one block; thread 0 takes the decisions.
-__device__ void finalize(const IterParams& p, const StepInfo& si) {
-  __shared__ double red[(kBlock / 32) * kColParts];
-  __shared__ double rowv[kRowParts];
-  __shared__ double colv[kColParts];
-  double ra[kRowParts], ca[kColParts];
-#pragma unroll
-  for (int k = 0; k < kRowParts; ++k) ra[k] = 0.0;
-#pragma unroll
-  for (int k = 0; k < kColParts; ++k) ca[k] = 0.0;
-  for (int b = threadIdx.x; b < p.row_grid; b += kBlock) {
-#pragma unroll
-    for (int k = 0; k < kRowParts; ++k) {
-      const double v = __ldcg(p.rowp + b * kRowParts + k);
-      ra[k] = ((kRowMaxMask >> k) & 1u) ? amax(ra[k], v) : ra[k] + v;
-    }
-  }
-  for (int b = threadIdx.x; b < p.col_grid; b += kBlock) {
-#pragma unroll
-    for (int k = 0; k < kColParts; ++k) {
-      const double v = __ldcg(p.colp + b * kColParts + k);
-      ca[k] = ((kColMaxMask >> k) & 1u) ? amax(ca[k], v) : ca[k] + v;
-    }
-  }
-  block_reduce<kRowParts, kRowMaxMask>(ra, red, rowv);
-  block_reduce<kColParts, kColMaxMask>(ca, red, colv);
-  if (threadIdx.x != 0) return;
-
-  Ctrl* C = p.ctrl;
+// (pdhg.cpp:128-130 error, 301-368 next pass: time, check, limit), taken by
+// thread 0 on a shared-memory copy of the control block.
+__device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, Ctrl* C,
+                                       const double* rowv, const double* colv) {
   if (!si.init) {
     if (rowv[6] + colv[12] > 0.0) {  // PdhgNumericalError before commit
       C->stop = 5;
@@ -238,12 +226,57 @@ __device__ void finalize(const IterParams& p, const StepInfo& si) {
   }
 }
 
+static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied as 8-byte words");
+
+// Runs on the last block of k_cols: reduces every block's partials, then
+// decide() on a shared copy of the control block (one coalesced read and one
+// write instead of a chain of dependent global round trips).
+__device__ void finalize(const IterParams& p, const StepInfo& si) {
+  __shared__ double red[(kColsBlock / 32) * kColParts];
+  __shared__ double rowv[kRowParts];
+  __shared__ double colv[kColParts];
+  __shared__ Ctrl cs;
+  constexpr int kWords = sizeof(Ctrl) / 8;
+  long long* csw = reinterpret_cast<long long*>(&cs);
+  const long long* gw = reinterpret_cast<const long long*>(p.ctrl);
+  for (int w = threadIdx.x; w < kWords; w += kColsBlock) csw[w] = __ldcg(gw + w);
+  double ra[kRowParts], ca[kColParts];
+#pragma unroll
+  for (int k = 0; k < kRowParts; ++k) ra[k] = 0.0;
+#pragma unroll
+  for (int k = 0; k < kColParts; ++k) ca[k] = 0.0;
+  for (int b = threadIdx.x; b < p.row_grid; b += kColsBlock) {
+    double v[kRowParts];
+#pragma unroll
+    for (int k = 0; k < kRowParts; ++k) v[k] = __ldcg(p.rowp + b * kRowParts + k);
+#pragma unroll
+    for (int k = 0; k < kRowParts; ++k) ra[k] = ((kRowMaxMask >> k) & 1u) ? amax(ra[k], v[k]) : ra[k] + v[k];
+  }
+  for (int b = threadIdx.x; b < p.col_grid; b += kColsBlock) {
+    double v[kColParts];
+#pragma unroll
+    for (int k = 0; k < kColParts; ++k) v[k] = __ldcg(p.colp + b * kColParts + k);
+#pragma unroll
+    for (int k = 0; k < kColParts; ++k) ca[k] = ((kColMaxMask >> k) & 1u) ? amax(ca[k], v[k]) : ca[k] + v[k];
+  }
+  block_reduce<kRowParts, kRowMaxMask, kColsBlock>(ra, red, rowv);
+  block_reduce<kColParts, kColMaxMask, kColsBlock>(ca, red, colv);
+  if (threadIdx.x == 0) {
+    cs.t_cols_start = globaltimer();  // debug: reuse as "partials reduced" stamp
+    decide(p, si, &cs, rowv, colv);
+    cs.t_fin_end = globaltimer();
+  }
+  __syncthreads();
+  long long* out = reinterpret_cast<long long*>(p.ctrl);
+  for (int w = threadIdx.x; w < kWords; w += kColsBlock) out[w] = csw[w];
+}
+
 template <int G>
-__global__ void __launch_bounds__(kBlock) k_cols(const IterParams p, int init) {
+__global__ void __launch_bounds__(kColsBlock) k_cols(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
-  __shared__ double sums[kBlock];
-  __shared__ double red[(kBlock / 32) * kColParts];
+  __shared__ double wsum[kColsBlock];
+  __shared__ double red[(kColsBlock / 32) * kColParts];
   __shared__ double out[kColParts];
   __shared__ bool last;
   double acc[kColParts];
@@ -254,32 +287,48 @@ __global__ void __launch_bounds__(kBlock) k_cols(const IterParams p, int init) {
   double* cand_a = p.xc[si.xs2][1];
   const double* xcur = p.xc[si.xs][si.R];
   const int rb = p.col_start[blockIdx.x], re = p.col_start[blockIdx.x + 1];
-  tile_loop<G, 4>(rb, re, p.colptr, p.rowind, p.atval, GatherPlain{yg}, sums,
-                  [&](int j, double atyn) {
-                    const double s = p.s[j], c = p.c[j], l = p.l[j], u = p.u[j];
-                    const double x1 = xcur[j];
-                    const double cs = c * s, ls = l / s, us = u / s;  // apply_scaling
-                    cand_c[j] = primal_update(x1, atyn, cs, ls, us, p.tau);
-                    if (si.init) {
-                      p.aty[0][j] = atyn;
-                      col_report(x1, atyn, s, c, l, u, acc);
-                      return;
-                    }
-                    const double xs0 = p.xsum[si.s0][j], as0 = p.atysum[si.s0][j];
-                    const double xsn = (si.R ? 0.0 : xs0) + x1;
-                    const double asn = (si.R ? 0.0 : as0) + atyn;
-                    p.aty[si.s1][j] = atyn;
-                    p.xsum[si.s1][j] = xsn;
-                    p.atysum[si.s1][j] = asn;
-                    if (nonfinite(x1)) acc[12] += 1.0;
-                    if (si.check) {
-                      col_report(x1, atyn, s, c, l, u, acc);
-                      const double xa = xsn * si.inv1, aa = asn * si.inv1;
-                      col_report(xa, aa, s, c, l, u, acc + 6);
-                      cand_a[j] = primal_update(xa, aa, cs, ls, us, p.tau);
-                    }
-                  });
-  block_reduce<kColParts, kColMaxMask>(acc, red, out);
+  struct ColOps {
+    double s, c, l, u, x, xs, as;
+  };
+  warp_tiles<G>(rb, re, p.colptr, p.rowind, p.atval, GatherPlain{yg}, wsum + (threadIdx.x & ~31),
+                [&](int j) {
+                  ColOps o;
+                  o.s = p.s[j];
+                  o.c = p.c[j];
+                  o.l = p.l[j];
+                  o.u = p.u[j];
+                  o.x = xcur[j];
+                  o.xs = si.init ? 0.0 : p.xsum[si.s0][j];
+                  o.as = si.init ? 0.0 : p.atysum[si.s0][j];
+                  return o;
+                },
+                [&](int j, double atyn, const ColOps& o) {
+                  const double s = o.s, c = o.c, l = o.l, u = o.u;
+                  const double sinv = pow2_recip(s);
+                  const double x1 = o.x;
+                  // apply_scaling: c*s, l/s, u/s (l/s == l*(1/s) exactly)
+                  const double cs = c * s, ls = l * sinv, us = u * sinv;
+                  cand_c[j] = primal_update(x1, atyn, cs, ls, us, p.tau);
+                  if (si.init) {
+                    p.aty[0][j] = atyn;
+                    col_report(x1, atyn, s, sinv, c, l, u, acc);
+                    return;
+                  }
+                  const double xs0 = o.xs, as0 = o.as;
+                  const double xsn = (si.R ? 0.0 : xs0) + x1;
+                  const double asn = (si.R ? 0.0 : as0) + atyn;
+                  p.aty[si.s1][j] = atyn;
+                  p.xsum[si.s1][j] = xsn;
+                  p.atysum[si.s1][j] = asn;
+                  if (nonfinite(x1)) acc[12] += 1.0;
+                  if (si.check) {
+                    col_report(x1, atyn, s, sinv, c, l, u, acc);
+                    const double xa = xsn * si.inv1, aa = asn * si.inv1;
+                    col_report(xa, aa, s, sinv, c, l, u, acc + 6);
+                    cand_a[j] = primal_update(xa, aa, cs, ls, us, p.tau);
+                  }
+                });
+  block_reduce<kColParts, kColMaxMask, kColsBlock>(acc, red, out);
   if (threadIdx.x < kColParts) p.colp[blockIdx.x * kColParts + threadIdx.x] = out[threadIdx.x];
   __threadfence();
   __syncthreads();
@@ -290,6 +339,7 @@ __global__ void __launch_bounds__(kBlock) k_cols(const IterParams p, int init) {
   __syncthreads();
   if (!last) return;
   __threadfence();
+  if (threadIdx.x == 0) p.ctrl->t_fin_start = globaltimer();
   finalize(p, si);
   if (threadIdx.x == 0) *p.counter = 0u;
 }
@@ -333,7 +383,7 @@ __global__ void __launch_bounds__(kBlock) k_view_rows(const ViewParams v) {
     }
     const double r = p.r[i];
     v.y_out[i] = ys * r;
-    row_report(axs, ys, r, p.b[i], acc);
+    row_report(axs, ys, r, pow2_recip(r), p.b[i], acc);
   }
   block_reduce<kRowParts, kRowMaxMask>(acc, red, out);
   if (threadIdx.x < kRowParts) v.rowp[blockIdx.x * kRowParts + threadIdx.x] = out[threadIdx.x];
@@ -361,10 +411,11 @@ __global__ void __launch_bounds__(kBlock) k_view_cols(const ViewParams v, int ro
       as = p.aty[sl][j];
     }
     const double s = p.s[j], c = p.c[j], l = p.l[j], u = p.u[j];
+    const double sinv = pow2_recip(s);
     const double x = xs * s;
     v.x_out[j] = x;
-    v.z_out[j] = clip_z(c, as / s, x, l, u);
-    col_report(xs, as, s, c, l, u, acc);
+    v.z_out[j] = clip_z(c, as * sinv, x, l, u);
+    col_report(xs, as, s, sinv, c, l, u, acc);
   }
   block_reduce<kColParts, kColMaxMask>(acc, red, out);
   if (threadIdx.x < kColParts) v.colp[blockIdx.x * kColParts + threadIdx.x] = out[threadIdx.x];
@@ -389,8 +440,8 @@ __global__ void __launch_bounds__(kBlock) k_view_cols(const ViewParams v, int ro
       const double x = __ldcg(v.colp + b * kColParts + k);
       ca[k] = ((kColMaxMask >> k) & 1u) ? amax(ca[k], x) : ca[k] + x;
     }
-  block_reduce<kRowParts, kRowMaxMask>(ra, red, rowv);
-  block_reduce<kColParts, kColMaxMask>(ca, red, colv);
+  block_reduce<kRowParts, kRowMaxMask, kColsBlock>(ra, red, rowv);
+  block_reduce<kColParts, kColMaxMask, kColsBlock>(ca, red, colv);
   if (threadIdx.x == 0) {
     make_report(rowv, colv, p.b_norm, p.c_norm, v.report);
     *v.counter = 0u;

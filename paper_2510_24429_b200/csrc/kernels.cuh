@@ -79,7 +79,7 @@ struct IterParams {
 // ---------------------------------------------------------------------------
 // Block reductions (deterministic: fixed shuffle tree, fixed warp order).
 // ---------------------------------------------------------------------------
-template <int N, unsigned MAXMASK>
+template <int N, unsigned MAXMASK, int BS = kBlock>
 __device__ __forceinline__ void block_reduce(double (&v)[N], double* smem, double* out) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -96,7 +96,7 @@ __device__ __forceinline__ void block_reduce(double (&v)[N], double* smem, doubl
   if (threadIdx.x < N) {
     const int k = threadIdx.x;
     double a = smem[k];
-    for (int w = 1; w < kBlock / 32; ++w) {
+    for (int w = 1; w < BS / 32; ++w) {
       const double o = smem[w * N + k];
       a = ((MAXMASK >> k) & 1u) ? amax(a, o) : a + o;
     }
@@ -106,9 +106,7 @@ __device__ __forceinline__ void block_reduce(double (&v)[N], double* smem, doubl
 }
 
 // ---------------------------------------------------------------------------
-// Group-of-G-lanes row dot product: lane l accumulates elements l, l+G, ...
-// sequentially (U independent loads in flight), then an xor-butterfly. The
-// order is fixed, so results are bit-reproducible run to run.
+// Gathers of the dense operand of an SpMV.
 // ---------------------------------------------------------------------------
 struct GatherPlain {
   const double* v;
@@ -120,6 +118,11 @@ struct GatherDiv {  // v_j = u_j / nu (power iteration: v = u / norm, pdhg.cpp:6
   __device__ __forceinline__ double operator()(int j) const { return __ldg(v + j) / *nu; }
 };
 
+// Group-of-G-lanes row dot product: lane l of the group accumulates the row's
+// elements l, l+G, l+2G, ... in order (U independent idx/val loads and U
+// gathers in flight), then a fixed xor butterfly. Deterministic run to run.
+// With G = 1 a lane sums its row sequentially in ascending position — the
+// reference's (Eigen's) own order, so the result is bit-identical to it.
 template <int G, int U, class Gather>
 __device__ __forceinline__ double group_dot(int beg, int end, int lane, const int* __restrict__ idx,
                                             const double* __restrict__ val, const Gather& g) {
@@ -141,44 +144,61 @@ __device__ __forceinline__ double group_dot(int beg, int end, int lane, const in
     for (int k = 0; k < U; ++k)
       if (ii[k] >= 0) acc = acc + vv[k] * xx[k];
   }
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   return acc;
 }
 
-template <int G>
-__device__ __forceinline__ double group_allreduce(double s) {
-#pragma unroll
-  for (int off = G / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
-  return s;
-}
+// Barrier-free warp tiles shared by every "row" kernel. The block owns rows
+// [rb, re); its warps take 32-row tiles round-robin. Per tile: lane l first
+// issues pre(row) — the epilogue's operand loads for row tile+l — so their
+// latency overlaps the SpMV; then G passes in which each G-lane group
+// reduces one row (32/G rows per pass); the 32 sums go to a warp-private
+// shared slot and all 32 lanes run epi(row, sum, operands) on the tile's rows
+// (coalesced). Only __syncwarp, no block barrier.
+struct NoPre {
+  __device__ __forceinline__ int operator()(int) const { return 0; }
+};
 
-// Tile loop shared by every "row" kernel: the block owns rows [rb, re) and
-// walks them in tiles of kBlock rows. Phase 1 (SpMV): groups of G lanes
-// reduce one row each, G passes per tile, into smem. Phase 2 (epilogue): one
-// thread per row, coalesced, calls epi(row, sum).
-template <int G, int U, class Gather, class Epi>
-__device__ __forceinline__ void tile_loop(int rb, int re, const int* __restrict__ ptr,
-                                          const int* __restrict__ idx,
-                                          const double* __restrict__ val, const Gather& g,
-                                          double* sums, Epi&& epi) {
-  constexpr int GPB = kBlock / G;
-  const int gid = threadIdx.x / G, lane = threadIdx.x % G;
-  for (int tile = rb; tile < re; tile += kBlock) {
-    const int nrows = min(kBlock, re - tile);
+template <int G, class Gather, class Pre, class Epi>
+__device__ __forceinline__ void warp_tiles(int rb, int re, const int* __restrict__ ptr,
+                                           const int* __restrict__ idx,
+                                           const double* __restrict__ val, const Gather& g,
+                                           double* wsum, const Pre& pre, Epi&& epi) {
+  constexpr int GPW = 32 / G;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int gid = lane / G, gl = lane % G;
+  for (int tile = rb + warp * 32; tile < re; tile += nw * 32) {
+    const int nrows = min(32, re - tile);
+    const int pl = lane <= nrows ? __ldg(ptr + tile + lane) : 0;
+    const int pend = __ldg(ptr + tile + nrows);
+    const auto ops = pre(lane < nrows ? tile + lane : tile);
 #pragma unroll 1
     for (int k = 0; k < G; ++k) {
-      const int local = k * GPB + gid;
-      double s = 0.0;
-      if (local < nrows) {
-        const int row = tile + local;
-        s = group_dot<G, U>(__ldg(ptr + row), __ldg(ptr + row + 1), lane, idx, val, g);
-      }
-      s = group_allreduce<G>(s);
-      if (lane == 0 && local < nrows) sums[local] = s;
+      const int local = k * GPW + gid;
+      const int b = __shfl_sync(0xffffffffu, pl, local & 31);
+      const int e1 = __shfl_sync(0xffffffffu, pl, (local + 1) & 31);
+      const int e = local + 1 < 32 ? e1 : pend;
+      const bool ok = local < nrows;
+      const double s = group_dot<G, 4>(ok ? b : 0, ok ? e : 0, gl, idx, val, g);
+      if (gl == 0 && ok) wsum[local] = s;
     }
-    __syncthreads();
-    if (threadIdx.x < nrows) epi(tile + threadIdx.x, sums[threadIdx.x]);
-    __syncthreads();
+    __syncwarp();
+    if (lane < nrows) epi(tile + lane, wsum[lane], ops);
+    __syncwarp();
   }
+}
+
+// Exact reciprocal of a Ruiz factor (a power of two, scaling.hpp:22-26):
+// x / s == x * (1/s) bit for bit, without a double division. Falls back to
+// the division if s is not a normal power of two.
+__device__ __forceinline__ double pow2_recip(double s) {
+  const long long bits = __double_as_longlong(s);
+  const double r = __longlong_as_double(0x7FE0000000000000LL - bits);
+  return (bits & 0x000FFFFFFFFFFFFFLL) == 0 && bits > 0x0010000000000000LL &&
+                 bits < 0x7FE0000000000000LL
+             ? r
+             : 1.0 / s;
 }
 
 // ---------------------------------------------------------------------------
@@ -187,8 +207,9 @@ __device__ __forceinline__ void tile_loop(int rb, int re, const int* __restrict_
 // (pdhg.cpp:271-283: x*s, y*r, ax/r, aty/s).
 // ---------------------------------------------------------------------------
 // acc: [0] rp2 (sum), [1] rp_inf (max), [2] b.y (sum)
-__device__ __forceinline__ void row_report(double axs, double ys, double r, double b, double* acc) {
-  const double ax = axs / r;
+__device__ __forceinline__ void row_report(double axs, double ys, double r, double rinv, double b,
+                                           double* acc) {
+  const double ax = axs * rinv;  // == axs / r exactly (r is a power of two)
   const double y = ys * r;
   double v = 0.0;
   if (ax < b) {
@@ -220,10 +241,10 @@ __device__ __forceinline__ double clip_z(double c, double aty, double x, double 
 
 // acc: [0] rd2 (sum), [1] rd_inf (max), [2] bound violation inf (max),
 //      [3] complementarity (max), [4] dual bound terms (sum), [5] c.x (sum)
-__device__ __forceinline__ void col_report(double xs, double atys, double s, double c, double l,
-                                           double u, double* acc) {
+__device__ __forceinline__ void col_report(double xs, double atys, double s, double sinv, double c,
+                                           double l, double u, double* acc) {
   const double x = xs * s;
-  const double aty = atys / s;
+  const double aty = atys * sinv;  // == atys / s exactly (s is a power of two)
   const double z = clip_z(c, aty, x, l, u);
   double rd = aty + z;
   rd = rd - c;

@@ -68,12 +68,12 @@ __global__ void k_partition(const int* __restrict__ ptr, int rows, int grid, lon
 template <int G, class Gather>
 __global__ void __launch_bounds__(kBlock) k_spmv(const int* __restrict__ ptr, const int* __restrict__ idx,
                                                  const double* __restrict__ val, Gather g,
-                                                 const int* __restrict__ start, double* __restrict__ out,
-                                                 const int* stop_flag) {
+                                                 const int* __restrict__ start,
+                                                 double* __restrict__ out, const int* stop_flag) {
   if (stop_flag != nullptr && *stop_flag) return;
-  __shared__ double sums[kBlock];
-  const int rb = start[blockIdx.x], re = start[blockIdx.x + 1];
-  tile_loop<G, 4>(rb, re, ptr, idx, val, g, sums, [&](int i, double s) { out[i] = 0.0 + s; });
+  __shared__ double wsum[kBlock];
+  warp_tiles<G>(start[blockIdx.x], start[blockIdx.x + 1], ptr, idx, val, g, wsum + (threadIdx.x & ~31),
+                NoPre{}, [&](int i, double s, int) { out[i] = 0.0 + s; });
 }
 
 // ---- power iteration (estimate_matrix_norm, pdhg.cpp:46-65) ---------------
@@ -95,17 +95,17 @@ __global__ void __launch_bounds__(kBlock) k_power_cols(const int* __restrict__ p
                                                        double* __restrict__ u, double* part,
                                                        unsigned* counter, PowerCtrl* pc) {
   if (pc->zero) return;
-  __shared__ double sums[kBlock];
+  __shared__ double wsum[kBlock];
   __shared__ double red[(kBlock / 32) * 2];
   __shared__ double out[2];
   __shared__ bool last;
   double acc[2] = {0.0, 0.0};
   const double nu = pc->nu;
-  const int rb = start[blockIdx.x], re = start[blockIdx.x + 1];
-  tile_loop<G, 4>(rb, re, ptr, idx, val, GatherPlain{w}, sums, [&](int j, double s) {
+  warp_tiles<G>(start[blockIdx.x], start[blockIdx.x + 1], ptr, idx, val, GatherPlain{w},
+                wsum + (threadIdx.x & ~31), [&](int j) { return u_prev[j]; }, [&](int j, double s, double up) {
     const double uj = 0.0 + s;
     u[j] = uj;
-    const double vj = u_prev[j] / nu;
+    const double vj = up / nu;
     acc[0] += uj * uj;
     acc[1] += vj * uj;
   });

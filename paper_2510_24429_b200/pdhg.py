@@ -30,7 +30,7 @@ import numpy as np
 from .lp import LinearProgram
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcclp_cuda.so")
+LIB_PATH = os.environ.get("CCLP_CU_LIB", os.path.join(HERE, "libcclp_cuda.so"))
 
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
@@ -48,7 +48,8 @@ class _Config(C.Structure):
                 ("norm_iterations", C.c_int32), ("scaling_iterations", C.c_int32),
                 ("max_iterations", C.c_int64), ("check_interval", C.c_int32),
                 ("seed", C.c_uint64), ("log_interval", C.c_int64),
-                ("deterministic", C.c_int32), ("poll_interval", C.c_int32)]
+                ("deterministic", C.c_int32), ("poll_interval", C.c_int32),
+                ("exact_spmv", C.c_int32)]
 
 
 class _Tol(C.Structure):
@@ -150,7 +151,8 @@ def to_string(reason: PdhgStopReason) -> str:
 
 @dataclasses.dataclass
 class PdhgConfig:
-    """pdhg.hpp:29-42 (+ poll_interval: iterations per device batch)."""
+    """pdhg.hpp:29-42 (+ engine knobs: poll_interval = iterations per device
+    batch; exact_spmv = reference-order SpMV sums, bit-identical products)."""
     step_scale: float = 0.9
     primal_weight: float = 0.0
     restart_factor: float = 0.5
@@ -164,12 +166,14 @@ class PdhgConfig:
     log: Optional[Callable[[str], None]] = None
     deterministic: bool = True
     poll_interval: int = 0
+    exact_spmv: bool = False
 
     def _c(self) -> _Config:
         return _Config(self.step_scale, self.primal_weight, self.restart_factor, self.time_limit,
                        self.norm_iterations, self.scaling_iterations, self.max_iterations,
                        self.check_interval, self.seed, self.log_interval,
-                       1 if self.deterministic else 0, self.poll_interval)
+                       1 if self.deterministic else 0, self.poll_interval,
+                       1 if self.exact_spmv else 0)
 
 
 @dataclasses.dataclass
@@ -392,9 +396,10 @@ class Engine:
         return int(self.L.cclp_cu_stream(self.ctx) or 0)
 
     def describe(self) -> dict:
-        out = (C.c_int64 * 8)()
-        self.L.cclp_cu_describe(self.ctx, out, 8)
-        keys = ["m", "n", "nnz", "group_rows", "group_cols", "row_grid", "col_grid", "launches"]
+        keys = ["m", "n", "nnz", "group_rows", "group_cols", "row_grid", "col_grid", "launches",
+                "last_cols_body_ns", "last_finalize_ns"]
+        out = (C.c_int64 * len(keys))()
+        self.L.cclp_cu_describe(self.ctx, out, len(keys))
         return dict(zip(keys, list(out)))
 
 
