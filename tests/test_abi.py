@@ -1,0 +1,105 @@
+"""CPU: the C-ABI library builds, loads without a GPU and exports every symbol
+include/cclp_cu.h declares; host-only entry points behave."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "cclp_cu.h")
+LIB = os.path.join(ROOT, "paper_2510_24429_b200", "libcclp_cuda.so")
+
+
+def declared_symbols():
+    src = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(cclp_cu_[a-z_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    if not os.path.exists(LIB):
+        from paper_2510_24429_b200 import build
+        build.build()
+    return C.CDLL(LIB)
+
+
+def test_header_declares_the_run_pdhg_boundary():
+    syms = declared_symbols()
+    for s in ("cclp_cu_run_pdhg", "cclp_cu_create", "cclp_cu_solve", "cclp_cu_destroy",
+              "cclp_cu_matvec", "cclp_cu_matvec_transpose", "cclp_cu_ruiz",
+              "cclp_cu_estimate_norm"):
+        assert s in syms
+
+
+def test_every_declared_symbol_is_exported(lib):
+    missing = [s for s in declared_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_python_mirror_lists_every_symbol():
+    from paper_2510_24429_b200.pdhg import EXPORTED_SYMBOLS
+    assert sorted(EXPORTED_SYMBOLS) == declared_symbols()
+
+
+def test_stop_strings(lib):
+    # to_string(PdhgStopReason), pdhg.cpp:28-44
+    lib.cclp_cu_stop_string.restype = C.c_char_p
+    got = [lib.cclp_cu_stop_string(i).decode() for i in range(7)]
+    assert got == ["converged", "iteration-limit", "time-limit", "cancelled",
+                   "won-by-crossover", "numerical-error", "unknown"]
+
+
+def test_default_config_matches_reference(lib):
+    from paper_2510_24429_b200.pdhg import PdhgConfig, Tolerances, _Config, _Tol
+    c = _Config()
+    lib.cclp_cu_default_config(C.byref(c))
+    d = PdhgConfig()
+    # pdhg.hpp:29-42
+    assert (c.step_scale, c.primal_weight, c.restart_factor, c.norm_iterations,
+            c.scaling_iterations, c.max_iterations, c.check_interval, c.seed) == \
+        (d.step_scale, d.primal_weight, d.restart_factor, d.norm_iterations,
+         d.scaling_iterations, d.max_iterations, d.check_interval, d.seed) == \
+        (0.9, 0.0, 0.5, 100, 10, 2000000, 1, 0)
+    t = _Tol()
+    lib.cclp_cu_default_tolerances(C.byref(t))
+    assert (t.eps_rel, t.eps_abs, t.eps_cross, t.decrement) == (1e-6, 1e-6, 1e-2, 0.1)
+    assert Tolerances() == Tolerances(t.eps_rel, t.eps_abs, t.eps_cross, t.decrement)
+
+
+def test_struct_layouts_match_header():
+    """ctypes mirrors must match the C structs field for field."""
+    from paper_2510_24429_b200 import pdhg
+    src = open(HEADER).read()
+    for cname, py in (("cclp_cu_config", pdhg._Config), ("cclp_cu_result", pdhg._Result),
+                      ("cclp_cu_snapshot", pdhg._Snapshot), ("cclp_cu_lp", pdhg._LP)):
+        body = re.search(r"typedef struct \{([^{}]*)\}\s*" + cname + ";", src).group(1)
+        body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+        fields = []
+        for decl in body.split(";"):
+            decl = decl.strip()
+            if not decl:
+                continue
+            names = decl.split(None, 1)[1] if not decl.startswith("const") else \
+                decl.split(None, 2)[2]
+            for nm in names.split(","):
+                fields.append(nm.strip().lstrip("*").strip())
+        assert [f[0] for f in py._fields_] == fields, cname
+
+
+def test_create_without_gpu_fails_cleanly(lib):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    from paper_2510_24429_b200 import lpgen
+    from paper_2510_24429_b200.pdhg import Engine
+    with pytest.raises(RuntimeError):
+        Engine(lpgen.two_var_lp())
+
+
+def test_no_cpu_fallback_in_product():
+    """The product path never imports the oracle."""
+    for f in os.listdir(os.path.join(ROOT, "paper_2510_24429_b200")):
+        if f.endswith(".py"):
+            src = open(os.path.join(ROOT, "paper_2510_24429_b200", f)).read()
+            assert "oracle" not in src.replace("# ", ""), f
