@@ -142,9 +142,132 @@ def transportation_lp(sources: int = 200, sinks: int = 500, seed: int = 1) -> Li
     return to_standard_form(gen)
 
 
+def multicommodity_lp(nodes: int = 10_000, arcs_per_node: int = 10, commodities: int = 20,
+                      side_rows: int = 100_000, side_per_var: int = 7, seed: int = 3):
+    """C3: multicommodity flow on a ring-local random digraph.
+
+    Flow variables x[k, e] >= 0 (commodity-major), conservation rows
+    (k, v): out - in = d[k, v] (equality), capacity rows sum_k x[k, e] <= cap_e
+    and `side_rows` budget rows sum w x <= B over random (k, e) sets, each flow
+    variable in `side_per_var` of them (~10 nnz per flow variable). Arcs join
+    v to v + offset with small offsets (plus 5% long-range arcs), so the
+    matrix has the locality of a real network. Feasible and bounded by
+    construction: demands, capacities and budgets are set from a random
+    positive flow x0 with margins; costs are U(1, 10) > 0. Returned in
+    standard form (one slack per inequality row)."""
+    rng = np.random.default_rng(seed)
+    V, K = nodes, commodities
+    E = V * arcs_per_node
+    tail = np.repeat(np.arange(V), arcs_per_node)
+    off = rng.integers(1, 33, size=E) * np.where(rng.random(E) < 0.5, -1, 1)
+    far = rng.random(E) < 0.05
+    off[far] = rng.integers(1, V, size=int(far.sum()))
+    head = (tail + off) % V
+    head = np.where(head == tail, (head + 1) % V, head)
+    nf = K * E
+    # conservation: column (k, e) has +1 at row k*V + tail, -1 at row k*V + head
+    kk = np.repeat(np.arange(K), E)
+    ee = np.tile(np.arange(E), K)
+    r_tail = kk * V + tail[ee]
+    r_head = kk * V + head[ee]
+    # capacity rows K*V + e
+    r_cap = K * V + ee
+    # side rows: K*V + E + s
+    S = side_rows
+    r_side = K * V + E + rng.integers(0, S, size=(nf, side_per_var))
+    w_side = rng.uniform(0.5, 2.0, size=(nf, side_per_var))
+    rows = np.concatenate([r_tail[:, None], r_head[:, None], r_cap[:, None], r_side], axis=1)
+    vals = np.concatenate([np.ones((nf, 1)), -np.ones((nf, 1)), np.ones((nf, 1)), w_side], axis=1)
+    order = np.argsort(rows, axis=1, kind="stable")
+    rows = np.take_along_axis(rows, order, axis=1)
+    vals = np.take_along_axis(vals, order, axis=1)
+    # merge duplicate side rows within a column (sum, as make_sparse would)
+    dup = np.zeros_like(rows, dtype=bool)
+    dup[:, 1:] = rows[:, 1:] == rows[:, :-1]
+    if dup.any():
+        for j in np.nonzero(dup.any(axis=1))[0]:
+            r, v = rows[j], vals[j]
+            ur, inv = np.unique(r, return_inverse=True)
+            sv = np.zeros(ur.size)
+            np.add.at(sv, inv, v)
+            pad = rows.shape[1] - ur.size
+            rows[j] = np.concatenate([ur, np.full(pad, -1)])
+            vals[j] = np.concatenate([sv, np.zeros(pad)])
+    m = K * V + E + S
+    keep = rows >= 0
+    counts = keep.sum(axis=1)
+    colptr = np.zeros(nf + 1, dtype=np.int64)
+    colptr[1:] = np.cumsum(counts)
+    rowind = rows[keep].astype(np.int32)
+    val = vals[keep]
+    import scipy.sparse as sp
+    A = sp.csc_matrix((val, rowind, colptr), shape=(m, nf))
+    x0 = rng.uniform(0.1, 1.0, size=nf)
+    act = A @ x0
+    rl = np.empty(m)
+    ru = np.empty(m)
+    ncons = K * V
+    rl[:ncons] = act[:ncons]
+    ru[:ncons] = act[:ncons]
+    rl[ncons:] = -INF
+    ru[ncons:] = act[ncons:] * rng.uniform(1.05, 1.5, size=m - ncons)
+    c = rng.uniform(1.0, 10.0, size=nf)
+    gen = LinearProgram(m, nf, colptr.astype(np.int32), rowind, val, c, rl, ru, np.zeros(nf),
+                        np.full(nf, INF), name=f"mcf_{V}x{K}")
+    return to_standard_form(gen)
+
+
+def staircase_lp(stages: int = 1000, cols_per_stage: int = 10_000, rows_per_stage: int = 5_000,
+                 own_per_col: int = 6, next_per_col: int = 4, seed: int = 4):
+    """C4: staircase / block-angular LP. Stage t has `cols_per_stage` columns
+    and `rows_per_stage` rows; a column of stage t has `own_per_col` entries in
+    stage t's rows and `next_per_col` in stage t+1's rows (the last stage links
+    to none), values U(-2, 2). Known optimum as in C2 (test_util.hpp:71-112):
+    each row's band-diagonal support column carries a U(2,3) entry."""
+    rng = np.random.default_rng(seed)
+    T, nc, nr = stages, cols_per_stage, rows_per_stage
+    n, m = T * nc, T * nr
+    stage = np.repeat(np.arange(T), nc)
+    k1, k2 = own_per_col, next_per_col
+    own = _distinct_rows(rng, nr, n, k1) + (stage * nr)[:, None]
+    nxt = _distinct_rows(rng, nr, n, k2) + ((stage + 1) * nr)[:, None]
+    last = stage == T - 1
+    rows = np.concatenate([own, nxt], axis=1)
+    vals = _nonzero_uniform(rng, rows.shape)
+    # support: in each stage the first nr columns (after a seeded shuffle) own
+    # row (stage*nr + i) as a band diagonal
+    perm_in_stage = np.argsort(rng.random((T, nc)), axis=1)
+    support_local = perm_in_stage[:, :nr]  # (T, nr)
+    support = (support_local + (np.arange(T) * nc)[:, None]).reshape(-1)
+    diag_rows = np.arange(m)
+    r_sc = rows[support, :k1]
+    has = np.any(r_sc == diag_rows[:, None], axis=1)
+    r_sc[~has, 0] = diag_rows[~has]
+    rows[support, :k1] = r_sc
+    is_diag = np.zeros(rows.shape, dtype=bool)
+    is_diag[support, :k1] = rows[support, :k1] == diag_rows[:, None]
+    vals = np.where(is_diag, np.where(rng.random(rows.shape) < 0.5, -1.0, 1.0) *
+                    rng.uniform(2.0, 3.0, size=rows.shape), vals)
+    keep = np.ones(rows.shape, dtype=bool)
+    keep[last, k1:] = False
+    order = np.argsort(np.where(keep, rows, np.iinfo(np.int64).max), axis=1, kind="stable")
+    rows = np.take_along_axis(rows, order, axis=1)
+    vals = np.take_along_axis(vals, order, axis=1)
+    keep = np.take_along_axis(keep, order, axis=1)
+    counts = keep.sum(axis=1)
+    colptr = np.zeros(n + 1, dtype=np.int64)
+    colptr[1:] = np.cumsum(counts)
+    return _known_optimum(colptr, rows[keep], vals[keep], m, n, support, rng,
+                          f"staircase_{T}x{nc}")
+
+
 CONFIGS = {
     "C1": dict(kind="transportation", sources=200, sinks=500, seed=1),
     "C2": dict(kind="random", m=100_000, n=500_000, nnz_per_col=10, seed=2),
+    "C3": dict(kind="mcf", nodes=10_000, arcs_per_node=10, commodities=20, side_rows=100_000,
+               side_per_var=7, seed=3),
+    "C4": dict(kind="staircase", stages=1000, cols_per_stage=10_000, rows_per_stage=5_000,
+               own_per_col=6, next_per_col=4, seed=4),
 }
 
 
@@ -155,4 +278,8 @@ def make_config(name: str) -> LinearProgram:
         return transportation_lp(**spec)
     if kind == "random":
         return random_equality_lp(**spec)[0]
+    if kind == "mcf":
+        return multicommodity_lp(**spec)
+    if kind == "staircase":
+        return staircase_lp(**spec)[0]
     raise KeyError(name)

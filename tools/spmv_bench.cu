@@ -135,6 +135,310 @@ __global__ void v_warpstream(int m, const int* __restrict__ ptr, const int* __re
   }
 }
 
+
+// V3: TMA bulk-copy streamed CSR. Each block owns rows [rb, re) (nnz range
+// [pb, pe)); its idx/val stream is cut into 16B-aligned chunks of CH elements
+// that thread 0 copies into an S-stage shared ring with cp.async.bulk,
+// completing on per-stage mbarriers. Consumers: gather + product in place,
+// then each row's owner sums its products sequentially (reference order).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra.uni WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int CH, int S, int BS>
+__global__ void __launch_bounds__(BS) v_tma(int m, const int* __restrict__ ptr, const int* __restrict__ idx,
+                                            const double* __restrict__ val, const double* __restrict__ x,
+                                            double* __restrict__ y, const int* __restrict__ start) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  double* sval = reinterpret_cast<double*>(dsm);                 // [S][CH]
+  int* sidx = reinterpret_cast<int*>(dsm + sizeof(double) * S * CH);  // [S][CH]
+  __shared__ unsigned long long full[S];
+  __shared__ double carry[2];
+  const int tid = threadIdx.x;
+  const int rb = start[blockIdx.x], re = start[blockIdx.x + 1];
+  if (rb >= re) return;
+  const int pb = ptr[rb], pe = ptr[re];
+  const int base = pb & ~3;
+  const int nchunks = pe > base ? (pe - base + CH - 1) / CH : 0;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    carry[0] = carry[1] = 0.0;
+  }
+  __syncthreads();
+  auto issue = [&](int c) {
+    const int s = c % S;
+    const int e0 = base + c * CH;
+    int len = min(CH, pe - e0);
+    len = (len + 3) & ~3;
+    mbar_expect_tx(&full[s], len * 12);
+    bulk_g2s(sidx + s * CH, idx + e0, len * 4, &full[s]);
+    bulk_g2s(sval + s * CH, val + e0, len * 8, &full[s]);
+  };
+  if (tid == 0)
+    for (int c = 0; c < S && c < nchunks; ++c) issue(c);
+  // row ownership: rows are processed in windows of BS rows; thread t owns
+  // row win + t. A row may span several chunks; its running sum lives in acc.
+  int win = rb;  // first row of the current window
+  double acc = 0.0;
+  int myrow = win + tid;
+  int mb = myrow < re ? ptr[myrow] : pe, me = myrow < re ? ptr[myrow + 1] : pe;
+  for (int c = 0; c < nchunks; ++c) {
+    const int s = c % S;
+    const int e0 = base + c * CH;
+    const int e1 = min(e0 + CH, pe);
+    mbar_wait(&full[s], (c / S) & 1);
+    double* pv = sval + s * CH;
+    const int* pi = sidx + s * CH;
+    // products in place (gathers in flight: CH/BS per thread)
+#pragma unroll 4
+    for (int q = tid; q < CH; q += BS) {
+      const int e = e0 + q;
+      if (e >= pb && e < e1) pv[q] = pv[q] * __ldg(x + pi[q]);
+    }
+    __syncthreads();
+    // row sums for rows intersecting [e0, e1), windows of BS rows
+    while (true) {
+      const int a = max(mb, e0), b = min(me, e1);
+      for (int q = a; q < b; ++q) acc = acc + pv[q - e0];
+      // does every row of this window end inside the chunk?
+      const bool done_mine = myrow >= re || me <= e1;
+      if (myrow < re && me <= e1 && me > e0 - 1) {
+        // row complete (possibly empty rows too)
+      }
+      const int last_row_of_window = min(win + BS, re) - 1;
+      const int last_end = ptr[last_row_of_window + 1];
+      if (last_end <= e1) {
+        // whole window completes in this chunk: emit and advance window
+        if (myrow < re) y[myrow] = acc;
+        win += BS;
+        if (win >= re) break;
+        myrow = win + tid;
+        acc = 0.0;
+        mb = myrow < re ? ptr[myrow] : pe;
+        me = myrow < re ? ptr[myrow + 1] : pe;
+        continue;  // the new window may have rows inside this chunk
+      }
+      (void)done_mine;
+      break;
+    }
+    __syncthreads();
+    if (tid == 0 && c + S < nchunks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(c + S);
+    }
+  }
+}
+
+// V4: panel-staged x window. Rows are cut into panels whose column span fits
+// in shared memory (greedy, host-side); a block stages x[wlo, whi) of each of
+// its panels in smem (coalesced loads) and runs the G-lane vector SpMV with
+// gathers from smem. Panels whose span is too large gather from global.
+template <int G, int U, int BS>
+__global__ void __launch_bounds__(BS) v_window(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                               const double* __restrict__ val, const double* __restrict__ x,
+                                               double* __restrict__ y, const int* __restrict__ prow,
+                                               const int* __restrict__ pwlo, const int* __restrict__ pwhi,
+                                               const int* __restrict__ bpan) {
+  extern __shared__ double xs[];
+  const int lane = threadIdx.x % G, gid = threadIdx.x / G;
+  constexpr int GPB = BS / G;
+  for (int pnl = bpan[blockIdx.x]; pnl < bpan[blockIdx.x + 1]; ++pnl) {
+    const int r0 = prow[pnl], r1 = prow[pnl + 1];
+    const int wlo = pwlo[pnl], whi = pwhi[pnl];
+    const bool staged = whi >= wlo;
+    if (staged) {
+      for (int j = threadIdx.x; j < whi - wlo; j += BS) xs[j] = __ldg(x + wlo + j);
+      __syncthreads();
+    }
+    for (int row = r0 + gid; row - gid < r1; row += GPB) {
+      double acc = 0.0;
+      if (row < r1) {
+        const int b = ptr[row], e = ptr[row + 1];
+        for (int p = b + lane; p < e; p += G * U) {
+          int ii[U];
+          double vv[U];
+#pragma unroll
+          for (int k = 0; k < U; ++k) {
+            const int q = p + k * G;
+            ii[k] = q < e ? __ldcs(idx + q) : -1;
+            vv[k] = q < e ? __ldcs(val + q) : 0.0;
+          }
+#pragma unroll
+          for (int k = 0; k < U; ++k)
+            if (ii[k] >= 0) acc = acc + vv[k] * (staged ? xs[ii[k] - wlo] : __ldg(x + ii[k]));
+        }
+      }
+#pragma unroll
+      for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+      if (lane == 0 && row < r1) y[row] = acc;
+    }
+    if (staged) __syncthreads();
+  }
+}
+
+// Streaming ceilings: (a) vector-CSR traversal without the gather; (b) flat
+// grid-stride stream of idx/val with 16B vector loads.
+template <int G, int U, bool GATHER, int MODE>
+__global__ void v_nogather(int m, const int* __restrict__ ptr, const int* __restrict__ idx,
+                           const double* __restrict__ val, const double* __restrict__ x,
+                           double* __restrict__ y) {
+  const int lane = threadIdx.x % G;
+  const int gpb = blockDim.x / G;
+  for (int row = blockIdx.x * gpb + threadIdx.x / G; row - (threadIdx.x / G) < m;
+       row += gridDim.x * gpb) {
+    double acc = 0.0;
+    if (row < m) {
+      const int b = ptr[row], e = ptr[row + 1];
+      for (int p = b + lane; p < e; p += G * U) {
+        int ii[U];
+        double vv[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int q = p + k * G;
+          if (MODE == 0) {
+            ii[k] = q < e ? __ldcs(idx + q) : -1;
+            vv[k] = q < e ? __ldcs(val + q) : 0.0;
+          } else if (MODE == 1) {
+            ii[k] = q < e ? __ldg(idx + q) : -1;
+            vv[k] = q < e ? __ldg(val + q) : 0.0;
+          } else {
+            ii[k] = q < e ? idx[q] : -1;
+            vv[k] = q < e ? val[q] : 0.0;
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+          if (ii[k] >= 0) acc = acc + vv[k] * (GATHER ? __ldg(x + ii[k]) : (double)ii[k]);
+      }
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0 && row < m) y[row] = acc;
+  }
+}
+
+__global__ void v_flat(long long nnz, const int* __restrict__ idx, const double* __restrict__ val,
+                       double* __restrict__ y, int m) {
+  double acc = 0.0;
+  const long long n4 = nnz / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int4 a = __ldcs(reinterpret_cast<const int4*>(idx) + i);
+    const double2 v0 = __ldcs(reinterpret_cast<const double2*>(val) + 2 * i);
+    const double2 v1 = __ldcs(reinterpret_cast<const double2*>(val) + 2 * i + 1);
+    acc += v0.x * a.x + v0.y * a.y + v1.x * a.z + v1.y * a.w;
+  }
+  const long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (t < m) y[t] = acc;
+}
+
+// V5: pipelined warp-stream. Each warp owns contiguous 32-row tiles; the
+// nonzeros of its tiles form one stream cut into chunks of 32*K. While chunk
+// c's gathers are in flight, chunk c+1's idx/val loads (possibly of the next
+// tile) are already issued, so a chunk costs ~1 memory round trip. Products go
+// to a per-warp smem buffer; each row's owner lane sums them in order
+// (reference order: bit-exact).
+template <int K>
+__global__ void __launch_bounds__(256) v_wspipe(int m, const int* __restrict__ ptr, const int* __restrict__ idx,
+                                                const double* __restrict__ val, const double* __restrict__ x,
+                                                double* __restrict__ y) {
+  __shared__ double prod_all[8][32 * K];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* prod = prod_all[warp];
+  const int gw = blockIdx.x * 8 + warp, nw = gridDim.x * 8;
+  const int ntiles = (m + 31) / 32;
+  int tile = gw;
+  if (tile >= ntiles) return;
+  // current tile bounds
+  int r0 = tile * 32, nr = min(32, m - r0);
+  int my_b = lane < nr ? __ldg(ptr + r0 + lane) : 0;
+  int my_e = lane < nr ? __ldg(ptr + r0 + lane + 1) : 0;
+  int pb = __shfl_sync(~0u, my_b, 0), pe = __shfl_sync(~0u, my_e, nr - 1);
+  // next tile bounds (prefetched)
+  int ntile = tile + nw;
+  int nr0 = ntile * 32, nnr = ntile < ntiles ? min(32, m - nr0) : 0;
+  int n_my_b = lane < nnr ? __ldg(ptr + nr0 + lane) : 0;
+  int n_my_e = lane < nnr ? __ldg(ptr + nr0 + lane + 1) : 0;
+  int ii[K];
+  double vv[K];
+  int c0 = pb;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    const int q = c0 + lane + 32 * k;
+    ii[k] = q < pe ? __ldcs(idx + q) : 0;
+    vv[k] = q < pe ? __ldcs(val + q) : 0.0;
+  }
+  double acc = 0.0;
+  while (true) {
+    const int len = min(32 * K, pe - c0);
+    // where does the next chunk come from?
+    int nc0, npe;
+    bool same_tile = c0 + 32 * K < pe;
+    int npb = __shfl_sync(~0u, n_my_b, 0);
+    int npe_t = __shfl_sync(~0u, n_my_e, max(nnr - 1, 0));
+    if (same_tile) { nc0 = c0 + 32 * K; npe = pe; }
+    else { nc0 = npb; npe = nnr > 0 ? npe_t : npb; }
+    int ii2[K];
+    double vv2[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int q = nc0 + lane + 32 * k;
+      ii2[k] = q < npe ? __ldcs(idx + q) : 0;
+      vv2[k] = q < npe ? __ldcs(val + q) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int q = lane + 32 * k;
+      if (q < len) prod[q] = vv[k] * __ldg(x + ii[k]);
+    }
+    __syncwarp();
+    {
+      const int a = max(my_b, c0), e = min(my_e, c0 + len);
+      for (int q = a; q < e; ++q) acc = acc + prod[q - c0];
+    }
+    __syncwarp();
+    if (!same_tile) {
+      if (lane < nr) y[r0 + lane] = acc;
+      acc = 0.0;
+      if (nnr == 0) break;
+      tile = ntile; r0 = nr0; nr = nnr; my_b = n_my_b; my_e = n_my_e; pb = npb; pe = npe;
+      ntile = tile + nw; nr0 = ntile * 32; nnr = ntile < ntiles ? min(32, m - nr0) : 0;
+      n_my_b = lane < nnr ? __ldg(ptr + nr0 + lane) : 0;
+      n_my_e = lane < nnr ? __ldg(ptr + nr0 + lane + 1) : 0;
+    }
+    c0 = nc0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) { ii[k] = ii2[k]; vv[k] = vv2[k]; }
+  }
+}
+
 int main(int argc, char** argv) {
   char path[512];
   snprintf(path, sizeof path, "%s.meta", argv[1]);
@@ -145,6 +449,7 @@ int main(int argc, char** argv) {
   auto hp = readf<int>(path, m + 1);
   snprintf(path, sizeof path, "%s.idx", argv[1]);
   auto hi = readf<int>(path, nnz);
+  auto hi_idx = [&](long long p) { return hi[p]; };
   snprintf(path, sizeof path, "%s.val", argv[1]);
   auto hv = readf<double>(path, nnz);
   snprintf(path, sizeof path, "%s.x", argv[1]);
@@ -152,8 +457,8 @@ int main(int argc, char** argv) {
   int *dp, *di;
   double *dv, *dx, *dy;
   CK(cudaMalloc(&dp, sizeof(int) * (m + 1)));
-  CK(cudaMalloc(&di, sizeof(int) * nnz));
-  CK(cudaMalloc(&dv, sizeof(double) * nnz));
+  CK(cudaMalloc(&di, sizeof(int) * (nnz + 8)));
+  CK(cudaMalloc(&dv, sizeof(double) * (nnz + 8)));
   CK(cudaMalloc(&dx, sizeof(double) * ncols));
   CK(cudaMalloc(&dy, sizeof(double) * m));
   CK(cudaMemcpy(dp, hp.data(), sizeof(int) * (m + 1), cudaMemcpyHostToDevice));
@@ -206,8 +511,8 @@ int main(int argc, char** argv) {
   int sms;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   printf("m=%d ncols=%d nnz=%lld avg=%.1f bytes=%.1f MB\n", m, ncols, nnz, (double)nnz / m, bytes / 1e6);
-  for (int bs : {128, 256}) {
-    for (int mult : {4, 8, 16}) {
+  for (int bs : {128}) {
+    for (int mult : {8}) {
       const int grid = sms * mult * (256 / bs);
       char nm[64];
       snprintf(nm, sizeof nm, "scalar U4 bs%d g%d", bs, grid);
@@ -232,5 +537,108 @@ int main(int argc, char** argv) {
     run(nm, [&] { v_warpstream<K><<<grid, 256, 8 * 32 * K * 8>>>(m, dp, di, dv, dx, dy); }); \
   }
   WS(4) WS(8) WS(16)
+  // TMA variant needs a row partition: nnz-balanced contiguous ranges
+  auto tma_run = [&](auto kern, int CH, int S, int BS, int per_sm) {
+    const int grid = sms * per_sm;
+    std::vector<int> st(grid + 1);
+    const double total = (double)hp[m] + 8.0 * m;
+    for (int b = 0; b <= grid; ++b) {
+      const double target = total * b / grid;
+      int lo = 0, hi = m;
+      while (lo < hi) { int mid = (lo + hi) / 2; if (hp[mid] + 8.0 * mid >= target) hi = mid; else lo = mid + 1; }
+      st[b] = b == grid ? m : lo;
+    }
+    int* dst;
+    CK(cudaMalloc(&dst, sizeof(int) * (grid + 1)));
+    CK(cudaMemcpy(dst, st.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice));
+    const size_t smem = (size_t)S * CH * 12;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    char nm[64];
+    snprintf(nm, sizeof nm, "tma CH%d S%d BS%d x%d", CH, S, BS, per_sm);
+    run(nm, [&] { kern<<<grid, BS, smem>>>(m, dp, di, dv, dx, dy, dst); });
+    cudaFree(dst);
+  };
+  {
+    const int grid = sms * 32;
+    for (int mult : {4, 8}) {
+      char nm[64];
+      snprintf(nm, sizeof nm, "wspipe K4 x%d", mult);
+      run(nm, [&] { v_wspipe<4><<<sms * mult, 256>>>(m, dp, di, dv, dx, dy); });
+      snprintf(nm, sizeof nm, "wspipe K8 x%d", mult);
+      run(nm, [&] { v_wspipe<8><<<sms * mult, 256>>>(m, dp, di, dv, dx, dy); });
+      snprintf(nm, sizeof nm, "wspipe K2 x%d", mult);
+      run(nm, [&] { v_wspipe<2><<<sms * mult, 256>>>(m, dp, di, dv, dx, dy); });
+    }
+    run("flat int4+2xdouble2 stream", [&] { v_flat<<<sms * 16, 256>>>(nnz, di, dv, dy, m); });
+    run("nogather G4 U4 ldcs", [&] { v_nogather<4, 4, false, 0><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
+    run("nogather G8 U4 ldcs", [&] { v_nogather<8, 4, false, 0><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
+    run("nogather G8 U8 ldcs", [&] { v_nogather<8, 8, false, 0><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
+    run("nogather G32 U4 ldcs", [&] { v_nogather<32, 4, false, 0><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
+    run("gather G8 U4 ldg", [&] { v_nogather<8, 4, true, 1><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
+    run("gather G8 U4 plain", [&] { v_nogather<8, 4, true, 2><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
+    run("gather G8 U8 ldcs", [&] { v_nogather<8, 8, true, 0><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
+    run("gather G4 U8 ldcs", [&] { v_nogather<4, 8, true, 0><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
+  }
+  // window-staged panels
+  auto win_run = [&](auto kern, int G, int BS, int wcap, int panel_rows_max) {
+    std::vector<int> prow{0}, pwlo, pwhi;
+    int r = 0;
+    long long staged_nnz = 0;
+    while (r < m) {
+      int lo = 1 << 30, hi = -1, r1 = r;
+      while (r1 < m && r1 - r < panel_rows_max) {
+        int nlo = lo, nhi = hi;
+        for (int p = hp[r1]; p < hp[r1 + 1]; ++p) { nlo = std::min(nlo, hi_idx(p)); nhi = std::max(nhi, hi_idx(p)); }
+        if (r1 > r && nhi - nlo + 1 > wcap) break;
+        lo = nlo; hi = nhi; ++r1;
+      }
+      prow.push_back(r1);
+      if (hi - lo + 1 <= wcap && hi >= lo) { pwlo.push_back(lo); pwhi.push_back(hi + 1); staged_nnz += hp[r1] - hp[r]; }
+      else { pwlo.push_back(1); pwhi.push_back(0); }
+      r = r1;
+    }
+    const int np = (int)pwlo.size();
+    const int grid = sms;
+    std::vector<int> bp(grid + 1);
+    for (int b = 0; b <= grid; ++b) {  // balance panels by nnz
+      const long long target = (long long)hp[m] * b / grid;
+      int lo2 = 0, hi2 = np;
+      while (lo2 < hi2) { int mid = (lo2 + hi2) / 2; if (hp[prow[mid]] >= target) hi2 = mid; else lo2 = mid + 1; }
+      bp[b] = b == grid ? np : lo2;
+    }
+    int *d_prow, *d_wlo, *d_whi, *d_bp;
+    CK(cudaMalloc(&d_prow, sizeof(int) * (np + 1)));
+    CK(cudaMalloc(&d_wlo, sizeof(int) * np));
+    CK(cudaMalloc(&d_whi, sizeof(int) * np));
+    CK(cudaMalloc(&d_bp, sizeof(int) * (grid + 1)));
+    CK(cudaMemcpy(d_prow, prow.data(), sizeof(int) * (np + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_wlo, pwlo.data(), sizeof(int) * np, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_whi, pwhi.data(), sizeof(int) * np, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_bp, bp.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice));
+    const size_t smem = sizeof(double) * wcap;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    char nm[96];
+    snprintf(nm, sizeof nm, "window G%d BS%d cap%d pr%d np%d st%.0f%%", G, BS, wcap, panel_rows_max, np,
+             100.0 * staged_nnz / hp[m]);
+    run(nm, [&] { kern<<<grid, BS, smem>>>(dp, di, dv, dx, dy, d_prow, d_wlo, d_whi, d_bp); });
+    cudaFree(d_prow); cudaFree(d_wlo); cudaFree(d_whi); cudaFree(d_bp);
+  };
+  const int gsel = (double)nnz / m > 24 ? 8 : 4;
+  if (gsel == 8) {
+    win_run(v_window<8, 4, 1024>, 8, 1024, 24000, 1 << 20);
+    win_run(v_window<8, 4, 1024>, 8, 1024, 24000, 4096);
+    win_run(v_window<8, 4, 512>, 8, 512, 12000, 1 << 20);
+  } else {
+    win_run(v_window<4, 4, 1024>, 4, 1024, 24000, 1 << 20);
+    win_run(v_window<4, 4, 1024>, 4, 1024, 24000, 4096);
+    win_run(v_window<4, 4, 512>, 4, 512, 12000, 1 << 20);
+  }
+  tma_run(v_tma<1024, 3, 256>, 1024, 3, 256, 3);
+  tma_run(v_tma<1024, 4, 256>, 1024, 4, 256, 3);
+  tma_run(v_tma<2048, 3, 256>, 2048, 3, 256, 2);
+  tma_run(v_tma<2048, 2, 256>, 2048, 2, 256, 3);
+  tma_run(v_tma<1024, 3, 256>, 1024, 3, 256, 4);
+  tma_run(v_tma<1024, 4, 128>, 1024, 4, 128, 4);
+  tma_run(v_tma<4096, 2, 512>, 4096, 2, 512, 2);
   return 0;
 }
