@@ -275,17 +275,16 @@ def main():
     value = total_iters / (t_max * 1e-3)
 
     # per-kernel device time for the roofline (eager launches, events between)
-    rows_ms, cols_ms = eng.profile_kernels(100)
+    pk = eng.profile_kernels(100)
     ab = algorithmic_bytes(lp.m, lp.n, lp.nnz)
-    dom = "cols" if cols_ms >= rows_ms else "rows"
-    dom_ms = max(rows_ms, cols_ms)
+    dom = "rows" if pk["spmv_rows"] >= pk["spmv_cols"] else "cols"
+    dom_ms = pk["spmv_" + dom]
     achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peak_gbs()
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            tr = json.load(f).get(CONFIG_NAME, {})
-            traffic = tr.get("k_cols" if dom == "cols" else "k_rows")
+            traffic = json.load(f).get(CONFIG_NAME, {}).get("k_spmv_" + dom)
     except Exception:
         pass
     iter_us = dev_ms * 1e3 / (K * I)
@@ -339,13 +338,13 @@ def main():
                        "l2": "working set ~180 MB > 126 MB L2, no flush"},
             "us_per_iteration": iter_us,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": f"k_{dom}",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": f"k_spmv_{dom}",
                          "kernel_us": dom_ms * 1e3, "bytes_per_launch": ab[dom],
                          "peak_kind": peak_kind,
                          "iteration": {"bytes": ab["iteration"],
                                        "achieved": ab["iteration"] / (iter_us * 1e-6) / 1e9,
                                        "frac": ab["iteration"] / (iter_us * 1e-6) / 1e9 / peak},
-                         "rows_kernel_us": rows_ms * 1e3, "cols_kernel_us": cols_ms * 1e3},
+                         "kernels_us": {k: v * 1e3 for k, v in pk.items()}},
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "iters_per_step": args.e2e_iters,
                     "includes": "upload, CSR build, Ruiz, ||A|| power iteration, loop, download"},

@@ -169,9 +169,9 @@ int cclp_cu_begin(cclp_cu_ctx* ctx, const cclp_cu_config* cfg, const cclp_cu_tol
  * events on the engine stream; returns device milliseconds. */
 int cclp_cu_advance(cclp_cu_ctx* ctx, int64_t iters, double* device_ms);
 /* Per-kernel device time: runs `iters` iterations launching kernels eagerly
- * with events between them. out[0] = avg ms of the row kernel (A x + dual
- * update), out[1] = avg ms of the column kernel (A'y + primal update +
- * reports + finalize). */
+ * with events between them; out[0..3] = average ms of k_spmv_rows (A x),
+ * k_dual (dual update + row reports), k_spmv_cols (A'y) and k_primal (primal
+ * update + column reports + candidates + on-device decisions). */
 int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out);
 /* The engine's CUDA stream (cudaStream_t) for external event timing. */
 void* cclp_cu_stream(cclp_cu_ctx* ctx);

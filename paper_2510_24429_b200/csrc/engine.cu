@@ -67,6 +67,23 @@ int blocks_for(long long n, int per = kBlock, int cap = 148 * 8) {
   return static_cast<int>(std::max<long long>(1, std::min<long long>(b, cap)));
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel may begin
+// launching while its predecessor drains; it synchronizes with griddepcontrol.
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
+
 // Calls f(std::integral_constant<int, G>) for the runtime group size G.
 template <class F>
 void with_group(int G, F&& f) {
@@ -97,6 +114,7 @@ struct Context {
   bool equality = true;
   // partitions
   int Grow = 1, Gcol = 1, row_grid = 1, col_grid = 1;
+  int spmv_grid_r = 1, spmv_grid_c = 1, epi_grid = 1;
   int *row_start = nullptr, *col_start = nullptr;
   bool exact = false;  // G = 1: reference-order (bit-identical) SpMV sums
   // state
@@ -258,27 +276,33 @@ void Context::build_csr() {
 void Context::partition() {
   Grow = pick_group(nnz, m);
   Gcol = pick_group(nnz, n);
-  // Persistent-style grids: exactly the resident blocks of the whole GPU
-  // (148 SMs x occupancy), each owning a contiguous, nnz-balanced row range.
-  int sms = 148, occ_r = 1, occ_c = 1;
+  // Setup kernels use nnz-balanced row ranges of `row_grid` / `col_grid`
+  // blocks. The iteration's SpMV kernels run one full wave of resident
+  // blocks (grid-stride over rows); the epilogues one wave of kEpiBlock-thread
+  // blocks, so finalize reduces only that many partials.
+  int sms = 148, occ_r = 1, occ_c = 1, occ_d = 1, occ_p = 1;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   with_group(Grow, [&](auto g) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, k_rows<decltype(g)::value>, kRowsBlock, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, k_spmv_rows<decltype(g)::value>, kSpmvBlock, 0));
   });
   with_group(Gcol, [&](auto g) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_cols<decltype(g)::value>, kColsBlock, 0));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_spmv_cols<decltype(g)::value>, kSpmvBlock, 0));
   });
-  const long long cap_r = static_cast<long long>(sms) * std::max(occ_r, 1);
-  const long long cap_c = static_cast<long long>(sms) * std::max(occ_c, 1);
-  row_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap_r, (m + 31) / 32 + nnz / 1024)));
-  col_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap_c, (n + 31) / 32 + nnz / 1024)));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_dual, kEpiBlock, 0));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_primal, kEpiBlock, 0));
+  spmv_grid_r = sms * std::max(occ_r, 1);
+  spmv_grid_c = sms * std::max(occ_c, 1);
+  epi_grid = sms * std::max(1, std::min(occ_d, occ_p));
+  const long long cap = 148 * 4;
+  row_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (m + 31) / 32 + nnz / 1024)));
+  col_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (n + 31) / 32 + nnz / 1024)));
   row_start = dalloc<int>(row_grid + 1);
   col_start = dalloc<int>(col_grid + 1);
   k_partition<<<blocks_for(row_grid + 1), kBlock, 0, stream>>>(rowptr, m, row_grid, 8, row_start);
   k_partition<<<blocks_for(col_grid + 1), kBlock, 0, stream>>>(colptr, n, col_grid, 8, col_start);
   CKL("partition");
-  rowp = dalloc<double>(static_cast<size_t>(std::max(row_grid, 148 * 8)) * kRowParts);
-  colp = dalloc<double>(static_cast<size_t>(std::max(col_grid, 148 * 8)) * kColParts);
+  rowp = dalloc<double>(static_cast<size_t>(std::max(epi_grid, 148 * 8)) * kRowParts);
+  colp = dalloc<double>(static_cast<size_t>(std::max(epi_grid, 148 * 8)) * kColParts);
   // view kernels reuse rowp/colp with up to 148*4 blocks
   work_part = dalloc<double>(148 * 8 * 2);
   counter = dalloc<unsigned>(4);
@@ -420,9 +444,15 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled) {
 void Context::launch_iteration(bool init) {
   const IterParams& p = params;
   const int ii = init ? 1 : 0;
-  with_group(grow(), [&](auto g) { k_rows<decltype(g)::value><<<row_grid, kRowsBlock, 0, stream>>>(p, ii); });
-  with_group(gcol(), [&](auto g) { k_cols<decltype(g)::value><<<col_grid, kColsBlock, 0, stream>>>(p, ii); });
-  launches += 2;
+  with_group(grow(), [&](auto g) {
+    launch_pdl(k_spmv_rows<decltype(g)::value>, spmv_grid_r, kSpmvBlock, stream, p, ii);
+  });
+  launch_pdl(k_dual, epi_grid, kEpiBlock, stream, p, ii);
+  with_group(gcol(), [&](auto g) {
+    launch_pdl(k_spmv_cols<decltype(g)::value>, spmv_grid_c, kSpmvBlock, stream, p, ii);
+  });
+  launch_pdl(k_primal, epi_grid, kEpiBlock, stream, p, ii);
+  launches += kKernelsPerIteration;
 }
 
 void Context::build_graph(int k) {
@@ -516,7 +546,7 @@ void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
   p.rowptr = rowptr; p.colind = colind; p.aval = sval_csr;
   p.colptr = colptr; p.rowind = rowind; p.atval = sval_csc;
   p.row_start = row_start; p.col_start = col_start;
-  p.row_grid = row_grid; p.col_grid = col_grid;
+  p.row_grid = epi_grid; p.col_grid = epi_grid;  // partial counts for finalize
   p.c = c; p.l = l; p.u = u; p.b = b; p.r = r; p.s = s;
   for (int k = 0; k < 3; ++k)
     for (int q = 0; q < 2; ++q) p.xc[k][q] = xc[k][q];
@@ -718,7 +748,7 @@ int cclp_cu_advance(cclp_cu_ctx* ctx, int64_t iters, double* device_ms) {
     long long done = 0;
     while (done + k <= iters) {
       CK(cudaGraphLaunch(C.graph, C.stream));
-      C.launches += 2 * k;
+      C.launches += cclp_cu::kKernelsPerIteration * k;
       done += k;
     }
     while (done < iters) {
@@ -737,32 +767,37 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
   return guarded([&] {
     Context& C = ctx->c;
     if (!C.begun) throw std::invalid_argument("cclp_cu_profile_kernels: call cclp_cu_begin first");
-    std::vector<cudaEvent_t> ev(3 * iters);
+    constexpr int K = cclp_cu::kKernelsPerIteration;
+    std::vector<cudaEvent_t> ev((K + 1) * iters);
     for (auto& e : ev) CK(cudaEventCreate(&e));
+    const cclp_cu::IterParams& p = C.params;
     for (long long i = 0; i < iters; ++i) {
-      CK(cudaEventRecord(ev[3 * i], C.stream));
+      cudaEvent_t* e = &ev[(K + 1) * i];
+      CK(cudaEventRecord(e[0], C.stream));
       cclp_cu::with_group(C.grow(), [&](auto g) {
-        cclp_cu::k_rows<decltype(g)::value><<<C.row_grid, cclp_cu::kRowsBlock, 0, C.stream>>>(C.params, 0);
+        cclp_cu::k_spmv_rows<decltype(g)::value><<<C.spmv_grid_r, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
       });
-      CK(cudaEventRecord(ev[3 * i + 1], C.stream));
+      CK(cudaEventRecord(e[1], C.stream));
+      cclp_cu::k_dual<<<C.epi_grid, cclp_cu::kEpiBlock, 0, C.stream>>>(p, 0);
+      CK(cudaEventRecord(e[2], C.stream));
       cclp_cu::with_group(C.gcol(), [&](auto g) {
-        cclp_cu::k_cols<decltype(g)::value><<<C.col_grid, cclp_cu::kColsBlock, 0, C.stream>>>(C.params, 0);
+        cclp_cu::k_spmv_cols<decltype(g)::value><<<C.spmv_grid_c, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
       });
-      CK(cudaEventRecord(ev[3 * i + 2], C.stream));
-      C.launches += 2;
+      CK(cudaEventRecord(e[3], C.stream));
+      cclp_cu::k_primal<<<C.epi_grid, cclp_cu::kEpiBlock, 0, C.stream>>>(p, 0);
+      CK(cudaEventRecord(e[4], C.stream));
+      C.launches += K;
     }
     CK(cudaStreamSynchronize(C.stream));
-    double a = 0, b = 0;
-    for (long long i = 0; i < iters; ++i) {
-      float x, y;
-      CK(cudaEventElapsedTime(&x, ev[3 * i], ev[3 * i + 1]));
-      CK(cudaEventElapsedTime(&y, ev[3 * i + 1], ev[3 * i + 2]));
-      a += x;
-      b += y;
-    }
+    double acc[K] = {0, 0, 0, 0};
+    for (long long i = 0; i < iters; ++i)
+      for (int k = 0; k < K; ++k) {
+        float ms;
+        CK(cudaEventElapsedTime(&ms, ev[(K + 1) * i + k], ev[(K + 1) * i + k + 1]));
+        acc[k] += ms;
+      }
     for (auto& e : ev) cudaEventDestroy(e);
-    out[0] = iters ? a / iters : 0.0;
-    out[1] = iters ? b / iters : 0.0;
+    for (int k = 0; k < K; ++k) out[k] = iters ? acc[k] / iters : 0.0;
   });
 }
 
@@ -774,7 +809,7 @@ int cclp_cu_describe(cclp_cu_ctx* ctx, int64_t* out, int32_t nout) {
   std::memset(&st, 0, sizeof st);
   if (C.ctrl != nullptr && cudaMemcpy(&st, C.ctrl, sizeof st, cudaMemcpyDeviceToHost) != cudaSuccess)
     cudaGetLastError();
-  const int64_t v[] = {C.m, C.n, C.nnz, C.grow(), C.gcol(), C.row_grid, C.col_grid, C.launches,
+  const int64_t v[] = {C.m, C.n, C.nnz, C.grow(), C.gcol(), C.spmv_grid_r, C.epi_grid, C.launches,
                        static_cast<int64_t>(st.t_fin_start - st.t_cols_start),
                        static_cast<int64_t>(st.t_fin_end - st.t_fin_start)};
   for (int i = 0; i < nout && i < static_cast<int>(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
@@ -910,7 +945,7 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
       }
       // two batches in flight: launch, copy the control block, poll
       CK(cudaGraphLaunch(C.graph, C.stream));
-      C.launches += 2 * k;
+      C.launches += cclp_cu::kKernelsPerIteration * k;
       CK(cudaMemcpyAsync(&C.h_ctrl[0], C.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, C.stream));
       CK(cudaStreamSynchronize(C.stream));
       st = C.h_ctrl[0];

@@ -18,8 +18,9 @@
 namespace cclp_cu {
 
 constexpr int kBlock = 256;       // setup / view kernels
-constexpr int kRowsBlock = 256;
-constexpr int kColsBlock = 256;
+constexpr int kSpmvBlock = 256;   // lean SpMV kernels (8 resident blocks/SM)
+constexpr int kEpiBlock = 512;    // streaming epilogues (one wave, few partials)
+constexpr int kKernelsPerIteration = 4;
 constexpr int kRowParts = 8;   // per-block partials of the row kernel
 constexpr int kColParts = 14;  // per-block partials of the column kernel
 

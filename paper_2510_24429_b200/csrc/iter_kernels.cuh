@@ -1,20 +1,22 @@
-// The two fused kernels of one PDHG iteration, plus the on-device decision
-// tail. Step t (state t -> t+1, pdhg_step, pdhg.cpp:118-143) is:
+// The four kernels of one PDHG iteration, plus the on-device decision tail.
+// Step t (state t -> t+1, pdhg_step, pdhg.cpp:118-143) is:
 //
-//   k_rows(t): ax_{t+1} = A x_{t+1}  (x_{t+1} was produced by k_cols(t-1))
-//              y_{t+1}  = y' + sigma (b - (2 ax_{t+1} - ax'))     (:125-126)
-//              y_sum, ax_sum += ; row-side report partials for check(t+1)
-//   k_cols(t): aty_{t+1} = A' y_{t+1}
-//              x_sum, aty_sum += ; column-side report partials for check(t+1)
-//              next-x candidates x_{t+2} = proj(x - tau (c - aty)) for both
-//              outcomes of the restart test at check(t+1) (continue / restart
-//              from the average), so no restart kernel is ever launched;
-//              last block: finalize = check(t+1) decisions (:311-368).
+//   k_spmv_rows(t): ax_{t+1} = A x_{t+1}       (x_{t+1} produced by k_primal(t-1))
+//   k_dual(t):      y_{t+1} = y' + sigma (b - (2 ax_{t+1} - ax'))   (:125-126)
+//                   y_sum, ax_sum += ; row-side report partials for check(t+1)
+//   k_spmv_cols(t): aty_{t+1} = A' y_{t+1}
+//   k_primal(t):    x_sum, aty_sum += ; column-side report partials; next-x
+//                   candidates x_{t+2} = proj(x - tau (c - aty)) for both
+//                   outcomes of the restart test at check(t+1) (continue /
+//                   restart from the average), so no restart kernel is ever
+//                   launched; last block: finalize = check(t+1) decisions
+//                   (:311-368).
 //
-// (x', y', ax', aty') is state t after restart_if_improved (:145-165): when
-// check(t) restarted, the kernels read sums * (1/window) instead of the
-// current vectors — the same values the reference stores — and restart the
-// sums at zero.
+// The SpMV kernels are lean (few registers, high occupancy: the products are
+// gather-bound); the epilogues are coalesced streams. (x', y', ax', aty') is
+// state t after restart_if_improved (:145-165): when check(t) restarted, the
+// kernels read sums * (1/window) instead of the current vectors — the same
+// values the reference stores — and restart the sums at zero.
 #pragma once
 
 #include "kernels.cuh"
@@ -38,6 +40,7 @@ struct StepInfo {
 };
 
 __device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepInfo& si) {
+  pdl_wait();  // the previous kernel of the step (or step) must be complete
   const Ctrl* C = p.ctrl;
   if (C->stop >= 0 || C->halt) return false;
   if (init) {
@@ -68,71 +71,6 @@ __device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepIn
   si.check = (si.t1 % p.check_interval) == 0;
   si.init = false;
   return true;
-}
-
-template <int G>
-__global__ void __launch_bounds__(kRowsBlock) k_rows(const IterParams p, int init) {
-  StepInfo si;
-  if (!read_step(p, init != 0, si)) return;
-  __shared__ double wsum[kRowsBlock];
-  __shared__ double red[(kRowsBlock / 32) * kRowParts];
-  __shared__ double out[kRowParts];
-  double acc[kRowParts];
-#pragma unroll
-  for (int k = 0; k < kRowParts; ++k) acc[k] = 0.0;
-  const double* xg = p.xc[si.xs][si.R];
-  const int rb = p.row_start[blockIdx.x], re = p.row_start[blockIdx.x + 1];
-  struct RowOps {
-    double r, b, y, ax, ys, axs;
-  };
-  warp_tiles<G>(rb, re, p.rowptr, p.colind, p.aval, GatherPlain{xg}, wsum + (threadIdx.x & ~31),
-                [&](int i) {
-                  RowOps o;
-                  o.r = p.r[i];
-                  o.b = p.b[i];
-                  o.y = p.y[si.s0][i];
-                  o.ax = si.init ? 0.0 : p.ax[si.s0][i];
-                  o.ys = si.init ? 0.0 : p.ysum[si.s0][i];
-                  o.axs = si.init ? 0.0 : p.axsum[si.s0][i];
-                  return o;
-                },
-                [&](int i, double axn, const RowOps& o) {
-                  const double r = o.r, b = o.b;
-                  const double rinv = pow2_recip(r);
-                  if (si.init) {
-                    p.ax[0][i] = axn;
-                    row_report(axn, o.y, r, rinv, b, acc);
-                    return;
-                  }
-                  const double ys0 = o.ys, axs0 = o.axs;
-                  double yo, axo;
-                  if (si.R) {
-                    yo = ys0 * si.inv;
-                    axo = axs0 * si.inv;
-                  } else {
-                    yo = o.y;
-                    axo = o.ax;
-                  }
-                  const double bs = b * r;  // row_lower.cwiseProduct(r)
-                  double t = 2.0 * axn;
-                  t = t - axo;
-                  t = bs - t;
-                  t = p.sigma * t;
-                  const double yn = yo + t;
-                  const double ysn = (si.R ? 0.0 : ys0) + yn;
-                  const double axsn = (si.R ? 0.0 : axs0) + axn;
-                  p.y[si.s1][i] = yn;
-                  p.ax[si.s1][i] = axn;
-                  p.ysum[si.s1][i] = ysn;
-                  p.axsum[si.s1][i] = axsn;
-                  if (nonfinite(yn)) acc[6] += 1.0;
-                  if (si.check) {
-                    row_report(axn, yn, r, rinv, b, acc);
-                    row_report(axsn * si.inv1, ysn * si.inv1, r, rinv, b, acc + 3);
-                  }
-                });
-  block_reduce<kRowParts, kRowMaxMask, kRowsBlock>(acc, red, out);
-  if (threadIdx.x < kRowParts) p.rowp[blockIdx.x * kRowParts + threadIdx.x] = out[threadIdx.x];
 }
 
 // check(t+1) and everything after the step in the reference pass
@@ -232,35 +170,35 @@ static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied as 8-byte words");
 // decide() on a shared copy of the control block (one coalesced read and one
 // write instead of a chain of dependent global round trips).
 __device__ void finalize(const IterParams& p, const StepInfo& si) {
-  __shared__ double red[(kColsBlock / 32) * kColParts];
+  __shared__ double red[(kEpiBlock / 32) * kColParts];
   __shared__ double rowv[kRowParts];
   __shared__ double colv[kColParts];
   __shared__ Ctrl cs;
   constexpr int kWords = sizeof(Ctrl) / 8;
   long long* csw = reinterpret_cast<long long*>(&cs);
   const long long* gw = reinterpret_cast<const long long*>(p.ctrl);
-  for (int w = threadIdx.x; w < kWords; w += kColsBlock) csw[w] = __ldcg(gw + w);
+  for (int w = threadIdx.x; w < kWords; w += kEpiBlock) csw[w] = __ldcg(gw + w);
   double ra[kRowParts], ca[kColParts];
 #pragma unroll
   for (int k = 0; k < kRowParts; ++k) ra[k] = 0.0;
 #pragma unroll
   for (int k = 0; k < kColParts; ++k) ca[k] = 0.0;
-  for (int b = threadIdx.x; b < p.row_grid; b += kColsBlock) {
+  for (int b = threadIdx.x; b < p.row_grid; b += kEpiBlock) {
     double v[kRowParts];
 #pragma unroll
     for (int k = 0; k < kRowParts; ++k) v[k] = __ldcg(p.rowp + b * kRowParts + k);
 #pragma unroll
     for (int k = 0; k < kRowParts; ++k) ra[k] = ((kRowMaxMask >> k) & 1u) ? amax(ra[k], v[k]) : ra[k] + v[k];
   }
-  for (int b = threadIdx.x; b < p.col_grid; b += kColsBlock) {
+  for (int b = threadIdx.x; b < p.col_grid; b += kEpiBlock) {
     double v[kColParts];
 #pragma unroll
     for (int k = 0; k < kColParts; ++k) v[k] = __ldcg(p.colp + b * kColParts + k);
 #pragma unroll
     for (int k = 0; k < kColParts; ++k) ca[k] = ((kColMaxMask >> k) & 1u) ? amax(ca[k], v[k]) : ca[k] + v[k];
   }
-  block_reduce<kRowParts, kRowMaxMask, kColsBlock>(ra, red, rowv);
-  block_reduce<kColParts, kColMaxMask, kColsBlock>(ca, red, colv);
+  block_reduce<kRowParts, kRowMaxMask, kEpiBlock>(ra, red, rowv);
+  block_reduce<kColParts, kColMaxMask, kEpiBlock>(ca, red, colv);
   if (threadIdx.x == 0) {
     cs.t_cols_start = globaltimer();  // debug: reuse as "partials reduced" stamp
     decide(p, si, &cs, rowv, colv);
@@ -268,67 +206,136 @@ __device__ void finalize(const IterParams& p, const StepInfo& si) {
   }
   __syncthreads();
   long long* out = reinterpret_cast<long long*>(p.ctrl);
-  for (int w = threadIdx.x; w < kWords; w += kColsBlock) out[w] = csw[w];
+  for (int w = threadIdx.x; w < kWords; w += kEpiBlock) out[w] = csw[w];
+}
+
+// Lean SpMV of one half-step: out[r] = sum_k M[r,k] vec[k] over CSR M.
+// G lanes per row, grid-stride over row groups (fixed assignment ->
+// deterministic); G = 1 sums each row in the reference's own order.
+template <int G, class Gather>
+__device__ __forceinline__ void spmv_rows_grid(int rows, const int* __restrict__ ptr,
+                                               const int* __restrict__ idx,
+                                               const double* __restrict__ val, const Gather& g,
+                                               double* __restrict__ out) {
+  const int gl = threadIdx.x % G;
+  const int gpb = blockDim.x / G;
+  const int stride = gridDim.x * gpb;
+  for (int row = blockIdx.x * gpb + threadIdx.x / G; row - static_cast<int>(threadIdx.x / G) < rows;
+       row += stride) {
+    const bool ok = row < rows;
+    const int b = ok ? __ldg(ptr + row) : 0, e = ok ? __ldg(ptr + row + 1) : 0;
+    const double s = group_dot<G, 4>(b, e, gl, idx, val, g);
+    if (gl == 0 && ok) out[row] = 0.0 + s;
+  }
 }
 
 template <int G>
-__global__ void __launch_bounds__(kColsBlock) k_cols(const IterParams p, int init) {
+__global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
-  __shared__ double wsum[kColsBlock];
-  __shared__ double red[(kColsBlock / 32) * kColParts];
+  spmv_rows_grid<G>(p.m, p.rowptr, p.colind, p.aval, GatherPlain{p.xc[si.xs][si.R]}, p.ax[si.s1]);
+  pdl_trigger();
+}
+
+template <int G>
+__global__ void __launch_bounds__(kSpmvBlock) k_spmv_cols(const IterParams p, int init) {
+  StepInfo si;
+  if (!read_step(p, init != 0, si)) return;
+  spmv_rows_grid<G>(p.n, p.colptr, p.rowind, p.atval, GatherPlain{p.y[si.s1]}, p.aty[si.s1]);
+  pdl_trigger();
+}
+
+// Dual update + row-side report partials (one row per thread, coalesced).
+__global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init) {
+  StepInfo si;
+  if (!read_step(p, init != 0, si)) return;
+  __shared__ double red[(kEpiBlock / 32) * kRowParts];
+  __shared__ double out[kRowParts];
+  double acc[kRowParts];
+#pragma unroll
+  for (int k = 0; k < kRowParts; ++k) acc[k] = 0.0;
+  const double* axn_v = p.ax[si.s1];
+  for (int i = blockIdx.x * kEpiBlock + threadIdx.x; i < p.m; i += gridDim.x * kEpiBlock) {
+    const double r = p.r[i], b = p.b[i];
+    const double rinv = pow2_recip(r);
+    const double axn = axn_v[i];
+    if (si.init) {
+      row_report(axn, p.y[0][i], r, rinv, b, acc);
+      continue;
+    }
+    const double ys0 = p.ysum[si.s0][i], axs0 = p.axsum[si.s0][i];
+    double yo, axo;
+    if (si.R) {
+      yo = ys0 * si.inv;
+      axo = axs0 * si.inv;
+    } else {
+      yo = p.y[si.s0][i];
+      axo = p.ax[si.s0][i];
+    }
+    const double bs = b * r;  // row_lower.cwiseProduct(r)
+    double t = 2.0 * axn;
+    t = t - axo;
+    t = bs - t;
+    t = p.sigma * t;
+    const double yn = yo + t;
+    const double ysn = (si.R ? 0.0 : ys0) + yn;
+    const double axsn = (si.R ? 0.0 : axs0) + axn;
+    p.y[si.s1][i] = yn;
+    p.ysum[si.s1][i] = ysn;
+    p.axsum[si.s1][i] = axsn;
+    if (nonfinite(yn)) acc[6] += 1.0;
+    if (si.check) {
+      row_report(axn, yn, r, rinv, b, acc);
+      row_report(axsn * si.inv1, ysn * si.inv1, r, rinv, b, acc + 3);
+    }
+  }
+  pdl_trigger();
+  block_reduce<kRowParts, kRowMaxMask, kEpiBlock>(acc, red, out);
+  if (threadIdx.x < kRowParts) p.rowp[blockIdx.x * kRowParts + threadIdx.x] = out[threadIdx.x];
+}
+
+// Primal side: sums, column-side report partials, both next-x candidates;
+// the last block to finish runs finalize().
+__global__ void __launch_bounds__(kEpiBlock) k_primal(const IterParams p, int init) {
+  StepInfo si;
+  if (!read_step(p, init != 0, si)) return;
+  __shared__ double red[(kEpiBlock / 32) * kColParts];
   __shared__ double out[kColParts];
   __shared__ bool last;
   double acc[kColParts];
 #pragma unroll
   for (int k = 0; k < kColParts; ++k) acc[k] = 0.0;
-  const double* yg = p.y[si.s1];
+  const double* atyn_v = p.aty[si.s1];
   double* cand_c = p.xc[si.xs2][0];
   double* cand_a = p.xc[si.xs2][1];
   const double* xcur = p.xc[si.xs][si.R];
-  const int rb = p.col_start[blockIdx.x], re = p.col_start[blockIdx.x + 1];
-  struct ColOps {
-    double s, c, l, u, x, xs, as;
-  };
-  warp_tiles<G>(rb, re, p.colptr, p.rowind, p.atval, GatherPlain{yg}, wsum + (threadIdx.x & ~31),
-                [&](int j) {
-                  ColOps o;
-                  o.s = p.s[j];
-                  o.c = p.c[j];
-                  o.l = p.l[j];
-                  o.u = p.u[j];
-                  o.x = xcur[j];
-                  o.xs = si.init ? 0.0 : p.xsum[si.s0][j];
-                  o.as = si.init ? 0.0 : p.atysum[si.s0][j];
-                  return o;
-                },
-                [&](int j, double atyn, const ColOps& o) {
-                  const double s = o.s, c = o.c, l = o.l, u = o.u;
-                  const double sinv = pow2_recip(s);
-                  const double x1 = o.x;
-                  // apply_scaling: c*s, l/s, u/s (l/s == l*(1/s) exactly)
-                  const double cs = c * s, ls = l * sinv, us = u * sinv;
-                  cand_c[j] = primal_update(x1, atyn, cs, ls, us, p.tau);
-                  if (si.init) {
-                    p.aty[0][j] = atyn;
-                    col_report(x1, atyn, s, sinv, c, l, u, acc);
-                    return;
-                  }
-                  const double xs0 = o.xs, as0 = o.as;
-                  const double xsn = (si.R ? 0.0 : xs0) + x1;
-                  const double asn = (si.R ? 0.0 : as0) + atyn;
-                  p.aty[si.s1][j] = atyn;
-                  p.xsum[si.s1][j] = xsn;
-                  p.atysum[si.s1][j] = asn;
-                  if (nonfinite(x1)) acc[12] += 1.0;
-                  if (si.check) {
-                    col_report(x1, atyn, s, sinv, c, l, u, acc);
-                    const double xa = xsn * si.inv1, aa = asn * si.inv1;
-                    col_report(xa, aa, s, sinv, c, l, u, acc + 6);
-                    cand_a[j] = primal_update(xa, aa, cs, ls, us, p.tau);
-                  }
-                });
-  block_reduce<kColParts, kColMaxMask, kColsBlock>(acc, red, out);
+  for (int j = blockIdx.x * kEpiBlock + threadIdx.x; j < p.n; j += gridDim.x * kEpiBlock) {
+    const double s = p.s[j], c = p.c[j], l = p.l[j], u = p.u[j];
+    const double sinv = pow2_recip(s);
+    const double x1 = xcur[j];
+    const double atyn = atyn_v[j];
+    // apply_scaling: c*s, l/s, u/s (l/s == l*(1/s) exactly)
+    const double cs = c * s, ls = l * sinv, us = u * sinv;
+    cand_c[j] = primal_update(x1, atyn, cs, ls, us, p.tau);
+    if (si.init) {
+      col_report(x1, atyn, s, sinv, c, l, u, acc);
+      continue;
+    }
+    const double xs0 = p.xsum[si.s0][j], as0 = p.atysum[si.s0][j];
+    const double xsn = (si.R ? 0.0 : xs0) + x1;
+    const double asn = (si.R ? 0.0 : as0) + atyn;
+    p.xsum[si.s1][j] = xsn;
+    p.atysum[si.s1][j] = asn;
+    if (nonfinite(x1)) acc[12] += 1.0;
+    if (si.check) {
+      col_report(x1, atyn, s, sinv, c, l, u, acc);
+      const double xa = xsn * si.inv1, aa = asn * si.inv1;
+      col_report(xa, aa, s, sinv, c, l, u, acc + 6);
+      cand_a[j] = primal_update(xa, aa, cs, ls, us, p.tau);
+    }
+  }
+  pdl_trigger();
+  block_reduce<kColParts, kColMaxMask, kEpiBlock>(acc, red, out);
   if (threadIdx.x < kColParts) p.colp[blockIdx.x * kColParts + threadIdx.x] = out[threadIdx.x];
   __threadfence();
   __syncthreads();
@@ -440,8 +447,8 @@ __global__ void __launch_bounds__(kBlock) k_view_cols(const ViewParams v, int ro
       const double x = __ldcg(v.colp + b * kColParts + k);
       ca[k] = ((kColMaxMask >> k) & 1u) ? amax(ca[k], x) : ca[k] + x;
     }
-  block_reduce<kRowParts, kRowMaxMask, kColsBlock>(ra, red, rowv);
-  block_reduce<kColParts, kColMaxMask, kColsBlock>(ca, red, colv);
+  block_reduce<kRowParts, kRowMaxMask>(ra, red, rowv);
+  block_reduce<kColParts, kColMaxMask>(ca, red, colv);
   if (threadIdx.x == 0) {
     make_report(rowv, colv, p.b_norm, p.c_norm, v.report);
     *v.counter = 0u;

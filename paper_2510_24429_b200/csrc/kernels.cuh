@@ -24,6 +24,14 @@ __device__ __forceinline__ double amax(double acc, double v) { return (acc < v) 
 __device__ __forceinline__ bool isfin(double v) { return v > -CCLP_INF && v < CCLP_INF; }
 __device__ __forceinline__ bool nonfinite(double v) { return isnan(v - v); }
 
+// Programmatic dependent launch (PDL): a kernel launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// predecessor drains; pdl_wait() blocks until the predecessor grid has
+// completed and its writes are visible, pdl_trigger() lets the successor start
+// launching once this block's main work is done.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

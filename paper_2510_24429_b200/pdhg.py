@@ -387,16 +387,17 @@ class Engine:
         _check(self.L, self.L.cclp_cu_advance(self.ctx, iters, C.byref(ms)))
         return ms.value
 
-    def profile_kernels(self, iters: int):
-        out = (C.c_double * 2)()
+    def profile_kernels(self, iters: int) -> dict:
+        """Average ms per launch of the four iteration kernels."""
+        out = (C.c_double * 4)()
         _check(self.L, self.L.cclp_cu_profile_kernels(self.ctx, iters, out))
-        return out[0], out[1]
+        return dict(zip(["spmv_rows", "dual", "spmv_cols", "primal"], list(out)))
 
     def stream_ptr(self) -> int:
         return int(self.L.cclp_cu_stream(self.ctx) or 0)
 
     def describe(self) -> dict:
-        keys = ["m", "n", "nnz", "group_rows", "group_cols", "row_grid", "col_grid", "launches",
+        keys = ["m", "n", "nnz", "group_rows", "group_cols", "spmv_grid", "epi_grid", "launches",
                 "last_cols_body_ns", "last_finalize_ns"]
         out = (C.c_int64 * len(keys))()
         self.L.cclp_cu_describe(self.ctx, out, len(keys))

@@ -24,8 +24,8 @@ eng.advance(200)
 for it in (1000, 1000):
     ms = eng.advance(it)
     print(f"advance {it}: {ms:.2f} ms -> {it/ms*1e3:.0f} it/s, {ms/it*1e3:.2f} us/it", flush=True)
-a, b = eng.profile_kernels(200)
-print(f"kernels: rows {a*1e3:.2f} us, cols {b*1e3:.2f} us", flush=True)
+pk = eng.profile_kernels(200)
+print("kernels: " + ", ".join(f"{k} {v*1e3:.2f} us" for k, v in pk.items()), flush=True)
 d = eng.describe()
 print(f"last cols body (start->finalize) {d['last_cols_body_ns']/1e3:.2f} us, finalize {d['last_finalize_ns']/1e3:.2f} us", flush=True)
 nnz, m, n = lp.nnz, lp.m, lp.n
