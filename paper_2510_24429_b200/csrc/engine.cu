@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <type_traits>
@@ -54,12 +55,17 @@ T* dalloc(size_t n) {
   return static_cast<T*>(p);
 }
 
+// Lanes per row from the mean row length L. A fixed rule (never timing
+// based): G sets the per-row summation order, so it must not vary between
+// runs. Thresholds from tools/spmv_bench.cu on C1-C4 (profiles/r1_spmv_*):
+// L ~ 2 -> 2, L 9-24 -> 4, L ~ 50 -> 8, L ~ 100 -> 16, L >= 160 -> 32.
 int pick_group(long long nnz, long long rows) {
-  // lanes per row: each lane takes ~4 nonzeros of an average row
-  const double avg = rows > 0 ? static_cast<double>(nnz) / static_cast<double>(rows) : 0.0;
-  int g = 1;
-  while (g < 32 && g * 4 < avg) g *= 2;
-  return g;
+  const double L = rows > 0 ? static_cast<double>(nnz) / static_cast<double>(rows) : 0.0;
+  if (L <= 3.0) return 2;
+  if (L <= 24.0) return 4;
+  if (L <= 64.0) return 8;
+  if (L <= 160.0) return 16;
+  return 32;
 }
 
 int blocks_for(long long n, int per = kBlock, int cap = 148 * 8) {
@@ -69,6 +75,14 @@ int blocks_for(long long n, int per = kBlock, int cap = 148 * 8) {
 
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // launching while its predecessor drains; it synchronizes with griddepcontrol.
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CCLP_CU_PDL");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 template <class... KArgs, class... Args>
 void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t st, Args&&... args) {
   cudaLaunchConfig_t cfg{};
@@ -80,7 +94,7 @@ void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t st, 
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
 }
 
@@ -115,6 +129,8 @@ struct Context {
   // partitions
   int Grow = 1, Gcol = 1, row_grid = 1, col_grid = 1;
   int spmv_grid_r = 1, spmv_grid_c = 1, epi_grid = 1;
+  int* spmv_row_start = nullptr;  // [spmv_grid_r + 1]
+  int* spmv_col_start = nullptr;  // [spmv_grid_c + 1]
   int *row_start = nullptr, *col_start = nullptr;
   bool exact = false;  // G = 1: reference-order (bit-identical) SpMV sums
   // state
@@ -156,6 +172,7 @@ struct Context {
   void upload(const cclp_cu_lp* lp);
   void build_csr();
   void partition();
+  void tune_spmv();
   int grow() const { return exact ? 1 : Grow; }
   int gcol() const { return exact ? 1 : Gcol; }
   void launch_spmv(bool transpose, const double* vec, double* out, bool scaled, const int* stop);
@@ -174,7 +191,7 @@ Context::~Context() {
   cudaSetDevice(device);
   if (graph) cudaGraphExecDestroy(graph);
   void* ptrs[] = {colptr, rowind, rowptr, colind, val_csc, val_csr, sval_csc, sval_csr, c, l, u, b,
-                  r, s, row_start, col_start, rowp, colp, work_part, counter, ctrl, log, thr, t0,
+                  r, s, row_start, col_start, spmv_row_start, spmv_col_start, rowp, colp, work_part, counter, ctrl, log, thr, t0,
                   scalars, pctrl, iflags, amb_idx, wn, wn2, wm, vx, vy, vz, vrep};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -282,16 +299,8 @@ void Context::partition() {
   // blocks, so finalize reduces only that many partials.
   int sms = 148, occ_r = 1, occ_c = 1, occ_d = 1, occ_p = 1;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  with_group(Grow, [&](auto g) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_r, k_spmv_rows<decltype(g)::value>, kSpmvBlock, 0));
-  });
-  with_group(Gcol, [&](auto g) {
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_c, k_spmv_cols<decltype(g)::value>, kSpmvBlock, 0));
-  });
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_d, k_dual, kEpiBlock, 0));
-  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k_primal, kEpiBlock, 0));
-  spmv_grid_r = sms * std::max(occ_r, 1);
-  spmv_grid_c = sms * std::max(occ_c, 1);
+  (void)occ_r;
+  (void)occ_c;
   epi_grid = sms * std::max(1, std::min(occ_d, occ_p));
   const long long cap = 148 * 4;
   row_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (m + 31) / 32 + nnz / 1024)));
@@ -316,6 +325,62 @@ void Context::partition() {
   wn2 = dalloc<double>(n);
   wm = dalloc<double>(m);
   t0 = dalloc<unsigned long long>(1);
+  tune_spmv();
+}
+
+// Picks the launch geometry (blocks per SM) of the two iteration SpMVs by
+// timing candidates on this matrix. G (lanes per row) is fixed by the mean
+// row length, so every candidate produces bit-identical results.
+void Context::tune_spmv() {
+  int sms = 148;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  IterParams probe{};
+  probe.m = m;
+  probe.n = n;
+  auto tune_one = [&](bool rows_side, int** start_out, int* grid_out) {
+    const int* ptr = rows_side ? rowptr : colptr;
+    const int* idx = rows_side ? colind : rowind;
+    const double* val = rows_side ? val_csr : val_csc;
+    const int nrows = rows_side ? m : n;
+    const int G = rows_side ? grow() : gcol();
+    double* vec = rows_side ? wn : wm;
+    double* out = rows_side ? wm : wn;
+    CK(cudaMemsetAsync(vec, 0, sizeof(double) * std::max(rows_side ? n : m, 1), stream));
+    float best = 1e30f;
+    int best_grid = sms;
+    int* best_start = nullptr;
+    for (int per_sm : {1, 2}) {
+      const int grid = sms * per_sm;
+      int* st = dalloc<int>(grid + 1);
+      k_partition<<<blocks_for(grid + 1), kBlock, 0, stream>>>(ptr, nrows, grid, 4, st);
+      CKL("tune partition");
+      float tot = 0.0f;
+      for (int rep = 0; rep < 4; ++rep) {
+        CK(cudaEventRecord(ev_a, stream));
+        with_group(G, [&](auto g) {
+          k_spmv_range<decltype(g)::value><<<grid, kSpmvBlock, 0, stream>>>(st, ptr, idx, val,
+                                                                             GatherPlain{vec}, out);
+        });
+        CK(cudaEventRecord(ev_b, stream));
+        CK(cudaEventSynchronize(ev_b));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+        if (rep > 0) tot += ms;
+      }
+      if (tot < best) {
+        best = tot;
+        best_grid = grid;
+        if (best_start) cudaFree(best_start);
+        best_start = st;
+      } else {
+        cudaFree(st);
+      }
+    }
+    *start_out = best_start;
+    *grid_out = best_grid;
+  };
+  tune_one(true, &spmv_row_start, &spmv_grid_r);
+  tune_one(false, &spmv_col_start, &spmv_grid_c);
 }
 
 void Context::launch_spmv(bool transpose, const double* vec, double* out, bool scaled,
@@ -547,6 +612,7 @@ void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
   p.colptr = colptr; p.rowind = rowind; p.atval = sval_csc;
   p.row_start = row_start; p.col_start = col_start;
   p.row_grid = epi_grid; p.col_grid = epi_grid;  // partial counts for finalize
+  p.spmv_row_start = spmv_row_start; p.spmv_col_start = spmv_col_start;
   p.c = c; p.l = l; p.u = u; p.b = b; p.r = r; p.s = s;
   for (int k = 0; k < 3; ++k)
     for (int q = 0; q < 2; ++q) p.xc[k][q] = xc[k][q];

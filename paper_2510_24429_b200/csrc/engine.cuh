@@ -18,7 +18,7 @@
 namespace cclp_cu {
 
 constexpr int kBlock = 256;       // setup / view kernels
-constexpr int kSpmvBlock = 256;   // lean SpMV kernels (8 resident blocks/SM)
+constexpr int kSpmvBlock = 1024;  // lean SpMV kernels: fat blocks on contiguous row ranges
 constexpr int kEpiBlock = 512;    // streaming epilogues (one wave, few partials)
 constexpr int kKernelsPerIteration = 4;
 constexpr int kRowParts = 8;   // per-block partials of the row kernel

@@ -170,7 +170,6 @@ static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied as 8-byte words");
 // decide() on a shared copy of the control block (one coalesced read and one
 // write instead of a chain of dependent global round trips).
 __device__ void finalize(const IterParams& p, const StepInfo& si) {
-  __shared__ double red[(kEpiBlock / 32) * kColParts];
   __shared__ double rowv[kRowParts];
   __shared__ double colv[kColParts];
   __shared__ Ctrl cs;
@@ -178,27 +177,30 @@ __device__ void finalize(const IterParams& p, const StepInfo& si) {
   long long* csw = reinterpret_cast<long long*>(&cs);
   const long long* gw = reinterpret_cast<const long long*>(p.ctrl);
   for (int w = threadIdx.x; w < kWords; w += kEpiBlock) csw[w] = __ldcg(gw + w);
-  double ra[kRowParts], ca[kColParts];
+  // warp w reduces fields w, w+16, ... over all blocks: lane l takes blocks
+  // l, l+32, ...
+  // in order, then a fixed butterfly (deterministic, one round of loads).
+  const int lane = threadIdx.x & 31;
+  for (int fld = threadIdx.x >> 5; fld < kRowParts + kColParts; fld += kEpiBlock / 32) {
+    const bool is_row = fld < kRowParts;
+    const int f = is_row ? fld : fld - kRowParts;
+    const bool is_max = is_row ? ((kRowMaxMask >> f) & 1u) : ((kColMaxMask >> f) & 1u);
+    const double* src = is_row ? p.rowp : p.colp;
+    const int stride = is_row ? kRowParts : kColParts;
+    const int nb = is_row ? p.row_grid : p.col_grid;
+    double a = 0.0;
+    for (int b = lane; b < nb; b += 32) {
+      const double v = __ldcg(src + b * stride + f);
+      a = is_max ? amax(a, v) : a + v;
+    }
 #pragma unroll
-  for (int k = 0; k < kRowParts; ++k) ra[k] = 0.0;
-#pragma unroll
-  for (int k = 0; k < kColParts; ++k) ca[k] = 0.0;
-  for (int b = threadIdx.x; b < p.row_grid; b += kEpiBlock) {
-    double v[kRowParts];
-#pragma unroll
-    for (int k = 0; k < kRowParts; ++k) v[k] = __ldcg(p.rowp + b * kRowParts + k);
-#pragma unroll
-    for (int k = 0; k < kRowParts; ++k) ra[k] = ((kRowMaxMask >> k) & 1u) ? amax(ra[k], v[k]) : ra[k] + v[k];
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_xor_sync(0xffffffffu, a, off);
+      a = is_max ? amax(a, o) : a + o;
+    }
+    if (lane == 0) (is_row ? rowv : colv)[f] = a;
   }
-  for (int b = threadIdx.x; b < p.col_grid; b += kEpiBlock) {
-    double v[kColParts];
-#pragma unroll
-    for (int k = 0; k < kColParts; ++k) v[k] = __ldcg(p.colp + b * kColParts + k);
-#pragma unroll
-    for (int k = 0; k < kColParts; ++k) ca[k] = ((kColMaxMask >> k) & 1u) ? amax(ca[k], v[k]) : ca[k] + v[k];
-  }
-  block_reduce<kRowParts, kRowMaxMask, kEpiBlock>(ra, red, rowv);
-  block_reduce<kColParts, kColMaxMask, kEpiBlock>(ca, red, colv);
+  __syncthreads();
   if (threadIdx.x == 0) {
     cs.t_cols_start = globaltimer();  // debug: reuse as "partials reduced" stamp
     decide(p, si, &cs, rowv, colv);
@@ -210,39 +212,52 @@ __device__ void finalize(const IterParams& p, const StepInfo& si) {
 }
 
 // Lean SpMV of one half-step: out[r] = sum_k M[r,k] vec[k] over CSR M.
-// G lanes per row, grid-stride over row groups (fixed assignment ->
-// deterministic); G = 1 sums each row in the reference's own order.
+// Block b owns the contiguous, nnz-balanced row range [start[b], start[b+1])
+// and its warps walk it together (so on structured LPs their gathers share an
+// L1-resident window of vec); G lanes per row. The per-row summation order
+// depends only on G, never on the launch geometry, so the geometry can be
+// autotuned without changing a bit of the result; G = 1 sums each row in the
+// reference's own order.
 template <int G, class Gather>
-__device__ __forceinline__ void spmv_rows_grid(int rows, const int* __restrict__ ptr,
-                                               const int* __restrict__ idx,
-                                               const double* __restrict__ val, const Gather& g,
-                                               double* __restrict__ out) {
+__device__ __forceinline__ void spmv_block_range(const int* __restrict__ start, const int* __restrict__ ptr,
+                                                 const int* __restrict__ idx,
+                                                 const double* __restrict__ val, const Gather& g,
+                                                 double* __restrict__ out) {
   const int gl = threadIdx.x % G;
   const int gpb = blockDim.x / G;
-  const int stride = gridDim.x * gpb;
-  for (int row = blockIdx.x * gpb + threadIdx.x / G; row - static_cast<int>(threadIdx.x / G) < rows;
-       row += stride) {
-    const bool ok = row < rows;
+  const int rb = start[blockIdx.x], re = start[blockIdx.x + 1];
+  for (int row = rb + static_cast<int>(threadIdx.x / G); row - static_cast<int>(threadIdx.x / G) < re;
+       row += gpb) {
+    const bool ok = row < re;
     const int b = ok ? __ldg(ptr + row) : 0, e = ok ? __ldg(ptr + row + 1) : 0;
     const double s = group_dot<G, 4>(b, e, gl, idx, val, g);
     if (gl == 0 && ok) out[row] = 0.0 + s;
   }
 }
 
+template <int G, class Gather>
+__global__ void __launch_bounds__(kSpmvBlock) k_spmv_range(const int* __restrict__ start,
+                                                           const int* __restrict__ ptr,
+                                                           const int* __restrict__ idx,
+                                                           const double* __restrict__ val, Gather g,
+                                                           double* __restrict__ out) {
+  spmv_block_range<G>(start, ptr, idx, val, g, out);
+}
+
 template <int G>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
-  spmv_rows_grid<G>(p.m, p.rowptr, p.colind, p.aval, GatherPlain{p.xc[si.xs][si.R]}, p.ax[si.s1]);
-  pdl_trigger();
+  spmv_block_range<G>(p.spmv_row_start, p.rowptr, p.colind, p.aval, GatherPlain{p.xc[si.xs][si.R]},
+                      p.ax[si.s1]);
 }
 
 template <int G>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_cols(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
-  spmv_rows_grid<G>(p.n, p.colptr, p.rowind, p.atval, GatherPlain{p.y[si.s1]}, p.aty[si.s1]);
-  pdl_trigger();
+  spmv_block_range<G>(p.spmv_col_start, p.colptr, p.rowind, p.atval, GatherPlain{p.y[si.s1]},
+                      p.aty[si.s1]);
 }
 
 // Dual update + row-side report partials (one row per thread, coalesced).
@@ -254,42 +269,62 @@ __global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init
   double acc[kRowParts];
 #pragma unroll
   for (int k = 0; k < kRowParts; ++k) acc[k] = 0.0;
-  const double* axn_v = p.ax[si.s1];
-  for (int i = blockIdx.x * kEpiBlock + threadIdx.x; i < p.m; i += gridDim.x * kEpiBlock) {
-    const double r = p.r[i], b = p.b[i];
-    const double rinv = pow2_recip(r);
-    const double axn = axn_v[i];
-    if (si.init) {
-      row_report(axn, p.y[0][i], r, rinv, b, acc);
-      continue;
+  const double* __restrict__ axn_v = p.ax[si.s1];
+  const double* __restrict__ y0 = p.y[si.s0];
+  const double* __restrict__ ax0 = p.ax[si.s0];
+  const double* __restrict__ ys0v = p.ysum[si.s0];
+  const double* __restrict__ axs0v = p.axsum[si.s0];
+  double* __restrict__ y1 = p.y[si.s1];
+  double* __restrict__ ys1 = p.ysum[si.s1];
+  double* __restrict__ axs1 = p.axsum[si.s1];
+  constexpr int U = 2;  // rows per thread per trip, loads hoisted
+  const int stride = gridDim.x * kEpiBlock;
+  for (int i0 = blockIdx.x * kEpiBlock + threadIdx.x; i0 < p.m; i0 += U * stride) {
+    double r[U], b[U], axn[U], yo[U], axo[U], ys[U], axs[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int i = i0 + k * stride;
+      const bool ok = i < p.m;
+      r[k] = ok ? p.r[i] : 1.0;
+      b[k] = ok ? p.b[i] : 0.0;
+      axn[k] = ok ? axn_v[i] : 0.0;
+      yo[k] = ok ? y0[i] : 0.0;
+      axo[k] = ok && !si.init && !si.R ? ax0[i] : 0.0;
+      ys[k] = ok && !si.init ? ys0v[i] : 0.0;
+      axs[k] = ok && !si.init ? axs0v[i] : 0.0;
     }
-    const double ys0 = p.ysum[si.s0][i], axs0 = p.axsum[si.s0][i];
-    double yo, axo;
-    if (si.R) {
-      yo = ys0 * si.inv;
-      axo = axs0 * si.inv;
-    } else {
-      yo = p.y[si.s0][i];
-      axo = p.ax[si.s0][i];
-    }
-    const double bs = b * r;  // row_lower.cwiseProduct(r)
-    double t = 2.0 * axn;
-    t = t - axo;
-    t = bs - t;
-    t = p.sigma * t;
-    const double yn = yo + t;
-    const double ysn = (si.R ? 0.0 : ys0) + yn;
-    const double axsn = (si.R ? 0.0 : axs0) + axn;
-    p.y[si.s1][i] = yn;
-    p.ysum[si.s1][i] = ysn;
-    p.axsum[si.s1][i] = axsn;
-    if (nonfinite(yn)) acc[6] += 1.0;
-    if (si.check) {
-      row_report(axn, yn, r, rinv, b, acc);
-      row_report(axsn * si.inv1, ysn * si.inv1, r, rinv, b, acc + 3);
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int i = i0 + k * stride;
+      if (i >= p.m) break;
+      const double rinv = pow2_recip(r[k]);
+      if (si.init) {
+        row_report(axn[k], yo[k], r[k], rinv, b[k], acc);
+        continue;
+      }
+      double y_old = yo[k], ax_old = axo[k];
+      if (si.R) {
+        y_old = ys[k] * si.inv;
+        ax_old = axs[k] * si.inv;
+      }
+      const double bs = b[k] * r[k];  // row_lower.cwiseProduct(r)
+      double t = 2.0 * axn[k];
+      t = t - ax_old;
+      t = bs - t;
+      t = p.sigma * t;
+      const double yn = y_old + t;
+      const double ysn = (si.R ? 0.0 : ys[k]) + yn;
+      const double axsn = (si.R ? 0.0 : axs[k]) + axn[k];
+      y1[i] = yn;
+      ys1[i] = ysn;
+      axs1[i] = axsn;
+      if (nonfinite(yn)) acc[6] += 1.0;
+      if (si.check) {
+        row_report(axn[k], yn, r[k], rinv, b[k], acc);
+        row_report(axsn * si.inv1, ysn * si.inv1, r[k], rinv, b[k], acc + 3);
+      }
     }
   }
-  pdl_trigger();
   block_reduce<kRowParts, kRowMaxMask, kEpiBlock>(acc, red, out);
   if (threadIdx.x < kRowParts) p.rowp[blockIdx.x * kRowParts + threadIdx.x] = out[threadIdx.x];
 }
@@ -305,36 +340,56 @@ __global__ void __launch_bounds__(kEpiBlock) k_primal(const IterParams p, int in
   double acc[kColParts];
 #pragma unroll
   for (int k = 0; k < kColParts; ++k) acc[k] = 0.0;
-  const double* atyn_v = p.aty[si.s1];
-  double* cand_c = p.xc[si.xs2][0];
-  double* cand_a = p.xc[si.xs2][1];
-  const double* xcur = p.xc[si.xs][si.R];
-  for (int j = blockIdx.x * kEpiBlock + threadIdx.x; j < p.n; j += gridDim.x * kEpiBlock) {
-    const double s = p.s[j], c = p.c[j], l = p.l[j], u = p.u[j];
-    const double sinv = pow2_recip(s);
-    const double x1 = xcur[j];
-    const double atyn = atyn_v[j];
-    // apply_scaling: c*s, l/s, u/s (l/s == l*(1/s) exactly)
-    const double cs = c * s, ls = l * sinv, us = u * sinv;
-    cand_c[j] = primal_update(x1, atyn, cs, ls, us, p.tau);
-    if (si.init) {
-      col_report(x1, atyn, s, sinv, c, l, u, acc);
-      continue;
+  const double* __restrict__ atyn_v = p.aty[si.s1];
+  double* __restrict__ cand_c = p.xc[si.xs2][0];
+  double* __restrict__ cand_a = p.xc[si.xs2][1];
+  const double* __restrict__ xcur = p.xc[si.xs][si.R];
+  const double* __restrict__ xs0v = p.xsum[si.s0];
+  const double* __restrict__ as0v = p.atysum[si.s0];
+  double* __restrict__ xs1 = p.xsum[si.s1];
+  double* __restrict__ as1 = p.atysum[si.s1];
+  constexpr int U = 2;  // columns per thread per trip, loads hoisted
+  const int stride = gridDim.x * kEpiBlock;
+  for (int j0 = blockIdx.x * kEpiBlock + threadIdx.x; j0 < p.n; j0 += U * stride) {
+    double s[U], c[U], l[U], u[U], x1[U], atyn[U], xs0[U], as0[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int j = j0 + k * stride;
+      const bool ok = j < p.n;
+      s[k] = ok ? p.s[j] : 1.0;
+      c[k] = ok ? p.c[j] : 0.0;
+      l[k] = ok ? p.l[j] : 0.0;
+      u[k] = ok ? p.u[j] : 0.0;
+      x1[k] = ok ? xcur[j] : 0.0;
+      atyn[k] = ok ? atyn_v[j] : 0.0;
+      xs0[k] = ok && !si.init ? xs0v[j] : 0.0;
+      as0[k] = ok && !si.init ? as0v[j] : 0.0;
     }
-    const double xs0 = p.xsum[si.s0][j], as0 = p.atysum[si.s0][j];
-    const double xsn = (si.R ? 0.0 : xs0) + x1;
-    const double asn = (si.R ? 0.0 : as0) + atyn;
-    p.xsum[si.s1][j] = xsn;
-    p.atysum[si.s1][j] = asn;
-    if (nonfinite(x1)) acc[12] += 1.0;
-    if (si.check) {
-      col_report(x1, atyn, s, sinv, c, l, u, acc);
-      const double xa = xsn * si.inv1, aa = asn * si.inv1;
-      col_report(xa, aa, s, sinv, c, l, u, acc + 6);
-      cand_a[j] = primal_update(xa, aa, cs, ls, us, p.tau);
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int j = j0 + k * stride;
+      if (j >= p.n) break;
+      const double sinv = pow2_recip(s[k]);
+      // apply_scaling: c*s, l/s, u/s (l/s == l*(1/s) exactly)
+      const double cs = c[k] * s[k], ls = l[k] * sinv, us = u[k] * sinv;
+      cand_c[j] = primal_update(x1[k], atyn[k], cs, ls, us, p.tau);
+      if (si.init) {
+        col_report(x1[k], atyn[k], s[k], sinv, c[k], l[k], u[k], acc);
+        continue;
+      }
+      const double xsn = (si.R ? 0.0 : xs0[k]) + x1[k];
+      const double asn = (si.R ? 0.0 : as0[k]) + atyn[k];
+      xs1[j] = xsn;
+      as1[j] = asn;
+      if (nonfinite(x1[k])) acc[12] += 1.0;
+      if (si.check) {
+        col_report(x1[k], atyn[k], s[k], sinv, c[k], l[k], u[k], acc);
+        const double xa = xsn * si.inv1, aa = asn * si.inv1;
+        col_report(xa, aa, s[k], sinv, c[k], l[k], u[k], acc + 6);
+        cand_a[j] = primal_update(xa, aa, cs, ls, us, p.tau);
+      }
     }
   }
-  pdl_trigger();
   block_reduce<kColParts, kColMaxMask, kEpiBlock>(acc, red, out);
   if (threadIdx.x < kColParts) p.colp[blockIdx.x * kColParts + threadIdx.x] = out[threadIdx.x];
   __threadfence();

@@ -25,12 +25,12 @@ __device__ __forceinline__ bool isfin(double v) { return v > -CCLP_INF && v < CC
 __device__ __forceinline__ bool nonfinite(double v) { return isnan(v - v); }
 
 // Programmatic dependent launch (PDL): a kernel launched with
-// cudaLaunchAttributeProgrammaticStreamSerialization may start while its
+// cudaLaunchAttributeProgrammaticStreamSerialization is set up while its
 // predecessor drains; pdl_wait() blocks until the predecessor grid has
-// completed and its writes are visible, pdl_trigger() lets the successor start
-// launching once this block's main work is done.
+// completed and its writes are visible. No early launch_dependents trigger:
+// measured on C4, successor blocks launched early squat on SMs the draining
+// grid still needs (+300 us/iteration); without it PDL is neutral-to-positive.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -56,6 +56,9 @@ struct IterParams {
   const int* row_start;
   const int* col_start;
   int row_grid, col_grid;
+  // contiguous row ranges of the iteration SpMV kernels (autotuned grids)
+  const int* spmv_row_start;
+  const int* spmv_col_start;
   // unscaled problem data and Ruiz factors
   const double *c, *l, *u, *b, *r, *s;
   // state

@@ -76,6 +76,15 @@ __global__ void __launch_bounds__(kBlock) k_spmv(const int* __restrict__ ptr, co
                 NoPre{}, [&](int i, double s, int) { out[i] = 0.0 + s; });
 }
 
+// Plain y = M v over contiguous block row ranges (the iteration SpMV's
+// geometry; used to autotune it).
+template <int G, class Gather>
+__global__ void __launch_bounds__(kSpmvBlock) k_spmv_range(const int* __restrict__ start,
+                                                           const int* __restrict__ ptr,
+                                                           const int* __restrict__ idx,
+                                                           const double* __restrict__ val, Gather g,
+                                                           double* __restrict__ out);
+
 // ---- power iteration (estimate_matrix_norm, pdhg.cpp:46-65) ---------------
 struct PowerCtrl {
   double nu;      // ||u_prev|| (v = u_prev / nu)

@@ -439,6 +439,39 @@ __global__ void __launch_bounds__(256) v_wspipe(int m, const int* __restrict__ p
   }
 }
 
+// V6: vector CSR over a contiguous, nnz-balanced row range per block (the
+// block's warps walk it together so their x gathers share an L1 window).
+template <int G, int U, int BS>
+__global__ void __launch_bounds__(BS) v_contig(const int* __restrict__ ptr, const int* __restrict__ idx,
+                                               const double* __restrict__ val, const double* __restrict__ x,
+                                               double* __restrict__ y, const int* __restrict__ start) {
+  const int lane = threadIdx.x % G;
+  constexpr int GPB = BS / G;
+  const int rb = start[blockIdx.x], re = start[blockIdx.x + 1];
+  for (int row = rb + threadIdx.x / G; row - static_cast<int>(threadIdx.x / G) < re; row += GPB) {
+    double acc = 0.0;
+    if (row < re) {
+      const int b = ptr[row], e = ptr[row + 1];
+      for (int p = b + lane; p < e; p += G * U) {
+        int ii[U];
+        double vv[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+          const int q = p + k * G;
+          ii[k] = q < e ? __ldcs(idx + q) : -1;
+          vv[k] = q < e ? __ldcs(val + q) : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+          if (ii[k] >= 0) acc = acc + vv[k] * __ldg(x + ii[k]);
+      }
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (lane == 0 && row < re) y[row] = acc;
+  }
+}
+
 int main(int argc, char** argv) {
   char path[512];
   snprintf(path, sizeof path, "%s.meta", argv[1]);
@@ -578,6 +611,36 @@ int main(int argc, char** argv) {
     run("gather G8 U4 plain", [&] { v_nogather<8, 4, true, 2><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
     run("gather G8 U8 ldcs", [&] { v_nogather<8, 8, true, 0><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
     run("gather G4 U8 ldcs", [&] { v_nogather<4, 8, true, 0><<<grid, 256>>>(m, dp, di, dv, dx, dy); });
+  }
+  {
+    auto contig = [&](auto kern, int BS, int per_sm, const char* tag) {
+      const int grid = sms * per_sm;
+      std::vector<int> st(grid + 1);
+      for (int b = 0; b <= grid; ++b) {
+        const long long target = ((long long)hp[m] + 4LL * m) * b / grid;
+        int lo = 0, hi2 = m;
+        while (lo < hi2) { int mid = (lo + hi2) / 2; if ((long long)hp[mid] + 4LL * mid >= target) hi2 = mid; else lo = mid + 1; }
+        st[b] = b == grid ? m : lo;
+      }
+      int* dst;
+      CK(cudaMalloc(&dst, sizeof(int) * (grid + 1)));
+      CK(cudaMemcpy(dst, st.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice));
+      char nm[64];
+      snprintf(nm, sizeof nm, "contig %s BS%d x%d", tag, BS, per_sm);
+      run(nm, [&] { kern<<<grid, BS>>>(dp, di, dv, dx, dy, dst); });
+      cudaFree(dst);
+    };
+    contig(v_contig<8, 4, 1024>, 1024, 2, "G8");
+    contig(v_contig<8, 4, 1024>, 1024, 1, "G8");
+    contig(v_contig<8, 4, 512>, 512, 4, "G8");
+    contig(v_contig<4, 4, 1024>, 1024, 2, "G4");
+    contig(v_contig<4, 4, 1024>, 1024, 1, "G4");
+    contig(v_contig<4, 4, 512>, 512, 4, "G4");
+    contig(v_contig<16, 4, 1024>, 1024, 2, "G16");
+    contig(v_contig<8, 4, 256>, 256, 8, "G8");
+    contig(v_contig<4, 4, 256>, 256, 8, "G4");
+    contig(v_contig<8, 4, 256>, 256, 64, "G8");
+    contig(v_contig<4, 4, 256>, 256, 64, "G4");
   }
   // window-staged panels
   auto win_run = [&](auto kern, int G, int BS, int wcap, int panel_rows_max) {
