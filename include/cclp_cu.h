@@ -160,6 +160,11 @@ int cclp_cu_ruiz(cclp_cu_ctx* ctx, int32_t iterations, double* row_scale, double
 /* estimate_matrix_norm (pdhg.cpp:46-65) on the unscaled A. */
 int cclp_cu_estimate_norm(cclp_cu_ctx* ctx, int32_t iterations, uint64_t seed, double* out);
 
+/* The power iteration's start vector (host only, no device needed):
+ * out[j] = std::normal_distribution<double>(0,1) draws from
+ * std::mt19937_64(seed + 0x9e3779b97f4a7c15), pdhg.cpp:49-52, bit for bit. */
+void cclp_cu_gaussian_start(uint64_t seed, int64_t n, double* out);
+
 /* ---- measurement hooks (bench.py) ---------------------------------------- */
 
 /* Begin a solve without running the loop: scaling, norm, initial check. */

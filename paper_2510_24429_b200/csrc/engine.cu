@@ -17,9 +17,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <map>
+#include <mutex>
 #include <type_traits>
 #include <random>
 #include <stdexcept>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -48,11 +51,48 @@ void ck(cudaError_t e, const char* what) {
 
 namespace {
 
-template <class T>
-T* dalloc(size_t n) {
+// Device memory comes from the device's default stream-ordered pool with an
+// unbounded release threshold: a solve's buffers return to the pool on
+// destroy and the next context reuses them, so create/destroy never touch
+// the driver's allocator (cudaMalloc/cudaFree synchronize the device and cost
+// milliseconds each at these sizes).
+void ensure_pool(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> g(mu);
+  if (std::find(done.begin(), done.end(), device) != done.end()) return;
+  cudaMemPool_t pool;
+  CK(cudaDeviceGetDefaultMemPool(&pool, device));
+  uint64_t thr = UINT64_MAX;
+  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+  done.push_back(device);
+}
+
+// Pinned host buffers (control block, log, snapshot staging) are recycled
+// process-wide for the same reason: cudaHostAlloc/cudaFreeHost pin and unpin
+// pages synchronously.
+std::mutex g_pinned_mu;
+std::multimap<size_t, void*> g_pinned_free;
+
+void* pinned_alloc(size_t bytes) {
+  {
+    std::lock_guard<std::mutex> g(g_pinned_mu);
+    auto it = g_pinned_free.lower_bound(bytes);
+    if (it != g_pinned_free.end() && it->first <= 2 * bytes + 4096) {
+      void* p = it->second;
+      g_pinned_free.erase(it);
+      return p;
+    }
+  }
   void* p = nullptr;
-  CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
-  return static_cast<T*>(p);
+  CK(cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocDefault));
+  return p;
+}
+
+void pinned_release(void* p, size_t bytes) {
+  if (p == nullptr) return;
+  std::lock_guard<std::mutex> g(g_pinned_mu);
+  g_pinned_free.emplace(std::max<size_t>(bytes, 1), p);
 }
 
 // Lanes per row from the mean row length L. A fixed rule (never timing
@@ -167,6 +207,37 @@ struct Context {
   long long launches = 0;
   double b_norm = 0, c_norm = 0;
   double norm_est = 0, omega = 0, tau = 0, sigma = 0;
+  // host-side phase timings (seconds; stream synchronized at each border):
+  // 0 upload, 1 csr build, 2 partition + spmv tuning, 3 norms, 4 ruiz,
+  // 5 scale values, 6 power iteration, 7 state init + check(0),
+  // 8 graph build, 9 loop, 10 result view + download
+  static constexpr int kPhases = 11;
+  double phase[kPhases] = {};
+  std::chrono::steady_clock::time_point phase_t0;
+  template <class T>
+  T* alloc(size_t count) {
+    void* p = nullptr;
+    ck(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), stream), "cudaMallocAsync");
+    return static_cast<T*>(p);
+  }
+  void release(void* p) {
+    if (p) cudaFreeAsync(p, stream);
+  }
+  // pinned host buffers with their sizes (returned to the process cache)
+  std::vector<std::pair<void*, size_t>> pinned;
+  template <class T>
+  T* host_alloc(size_t count) {
+    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
+    void* p = pinned_alloc(bytes);
+    pinned.emplace_back(p, bytes);
+    return static_cast<T*>(p);
+  }
+  void mark(int k) {
+    CK(cudaStreamSynchronize(stream));
+    const auto now = std::chrono::steady_clock::now();
+    phase[k] = std::chrono::duration<double>(now - phase_t0).count();
+    phase_t0 = now;
+  }
 
   ~Context();
   void upload(const cclp_cu_lp* lp);
@@ -178,7 +249,8 @@ struct Context {
   void launch_spmv(bool transpose, const double* vec, double* out, bool scaled, const int* stop);
   double reduce(const double* a, const double* bvec, long long len, int mode);
   void ruiz(int iterations);
-  double power_norm(int iterations, uint64_t seed, bool scaled);
+  double power_norm(int iterations, uint64_t seed, bool scaled, bool pregenerated = false);
+  double* h_v0 = nullptr;  // pinned start vector of the power iteration
   void begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thresholds,
              int nthr);
   void launch_iteration(bool init);
@@ -190,25 +262,24 @@ struct Context {
 Context::~Context() {
   cudaSetDevice(device);
   if (graph) cudaGraphExecDestroy(graph);
-  void* ptrs[] = {colptr, rowind, rowptr, colind, val_csc, val_csr, sval_csc, sval_csr, c, l, u, b,
-                  r, s, row_start, col_start, spmv_row_start, spmv_col_start, rowp, colp, work_part, counter, ctrl, log, thr, t0,
-                  scalars, pctrl, iflags, amb_idx, wn, wn2, wm, vx, vy, vz, vrep};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
-  for (int k = 0; k < 3; ++k)
-    for (int q = 0; q < 2; ++q)
-      if (xc[k][q]) cudaFree(xc[k][q]);
-  for (int q = 0; q < 2; ++q) {
-    double* v[] = {aty[q], xsum[q], atysum[q], y[q], ax[q], ysum[q], axsum[q]};
-    for (double* p : v)
-      if (p) cudaFree(p);
+  if (stream) {
+    void* ptrs[] = {colptr, rowind, rowptr, colind, val_csc, val_csr, sval_csc, sval_csr, c, l, u, b,
+                    r, s, row_start, col_start, spmv_row_start, spmv_col_start, rowp, colp, work_part,
+                    counter, ctrl, log, thr, t0, scalars, pctrl, iflags, amb_idx, wn, wn2, wm, vx, vy,
+                    vz, vrep};
+    for (void* p : ptrs) release(p);
+    for (int k = 0; k < 3; ++k)
+      for (int q = 0; q < 2; ++q) release(xc[k][q]);
+    for (int q = 0; q < 2; ++q) {
+      double* v[] = {aty[q], xsum[q], atysum[q], y[q], ax[q], ysum[q], axsum[q]};
+      for (double* p : v) release(p);
+    }
+    // pinned buffers may still be targets of queued copies
+    cudaStreamSynchronize(stream);
+    if (side) cudaStreamSynchronize(side);
   }
-  if (h_ctrl) cudaFreeHost(h_ctrl);
-  if (h_log) cudaFreeHost(h_log);
-  if (h_scalars) cudaFreeHost(h_scalars);
-  if (h_sx) cudaFreeHost(h_sx);
-  if (h_sy) cudaFreeHost(h_sy);
-  if (h_sz) cudaFreeHost(h_sz);
+  cudaGetLastError();
+  for (auto& pb : pinned) pinned_release(pb.first, pb.second);
   if (ev_snap) cudaEventDestroy(ev_snap);
   if (ev_a) cudaEventDestroy(ev_a);
   if (ev_b) cudaEventDestroy(ev_b);
@@ -220,20 +291,22 @@ void Context::upload(const cclp_cu_lp* lp) {
   m = lp->m;
   n = lp->n;
   nnz = lp->colptr[n];
+  phase_t0 = std::chrono::steady_clock::now();
+  ensure_pool(device);
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&ev_snap, cudaEventDisableTiming));
   CK(cudaEventCreate(&ev_a));
   CK(cudaEventCreate(&ev_b));
-  colptr = dalloc<int>(n + 1);
-  rowind = dalloc<int>(nnz);
-  val_csc = dalloc<double>(nnz);
-  c = dalloc<double>(n);
-  l = dalloc<double>(n);
-  u = dalloc<double>(n);
-  b = dalloc<double>(m);
-  r = dalloc<double>(m);
-  s = dalloc<double>(n);
+  colptr = alloc<int>(n + 1);
+  rowind = alloc<int>(nnz);
+  val_csc = alloc<double>(nnz);
+  c = alloc<double>(n);
+  l = alloc<double>(n);
+  u = alloc<double>(n);
+  b = alloc<double>(m);
+  r = alloc<double>(m);
+  s = alloc<double>(n);
   CK(cudaMemcpyAsync(colptr, lp->colptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, stream));
   CK(cudaMemcpyAsync(rowind, lp->rowind, sizeof(int) * nnz, cudaMemcpyHostToDevice, stream));
   CK(cudaMemcpyAsync(val_csc, lp->val, sizeof(double) * nnz, cudaMemcpyHostToDevice, stream));
@@ -250,24 +323,27 @@ void Context::upload(const cclp_cu_lp* lp) {
     }
   }
   CK(cudaMemcpyAsync(b, lp->row_lower, sizeof(double) * m, cudaMemcpyHostToDevice, stream));
+  mark(0);
   build_csr();
+  mark(1);
   partition();
+  mark(2);
 }
 
 void Context::build_csr() {
-  rowptr = dalloc<int>(m + 1);
-  colind = dalloc<int>(nnz);
-  val_csr = dalloc<double>(nnz);
+  rowptr = alloc<int>(m + 1);
+  colind = alloc<int>(nnz);
+  val_csr = alloc<double>(nnz);
   if (nnz == 0) {
     CK(cudaMemsetAsync(rowptr, 0, sizeof(int) * (m + 1), stream));
     return;
   }
   // Stable radix sort of the CSC entries by row: within a row the entries
   // keep CSC order, i.e. ascending column, as a CSR requires.
-  int* col_of = dalloc<int>(nnz);
-  int* keys_out = dalloc<int>(nnz);
-  int* perm_in = dalloc<int>(nnz);
-  int* perm_out = dalloc<int>(nnz);
+  int* col_of = alloc<int>(nnz);
+  int* keys_out = alloc<int>(nnz);
+  int* perm_in = alloc<int>(nnz);
+  int* perm_out = alloc<int>(nnz);
   k_expand_major<<<blocks_for(n), kBlock, 0, stream>>>(colptr, n, col_of);
   k_iota<<<blocks_for(nnz), kBlock, 0, stream>>>(perm_in, nnz);
   CKL("expand");
@@ -276,18 +352,18 @@ void Context::build_csr() {
   size_t tmp_bytes = 0;
   CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, rowind, keys_out, perm_in, perm_out,
                                      static_cast<int>(nnz), 0, bits, stream));
-  void* tmp = dalloc<char>(tmp_bytes);
+  void* tmp = alloc<char>(tmp_bytes);
   CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, rowind, keys_out, perm_in, perm_out,
                                      static_cast<int>(nnz), 0, bits, stream));
   k_offsets_from_sorted<<<blocks_for(m + 1), kBlock, 0, stream>>>(keys_out, nnz, m, rowptr);
   k_gather_csr<<<blocks_for(nnz), kBlock, 0, stream>>>(perm_out, nnz, col_of, val_csc, colind, val_csr);
   CKL("csr");
   CK(cudaStreamSynchronize(stream));
-  cudaFree(tmp);
-  cudaFree(col_of);
-  cudaFree(keys_out);
-  cudaFree(perm_in);
-  cudaFree(perm_out);
+  release(tmp);
+  release(col_of);
+  release(keys_out);
+  release(perm_in);
+  release(perm_out);
 }
 
 void Context::partition() {
@@ -305,26 +381,26 @@ void Context::partition() {
   const long long cap = 148 * 4;
   row_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (m + 31) / 32 + nnz / 1024)));
   col_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (n + 31) / 32 + nnz / 1024)));
-  row_start = dalloc<int>(row_grid + 1);
-  col_start = dalloc<int>(col_grid + 1);
+  row_start = alloc<int>(row_grid + 1);
+  col_start = alloc<int>(col_grid + 1);
   k_partition<<<blocks_for(row_grid + 1), kBlock, 0, stream>>>(rowptr, m, row_grid, 8, row_start);
   k_partition<<<blocks_for(col_grid + 1), kBlock, 0, stream>>>(colptr, n, col_grid, 8, col_start);
   CKL("partition");
-  rowp = dalloc<double>(static_cast<size_t>(std::max(epi_grid, 148 * 8)) * kRowParts);
-  colp = dalloc<double>(static_cast<size_t>(std::max(epi_grid, 148 * 8)) * kColParts);
+  rowp = alloc<double>(static_cast<size_t>(std::max(epi_grid, 148 * 8)) * kRowParts);
+  colp = alloc<double>(static_cast<size_t>(std::max(epi_grid, 148 * 8)) * kColParts);
   // view kernels reuse rowp/colp with up to 148*4 blocks
-  work_part = dalloc<double>(148 * 8 * 2);
-  counter = dalloc<unsigned>(4);
+  work_part = alloc<double>(148 * 8 * 2);
+  counter = alloc<unsigned>(4);
   CK(cudaMemsetAsync(counter, 0, sizeof(unsigned) * 4, stream));
-  scalars = dalloc<double>(16);
-  CK(cudaHostAlloc(&h_scalars, sizeof(double) * 16, cudaHostAllocDefault));
-  pctrl = dalloc<PowerCtrl>(1);
-  iflags = dalloc<int>(4);
-  amb_idx = dalloc<int>(512);
-  wn = dalloc<double>(n);
-  wn2 = dalloc<double>(n);
-  wm = dalloc<double>(m);
-  t0 = dalloc<unsigned long long>(1);
+  scalars = alloc<double>(16);
+  h_scalars = host_alloc<double>(16);
+  pctrl = alloc<PowerCtrl>(1);
+  iflags = alloc<int>(4);
+  amb_idx = alloc<int>(512);
+  wn = alloc<double>(n);
+  wn2 = alloc<double>(n);
+  wm = alloc<double>(m);
+  t0 = alloc<unsigned long long>(1);
   tune_spmv();
 }
 
@@ -351,7 +427,7 @@ void Context::tune_spmv() {
     int* best_start = nullptr;
     for (int per_sm : {1, 2}) {
       const int grid = sms * per_sm;
-      int* st = dalloc<int>(grid + 1);
+      int* st = alloc<int>(grid + 1);
       k_partition<<<blocks_for(grid + 1), kBlock, 0, stream>>>(ptr, nrows, grid, 4, st);
       CKL("tune partition");
       float tot = 0.0f;
@@ -370,10 +446,10 @@ void Context::tune_spmv() {
       if (tot < best) {
         best = tot;
         best_grid = grid;
-        if (best_start) cudaFree(best_start);
+        if (best_start) release(best_start);
         best_start = st;
       } else {
-        cudaFree(st);
+        release(st);
       }
     }
     *start_out = best_start;
@@ -464,41 +540,91 @@ void Context::ruiz(int iterations) {
   }
 }
 
+// The power iteration's start vector, v_j = normal_distribution(mt19937_64(
+// seed + 0x9e3779b97f4a7c15)) (pdhg.cpp:49-52), restated in two stages so it
+// costs ~3 ns per entry instead of the reference's ~20: (1) one thread runs the
+// engine and libstdc++'s polar-method rejection loop (generate_canonical<double,
+// 53> on a 64-bit engine is exactly u * 2^-64, clamped below 1), keeping the
+// accepted (x, y, r2); (2) all host cores apply mult = sqrt(-2 log(r2) / r2)
+// with the same libm. Entry 2k is y*mult (the returned value), 2k+1 is x*mult
+// (the saved one), then `* stddev + mean` = `* 1.0 + 0.0`. Bit-identical to
+// std::normal_distribution<double> (checked against the oracle in tests).
+void gaussian_start(uint64_t seed, long long n, double* v) {
+  std::mt19937_64 rng(seed + 0x9e3779b97f4a7c15ull);
+  const long long pairs = n / 2;  // full pairs; an odd n leaves one tail pair
+  auto canon = [&rng]() {
+    const double r = static_cast<double>(rng()) * 0x1p-64;
+    return r >= 1.0 ? std::nextafter(1.0, 0.0) : r;
+  };
+  auto draw = [&](double& x, double& y) {
+    double r2;
+    do {
+      x = 2.0 * canon() - 1.0;
+      y = 2.0 * canon() - 1.0;
+      r2 = x * x + y * y;
+    } while (r2 > 1.0 || r2 == 0.0);
+  };
+  // stage 1 (serial): accepted (x, y) stored in place as v[2k] = y, v[2k+1] = x
+  for (long long k = 0; k < pairs; ++k) draw(v[2 * k + 1], v[2 * k]);
+  auto finish = [](double x, double y, double* out2, bool both) {
+    const double r2 = x * x + y * y;  // recomputed: the same two products and sum
+    const double mult = std::sqrt(-2 * std::log(r2) / r2);
+    out2[0] = y * mult * 1.0 + 0.0;
+    if (both) out2[1] = x * mult * 1.0 + 0.0;
+  };
+  if (n & 1) {
+    double x, y;
+    draw(x, y);
+    finish(x, y, v + n - 1, false);
+  }
+  // stage 2 (all cores): the transcendental half
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  const long long per = std::max<long long>(1 << 16, (pairs + hw - 1) / hw);
+  auto work = [&](long long a, long long b) {
+    for (long long k = a; k < b; ++k) finish(v[2 * k + 1], v[2 * k], v + 2 * k, true);
+  };
+  std::vector<std::thread> th;
+  for (long long a = per; a < pairs; a += per) th.emplace_back(work, a, std::min(pairs, a + per));
+  work(0, std::min(pairs, per));
+  for (auto& t : th) t.join();
+}
+
 // estimate_matrix_norm (pdhg.cpp:46-65) on the scaled or unscaled matrix.
-double Context::power_norm(int iterations, uint64_t seed, bool scaled) {
+// Per iteration: w = A v and u = A' w with the iteration's tuned SpMV
+// geometry (G lanes per row), nu = ||u|| and lambda = v.u in one reduction,
+// then v = u / nu materialized (the reference's `v = u / norm`, :62).
+double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool pregenerated) {
   if (m == 0 || n == 0 || nnz == 0) return 0.0;
   // start vector: mt19937_64 + normal_distribution, as the reference (:49-52)
-  std::vector<double> v0(n);
-  {
-    std::mt19937_64 rng(seed + 0x9e3779b97f4a7c15ull);
-    std::normal_distribution<double> gauss(0.0, 1.0);
-    for (int j = 0; j < n; ++j) v0[j] = gauss(rng);
-  }
-  double* u_prev = wn;
+  if (!h_v0) h_v0 = host_alloc<double>(n);
+  if (!pregenerated) gaussian_start(seed, n, h_v0);
+  const double* v0 = h_v0;
+  double* v = wn;
   double* u = wn2;
-  CK(cudaMemcpyAsync(u_prev, v0.data(), sizeof(double) * n, cudaMemcpyHostToDevice, stream));
-  double nv = reduce(u_prev, nullptr, n, 0);
+  CK(cudaMemcpyAsync(v, v0, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+  double nv = reduce(v, nullptr, n, 0);
   if (std::sqrt(nv) == 0.0) {
-    k_fill<<<blocks_for(n), kBlock, 0, stream>>>(u_prev, n, 1.0);
-    nv = reduce(u_prev, nullptr, n, 0);
+    k_fill<<<blocks_for(n), kBlock, 0, stream>>>(v, n, 1.0);
+    nv = reduce(v, nullptr, n, 0);
   }
   PowerCtrl pc{std::sqrt(nv), 0.0, 0, 0};
   CK(cudaMemcpyAsync(pctrl, &pc, sizeof(pc), cudaMemcpyHostToDevice, stream));
+  k_div_scalar<<<blocks_for(n), kBlock, 0, stream>>>(v, &pctrl->nu, v, n);  // v /= v.norm()
   const double* aval = scaled ? sval_csr : val_csr;
   const double* atval = scaled ? sval_csc : val_csc;
+  const int rgrid = blocks_for(n, kBlock, 148 * 4);
   for (int t = 0; t < iterations; ++t) {
-    // w = A v with v = u_prev / nu  (Vector w = A * v, :57)
-    with_group(grow(), [&](auto g) {
-      k_spmv<decltype(g)::value><<<row_grid, kBlock, 0, stream>>>(
-          rowptr, colind, aval, GatherDiv{u_prev, &pctrl->nu}, row_start, wm, &pctrl->zero);
+    with_group(grow(), [&](auto g) {  // w = A v (:57)
+      k_spmv_range<decltype(g)::value><<<spmv_grid_r, kSpmvBlock, 0, stream>>>(
+          spmv_row_start, rowptr, colind, aval, GatherPlain{v}, wm);
     });
-    // u = A' w; nu = ||u||; lambda = v.u  (:58-61)
-    with_group(gcol(), [&](auto g) {
-      k_power_cols<decltype(g)::value><<<col_grid, kBlock, 0, stream>>>(
-          colptr, rowind, atval, wm, col_start, u_prev, u, work_part, counter + 2, pctrl);
+    with_group(gcol(), [&](auto g) {  // u = A' w (:58)
+      k_spmv_range<decltype(g)::value><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(
+          spmv_col_start, colptr, rowind, atval, GatherPlain{wm}, u);
     });
+    k_power_reduce<<<rgrid, kBlock, 0, stream>>>(u, v, n, work_part, counter + 2, pctrl);
+    k_div_scalar<<<blocks_for(n), kBlock, 0, stream>>>(u, &pctrl->nu, v, n);  // v = u / norm
     CKL("power");
-    std::swap(u_prev, u);
   }
   CK(cudaMemcpyAsync(&pc, pctrl, sizeof(pc), cudaMemcpyDeviceToHost, stream));
   CK(cudaStreamSynchronize(stream));
@@ -546,19 +672,33 @@ void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
   }
   k_stamp<<<1, 1, 0, stream>>>(t0);
   CKL("stamp");
-  const auto h0 = std::chrono::steady_clock::now();
+  phase_t0 = std::chrono::steady_clock::now();
+  // the power iteration's start vector is host work: overlap it with the
+  // device-side norms, Ruiz passes and value scaling
+  if (!h_v0) h_v0 = host_alloc<double>(n);
+  std::thread rng_thread;
+  if (m > 0 && n > 0 && nnz > 0) rng_thread = std::thread(gaussian_start, cfg.seed, (long long)n, h_v0);
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() { if (t.joinable()) t.join(); }
+  } joiner{rng_thread};
   // norms on the unscaled model (pdhg.cpp:253-254)
   b_norm = std::sqrt(reduce(b, nullptr, m, 0));
   c_norm = std::sqrt(reduce(c, nullptr, n, 0));
+  mark(3);
   ruiz(cfg.scaling_iterations);
-  if (!sval_csr) sval_csr = dalloc<double>(nnz);
-  if (!sval_csc) sval_csc = dalloc<double>(nnz);
+  mark(4);
+  if (!sval_csr) sval_csr = alloc<double>(nnz);
+  if (!sval_csc) sval_csc = alloc<double>(nnz);
   k_scale_values<<<blocks_for(static_cast<long long>(m) * 32), kBlock, 0, stream>>>(
       rowptr, m, colind, val_csr, r, s, 1, sval_csr);
   k_scale_values<<<blocks_for(static_cast<long long>(n) * 32), kBlock, 0, stream>>>(
       colptr, n, rowind, val_csc, s, r, 0, sval_csc);
   CKL("scale");
-  norm_est = power_norm(cfg.norm_iterations, cfg.seed, true);
+  mark(5);
+  if (rng_thread.joinable()) rng_thread.join();
+  norm_est = power_norm(cfg.norm_iterations, cfg.seed, true, true);
+  mark(6);
   const double a_norm = norm_est > 0.0 ? norm_est : 1.0;
   omega = cfg.primal_weight;
   if (omega <= 0.0) {  // pdhg.cpp:260-265 on the scaled model
@@ -570,8 +710,8 @@ void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
   sigma = cfg.step_scale / (omega * a_norm);
 
   // state buffers
-  auto alloc_n = [&](double*& p) { if (!p) p = dalloc<double>(n); };
-  auto alloc_m = [&](double*& p) { if (!p) p = dalloc<double>(m); };
+  auto alloc_n = [&](double*& p) { if (!p) p = alloc<double>(n); };
+  auto alloc_m = [&](double*& p) { if (!p) p = alloc<double>(m); };
   for (int k = 0; k < 3; ++k)
     for (int q = 0; q < 2; ++q) alloc_n(xc[k][q]);
   for (int q = 0; q < 2; ++q) {
@@ -586,10 +726,10 @@ void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
     CK(cudaMemsetAsync(atysum[q], 0, sizeof(double) * std::max(n, 1), stream));
   }
   if (!ctrl) {
-    ctrl = dalloc<Ctrl>(1);
-    CK(cudaHostAlloc(&h_ctrl, sizeof(Ctrl) * 4, cudaHostAllocDefault));
-    log = dalloc<LogEntry>(log_cap);
-    CK(cudaHostAlloc(&h_log, sizeof(LogEntry) * log_cap, cudaHostAllocDefault));
+    ctrl = alloc<Ctrl>(1);
+    h_ctrl = host_alloc<Ctrl>(4);
+    log = alloc<LogEntry>(log_cap);
+    h_log = host_alloc<LogEntry>(log_cap);
   }
   Ctrl c0;
   std::memset(&c0, 0, sizeof c0);
@@ -597,8 +737,8 @@ void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
   c0.last_restart_resid = INFINITY;
   CK(cudaMemcpyAsync(ctrl, &c0, sizeof c0, cudaMemcpyHostToDevice, stream));
   if (nthr > thr_cap) {
-    if (thr) cudaFree(thr);
-    thr = dalloc<double>(nthr);
+    if (thr) release(thr);
+    thr = alloc<double>(nthr);
     thr_cap = nthr;
   }
   if (nthr > 0)
@@ -632,8 +772,7 @@ void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
     cudaGraphExecDestroy(graph);
     graph = nullptr;
   }
-  CK(cudaStreamSynchronize(stream));
-  (void)h0;
+  mark(7);
   begun = true;
 }
 
@@ -646,10 +785,10 @@ void Context::fetch_ctrl(Ctrl* dst) {
 // vy, vz, vrep.
 void Context::extract_view(int view, const Ctrl& st, bool need_report) {
   if (!vx) {
-    vx = dalloc<double>(n);
-    vz = dalloc<double>(n);
-    vy = dalloc<double>(m);
-    vrep = dalloc<double>(kRepN);
+    vx = alloc<double>(n);
+    vz = alloc<double>(n);
+    vy = alloc<double>(m);
+    vrep = alloc<double>(kRepN);
   }
   ViewParams v;
   v.it = params;
@@ -732,6 +871,10 @@ void copy_report(const double* src, cclp_cu_report* dst) {
 extern "C" {
 
 const char* cclp_cu_last_error(void) { return g_err.c_str(); }
+
+void cclp_cu_gaussian_start(uint64_t seed, int64_t n, double* out) {
+  cclp_cu::gaussian_start(seed, n, out);
+}
 
 const char* cclp_cu_stop_string(int32_t stop) {
   switch (stop) {  // pdhg.cpp:28-44
@@ -877,7 +1020,14 @@ int cclp_cu_describe(cclp_cu_ctx* ctx, int64_t* out, int32_t nout) {
     cudaGetLastError();
   const int64_t v[] = {C.m, C.n, C.nnz, C.grow(), C.gcol(), C.spmv_grid_r, C.epi_grid, C.launches,
                        static_cast<int64_t>(st.t_fin_start - st.t_cols_start),
-                       static_cast<int64_t>(st.t_fin_end - st.t_fin_start)};
+                       static_cast<int64_t>(st.t_fin_end - st.t_fin_start),
+                       // 10..20: phase timings in ns (Context::phase)
+                       static_cast<int64_t>(1e9 * C.phase[0]), static_cast<int64_t>(1e9 * C.phase[1]),
+                       static_cast<int64_t>(1e9 * C.phase[2]), static_cast<int64_t>(1e9 * C.phase[3]),
+                       static_cast<int64_t>(1e9 * C.phase[4]), static_cast<int64_t>(1e9 * C.phase[5]),
+                       static_cast<int64_t>(1e9 * C.phase[6]), static_cast<int64_t>(1e9 * C.phase[7]),
+                       static_cast<int64_t>(1e9 * C.phase[8]), static_cast<int64_t>(1e9 * C.phase[9]),
+                       static_cast<int64_t>(1e9 * C.phase[10])};
   for (int i = 0; i < nout && i < static_cast<int>(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
   return CCLP_CU_OK;
 }
@@ -939,6 +1089,7 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
     const int k = cfg.poll_interval > 0 ? cfg.poll_interval : 64;
     C.build_graph(k);
+    C.mark(8);
     CK(cudaEventRecord(C.ev_a, C.stream));
 
     Ctrl st;
@@ -964,9 +1115,9 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
       // PdhgSnapshot of the better view (pdhg.cpp:346-358)
       C.extract_view(q.snap_use_avg ? cclp_cu::kViewAvg : cclp_cu::kViewCur, q, false);
       if (!C.h_sx) {
-        CK(cudaHostAlloc(&C.h_sx, sizeof(double) * std::max(C.n, 1), cudaHostAllocDefault));
-        CK(cudaHostAlloc(&C.h_sz, sizeof(double) * std::max(C.n, 1), cudaHostAllocDefault));
-        CK(cudaHostAlloc(&C.h_sy, sizeof(double) * std::max(C.m, 1), cudaHostAllocDefault));
+        C.h_sx = C.host_alloc<double>(C.n);
+        C.h_sz = C.host_alloc<double>(C.n);
+        C.h_sy = C.host_alloc<double>(C.m);
       }
       CK(cudaEventRecord(C.ev_snap, C.stream));
       CK(cudaStreamWaitEvent(C.side, C.ev_snap, 0));
@@ -1020,6 +1171,7 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
     CK(cudaEventSynchronize(C.ev_b));
     float loop_ms = 0;
     CK(cudaEventElapsedTime(&loop_ms, C.ev_a, C.ev_b));
+    C.mark(9);
 
     int view = st.result_view;
     int stop = st.stop;
@@ -1036,7 +1188,7 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
     CK(cudaMemcpyAsync(z_out, C.vz, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.stream));
     double rep[cclp_cu::kRepN];
     CK(cudaMemcpyAsync(rep, C.vrep, sizeof(rep), cudaMemcpyDeviceToHost, C.stream));
-    CK(cudaStreamSynchronize(C.stream));
+    C.mark(10);
     res->stop = stop;
     res->iterations = st.iteration;
     res->restarts = st.restarts;

@@ -144,6 +144,49 @@ __global__ void __launch_bounds__(kBlock) k_power_cols(const int* __restrict__ p
   }
 }
 
+// nu = ||u||, lambda = v.u (pdhg.cpp:59-61) over the materialized u and v;
+// the last block finalizes (a zero norm sets `zero`: the reference returns 0).
+__global__ void __launch_bounds__(kBlock) k_power_reduce(const double* __restrict__ u,
+                                                         const double* __restrict__ v, long long n,
+                                                         double* part, unsigned* counter,
+                                                         PowerCtrl* pc) {
+  if (pc->zero) return;
+  __shared__ double red[(kBlock / 32) * 2];
+  __shared__ double out[2];
+  __shared__ bool last;
+  double acc[2] = {0.0, 0.0};
+  for (long long i = blockIdx.x * (long long)kBlock + threadIdx.x; i < n;
+       i += (long long)gridDim.x * kBlock) {
+    const double ui = u[i];
+    acc[0] += ui * ui;
+    acc[1] += v[i] * ui;
+  }
+  block_reduce<2, 0u>(acc, red, out);
+  if (threadIdx.x < 2) part[blockIdx.x * 2 + threadIdx.x] = out[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double a2[2] = {0.0, 0.0};
+  for (int b = threadIdx.x; b < gridDim.x; b += kBlock) {
+    a2[0] += __ldcg(part + 2 * b);
+    a2[1] += __ldcg(part + 2 * b + 1);
+  }
+  block_reduce<2, 0u>(a2, red, out);
+  if (threadIdx.x == 0) {
+    const double norm = sqrt(out[0]);
+    if (norm == 0.0) {
+      pc->zero = 1;
+    } else {
+      pc->lambda = out[1];
+      pc->nu = norm;
+    }
+    *counter = 0u;
+  }
+}
+
 // ---- deterministic reductions over a vector --------------------------------
 // mode 0: sum a[i]^2      mode 1: sum (a[i]*b[i])^2      mode 2: sum a[i]*b[i]
 __global__ void __launch_bounds__(kBlock) k_reduce(const double* __restrict__ a, const double* __restrict__ b,

@@ -117,6 +117,8 @@ def load_library(path: str = LIB_PATH):
         L.cclp_cu_stream.restype = C.c_void_p
         L.cclp_cu_stream.argtypes = [C.c_void_p]
         L.cclp_cu_describe.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]
+        L.cclp_cu_gaussian_start.argtypes = [C.c_uint64, C.c_int64, _dp]
+        L.cclp_cu_gaussian_start.restype = None
         _lib = L
         return L
 
@@ -126,8 +128,13 @@ EXPORTED_SYMBOLS = [
     "cclp_cu_default_tolerances", "cclp_cu_create", "cclp_cu_destroy", "cclp_cu_solve",
     "cclp_cu_run_pdhg", "cclp_cu_matvec", "cclp_cu_matvec_transpose", "cclp_cu_ruiz",
     "cclp_cu_estimate_norm", "cclp_cu_begin", "cclp_cu_advance", "cclp_cu_profile_kernels",
-    "cclp_cu_stream", "cclp_cu_describe",
+    "cclp_cu_stream", "cclp_cu_describe", "cclp_cu_gaussian_start",
 ]
+
+
+# Host phase timings reported by cclp_cu_describe (engine.cu, Context::phase).
+PHASES = ["upload", "csr_build", "partition_tune", "norms", "ruiz", "scale_values", "power_norm",
+          "init_check0", "graph_build", "loop", "result_download"]
 
 
 class PdhgStopReason(enum.IntEnum):
@@ -399,9 +406,19 @@ class Engine:
     def describe(self) -> dict:
         keys = ["m", "n", "nnz", "group_rows", "group_cols", "spmv_grid", "epi_grid", "launches",
                 "last_cols_body_ns", "last_finalize_ns"]
-        out = (C.c_int64 * len(keys))()
-        self.L.cclp_cu_describe(self.ctx, out, len(keys))
-        return dict(zip(keys, list(out)))
+        out = (C.c_int64 * (len(keys) + len(PHASES)))()
+        self.L.cclp_cu_describe(self.ctx, out, len(out))
+        d = dict(zip(keys, list(out)))
+        d["phase_seconds"] = {k: out[len(keys) + i] * 1e-9 for i, k in enumerate(PHASES)}
+        return d
+
+
+def gaussian_start(seed: int, n: int) -> np.ndarray:
+    """The power iteration's start vector (pdhg.cpp:49-52), host-side."""
+    L = load_library()
+    v = np.empty(n)
+    L.cclp_cu_gaussian_start(seed, n, v.ctypes.data_as(_dp))
+    return v
 
 
 def run_pdhg(std_lp: LinearProgram, config: Optional[PdhgConfig] = None,

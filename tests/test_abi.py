@@ -103,3 +103,16 @@ def test_no_cpu_fallback_in_product():
         if f.endswith(".py"):
             src = open(os.path.join(ROOT, "paper_2510_24429_b200", f)).read()
             assert "oracle" not in src.replace("# ", ""), f
+
+
+@pytest.mark.parametrize("seed,n", [(0, 1), (0, 7), (3, 1000), (12345, 200001)])
+def test_gaussian_start_matches_oracle(seed, n):
+    """The engine's two-stage start vector equals the oracle's sequential
+    mt19937_64 + normal_distribution restatement bit for bit (host only)."""
+    import numpy as np
+
+    from oracle.pyoracle import Restatement
+    from paper_2510_24429_b200.pdhg import gaussian_start
+    ours = gaussian_start(seed, n)
+    ref = Restatement().gaussian_start(seed, n)
+    assert np.array_equal(ours.view(np.uint64), ref.view(np.uint64))
