@@ -222,10 +222,24 @@ template <int G, class Gather>
 __device__ __forceinline__ void spmv_block_range(const int* __restrict__ start, const int* __restrict__ ptr,
                                                  const int* __restrict__ idx,
                                                  const double* __restrict__ val, const Gather& g,
-                                                 double* __restrict__ out) {
+                                                 double* __restrict__ out, int rpg = 1) {
   const int gl = threadIdx.x % G;
   const int gpb = blockDim.x / G;
   const int rb = start[blockIdx.x], re = start[blockIdx.x + 1];
+  if (rpg == 2) {  // two rows per group in flight: rows r and r + gpb of a 2*gpb round
+    for (int row = rb + static_cast<int>(threadIdx.x / G); row - static_cast<int>(threadIdx.x / G) < re;
+         row += 2 * gpb) {
+      const int row1 = row + gpb;
+      const bool ok0 = row < re, ok1 = row1 < re;
+      const int b0 = ok0 ? __ldg(ptr + row) : 0, e0 = ok0 ? __ldg(ptr + row + 1) : 0;
+      const int b1 = ok1 ? __ldg(ptr + row1) : 0, e1 = ok1 ? __ldg(ptr + row1 + 1) : 0;
+      double s0, s1;
+      group_dot2<G, 2>(b0, e0, b1, e1, gl, idx, val, g, s0, s1);
+      if (gl == 0 && ok0) out[row] = 0.0 + s0;
+      if (gl == 0 && ok1) out[row1] = 0.0 + s1;
+    }
+    return;
+  }
   for (int row = rb + static_cast<int>(threadIdx.x / G); row - static_cast<int>(threadIdx.x / G) < re;
        row += gpb) {
     const bool ok = row < re;
@@ -240,8 +254,8 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_range(const int* __restrict
                                                            const int* __restrict__ ptr,
                                                            const int* __restrict__ idx,
                                                            const double* __restrict__ val, Gather g,
-                                                           double* __restrict__ out) {
-  spmv_block_range<G>(start, ptr, idx, val, g, out);
+                                                           double* __restrict__ out, int rpg = 1) {
+  spmv_block_range<G>(start, ptr, idx, val, g, out, rpg);
 }
 
 template <int G>
@@ -249,7 +263,7 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows(const IterParams p, in
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
   spmv_block_range<G>(p.spmv_row_start, p.rowptr, p.colind, p.aval, GatherPlain{p.xc[si.xs][si.R]},
-                      p.ax[si.s1]);
+                      p.ax[si.s1], p.rpg_rows);
 }
 
 template <int G>
@@ -257,7 +271,7 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_cols(const IterParams p, in
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
   spmv_block_range<G>(p.spmv_col_start, p.colptr, p.rowind, p.atval, GatherPlain{p.y[si.s1]},
-                      p.aty[si.s1]);
+                      p.aty[si.s1], p.rpg_cols);
 }
 
 // Dual update + row-side report partials (one row per thread, coalesced).

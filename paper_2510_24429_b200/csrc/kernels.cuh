@@ -85,6 +85,7 @@ struct IterParams {
   int nthr;
   const double* thr;
   const unsigned long long* t0_ns;
+  int rpg_rows, rpg_cols;  // rows per lane group in flight in the SpMV (1 or 2)
 };
 
 // ---------------------------------------------------------------------------
@@ -158,6 +159,49 @@ __device__ __forceinline__ double group_dot(int beg, int end, int lane, const in
 #pragma unroll
   for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
   return acc;
+}
+
+// Two rows per G-lane group in flight: the same per-row, per-lane order as
+// group_dot (so bit-identical results), with both rows' loads and gathers
+// issued before either row's multiply-adds.
+template <int G, int U, class Gather>
+__device__ __forceinline__ void group_dot2(int b0, int e0, int b1, int e1, int lane,
+                                           const int* __restrict__ idx,
+                                           const double* __restrict__ val, const Gather& g,
+                                           double& s0, double& s1) {
+  double a0 = 0.0, a1 = 0.0;
+  for (int p0 = b0 + lane, p1 = b1 + lane; p0 < e0 || p1 < e1; p0 += G * U, p1 += G * U) {
+    int i0[U], i1[U];
+    double v0[U], v1[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int q0 = p0 + k * G, q1 = p1 + k * G;
+      const bool ok0 = q0 < e0, ok1 = q1 < e1;
+      i0[k] = ok0 ? __ldcs(idx + q0) : -1;
+      v0[k] = ok0 ? __ldcs(val + q0) : 0.0;
+      i1[k] = ok1 ? __ldcs(idx + q1) : -1;
+      v1[k] = ok1 ? __ldcs(val + q1) : 0.0;
+    }
+    double x0[U], x1[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      x0[k] = i0[k] >= 0 ? g(i0[k]) : 0.0;
+      x1[k] = i1[k] >= 0 ? g(i1[k]) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (i0[k] >= 0) a0 = a0 + v0[k] * x0[k];
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (i1[k] >= 0) a1 = a1 + v1[k] * x1[k];
+  }
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) {
+    a0 += __shfl_xor_sync(0xffffffffu, a0, off);
+    a1 += __shfl_xor_sync(0xffffffffu, a1, off);
+  }
+  s0 = a0;
+  s1 = a1;
 }
 
 // Barrier-free warp tiles shared by every "row" kernel. The block owns rows

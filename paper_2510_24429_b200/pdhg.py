@@ -404,7 +404,8 @@ class Engine:
         return int(self.L.cclp_cu_stream(self.ctx) or 0)
 
     def describe(self) -> dict:
-        keys = ["m", "n", "nnz", "group_rows", "group_cols", "spmv_grid", "epi_grid", "launches",
+        keys = ["m", "n", "nnz", "group_rows", "group_cols", "spmv_rows_grid_x10_rpg",
+                "spmv_cols_grid_x10_rpg", "launches",
                 "last_cols_body_ns", "last_finalize_ns"]
         out = (C.c_int64 * (len(keys) + len(PHASES)))()
         self.L.cclp_cu_describe(self.ctx, out, len(out))

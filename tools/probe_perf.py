@@ -1,47 +1,31 @@
-"""Quick performance probe (not the bench): C2 device loop, per-kernel times,
-time-to-tolerance, reference CPU timing."""
-import json
+"""Performance probe (not the bench): device loop rate and per-kernel times
+with algorithmic bytes, for one config."""
 import sys
 import time
 
-import numpy as np
-
 sys.path.insert(0, ".")
 from paper_2510_24429_b200 import lpgen  # noqa: E402
-from paper_2510_24429_b200.pdhg import Engine, PdhgConfig, Tolerances  # noqa: E402
+from paper_2510_24429_b200.pdhg import Engine, PdhgConfig  # noqa: E402
 
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "C2"
 t = time.time()
 lp = lpgen.make_config(cfgname)
-print("gen", cfgname, lp.m, lp.n, lp.nnz, f"{time.time()-t:.2f}s", flush=True)
-t = time.time()
+m, n, nnz = lp.m, lp.n, lp.nnz
+print("gen", cfgname, m, n, nnz, f"{time.time()-t:.2f}s", flush=True)
 eng = Engine(lp)
-print("create", f"{time.time()-t:.3f}s", eng.describe(), flush=True)
-t = time.time()
 eng.begin(PdhgConfig())
-print("begin", f"{time.time()-t:.3f}s", flush=True)
-eng.advance(200)
-for it in (1000, 1000):
-    ms = eng.advance(it)
-    print(f"advance {it}: {ms:.2f} ms -> {it/ms*1e3:.0f} it/s, {ms/it*1e3:.2f} us/it", flush=True)
-pk = eng.profile_kernels(200)
-print("kernels: " + ", ".join(f"{k} {v*1e3:.2f} us" for k, v in pk.items()), flush=True)
 d = eng.describe()
-print(f"last cols body (start->finalize) {d['last_cols_body_ns']/1e3:.2f} us, finalize {d['last_finalize_ns']/1e3:.2f} us", flush=True)
-nnz, m, n = lp.nnz, lp.m, lp.n
+print({k: v for k, v in d.items() if k != "phase_seconds"}, flush=True)
+eng.advance(100)
+its = max(50, int(2e11 / (24 * nnz)) // 10)
+ms = eng.advance(its)
 B = 24 * nnz + 20 * (m + n) + 8
-print(f"B_iter {B/1e6:.1f} MB; at advance rate: {B/(ms/it*1e-3)/1e9:.0f} GB/s", flush=True)
-for eps in ():
-    t = time.time()
-    res = eng.solve(PdhgConfig(max_iterations=200000), Tolerances(eps_rel=eps))
-    print(f"solve eps={eps}: stop={res.stop.name} it={res.iterations} restarts={res.restarts} "
-          f"wall={time.time()-t:.3f}s setup={res.setup_seconds:.3f}s loop={res.loop_seconds:.3f}s "
-          f"maxresid={res.report.maxresid_rel:.3e} obj={res.report.primal_objective:.10g}", flush=True)
+print(f"advance {its}: {ms/its*1e3:.2f} us/it, {its/ms*1e3:.0f} it/s, B_iter {B/1e6:.1f} MB "
+      f"-> {B/(ms/its*1e-3)/1e9:.0f} GB/s", flush=True)
+pk = eng.profile_kernels(50)
+kb = dict(spmv_rows=12 * nnz + 4 * (m + 1) + 8 * n + 8 * m,
+          spmv_cols=12 * nnz + 4 * (n + 1) + 8 * m + 8 * n,
+          dual=8 * m * 10, primal=8 * n * 12)
+for k, v in pk.items():
+    print(f"  {k:10s} {v*1e3:9.2f} us  {kb[k]/1e6:8.1f} MB  {kb[k]/(v*1e-3)/1e9:7.0f} GB/s", flush=True)
 eng.close()
-if len(sys.argv) > 2:
-    from oracle.pyoracle import Reference
-    R = Reference()
-    for S in (0, int(sys.argv[2])):
-        t = time.time()
-        r = R.run_pdhg(lp, config=dict(max_iterations=S))
-        print(f"ref max_iter={S}: {time.time()-t:.2f}s stop={r['stop']} it={r['iterations']}", flush=True)
