@@ -218,59 +218,86 @@ __device__ void finalize(const IterParams& p, const StepInfo& si) {
 // depends only on G, never on the launch geometry, so the geometry can be
 // autotuned without changing a bit of the result; G = 1 sums each row in the
 // reference's own order.
-template <int G, class Gather>
-__device__ __forceinline__ void spmv_block_range(const int* __restrict__ start, const int* __restrict__ ptr,
+template <int G, bool LONG, class Gather>
+__device__ __forceinline__ void spmv_block_range(const SpmvPlan& P, const int* __restrict__ ptr,
                                                  const int* __restrict__ idx,
                                                  const double* __restrict__ val, const Gather& g,
                                                  double* __restrict__ out, int rpg = 1) {
   const int gl = threadIdx.x % G;
   const int gpb = blockDim.x / G;
-  const int rb = start[blockIdx.x], re = start[blockIdx.x + 1];
+  const int rb = P.start[blockIdx.x], re = P.start[blockIdx.x + 1];
+  const int thr = LONG ? P.thr : 0x7fffffff;
   if (rpg == 2) {  // two rows per group in flight: rows r and r + gpb of a 2*gpb round
     for (int row = rb + static_cast<int>(threadIdx.x / G); row - static_cast<int>(threadIdx.x / G) < re;
          row += 2 * gpb) {
       const int row1 = row + gpb;
-      const bool ok0 = row < re, ok1 = row1 < re;
-      const int b0 = ok0 ? __ldg(ptr + row) : 0, e0 = ok0 ? __ldg(ptr + row + 1) : 0;
-      const int b1 = ok1 ? __ldg(ptr + row1) : 0, e1 = ok1 ? __ldg(ptr + row1 + 1) : 0;
+      bool ok0 = row < re, ok1 = row1 < re;
+      int b0 = ok0 ? __ldg(ptr + row) : 0, e0 = ok0 ? __ldg(ptr + row + 1) : 0;
+      int b1 = ok1 ? __ldg(ptr + row1) : 0, e1 = ok1 ? __ldg(ptr + row1 + 1) : 0;
+      if (LONG && e0 - b0 > thr) ok0 = false, e0 = b0;  // long row: summed by segments
+      if (LONG && e1 - b1 > thr) ok1 = false, e1 = b1;
       double s0, s1;
       group_dot2<G, 2>(b0, e0, b1, e1, gl, idx, val, g, s0, s1);
       if (gl == 0 && ok0) out[row] = 0.0 + s0;
       if (gl == 0 && ok1) out[row1] = 0.0 + s1;
     }
-    return;
+  } else {
+    for (int row = rb + static_cast<int>(threadIdx.x / G); row - static_cast<int>(threadIdx.x / G) < re;
+         row += gpb) {
+      bool ok = row < re;
+      int b = ok ? __ldg(ptr + row) : 0, e = ok ? __ldg(ptr + row + 1) : 0;
+      if (LONG && e - b > thr) ok = false, e = b;
+      const double s = group_dot<G, 4>(b, e, gl, idx, val, g);
+      if (gl == 0 && ok) out[row] = 0.0 + s;
+    }
   }
-  for (int row = rb + static_cast<int>(threadIdx.x / G); row - static_cast<int>(threadIdx.x / G) < re;
-       row += gpb) {
-    const bool ok = row < re;
-    const int b = ok ? __ldg(ptr + row) : 0, e = ok ? __ldg(ptr + row + 1) : 0;
-    const double s = group_dot<G, 4>(b, e, gl, idx, val, g);
-    if (gl == 0 && ok) out[row] = 0.0 + s;
+  if (!LONG) return;
+  // long-row segments: one warp per segment, 32 lanes strided, then combine
+  const int lane = threadIdx.x & 31;
+  const int sb = P.start[P.grid + 1 + blockIdx.x], se = P.start[P.grid + 2 + blockIdx.x];
+  for (int k = sb + static_cast<int>(threadIdx.x >> 5); k < se; k += static_cast<int>(blockDim.x >> 5)) {
+    const int4 sg = P.seg[k];  // row, begin, end, long-row index
+    const double s = group_dot<32, 4>(sg.y, sg.z, lane, idx, val, g);
+    if (lane == 0) {
+      const int f0 = __ldg(P.lr_first + sg.w), f1 = __ldg(P.lr_first + sg.w + 1);
+      if (f1 - f0 == 1) {  // a single-segment row: no combine
+        out[sg.x] = 0.0 + s;
+      } else {
+        P.part[k] = s;
+        __threadfence();
+        if (atomicAdd(P.cnt + sg.w, 1u) == static_cast<unsigned>(f1 - f0 - 1)) {
+          __threadfence();
+          double acc = 0.0;
+          for (int q = f0; q < f1; ++q) acc = acc + __ldcg(P.part + q);
+          out[sg.x] = 0.0 + acc;
+          P.cnt[sg.w] = 0u;
+        }
+      }
+    }
   }
 }
 
-template <int G, class Gather>
-__global__ void __launch_bounds__(kSpmvBlock) k_spmv_range(const int* __restrict__ start,
-                                                           const int* __restrict__ ptr,
+template <int G, bool LONG, class Gather>
+__global__ void __launch_bounds__(kSpmvBlock) k_spmv_range(const SpmvPlan P, const int* __restrict__ ptr,
                                                            const int* __restrict__ idx,
                                                            const double* __restrict__ val, Gather g,
                                                            double* __restrict__ out, int rpg = 1) {
-  spmv_block_range<G>(start, ptr, idx, val, g, out, rpg);
+  spmv_block_range<G, LONG>(P, ptr, idx, val, g, out, rpg);
 }
 
-template <int G>
+template <int G, bool LONG>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
-  spmv_block_range<G>(p.spmv_row_start, p.rowptr, p.colind, p.aval, GatherPlain{p.xc[si.xs][si.R]},
+  spmv_block_range<G, LONG>(p.plan_r, p.rowptr, p.colind, p.aval, GatherPlain{p.xc[si.xs][si.R]},
                       p.ax[si.s1], p.rpg_rows);
 }
 
-template <int G>
+template <int G, bool LONG>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_cols(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
-  spmv_block_range<G>(p.spmv_col_start, p.colptr, p.rowind, p.atval, GatherPlain{p.y[si.s1]},
+  spmv_block_range<G, LONG>(p.plan_c, p.colptr, p.rowind, p.atval, GatherPlain{p.y[si.s1]},
                       p.aty[si.s1], p.rpg_cols);
 }
 

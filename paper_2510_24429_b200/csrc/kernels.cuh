@@ -39,6 +39,28 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 }
 
 // ---------------------------------------------------------------------------
+// Work plan of one SpMV side (A or A^T) for a given launch geometry. Block b
+// owns rows [start[b], start[b+1]) and long-row segments [start[grid+1+b],
+// start[grid+2+b]). Rows longer than `thr` nonzeros are not summed by their
+// lane group: they are cut into fixed kSegLen-element segments (a function of
+// the matrix alone, so the result never depends on the geometry), each summed
+// by a full warp; the last segment of a row to finish adds the segment sums in
+// segment order (deterministic). The unified row+segment sequence is split by
+// weight, so power-law row lengths stay balanced (merge-path in spirit).
+// ---------------------------------------------------------------------------
+constexpr int kSegLen = 4096;
+
+struct SpmvPlan {
+  const int* start;     // [2 * (grid + 1)]
+  const int4* seg;      // [nseg]: row, begin, end, long-row index
+  const int* lr_first;  // [nlong + 1]: first segment of each long row
+  double* part;         // [nseg] segment sums
+  unsigned* cnt;        // [nlong] finished segments per long row (self-resetting)
+  int thr;              // rows with more nonzeros are segmented (INT_MAX: none)
+  int grid;
+};
+
+// ---------------------------------------------------------------------------
 // Parameters of the fused iteration kernels (passed by value, captured into
 // CUDA graphs once per solve).
 // ---------------------------------------------------------------------------
@@ -56,9 +78,8 @@ struct IterParams {
   const int* row_start;
   const int* col_start;
   int row_grid, col_grid;
-  // contiguous row ranges of the iteration SpMV kernels (autotuned grids)
-  const int* spmv_row_start;
-  const int* spmv_col_start;
+  // work plans of the iteration SpMV kernels (autotuned grids)
+  SpmvPlan plan_r, plan_c;
   // unscaled problem data and Ruiz factors
   const double *c, *l, *u, *b, *r, *s;
   // state

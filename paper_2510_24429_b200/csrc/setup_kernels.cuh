@@ -43,6 +43,12 @@ __global__ void k_gather_csr(const int* __restrict__ perm, long long nnz,
   }
 }
 
+// Number of rows with more than `thr` nonzeros.
+__global__ void k_count_long(const int* __restrict__ ptr, int rows, int thr, int* count) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)
+    if (ptr[i + 1] - ptr[i] > thr) atomicAdd(count, 1);
+}
+
 // Block b owns rows [start[b], start[b+1]) with ~equal weight
 // w(i) = ptr[i] + alpha * i (nonzeros plus a per-row epilogue cost).
 __global__ void k_partition(const int* __restrict__ ptr, int rows, int grid, long long alpha,
@@ -75,15 +81,6 @@ __global__ void __launch_bounds__(kBlock) k_spmv(const int* __restrict__ ptr, co
   warp_tiles<G>(start[blockIdx.x], start[blockIdx.x + 1], ptr, idx, val, g, wsum + (threadIdx.x & ~31),
                 NoPre{}, [&](int i, double s, int) { out[i] = 0.0 + s; });
 }
-
-// Plain y = M v over contiguous block row ranges (the iteration SpMV's
-// geometry; used to autotune it).
-template <int G, class Gather>
-__global__ void __launch_bounds__(kSpmvBlock) k_spmv_range(const int* __restrict__ start,
-                                                           const int* __restrict__ ptr,
-                                                           const int* __restrict__ idx,
-                                                           const double* __restrict__ val, Gather g,
-                                                           double* __restrict__ out);
 
 // ---- power iteration (estimate_matrix_norm, pdhg.cpp:46-65) ---------------
 struct PowerCtrl {

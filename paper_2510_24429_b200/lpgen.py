@@ -261,6 +261,53 @@ def staircase_lp(stages: int = 1000, cols_per_stage: int = 10_000, rows_per_stag
                           f"staircase_{T}x{nc}")
 
 
+def powerlaw_lp(m: int = 10_000_000, n: int = 50_000_000, nnz: int = 500_000_000,
+                alpha: float = 1.8, min_len: int = 8, max_len: int | None = None, seed: int = 5):
+    """C5: power-law row lengths: row lengths follow a
+    truncated Pareto law with exponent `alpha` (P(L >= k) ~ k^(1-alpha), from
+    `min_len` up to `max_len`, default n/50), rescaled to `nnz` in total;
+    columns uniform (distinct within a row), values U(-2,2). Known optimum as
+    in C2 (test_util.hpp:71-112): the m support columns perm[:m] carry a
+    band-diagonal U(2,3) entry at their own row. One int64 sort of the keys
+    col*m + row gives the CSC directly. Returns (lp, x*, y*, z*)."""
+    rng = np.random.default_rng(seed)
+    max_len = max_len or max(min_len + 1, n // 50)
+    u = rng.random(m)
+    L = min_len * u ** (-1.0 / (alpha - 1.0))
+    L = np.minimum(L, max_len)
+    L = np.maximum(1, np.rint(L * ((nnz - m) / L.sum()))).astype(np.int64)
+    L = np.minimum(L, max_len)
+    diff = (nnz - m) - int(L.sum())  # exact total: spread the residual over rows
+    if diff != 0:
+        idx = rng.choice(m, size=abs(diff), replace=abs(diff) > m)
+        np.add.at(L, idx, 1 if diff > 0 else -1)
+        L = np.maximum(L, 1)
+    perm = rng.permutation(n)
+    support = perm[:m]
+    rows = np.repeat(np.arange(m, dtype=np.int64), L)
+    cols = rng.integers(0, n, size=rows.size, dtype=np.int64)
+    # key*2 + flag: the diagonal entry (flag 0) sorts first among equal keys
+    keys = np.concatenate([(cols * m + rows) * 2 + 1,
+                           (support.astype(np.int64) * m + np.arange(m)) * 2])
+    del rows, cols
+    keys.sort(kind="stable")
+    first = np.ones(keys.size, dtype=bool)
+    first[1:] = (keys[1:] >> 1) != (keys[:-1] >> 1)
+    keys = keys[first]
+    is_diag = (keys & 1) == 0
+    keys >>= 1
+    rowind = (keys % m).astype(np.int32)
+    col_of = keys // m
+    del keys
+    colptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(col_of, minlength=n), out=colptr[1:])
+    del col_of
+    vals = _nonzero_uniform(rng, rowind.size)
+    nd = int(is_diag.sum())
+    vals[is_diag] = np.where(rng.random(nd) < 0.5, -1.0, 1.0) * rng.uniform(2.0, 3.0, size=nd)
+    return _known_optimum(colptr, rowind, vals, m, n, support, rng, f"powerlaw_{m}x{n}")
+
+
 CONFIGS = {
     "C1": dict(kind="transportation", sources=200, sinks=500, seed=1),
     "C2": dict(kind="random", m=100_000, n=500_000, nnz_per_col=10, seed=2),
@@ -268,6 +315,10 @@ CONFIGS = {
                side_per_var=7, seed=3),
     "C4": dict(kind="staircase", stages=1000, cols_per_stage=10_000, rows_per_stage=5_000,
                own_per_col=6, next_per_col=4, seed=4),
+    "C5": dict(kind="powerlaw", m=10_000_000, n=50_000_000, nnz=500_000_000, seed=5),
+    # C5 at 1/10 and 1/100 scale: the same row-length law for tests and probes
+    "C5s": dict(kind="powerlaw", m=1_000_000, n=5_000_000, nnz=50_000_000, seed=5),
+    "C5xs": dict(kind="powerlaw", m=100_000, n=500_000, nnz=5_000_000, seed=5),
 }
 
 
@@ -282,4 +333,6 @@ def make_config(name: str) -> LinearProgram:
         return multicommodity_lp(**spec)
     if kind == "staircase":
         return staircase_lp(**spec)[0]
+    if kind == "powerlaw":
+        return powerlaw_lp(**spec)[0]
     raise KeyError(name)
