@@ -15,7 +15,11 @@ are all inside the timed region. The working set (~180 MB) exceeds the
 
 Multi-GPU (torchrun, N>1): C2 fits one GPU, so ranks run independent
 replicas ("replicas only" for C1-C3); value sums iterations over
-ranks, time is the max over ranks.
+ranks, time is the max over ranks. `--workload C4|C5|C5s` with N>1 runs the
+row-block sharded solve instead (one shard per rank, NCCL all-gathers of y,
+x and the report sums each iteration; iterates bit-identical to one GPU):
+value = iterations/s of that one solve (strong scaling), device time max
+over ranks.
 
 `--impl reference` times the reference's own run_pdhg (oracle/_ref, built
 from /root/reference's sources) on the host cores of rank 0.
@@ -221,6 +225,66 @@ def run_reference_arm(args, world, rank, pg):
     print(json.dumps(line), flush=True)
 
 
+SHARDED_WORKLOADS = ("C3", "C4", "C5", "C5s")
+
+
+def metric_for(workload: str) -> str:
+    if workload == CONFIG_NAME:
+        return METRIC
+    return f"PDHG iterations/s ({workload} synthetic LP, fp64, check every iteration)"
+
+
+def run_sharded_arm(args, world, rank, local, pg):
+    """N ranks, one row-block shard each (cclp_cu_sharded over NCCL)."""
+    import torch
+    from paper_2510_24429_b200 import lpgen
+    from paper_2510_24429_b200.pdhg import PdhgConfig, ShardedEngine, nccl_unique_id
+
+    dev = torch.device("cuda", local)
+    idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        idt.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    pg.broadcast(idt, src=0)
+    nccl_id = bytes(idt.cpu().numpy().tobytes())
+    lp = lpgen.make_config(args.workload)
+    eng = ShardedEngine(lp, 1, device=local, rank=rank, nranks=world, nccl_id=nccl_id)
+    eng.begin(PdhgConfig())
+    K, W, I = args.steps, args.warmup, args.iters_per_step
+    for _ in range(W):
+        eng.advance(I)
+    torch.cuda.synchronize(dev)
+    barrier(pg)
+    with ClockSampler(local) as clk:
+        dev_ms = sum(eng.advance(I) for _ in range(K))
+    barrier(pg)
+    t_max = allreduce_max(pg, dev_ms, dev)
+    d = eng.describe()
+    eng.close()
+    value = K * I / (t_max * 1e-3)
+    B = 24 * lp.nnz + 20 * (lp.m + lp.n) + 8
+    peak, peak_kind = measured_peak_gbs()
+    if rank == 0:
+        line = {
+            "metric": metric_for(args.workload), "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": t_max / K, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded generator, paper_2510_24429_b200/lpgen.py)",
+            "config": {"workload": args.workload, "m": lp.m, "n": lp.n, "nnz": lp.nnz,
+                       "iters_per_step": I, "check_interval": 1,
+                       "parallelism": f"row-block sharded x{world} (NCCL all-gather)",
+                       "row_bounds": d["row_bounds"], "col_bounds": d["col_bounds"],
+                       "l2": "matrix >> 126 MB L2, no flush"},
+            "us_per_iteration": t_max * 1e3 / (K * I),
+            "roofline": {"bound": "hbm", "achieved": B * value / 1e9 / world, "peak": peak,
+                         "unit": "GB/s", "frac": B * value / 1e9 / world / peak,
+                         "traffic": None, "kernel": "whole iteration, per GPU",
+                         "bytes_per_launch": B, "peak_kind": peak_kind},
+            "gpu_launches": int(d["launches"]),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -233,12 +297,18 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=20)
     ap.add_argument("--cpu-iters", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default=CONFIG_NAME,
+                    help="C2 (default, configs[1]); C3/C4/C5/C5s: with N>1 the sharded solve")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     world, rank, local, pg = dist_setup(args)
     if args.impl == "reference":
         run_reference_arm(args, world, rank, pg)
+        return
+    if world > 1 and args.workload in SHARDED_WORKLOADS:
+        run_sharded_arm(args, world, rank, local, pg)
+        pg.destroy_process_group()
         return
 
     import torch
@@ -247,7 +317,7 @@ def main():
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    lp = lpgen.make_config(CONFIG_NAME)
+    lp = lpgen.make_config(args.workload)
     eng = Engine(lp, device=local)
     eng.begin(PdhgConfig())
     stream = torch.cuda.ExternalStream(eng.stream_ptr(), device=dev)
@@ -284,7 +354,7 @@ def main():
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(CONFIG_NAME, {}).get("k_spmv_" + dom)
+            traffic = json.load(f).get(args.workload, {}).get("k_spmv_" + dom)
     except Exception:
         pass
     iter_us = dev_ms * 1e3 / (K * I)
@@ -310,7 +380,7 @@ def main():
 
     # time to tolerance (one solve, rank 0)
     ttt = None
-    if rank == 0:
+    if rank == 0 and lp.nnz <= 25_000_000:  # ~1 s on C2; C4/C5 would take minutes
         t = time.perf_counter()
         r4 = run_pdhg(plp, PdhgConfig(max_iterations=200000),
                       tol=Tolerances(eps_rel=1e-4),
@@ -320,19 +390,20 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cb = cpu_reference_rate(lp, args.cpu_iters)
+        cpu_iters = max(3, int(args.cpu_iters * 5_000_000 / max(lp.nnz, 1)))
+        cb = cpu_reference_rate(lp, cpu_iters)
         cpu = {"value": cb["value"], "unit": UNIT, "cores": 1, "kind": cb["kind"],
-               "sample": f"C2, run_pdhg(max_iterations={args.cpu_iters}) minus "
+               "sample": f"{args.workload}, run_pdhg(max_iterations={cpu_iters}) minus "
                          f"run_pdhg(max_iterations=0) ({cb['setup_s']:.2f} s setup), 1 thread "
                          "(the reference loop is single-threaded)"}
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "metric": metric_for(args.workload), "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": t_max / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, paper_2510_24429_b200/lpgen.py)",
-            "config": {"workload": CONFIG_NAME, "m": lp.m, "n": lp.n, "nnz": lp.nnz,
+            "config": {"workload": args.workload, "m": lp.m, "n": lp.n, "nnz": lp.nnz,
                        "iters_per_step": I, "check_interval": 1,
                        "parallelism": "replicas" if world > 1 else "single",
                        "l2": "working set ~180 MB > 126 MB L2, no flush"},

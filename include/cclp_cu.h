@@ -41,6 +41,7 @@ extern "C" {
 #define CCLP_CU_EINVAL 1
 #define CCLP_CU_ECUDA 2
 #define CCLP_CU_ENOMEM 3
+#define CCLP_CU_ENCCL 4
 
 /* PdhgStopReason (pdhg.hpp:44-51), same order. */
 #define CCLP_CU_STOP_CONVERGED 0
@@ -182,6 +183,38 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out);
 void* cclp_cu_stream(cclp_cu_ctx* ctx);
 /* Static description: nnz, CSR/CSC group sizes, grid sizes, bytes/iteration. */
 int cclp_cu_describe(cclp_cu_ctx* ctx, int64_t* out, int32_t nout);
+
+/* ---- sharded solve: row-block partition over several GPUs --
+ * A is split by rows and A' (the CSC) by columns into P nnz-balanced blocks;
+ * each shard computes its rows of A x and A' y completely (no cross-shard
+ * sums: iterates bit-identical to one GPU) and all-gathers y, the 22 report
+ * sums and x once per iteration. Two transports behind one API:
+ *   nccl_id NULL: `nshards` shards in this process on `device`, exchanging
+ *                by device copies (development and tests on one GPU);
+ *   nccl_id set: NCCL, this process is `rank` of `nranks` (one GPU each,
+ *                nshards = 1); `nccl_id` = the 128-byte id from
+ *                cclp_cu_nccl_unique_id on rank 0, broadcast by the caller
+ *                (nranks may be 1: the collective path on one GPU).
+ * Every rank passes the full LP and receives the full result. The run_pdhg
+ * setup (Ruiz, ||A||) is replicated per rank; the iteration is sharded. */
+typedef struct cclp_cu_sharded cclp_cu_sharded;
+int cclp_cu_nccl_unique_id(uint8_t* out128);
+int cclp_cu_sharded_create(const cclp_cu_lp* lp, int device, int32_t nshards, int32_t rank,
+                           int32_t nranks, const uint8_t* nccl_id, cclp_cu_sharded** out);
+int cclp_cu_sharded_solve(cclp_cu_sharded* ctx, const cclp_cu_config* cfg,
+                          const cclp_cu_tolerances* tol, const double* thresholds, int32_t nthr,
+                          cclp_cu_sink_fn sink, void* sink_user, const volatile uint8_t* cancel,
+                          double* x_out, double* y_out, double* z_out, cclp_cu_result* res);
+/* measurement hooks, as cclp_cu_begin / cclp_cu_advance */
+int cclp_cu_sharded_begin(cclp_cu_sharded* ctx, const cclp_cu_config* cfg,
+                          const cclp_cu_tolerances* tol);
+int cclp_cu_sharded_advance(cclp_cu_sharded* ctx, int64_t iters, double* device_ms);
+/* out: P, then row bounds [P+1], then column bounds [P+1] */
+int cclp_cu_sharded_describe(cclp_cu_sharded* ctx, int64_t* out, int32_t nout);
+int cclp_cu_sharded_destroy(cclp_cu_sharded* ctx);
+/* The nnz-balanced split used for the shards (host only): part b starts at
+ * the first i with ptr[i] + 4 i >= (ptr[rows] + 4 rows) b / parts. */
+int cclp_cu_partition(const int32_t* ptr, int32_t rows, int32_t parts, int32_t* bounds);
 
 #ifdef __cplusplus
 }

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB = os.path.join(HERE, "libcclp_cuda.so")
 SOURCES = ["csrc/engine.cu"]
 HEADERS = ["csrc/engine.cuh", "csrc/kernels.cuh", "csrc/iter_kernels.cuh",
-           "csrc/setup_kernels.cuh", "../include/cclp_cu.h"]
+           "csrc/setup_kernels.cuh", "csrc/sharded.cuh", "../include/cclp_cu.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

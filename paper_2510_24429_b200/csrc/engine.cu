@@ -178,7 +178,7 @@ struct Context {
   double *r = nullptr, *s = nullptr;
   bool equality = true;
   // partitions
-  int Grow = 1, Gcol = 1, row_grid = 1, col_grid = 1;
+  int Grow = 0, Gcol = 0, row_grid = 1, col_grid = 1;  // G = 0: pick from the mean row length
   int spmv_grid_r = 1, spmv_grid_c = 1, epi_grid = 1;
   int rpg_r = 1, rpg_c = 1;  // SpMV rows per lane group in flight (tuned)
   struct SidePlan {  // long-row segments of one SpMV side (SpmvPlan)
@@ -275,9 +275,24 @@ struct Context {
   void ruiz(int iterations);
   double power_norm(int iterations, uint64_t seed, bool scaled, bool pregenerated = false);
   double* h_v0 = nullptr;  // pinned start vector of the power iteration
+  // ---- sharded mode (sharded.cuh): this context is shard `shard_rank` of
+  // `shard_count`, owning rows [r0, r0 + m) of A and columns [c0, c0 + n)
+  bool own_stream = true;
+  int shard_rank = 0, shard_count = 1, r0 = 0, c0 = 0, Sm = 0, Sn = 0;
+  double* x_full = nullptr;  // [P * Sn] padded full x (gather source of the row SpMV)
+  double* y_full = nullptr;  // [P * Sm] padded full y (gather source of the column SpMV)
+  double* xpart = nullptr;   // [P][kRowParts + kColParts] exchanged report sums
+  double* vparts = nullptr;  // [kRowParts + kColParts] report sums of the last view
+  void setup(const cclp_cu_config& cfg);
+  void init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thresholds,
+                  int nthr, bool launch_init);
+  void shard_from(Context& F, int rank, int P, const std::vector<int>& rb, const std::vector<int>& cb,
+                  cudaStream_t shared);
   void begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thresholds,
              int nthr);
   void launch_iteration(bool init);
+  void launch_rows_half(bool init);  // k_spmv_rows + k_dual
+  void launch_cols_half(bool init);  // k_spmv_cols + k_primal
   void build_graph(int k);
   void fetch_ctrl(Ctrl* dst);
   void extract_view(int view, const Ctrl& st, bool need_report);
@@ -291,7 +306,8 @@ Context::~Context() {
                     r, s, row_start, col_start, spmv_row_start, spmv_col_start, rowp, colp, work_part,
                     counter, ctrl, log, thr, t0, scalars, pctrl, iflags, amb_idx, wn, wn2, wm, vx, vy,
                     vz, vrep, plan_rows.seg, plan_rows.lr_first, plan_rows.part, plan_rows.cnt,
-                    plan_cols.seg, plan_cols.lr_first, plan_cols.part, plan_cols.cnt};
+                    plan_cols.seg, plan_cols.lr_first, plan_cols.part, plan_cols.cnt, x_full, y_full,
+                    xpart, vparts};
     for (void* p : ptrs) release(p);
     for (int k = 0; k < 3; ++k)
       for (int q = 0; q < 2; ++q) release(xc[k][q]);
@@ -308,7 +324,7 @@ Context::~Context() {
   if (ev_snap) cudaEventDestroy(ev_snap);
   if (ev_a) cudaEventDestroy(ev_a);
   if (ev_b) cudaEventDestroy(ev_b);
-  if (stream) cudaStreamDestroy(stream);
+  if (stream && own_stream) cudaStreamDestroy(stream);
   if (side) cudaStreamDestroy(side);
 }
 
@@ -392,8 +408,8 @@ void Context::build_csr() {
 }
 
 void Context::partition() {
-  Grow = pick_group(nnz, m);
-  Gcol = pick_group(nnz, n);
+  if (Grow == 0) Grow = pick_group(nnz, m);
+  if (Gcol == 0) Gcol = pick_group(nnz, n);
   // Setup kernels use nnz-balanced row ranges of `row_grid` / `col_grid`
   // blocks. The iteration's SpMV kernels run one full wave of resident
   // blocks (grid-stride over rows); the epilogues one wave of kEpiBlock-thread
@@ -559,12 +575,12 @@ void Context::tune_spmv() {
     if (rows_side) {
       with_group_long(grow(), lng, [&](auto g, auto l) {
         k_spmv_range<decltype(g)::value, decltype(l)::value><<<grid, kSpmvBlock, 0, stream>>>(
-            P, rowptr, colind, val_csr, GatherPlain{wn}, wm, rpg);
+            P, rowptr, colind, val_csr, GatherPlain{x_full ? x_full : wn}, wm, rpg);
       });
     } else {
       with_group_long(gcol(), lng, [&](auto g, auto l) {
         k_spmv_range<decltype(g)::value, decltype(l)::value><<<grid, kSpmvBlock, 0, stream>>>(
-            P, colptr, rowind, val_csc, GatherPlain{wm}, wn, rpg);
+            P, colptr, rowind, val_csc, GatherPlain{y_full ? y_full : wm}, wn, rpg);
       });
     }
     CKL("tune spmv");
@@ -793,17 +809,27 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
   return std::sqrt(std::max(pc.lambda, 0.0));
 }
 
-void Context::launch_iteration(bool init) {
+void Context::launch_rows_half(bool init) {
   const IterParams& p = params;
   const int ii = init ? 1 : 0;
   with_group_long(grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
     launch_pdl(k_spmv_rows<decltype(g)::value, decltype(l)::value>, spmv_grid_r, kSpmvBlock, stream, p, ii);
   });
   launch_pdl(k_dual, epi_grid, kEpiBlock, stream, p, ii);
+}
+
+void Context::launch_cols_half(bool init) {
+  const IterParams& p = params;
+  const int ii = init ? 1 : 0;
   with_group_long(gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
     launch_pdl(k_spmv_cols<decltype(g)::value, decltype(l)::value>, spmv_grid_c, kSpmvBlock, stream, p, ii);
   });
   launch_pdl(k_primal, epi_grid, kEpiBlock, stream, p, ii);
+}
+
+void Context::launch_iteration(bool init) {
+  launch_rows_half(init);
+  launch_cols_half(init);
   launches += kKernelsPerIteration;
 }
 
@@ -833,6 +859,12 @@ void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
   }
   k_stamp<<<1, 1, 0, stream>>>(t0);
   CKL("stamp");
+  setup(cfg);
+  init_state(cfg, tol, thresholds, nthr, true);
+}
+
+// Scaling, norms, ||A|| and the step sizes (pdhg.cpp:245-267).
+void Context::setup(const cclp_cu_config& cfg) {
   phase_t0 = std::chrono::steady_clock::now();
   // the power iteration's start vector is host work: overlap it with the
   // device-side norms, Ruiz passes and value scaling
@@ -869,7 +901,12 @@ void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
   }
   tau = cfg.step_scale * omega / a_norm;
   sigma = cfg.step_scale / (omega * a_norm);
+}
 
+// State buffers, control block, x_0 and (optionally) the initial products
+// and check(0) (make_initial_state, pdhg.cpp:67-82; the first check block).
+void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
+                         const double* thresholds, int nthr, bool launch_init) {
   // state buffers
   auto alloc_n = [&](double*& p) { if (!p) p = alloc<double>(n); };
   auto alloc_m = [&](double*& p) { if (!p) p = alloc<double>(m); };
@@ -928,8 +965,19 @@ void Context::begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
   p.b_norm = b_norm; p.c_norm = c_norm; p.time_limit = cfg.time_limit;
   p.max_iter = cfg.max_iterations; p.check_interval = cfg.check_interval;
   p.nthr = nthr; p.thr = thr; p.t0_ns = t0;
+  p.xg = nullptr; p.yg = nullptr; p.y_full_loc = nullptr; p.xpart_loc = nullptr;
+  if (shard_count > 1 || x_full != nullptr) {  // sharded: gathers from the padded full vectors
+    p.xg = x_full;
+    p.yg = y_full;
+    p.y_full_loc = y_full + static_cast<size_t>(shard_rank) * Sm;
+    p.xpart_loc = xpart + shard_rank * (kRowParts + kColParts);
+    p.time_limit = INFINITY;  // checked on the host so every shard stops together
+    CK(cudaMemsetAsync(y_full, 0, sizeof(double) * std::max<size_t>(1, size_t(shard_count) * Sm), stream));
+    CK(cudaMemcpyAsync(x_full + static_cast<size_t>(shard_rank) * Sn, xc[0][0], sizeof(double) * n,
+                       cudaMemcpyDeviceToDevice, stream));
+  }
   // initial products and check(0)
-  launch_iteration(true);
+  if (launch_init) launch_iteration(true);
   if (graph) {
     cudaGraphExecDestroy(graph);
     graph = nullptr;
@@ -967,6 +1015,7 @@ void Context::extract_view(int view, const Ctrl& st, bool need_report) {
   v.colp = colp;
   v.counter = counter + 3;
   v.report = vrep;
+  v.parts_out = vparts;
   const int gr = blocks_for(m, kBlock, 148 * 4);
   const int gc = blocks_for(n, kBlock, 148 * 4);
   k_view_rows<<<gr, kBlock, 0, stream>>>(v);
@@ -977,6 +1026,8 @@ void Context::extract_view(int view, const Ctrl& st, bool need_report) {
 
 }  // namespace cclp_cu
 
+#include "sharded.cuh"
+
 using cclp_cu::Context;
 using cclp_cu::Ctrl;
 using cclp_cu::Error;
@@ -984,6 +1035,10 @@ using cclp_cu::g_err;
 
 struct cclp_cu_ctx {
   Context c;
+};
+
+struct cclp_cu_sharded {
+  cclp_cu::Sharded s;
 };
 
 namespace {
@@ -1008,10 +1063,10 @@ int guarded(F&& f) {
   }
 }
 
-void validate_inputs(const cclp_cu_ctx* ctx, const cclp_cu_config& cfg,
-                     const cclp_cu_tolerances& tol, const double* thr, int nthr) {
+void validate_inputs_eq(bool equality, const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
+                        const double* thr, int nthr) {
   // run_pdhg preconditions (pdhg.cpp:235-244, kkt.cpp:26-37)
-  if (!ctx->c.equality) throw std::invalid_argument("run_pdhg: LP must be in equality form");
+  if (!equality) throw std::invalid_argument("run_pdhg: LP must be in equality form");
   if (!(tol.decrement > 0.0 && tol.decrement < 1.0))
     throw std::invalid_argument("tolerances: decrement must be in (0,1)");
   if (!(tol.eps_rel > 0.0 && tol.eps_rel <= tol.eps_cross))
@@ -1022,6 +1077,11 @@ void validate_inputs(const cclp_cu_ctx* ctx, const cclp_cu_config& cfg,
       throw std::invalid_argument("run_pdhg: thresholds must be strictly decreasing");
   if (cfg.check_interval <= 0)  // modulo by zero in the reference (pdhg.cpp:311)
     throw std::invalid_argument("run_pdhg: check_interval must be positive");
+}
+
+void validate_inputs(const cclp_cu_ctx* ctx, const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
+                     const double* thr, int nthr) {
+  validate_inputs_eq(ctx->c.equality, cfg, tol, thr, nthr);
 }
 
 void copy_report(const double* src, cclp_cu_report* dst) {
@@ -1368,6 +1428,195 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
     res->loop_seconds = loop_ms * 1e-3;
     res->kernel_launches = C.launches;
     C.begun = false;
+  });
+}
+
+int cclp_cu_partition(const int32_t* ptr, int32_t rows, int32_t parts, int32_t* bounds) {
+  return guarded([&] {
+    if (ptr == nullptr || bounds == nullptr || rows < 0 || parts < 1)
+      throw std::invalid_argument("cclp_cu_partition: bad arguments");
+    cclp_cu::host_partition(ptr, rows, parts, 4, bounds);
+  });
+}
+
+int cclp_cu_nccl_unique_id(uint8_t* out128) {
+  return guarded([&] {
+    auto& api = cclp_cu::nccl();
+    if (!api.ok) throw Error(CCLP_CU_ENCCL, api.err);
+    ncclUniqueId id;
+    cclp_cu::nck(api.GetUniqueId(&id), "ncclGetUniqueId");
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int cclp_cu_sharded_create(const cclp_cu_lp* lp, int device, int32_t nshards, int32_t rank,
+                           int32_t nranks, const uint8_t* nccl_id, cclp_cu_sharded** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (lp == nullptr || lp->m < 0 || lp->n < 0 || lp->colptr == nullptr)
+      throw std::invalid_argument("cclp_cu_sharded_create: bad LP");
+    if (nranks < 1 || rank < 0 || rank >= nranks || nshards < 1)
+      throw std::invalid_argument("cclp_cu_sharded_create: bad rank / shard counts");
+    if (nranks > 1 && nccl_id == nullptr)
+      throw std::invalid_argument("cclp_cu_sharded_create: NCCL needs the unique id");
+    cclp_cu::ck(cudaSetDevice(device), "cudaSetDevice");
+    auto* ctx = new cclp_cu_sharded();
+    try {
+      ncclUniqueId id;
+      if (nccl_id) std::memcpy(&id, nccl_id, sizeof(id));
+      ctx->s.create(lp, device, nshards, rank, nranks, nccl_id ? &id : nullptr);
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
+int cclp_cu_sharded_destroy(cclp_cu_sharded* ctx) {
+  if (ctx) cudaSetDevice(ctx->s.device);
+  delete ctx;
+  return CCLP_CU_OK;
+}
+
+int cclp_cu_sharded_describe(cclp_cu_sharded* ctx, int64_t* out, int32_t nout) {
+  const auto& S = ctx->s;
+  std::vector<int64_t> v;
+  v.push_back(S.P);
+  for (int b : S.rb) v.push_back(b);
+  for (int b : S.cb) v.push_back(b);
+  v.push_back(S.launches);
+  for (int i = 0; i < nout && i < static_cast<int>(v.size()); ++i) out[i] = v[i];
+  return CCLP_CU_OK;
+}
+
+int cclp_cu_sharded_begin(cclp_cu_sharded* ctx, const cclp_cu_config* cfg, const cclp_cu_tolerances* tol) {
+  return guarded([&] {
+    auto& S = ctx->s;
+    cclp_cu::ck(cudaSetDevice(S.device), "cudaSetDevice");
+    validate_inputs_eq(S.full->equality, *cfg, *tol, nullptr, 0);
+    S.begin(*cfg, *tol, nullptr, 0);
+    for (auto& sh : S.shards) {  // measurement mode: never converge, never hit the limit
+      sh->params.eps_rel = -1.0;
+      sh->params.max_iter = (1LL << 62);
+    }
+    if (S.graph) {
+      cudaGraphExecDestroy(S.graph);
+      S.graph = nullptr;
+    }
+  });
+}
+
+int cclp_cu_sharded_advance(cclp_cu_sharded* ctx, int64_t iters, double* device_ms) {
+  return guarded([&] {
+    auto& S = ctx->s;
+    if (!S.begun) throw std::invalid_argument("cclp_cu_sharded_advance: call begin first");
+    Context& C = S.s0();
+    const int k = 16;
+    CK(cudaEventRecord(C.ev_a, S.stream));
+    long long done = 0;
+    while (done + k <= iters) {
+      S.run_batch(k);
+      done += k;
+    }
+    while (done < iters) {
+      S.launch_round(false);
+      ++done;
+    }
+    CK(cudaEventRecord(C.ev_b, S.stream));
+    CK(cudaEventSynchronize(C.ev_b));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, C.ev_a, C.ev_b));
+    if (device_ms) *device_ms = ms;
+  });
+}
+
+int cclp_cu_sharded_solve(cclp_cu_sharded* ctx, const cclp_cu_config* cfg_in, const cclp_cu_tolerances* tol,
+                          const double* thresholds, int32_t nthr, cclp_cu_sink_fn sink, void* sink_user,
+                          const volatile uint8_t* cancel, double* x_out, double* y_out, double* z_out,
+                          cclp_cu_result* res) {
+  return guarded([&] {
+    auto& S = ctx->s;
+    cclp_cu::ck(cudaSetDevice(S.device), "cudaSetDevice");
+    const cclp_cu_config cfg = *cfg_in;
+    validate_inputs_eq(S.full->equality, cfg, *tol, thresholds, nthr);
+    const auto wall0 = std::chrono::steady_clock::now();
+    S.launches = 0;
+    S.begin(cfg, *tol, thresholds, nthr);
+    const double setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    const int k = cfg.poll_interval > 0 ? cfg.poll_interval : 32;
+    S.build_graph(k);
+    Context& C0 = S.s0();
+    CK(cudaEventRecord(C0.ev_a, S.stream));
+    Ctrl st;
+    S.fetch_ctrl(&st);
+    std::vector<double> hx(S.n), hy(S.m), hz(S.n);
+    double sums[cclp_cu::kRowParts + cclp_cu::kColParts];
+    bool cancelled = false, timed_out = false;
+    while (true) {
+      if (st.halt && st.snap_pending) {  // PdhgSnapshot of the better view (pdhg.cpp:346-358)
+        S.assemble_view(st.snap_use_avg ? cclp_cu::kViewAvg : cclp_cu::kViewCur, st, hx.data(), hy.data(),
+                        hz.data(), sums);
+        if (sink) {
+          cclp_cu_snapshot sp;
+          sp.x = hx.data();
+          sp.y = hy.data();
+          sp.z = hz.data();
+          sp.m = S.m;
+          sp.n = S.n;
+          sp.threshold = thresholds[st.snap_thr_idx];
+          sp.maxresid = st.snap_maxresid;
+          sp.from_average = st.snap_use_avg;
+          sp.iteration = st.snap_iteration;
+          sink(&sp, sink_user);
+        }
+        S.clear_halt();
+        st.halt = 0;
+      }
+      if (st.stop >= 0) break;
+      if (cancel != nullptr && *cancel) {
+        cancelled = true;
+        break;
+      }
+      if (std::isfinite(cfg.time_limit) &&
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count() > cfg.time_limit) {
+        timed_out = true;
+        break;
+      }
+      S.run_batch(k);
+      S.fetch_ctrl(&st);
+    }
+    CK(cudaEventRecord(C0.ev_b, S.stream));
+    CK(cudaEventSynchronize(C0.ev_b));
+    float loop_ms = 0;
+    CK(cudaEventElapsedTime(&loop_ms, C0.ev_a, C0.ev_b));
+    int view = st.result_view;
+    int stop = st.stop;
+    bool rep_valid = st.result_report_valid != 0;
+    if (cancelled || timed_out) {
+      stop = cancelled ? CCLP_CU_STOP_CANCELLED : CCLP_CU_STOP_TIME_LIMIT;
+      view = cclp_cu::kViewCurEff;
+      rep_valid = st.checked != 0;
+      if (rep_valid) std::memcpy(st.result_report, st.R ? st.avg : st.cur, sizeof(st.result_report));
+    }
+    S.assemble_view(view, st, x_out, y_out, z_out, sums);
+    double rep[cclp_cu::kRepN];
+    cclp_cu::host_make_report(sums, sums + cclp_cu::kRowParts, C0.b_norm, C0.c_norm, rep);
+    res->stop = stop;
+    res->iterations = st.iteration;
+    res->restarts = st.restarts;
+    res->error_iteration = stop == CCLP_CU_STOP_NUMERICAL_ERROR ? st.error_iteration : -1;
+    copy_report(rep_valid ? st.result_report : rep, &res->report);
+    res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
+    res->norm_estimate = C0.norm_est;
+    res->omega = C0.omega;
+    res->tau = C0.tau;
+    res->sigma = C0.sigma;
+    res->setup_seconds = setup_s;
+    res->loop_seconds = loop_ms * 1e-3;
+    res->kernel_launches = S.launches;
+    S.begun = false;
   });
 }
 

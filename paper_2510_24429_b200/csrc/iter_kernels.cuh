@@ -166,28 +166,20 @@ __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, 
 
 static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied as 8-byte words");
 
-// Runs on the last block of k_cols: reduces every block's partials, then
-// decide() on a shared copy of the control block (one coalesced read and one
-// write instead of a chain of dependent global round trips).
-__device__ void finalize(const IterParams& p, const StepInfo& si) {
-  __shared__ double rowv[kRowParts];
-  __shared__ double colv[kColParts];
-  __shared__ Ctrl cs;
-  constexpr int kWords = sizeof(Ctrl) / 8;
-  long long* csw = reinterpret_cast<long long*>(&cs);
-  const long long* gw = reinterpret_cast<const long long*>(p.ctrl);
-  for (int w = threadIdx.x; w < kWords; w += kEpiBlock) csw[w] = __ldcg(gw + w);
-  // warp w reduces fields w, w+16, ... over all blocks: lane l takes blocks
-  // l, l+32, ...
-  // in order, then a fixed butterfly (deterministic, one round of loads).
+// Reduces every epilogue block's partials into rowv[kRowParts] and
+// colv[kColParts] (shared memory): warp w takes fields w, w+nwarps, ...; lane
+// l takes blocks l, l+32, ... in order, then a fixed butterfly
+// (deterministic, one round of loads).
+__device__ __forceinline__ void reduce_partials(const double* rowsrc, int nrow, const double* colsrc,
+                                                int ncol, double* rowv, double* colv) {
   const int lane = threadIdx.x & 31;
-  for (int fld = threadIdx.x >> 5; fld < kRowParts + kColParts; fld += kEpiBlock / 32) {
+  for (int fld = threadIdx.x >> 5; fld < kRowParts + kColParts; fld += blockDim.x / 32) {
     const bool is_row = fld < kRowParts;
     const int f = is_row ? fld : fld - kRowParts;
     const bool is_max = is_row ? ((kRowMaxMask >> f) & 1u) : ((kColMaxMask >> f) & 1u);
-    const double* src = is_row ? p.rowp : p.colp;
+    const double* src = is_row ? rowsrc : colsrc;
     const int stride = is_row ? kRowParts : kColParts;
-    const int nb = is_row ? p.row_grid : p.col_grid;
+    const int nb = is_row ? nrow : ncol;
     double a = 0.0;
     for (int b = lane; b < nb; b += 32) {
       const double v = __ldcg(src + b * stride + f);
@@ -201,6 +193,18 @@ __device__ void finalize(const IterParams& p, const StepInfo& si) {
     if (lane == 0) (is_row ? rowv : colv)[f] = a;
   }
   __syncthreads();
+}
+
+// decide() on a shared-memory copy of the control block (one coalesced read
+// and one write instead of a chain of dependent global round trips).
+__device__ void decide_and_store(const IterParams& p, const StepInfo& si, const double* rowv,
+                                 const double* colv) {
+  __shared__ Ctrl cs;
+  constexpr int kWords = sizeof(Ctrl) / 8;
+  long long* csw = reinterpret_cast<long long*>(&cs);
+  const long long* gw = reinterpret_cast<const long long*>(p.ctrl);
+  for (int w = threadIdx.x; w < kWords; w += blockDim.x) csw[w] = __ldcg(gw + w);
+  __syncthreads();
   if (threadIdx.x == 0) {
     cs.t_cols_start = globaltimer();  // debug: reuse as "partials reduced" stamp
     decide(p, si, &cs, rowv, colv);
@@ -208,7 +212,59 @@ __device__ void finalize(const IterParams& p, const StepInfo& si) {
   }
   __syncthreads();
   long long* out = reinterpret_cast<long long*>(p.ctrl);
-  for (int w = threadIdx.x; w < kWords; w += kEpiBlock) out[w] = csw[w];
+  for (int w = threadIdx.x; w < kWords; w += blockDim.x) out[w] = csw[w];
+}
+
+// Runs on the last block of k_primal: all partials, then the decisions. In
+// sharded mode it only publishes this shard's sums (k_finalize_shard decides
+// once every shard's sums have been exchanged).
+__device__ void finalize(const IterParams& p, const StepInfo& si) {
+  __shared__ double rowv[kRowParts];
+  __shared__ double colv[kColParts];
+  reduce_partials(p.rowp, p.row_grid, p.colp, p.col_grid, rowv, colv);
+  if (p.xpart_loc != nullptr) {
+    if (threadIdx.x < kRowParts) p.xpart_loc[threadIdx.x] = rowv[threadIdx.x];
+    if (threadIdx.x < kColParts) p.xpart_loc[kRowParts + threadIdx.x] = colv[threadIdx.x];
+    return;
+  }
+  decide_and_store(p, si, rowv, colv);
+}
+
+// Sharded mode: every shard reduces the exchanged per-shard sums
+// xpart[P][kRowParts + kColParts] in shard order (so all shards take
+// identical decisions), then decides.
+__global__ void __launch_bounds__(kEpiBlock) k_finalize_shard(const IterParams p, const double* xpart,
+                                                              int nshards, int init) {
+  StepInfo si;
+  if (!read_step(p, init != 0, si)) return;
+  __shared__ double rowv[kRowParts];
+  __shared__ double colv[kColParts];
+  constexpr int W = kRowParts + kColParts;
+  if (threadIdx.x < W) {
+    const int f = threadIdx.x;
+    const bool is_row = f < kRowParts;
+    const int k = is_row ? f : f - kRowParts;
+    const bool is_max = is_row ? ((kRowMaxMask >> k) & 1u) : ((kColMaxMask >> k) & 1u);
+    double a = 0.0;
+    for (int b = 0; b < nshards; ++b) {
+      const double v = __ldcg(xpart + b * W + f);
+      a = is_max ? amax(a, v) : a + v;
+    }
+    (is_row ? rowv : colv)[k] = a;
+  }
+  __syncthreads();
+  decide_and_store(p, si, rowv, colv);
+}
+
+// Sharded mode: this shard's slice of the next iterate, x_{t+2} =
+// xc[(t+1) % 3][R] after check(t+1), into its region of the full x
+// (idempotent, so it may run after a stop or halt).
+__global__ void k_select_x(const IterParams p, double* __restrict__ x_full_loc) {
+  pdl_wait();
+  const Ctrl* C = p.ctrl;
+  const double* __restrict__ src = p.xc[(C->iteration + 1) % 3][C->R];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x)
+    x_full_loc[j] = src[j];
 }
 
 // Lean SpMV of one half-step: out[r] = sum_k M[r,k] vec[k] over CSR M.
@@ -289,7 +345,8 @@ template <int G, bool LONG>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
-  spmv_block_range<G, LONG>(p.plan_r, p.rowptr, p.colind, p.aval, GatherPlain{p.xc[si.xs][si.R]},
+  spmv_block_range<G, LONG>(p.plan_r, p.rowptr, p.colind, p.aval,
+                            GatherPlain{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]},
                       p.ax[si.s1], p.rpg_rows);
 }
 
@@ -297,7 +354,8 @@ template <int G, bool LONG>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_cols(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
-  spmv_block_range<G, LONG>(p.plan_c, p.colptr, p.rowind, p.atval, GatherPlain{p.y[si.s1]},
+  spmv_block_range<G, LONG>(p.plan_c, p.colptr, p.rowind, p.atval,
+                            GatherPlain{p.yg != nullptr ? p.yg : p.y[si.s1]},
                       p.aty[si.s1], p.rpg_cols);
 }
 
@@ -357,6 +415,7 @@ __global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init
       const double ysn = (si.R ? 0.0 : ys[k]) + yn;
       const double axsn = (si.R ? 0.0 : axs[k]) + axn[k];
       y1[i] = yn;
+      if (p.y_full_loc != nullptr) p.y_full_loc[i] = yn;
       ys1[i] = ysn;
       axs1[i] = axsn;
       if (nonfinite(yn)) acc[6] += 1.0;
@@ -464,7 +523,8 @@ struct ViewParams {
   double* rowp;
   double* colp;
   unsigned* counter;
-  double* report;  // [kRepN]
+  double* report;     // [kRepN]
+  double* parts_out;  // optional: the reduced sums [kRowParts + kColParts] (sharded mode)
 };
 
 __global__ void __launch_bounds__(kBlock) k_view_rows(const ViewParams v) {
@@ -545,6 +605,10 @@ __global__ void __launch_bounds__(kBlock) k_view_cols(const ViewParams v, int ro
     }
   block_reduce<kRowParts, kRowMaxMask>(ra, red, rowv);
   block_reduce<kColParts, kColMaxMask>(ca, red, colv);
+  if (v.parts_out != nullptr) {
+    if (threadIdx.x < kRowParts) v.parts_out[threadIdx.x] = rowv[threadIdx.x];
+    if (threadIdx.x < kColParts) v.parts_out[kRowParts + threadIdx.x] = colv[threadIdx.x];
+  }
   if (threadIdx.x == 0) {
     make_report(rowv, colv, p.b_norm, p.c_norm, v.report);
     *v.counter = 0u;

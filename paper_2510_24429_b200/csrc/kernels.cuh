@@ -107,6 +107,11 @@ struct IterParams {
   const double* thr;
   const unsigned long long* t0_ns;
   int rpg_rows, rpg_cols;  // rows per lane group in flight in the SpMV (1 or 2)
+  // sharded mode (row-block partition, sharded.cuh); all null on one device
+  const double* xg;    // gather source of the row SpMV: the full (padded) x
+  const double* yg;    // gather source of the column SpMV: the full (padded) y
+  double* y_full_loc;  // this shard's region of the full y (k_dual also writes y there)
+  double* xpart_loc;   // k_primal's last block writes the shard's 22 report sums here
 };
 
 // ---------------------------------------------------------------------------

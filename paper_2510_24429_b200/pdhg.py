@@ -119,6 +119,17 @@ def load_library(path: str = LIB_PATH):
         L.cclp_cu_describe.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]
         L.cclp_cu_gaussian_start.argtypes = [C.c_uint64, C.c_int64, _dp]
         L.cclp_cu_gaussian_start.restype = None
+        L.cclp_cu_partition.argtypes = [_ip, C.c_int32, C.c_int32, _ip]
+        L.cclp_cu_nccl_unique_id.argtypes = [C.POINTER(C.c_uint8)]
+        L.cclp_cu_sharded_create.argtypes = [C.POINTER(_LP), C.c_int, C.c_int32, C.c_int32, C.c_int32,
+                                             C.POINTER(C.c_uint8), C.POINTER(C.c_void_p)]
+        L.cclp_cu_sharded_solve.argtypes = [C.c_void_p, C.POINTER(_Config), C.POINTER(_Tol), _dp,
+                                            C.c_int32, _SINK, C.c_void_p, C.POINTER(C.c_uint8), _dp,
+                                            _dp, _dp, C.POINTER(_Result)]
+        L.cclp_cu_sharded_begin.argtypes = [C.c_void_p, C.POINTER(_Config), C.POINTER(_Tol)]
+        L.cclp_cu_sharded_advance.argtypes = [C.c_void_p, C.c_int64, _dp]
+        L.cclp_cu_sharded_describe.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]
+        L.cclp_cu_sharded_destroy.argtypes = [C.c_void_p]
         _lib = L
         return L
 
@@ -128,7 +139,10 @@ EXPORTED_SYMBOLS = [
     "cclp_cu_default_tolerances", "cclp_cu_create", "cclp_cu_destroy", "cclp_cu_solve",
     "cclp_cu_run_pdhg", "cclp_cu_matvec", "cclp_cu_matvec_transpose", "cclp_cu_ruiz",
     "cclp_cu_estimate_norm", "cclp_cu_begin", "cclp_cu_advance", "cclp_cu_profile_kernels",
-    "cclp_cu_stream", "cclp_cu_describe", "cclp_cu_gaussian_start",
+    "cclp_cu_stream", "cclp_cu_describe", "cclp_cu_gaussian_start", "cclp_cu_partition",
+    "cclp_cu_nccl_unique_id", "cclp_cu_sharded_create", "cclp_cu_sharded_solve",
+    "cclp_cu_sharded_begin", "cclp_cu_sharded_advance", "cclp_cu_sharded_describe",
+    "cclp_cu_sharded_destroy",
 ]
 
 
@@ -420,6 +434,144 @@ def gaussian_start(seed: int, n: int) -> np.ndarray:
     v = np.empty(n)
     L.cclp_cu_gaussian_start(seed, n, v.ctypes.data_as(_dp))
     return v
+
+
+def partition(ptr, parts: int) -> np.ndarray:
+    """The nnz-balanced split of rows used for the shards (host only)."""
+    L = load_library()
+    ptr = np.ascontiguousarray(ptr, np.int32)
+    out = np.empty(parts + 1, np.int32)
+    _check(L, L.cclp_cu_partition(ptr.ctypes.data_as(_ip), ptr.size - 1, parts,
+                                  out.ctypes.data_as(_ip)))
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0), to be broadcast to the other ranks."""
+    L = load_library()
+    buf = (C.c_uint8 * 128)()
+    _check(L, L.cclp_cu_nccl_unique_id(buf))
+    return bytes(buf)
+
+
+class ShardedEngine:
+    """Row-block sharded solve (cclp_cu_sharded).
+
+    nranks == 1: `nshards` shards in this process on `device` (exchanges by
+    device copies); nranks > 1: one shard per process over NCCL, `nccl_id`
+    from rank 0's nccl_unique_id()."""
+
+    def __init__(self, lp: LinearProgram, nshards: int = 1, device: int = 0, rank: int = 0,
+                 nranks: int = 1, nccl_id: Optional[bytes] = None):
+        self.L = load_library()
+        self.lp = lp
+        self._keep = dict(colptr=np.ascontiguousarray(lp.colptr, np.int32),
+                          rowind=np.ascontiguousarray(lp.rowind, np.int32),
+                          val=np.ascontiguousarray(lp.val, np.float64),
+                          c=np.ascontiguousarray(lp.c, np.float64),
+                          rl=np.ascontiguousarray(lp.row_lower, np.float64),
+                          ru=np.ascontiguousarray(lp.row_upper, np.float64),
+                          cl=np.ascontiguousarray(lp.col_lower, np.float64),
+                          cu=np.ascontiguousarray(lp.col_upper, np.float64))
+        k = self._keep
+        d = lambda a: a.ctypes.data_as(_dp)  # noqa: E731
+        i = lambda a: a.ctypes.data_as(_ip)  # noqa: E731
+        self._lp = _LP(lp.m, lp.n, i(k["colptr"]), i(k["rowind"]), d(k["val"]), d(k["c"]),
+                       d(k["rl"]), d(k["ru"]), d(k["cl"]), d(k["cu"]))
+        idbuf = None
+        if nccl_id is not None:
+            idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
+        self.ctx = C.c_void_p()
+        _check(self.L, self.L.cclp_cu_sharded_create(C.byref(self._lp), device, nshards, rank,
+                                                     nranks, idbuf, C.byref(self.ctx)))
+
+    def close(self) -> None:
+        if self.ctx:
+            self.L.cclp_cu_sharded_destroy(self.ctx)
+            self.ctx = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def describe(self) -> dict:
+        out = (C.c_int64 * 64)()
+        self.L.cclp_cu_sharded_describe(self.ctx, out, 64)
+        P = int(out[0])
+        rb = list(out[1:P + 2])
+        cb = list(out[P + 2:2 * P + 3])
+        return dict(shards=P, row_bounds=rb, col_bounds=cb, launches=int(out[2 * P + 3]))
+
+    def solve(self, config: Optional[PdhgConfig] = None, tol: Optional[Tolerances] = None,
+              thresholds: Sequence[float] = (), sink=None, cancel=None) -> PdhgResult:
+        config = config or PdhgConfig()
+        tol = tol or Tolerances()
+        lp = self.lp
+        thr = np.ascontiguousarray(list(thresholds), np.float64)
+        x, y, z = np.empty(lp.n), np.empty(lp.m), np.empty(lp.n)
+        res = _Result()
+        errors = []
+
+        def _sink(sp, _u):
+            try:
+                s = sp.contents
+                it = Iterate(np.ctypeslib.as_array(s.x, (lp.n,)).copy() if lp.n else np.empty(0),
+                             np.ctypeslib.as_array(s.y, (lp.m,)).copy() if lp.m else np.empty(0),
+                             np.ctypeslib.as_array(s.z, (lp.n,)).copy() if lp.n else np.empty(0),
+                             int(s.iteration))
+                if sink is not None:
+                    sink(PdhgSnapshot(it, s.threshold, s.maxresid, bool(s.from_average),
+                                      int(s.iteration)))
+            except Exception as e:  # surfaced after the solve
+                errors.append(e)
+
+        cb = _SINK(_sink)
+        flag = cancel if cancel is not None else (C.c_uint8 * 1)(0)
+        rc = self.L.cclp_cu_sharded_solve(
+            self.ctx, C.byref(config._c()), C.byref(_Tol(tol.eps_rel, tol.eps_abs, tol.eps_cross,
+                                                         tol.decrement)),
+            thr.ctypes.data_as(_dp) if thr.size else None, thr.size, cb, None,
+            C.cast(flag, C.POINTER(C.c_uint8)), x.ctypes.data_as(_dp), y.ctypes.data_as(_dp),
+            z.ctypes.data_as(_dp), C.byref(res))
+        _check(self.L, rc)
+        if errors:
+            raise errors[0]
+        rep = ResidualReport(**{f: getattr(res.report, f) for f in REPORT_FIELDS})
+        return PdhgResult(Iterate(x, y, z, int(res.iterations)), rep,
+                          PdhgStopReason(res.stop), int(res.iterations), int(res.restarts),
+                          float(res.seconds), int(res.error_iteration), res.norm_estimate,
+                          res.omega, res.tau, res.sigma, res.setup_seconds, res.loop_seconds,
+                          int(res.kernel_launches))
+
+    def begin(self, config: Optional[PdhgConfig] = None, tol: Optional[Tolerances] = None):
+        config = config or PdhgConfig()
+        tol = tol or Tolerances()
+        _check(self.L, self.L.cclp_cu_sharded_begin(self.ctx, C.byref(config._c()), C.byref(
+            _Tol(tol.eps_rel, tol.eps_abs, tol.eps_cross, tol.decrement))))
+
+    def advance(self, iters: int) -> float:
+        ms = C.c_double()
+        _check(self.L, self.L.cclp_cu_sharded_advance(self.ctx, iters, C.byref(ms)))
+        return ms.value
+
+
+def run_pdhg_sharded(std_lp: LinearProgram, nshards: int, config: Optional[PdhgConfig] = None,
+                     tol: Optional[Tolerances] = None, thresholds: Sequence[float] = (),
+                     sink=None, cancel=None, device: int = 0) -> PdhgResult:
+    """run_pdhg over `nshards` row-block shards in this process (one GPU)."""
+    if not std_lp.all_rows_equality():
+        raise ValueError("run_pdhg: LP must be in equality form")
+    (tol or Tolerances()).validate()
+    with ShardedEngine(std_lp, nshards, device) as eng:
+        return eng.solve(config, tol, thresholds, sink, cancel)
 
 
 def run_pdhg(std_lp: LinearProgram, config: Optional[PdhgConfig] = None,
