@@ -410,6 +410,8 @@ void Context::build_csr() {
 void Context::partition() {
   if (Grow == 0) Grow = pick_group(nnz, m);
   if (Gcol == 0) Gcol = pick_group(nnz, n);
+  if (const char* e = std::getenv("CCLP_CU_G_ROWS")) Grow = std::atoi(e);  // A/B experiments only
+  if (const char* e = std::getenv("CCLP_CU_G_COLS")) Gcol = std::atoi(e);
   // Setup kernels use nnz-balanced row ranges of `row_grid` / `col_grid`
   // blocks. The iteration's SpMV kernels run one full wave of resident
   // blocks (grid-stride over rows); the epilogues one wave of kEpiBlock-thread
