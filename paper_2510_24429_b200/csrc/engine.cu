@@ -8,6 +8,7 @@
 // stream into pinned memory; the sink is called on the caller's thread.
 // Reference: run_pdhg, proj/src/pdhg.cpp:230-378.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -191,7 +192,30 @@ struct Context {
     std::vector<long long> wrow, wseg;  // host weights while planning
   } plan_rows, plan_cols;
   void plan_side(bool rows_side, int G, SidePlan& sp);
+  void plan_side_ptr(const int* dptr, int rows, int G, SidePlan& sp);
   int* plan_starts(bool rows_side, const SidePlan& sp, int grid);
+  int* plan_starts_ptr(const int* dptr, int rows, const SidePlan& sp, int grid);
+  // ---- column panels of the row SpMV: when the gathered x is larger than
+  // the L2 can keep (C5: 400 MB), A is split by columns into panels of
+  // kPanelBytes of x, stored panel-major (each panel a CSR over all rows with
+  // its rows' entries in column order), and A x = sum over panels in panel
+  // order, each panel's gathers L2-resident.
+  static constexpr size_t kPanelBytes = size_t(48) << 20;
+  struct Panel {
+    int* ptr = nullptr;    // [m + 1]
+    int* idx = nullptr;    // [nnz_k] global (gather-space) column indices
+    int* perm = nullptr;   // [nnz_k] position in CSR(A) (values are gathered per solve)
+    double* val = nullptr; // [nnz_k] scaled values
+    long long nnz = 0;
+    int G = 1;
+    SidePlan sp;
+    int* start = nullptr;
+  };
+  std::vector<Panel> panels;
+  int panel_grid = 0;
+  void build_panels(long long gather_len);
+  bool use_panels() const { return !panels.empty() && !exact; }
+  PanelArgs panel_args(int k) const;
   SpmvPlan plan(bool rows_side) const;
   int* spmv_row_start = nullptr;  // [spmv_grid_r + 1]
   int* spmv_col_start = nullptr;  // [spmv_grid_c + 1]
@@ -314,6 +338,10 @@ Context::~Context() {
     for (int q = 0; q < 2; ++q) {
       double* v[] = {aty[q], xsum[q], atysum[q], y[q], ax[q], ysum[q], axsum[q]};
       for (double* p : v) release(p);
+    }
+    for (auto& pn : panels) {
+      void* pp[] = {pn.ptr, pn.idx, pn.perm, pn.val, pn.start, pn.sp.seg, pn.sp.lr_first, pn.sp.part, pn.sp.cnt};
+      for (void* q : pp) release(q);
     }
     // pinned buffers may still be targets of queued copies
     cudaStreamSynchronize(stream);
@@ -447,19 +475,14 @@ void Context::partition() {
   tune_spmv();
 }
 
-// Picks the launch geometry of the two iteration SpMVs (blocks per SM, rows
-// per lane group in flight) by timing candidates on this matrix. Each timed
-// launch is preceded by the other half-step's SpMV so the L2 holds what it
-// holds inside the iteration (C2's matrix alone fits the 126 MB L2; timing a
-// kernel back to back would measure an L2-resident matrix). G (lanes per row)
-// is fixed by the mean row length, so every candidate produces bit-identical
-// results.
 // Long-row segmentation of one SpMV side (see SpmvPlan): segments and their
 // combine bookkeeping depend on the matrix only; the per-geometry part is the
 // weight-balanced split of the row+segment sequence into `grid` blocks.
 void Context::plan_side(bool rows_side, int G, SidePlan& sp) {
-  const int rows = rows_side ? m : n;
-  const int* dptr = rows_side ? rowptr : colptr;
+  plan_side_ptr(rows_side ? rowptr : colptr, rows_side ? m : n, G, sp);
+}
+
+void Context::plan_side_ptr(const int* dptr, int rows, int G, SidePlan& sp) {
   // rows past 32 G nonzeros (> 32 strided loads per lane) would leave their
   // lane group straggling behind the block: they go to whole warps instead
   sp.thr = 32 * G;
@@ -508,11 +531,13 @@ void Context::plan_side(bool rows_side, int G, SidePlan& sp) {
 
 // Block starts [2 * (grid + 1)] for one geometry: rows then segments.
 int* Context::plan_starts(bool rows_side, const SidePlan& sp, int grid) {
-  const int rows = rows_side ? m : n;
+  return plan_starts_ptr(rows_side ? rowptr : colptr, rows_side ? m : n, sp, grid);
+}
+
+int* Context::plan_starts_ptr(const int* dptr, int rows, const SidePlan& sp, int grid) {
   int* st = alloc<int>(2 * (grid + 1));
   if (!sp.has_long) {  // device split by nonzeros + per-row overhead; no segments
-    k_partition<<<blocks_for(grid + 1), kBlock, 0, stream>>>(rows_side ? rowptr : colptr, rows, grid, 4,
-                                                               st);
+    k_partition<<<blocks_for(grid + 1), kBlock, 0, stream>>>(dptr, rows, grid, 4, st);
     CK(cudaMemsetAsync(st + grid + 1, 0, sizeof(int) * (grid + 1), stream));
     CKL("plan partition");
     return st;
@@ -549,6 +574,66 @@ SpmvPlan Context::plan(bool rows_side) const {
   P.cnt = sp.cnt;
   P.thr = (exact || !sp.has_long) ? 0x7fffffff : sp.thr;
   return P;
+}
+
+void Context::build_panels(long long gather_len) {
+  long long pb = static_cast<long long>(kPanelBytes);
+  if (const char* e = std::getenv("CCLP_CU_PANEL_BYTES")) pb = std::max(64LL, std::atoll(e));  // tests
+  const long long K = (gather_len * 8 + pb - 1) / pb;
+  if (K < 3 || m == 0 || nnz == 0) return;  // x (nearly) fits the L2: one pass
+  const long long W = (gather_len + K - 1) / K;
+  int sms = 148;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  panel_grid = 2 * sms;
+  int* cnt = alloc<int>(static_cast<size_t>(m) + 1);
+  size_t tmp_bytes = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, cnt, m + 1, stream));
+  void* tmp = alloc<char>(tmp_bytes);
+  panels.resize(K);
+  for (long long k = 0; k < K; ++k) {
+    Panel& pn = panels[k];
+    const int lo = static_cast<int>(std::min<long long>(k * W, gather_len));
+    const int hi = static_cast<int>(std::min<long long>((k + 1) * W, gather_len));
+    k_panel_count<<<blocks_for(m + 1), kBlock, 0, stream>>>(rowptr, colind, m, lo, hi, cnt);
+    CKL("panel count");
+    pn.ptr = alloc<int>(static_cast<size_t>(m) + 1);
+    CK(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, pn.ptr, m + 1, stream));
+    int total = 0;
+    CK(cudaMemcpyAsync(&total, pn.ptr + m, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    pn.nnz = total;
+    pn.idx = alloc<int>(total);
+    pn.perm = alloc<int>(total);
+    pn.val = alloc<double>(total);
+    k_panel_fill<<<blocks_for(m), kBlock, 0, stream>>>(rowptr, colind, m, lo, pn.ptr, pn.idx, pn.perm);
+    CKL("panel fill");
+    pn.G = pick_group(pn.nnz, m);
+    plan_side_ptr(pn.ptr, m, pn.G, pn.sp);
+    pn.start = plan_starts_ptr(pn.ptr, m, pn.sp, panel_grid);
+    pn.sp.wrow.clear();
+    pn.sp.wrow.shrink_to_fit();
+    pn.sp.wseg.clear();
+    pn.sp.wseg.shrink_to_fit();
+  }
+  release(tmp);
+  release(cnt);
+}
+
+PanelArgs Context::panel_args(int k) const {
+  const Panel& pn = panels[k];
+  PanelArgs a;
+  a.plan.start = pn.start;
+  a.plan.grid = panel_grid;
+  a.plan.seg = pn.sp.seg;
+  a.plan.lr_first = pn.sp.lr_first;
+  a.plan.part = pn.sp.part;
+  a.plan.cnt = pn.sp.cnt;
+  a.plan.thr = pn.sp.has_long ? pn.sp.thr : 0x7fffffff;
+  a.ptr = pn.ptr;
+  a.idx = pn.idx;
+  a.val = pn.val;
+  a.accumulate = k > 0 ? 1 : 0;
+  return a;
 }
 
 // Picks the launch geometry of the two iteration SpMVs (blocks per SM, rows
@@ -627,6 +712,7 @@ void Context::tune_spmv() {
   spmv_col_start = cols_st[ps_c];
   release(rows_st[3 - ps_r]);
   release(cols_st[3 - ps_c]);
+  build_panels(x_full ? static_cast<long long>(shard_count) * Sn : n);
   plan_rows.wrow.clear();
   plan_rows.wrow.shrink_to_fit();
   plan_rows.wseg.clear();
@@ -793,10 +879,20 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
   const int rgrid = blocks_for(n, kBlock, 148 * 4);
   for (int t = 0; t < iterations; ++t) {
     const SpmvPlan Pr = plan(true), Pc = plan(false);
-    with_group_long(grow(), Pr.thr != 0x7fffffff, [&](auto g, auto l) {  // w = A v (:57)
-      k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_r, kSpmvBlock, 0, stream>>>(
-          Pr, rowptr, colind, aval, GatherPlain{v}, wm, rpg_r);
-    });
+    if (scaled && use_panels()) {  // w = A v (:57), panel by panel
+      for (int k = 0; k < static_cast<int>(panels.size()); ++k) {
+        const PanelArgs a = panel_args(k);
+        with_group_long(panels[k].G, a.plan.thr != 0x7fffffff, [&](auto g, auto l) {
+          k_spmv_range<decltype(g)::value, decltype(l)::value><<<panel_grid, kSpmvBlock, 0, stream>>>(
+              a.plan, a.ptr, a.idx, a.val, GatherPlain{v}, wm, 1, a.accumulate);
+        });
+      }
+    } else {
+      with_group_long(grow(), Pr.thr != 0x7fffffff, [&](auto g, auto l) {  // w = A v (:57)
+        k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_r, kSpmvBlock, 0, stream>>>(
+            Pr, rowptr, colind, aval, GatherPlain{v}, wm, rpg_r);
+      });
+    }
     with_group_long(gcol(), Pc.thr != 0x7fffffff, [&](auto g, auto l) {  // u = A' w (:58)
       k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(
           Pc, colptr, rowind, atval, GatherPlain{wm}, u, rpg_c);
@@ -814,9 +910,21 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
 void Context::launch_rows_half(bool init) {
   const IterParams& p = params;
   const int ii = init ? 1 : 0;
-  with_group_long(grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
-    launch_pdl(k_spmv_rows<decltype(g)::value, decltype(l)::value>, spmv_grid_r, kSpmvBlock, stream, p, ii);
-  });
+  if (use_panels()) {
+    for (int k = 0; k < static_cast<int>(panels.size()); ++k) {
+      const PanelArgs a = panel_args(k);
+      with_group_long(panels[k].G, a.plan.thr != 0x7fffffff, [&](auto g, auto l) {
+        launch_pdl(k_spmv_rows_panel<decltype(g)::value, decltype(l)::value>, panel_grid, kSpmvBlock, stream,
+                   p, ii, a);
+      });
+    }
+    launches += static_cast<long long>(panels.size()) - 1;
+  } else {
+    with_group_long(grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
+      launch_pdl(k_spmv_rows<decltype(g)::value, decltype(l)::value>, spmv_grid_r, kSpmvBlock, stream, p,
+                 ii);
+    });
+  }
   launch_pdl(k_dual, epi_grid, kEpiBlock, stream, p, ii);
 }
 
@@ -890,6 +998,10 @@ void Context::setup(const cclp_cu_config& cfg) {
   k_scale_values<<<blocks_for(static_cast<long long>(n) * 32), kBlock, 0, stream>>>(
       colptr, n, rowind, val_csc, s, r, 0, sval_csc);
   CKL("scale");
+  for (auto& pn : panels)  // panel-major copies of the scaled values
+    if (pn.nnz > 0)
+      k_gather_vals<<<blocks_for(pn.nnz), kBlock, 0, stream>>>(pn.perm, pn.nnz, sval_csr, pn.val);
+  CKL("panel values");
   mark(5);
   if (rng_thread.joinable()) rng_thread.join();
   norm_est = power_norm(cfg.norm_iterations, cfg.seed, true, true);
@@ -1207,10 +1319,20 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
     for (long long i = 0; i < iters; ++i) {
       cudaEvent_t* e = &ev[(K + 1) * i];
       CK(cudaEventRecord(e[0], C.stream));
-      cclp_cu::with_group_long(C.grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
-        cclp_cu::k_spmv_rows<decltype(g)::value, decltype(l)::value>
-            <<<C.spmv_grid_r, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
-      });
+      if (C.use_panels()) {
+        for (int k = 0; k < static_cast<int>(C.panels.size()); ++k) {
+          const cclp_cu::PanelArgs a = C.panel_args(k);
+          cclp_cu::with_group_long(C.panels[k].G, a.plan.thr != 0x7fffffff, [&](auto g, auto l) {
+            cclp_cu::k_spmv_rows_panel<decltype(g)::value, decltype(l)::value>
+                <<<C.panel_grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0, a);
+          });
+        }
+      } else {
+        cclp_cu::with_group_long(C.grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
+          cclp_cu::k_spmv_rows<decltype(g)::value, decltype(l)::value>
+              <<<C.spmv_grid_r, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
+        });
+      }
       CK(cudaEventRecord(e[1], C.stream));
       cclp_cu::k_dual<<<C.epi_grid, cclp_cu::kEpiBlock, 0, C.stream>>>(p, 0);
       CK(cudaEventRecord(e[2], C.stream));

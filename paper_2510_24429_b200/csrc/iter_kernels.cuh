@@ -278,7 +278,8 @@ template <int G, bool LONG, class Gather>
 __device__ __forceinline__ void spmv_block_range(const SpmvPlan& P, const int* __restrict__ ptr,
                                                  const int* __restrict__ idx,
                                                  const double* __restrict__ val, const Gather& g,
-                                                 double* __restrict__ out, int rpg = 1) {
+                                                 double* __restrict__ out, int rpg = 1,
+                                                 int accumulate = 0) {
   const int gl = threadIdx.x % G;
   const int gpb = blockDim.x / G;
   const int rb = P.start[blockIdx.x], re = P.start[blockIdx.x + 1];
@@ -294,8 +295,8 @@ __device__ __forceinline__ void spmv_block_range(const SpmvPlan& P, const int* _
       if (LONG && e1 - b1 > thr) ok1 = false, e1 = b1;
       double s0, s1;
       group_dot2<G, 2>(b0, e0, b1, e1, gl, idx, val, g, s0, s1);
-      if (gl == 0 && ok0) out[row] = 0.0 + s0;
-      if (gl == 0 && ok1) out[row1] = 0.0 + s1;
+      if (gl == 0 && ok0) out[row] = (accumulate ? out[row] : 0.0) + s0;
+      if (gl == 0 && ok1) out[row1] = (accumulate ? out[row1] : 0.0) + s1;
     }
   } else {
     for (int row = rb + static_cast<int>(threadIdx.x / G); row - static_cast<int>(threadIdx.x / G) < re;
@@ -304,7 +305,7 @@ __device__ __forceinline__ void spmv_block_range(const SpmvPlan& P, const int* _
       int b = ok ? __ldg(ptr + row) : 0, e = ok ? __ldg(ptr + row + 1) : 0;
       if (LONG && e - b > thr) ok = false, e = b;
       const double s = group_dot<G, 4>(b, e, gl, idx, val, g);
-      if (gl == 0 && ok) out[row] = 0.0 + s;
+      if (gl == 0 && ok) out[row] = (accumulate ? out[row] : 0.0) + s;
     }
   }
   if (!LONG) return;
@@ -317,7 +318,7 @@ __device__ __forceinline__ void spmv_block_range(const SpmvPlan& P, const int* _
     if (lane == 0) {
       const int f0 = __ldg(P.lr_first + sg.w), f1 = __ldg(P.lr_first + sg.w + 1);
       if (f1 - f0 == 1) {  // a single-segment row: no combine
-        out[sg.x] = 0.0 + s;
+        out[sg.x] = (accumulate ? out[sg.x] : 0.0) + s;
       } else {
         P.part[k] = s;
         __threadfence();
@@ -325,7 +326,7 @@ __device__ __forceinline__ void spmv_block_range(const SpmvPlan& P, const int* _
           __threadfence();
           double acc = 0.0;
           for (int q = f0; q < f1; ++q) acc = acc + __ldcg(P.part + q);
-          out[sg.x] = 0.0 + acc;
+          out[sg.x] = (accumulate ? out[sg.x] : 0.0) + acc;
           P.cnt[sg.w] = 0u;
         }
       }
@@ -337,8 +338,21 @@ template <int G, bool LONG, class Gather>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_range(const SpmvPlan P, const int* __restrict__ ptr,
                                                            const int* __restrict__ idx,
                                                            const double* __restrict__ val, Gather g,
-                                                           double* __restrict__ out, int rpg = 1) {
-  spmv_block_range<G, LONG>(P, ptr, idx, val, g, out, rpg);
+                                                           double* __restrict__ out, int rpg = 1,
+                                                           int accumulate = 0) {
+  spmv_block_range<G, LONG>(P, ptr, idx, val, g, out, rpg, accumulate);
+}
+
+// One column panel of ax_{t+1} = A x_{t+1} (panels run in panel order; the
+// first writes, the others add).
+template <int G, bool LONG>
+__global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows_panel(const IterParams p, int init,
+                                                                const PanelArgs a) {
+  StepInfo si;
+  if (!read_step(p, init != 0, si)) return;
+  spmv_block_range<G, LONG>(a.plan, a.ptr, a.idx, a.val,
+                            GatherPlain{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]}, p.ax[si.s1], 1,
+                            a.accumulate);
 }
 
 template <int G, bool LONG>

@@ -60,6 +60,15 @@ struct SpmvPlan {
   int grid;
 };
 
+// One column panel of the row SpMV (engine.cu, Context::build_panels).
+struct PanelArgs {
+  SpmvPlan plan;
+  const int* ptr;
+  const int* idx;
+  const double* val;
+  int accumulate;  // 0: out = sum; 1: out += sum (panel order)
+};
+
 // ---------------------------------------------------------------------------
 // Parameters of the fused iteration kernels (passed by value, captured into
 // CUDA graphs once per solve).

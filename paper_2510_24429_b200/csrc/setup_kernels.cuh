@@ -43,6 +43,47 @@ __global__ void k_gather_csr(const int* __restrict__ perm, long long nnz,
   }
 }
 
+// Column panels (Context::build_panels): entries of row i with column in
+// [lo, hi) - a contiguous run, since rows keep ascending column order.
+__device__ __forceinline__ int lower_in_row(const int* __restrict__ idx, int b, int e, int key) {
+  while (b < e) {
+    const int mid = b + (e - b) / 2;
+    if (idx[mid] < key) b = mid + 1; else e = mid;
+  }
+  return b;
+}
+
+__global__ void k_panel_count(const int* __restrict__ ptr, const int* __restrict__ idx, int rows, int lo,
+                              int hi, int* __restrict__ cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= rows; i += gridDim.x * blockDim.x) {
+    if (i == rows) {
+      cnt[i] = 0;
+      continue;
+    }
+    const int b = ptr[i], e = ptr[i + 1];
+    cnt[i] = lower_in_row(idx, b, e, hi) - lower_in_row(idx, b, e, lo);
+  }
+}
+
+__global__ void k_panel_fill(const int* __restrict__ ptr, const int* __restrict__ idx, int rows, int lo,
+                             const int* __restrict__ pptr, int* __restrict__ pidx, int* __restrict__ perm) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+    const int b = lower_in_row(idx, ptr[i], ptr[i + 1], lo);
+    const int base = pptr[i], len = pptr[i + 1] - base;
+    for (int q = 0; q < len; ++q) {
+      pidx[base + q] = idx[b + q];
+      perm[base + q] = b + q;
+    }
+  }
+}
+
+__global__ void k_gather_vals(const int* __restrict__ perm, long long cnt, const double* __restrict__ src,
+                              double* __restrict__ dst) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < cnt;
+       q += (long long)gridDim.x * blockDim.x)
+    dst[q] = src[perm[q]];
+}
+
 // Number of rows with more than `thr` nonzeros.
 __global__ void k_count_long(const int* __restrict__ ptr, int rows, int thr, int* count) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x)

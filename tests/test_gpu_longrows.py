@@ -78,3 +78,28 @@ def test_powerlaw_c5xs_parity(oracle):
     assert res.iterations == ref["iterations"] == 20
     assert rel(res.iterate.x, ref["x"]) <= REL_TOL
     assert rel(res.iterate.y, ref["y"]) <= REL_TOL
+
+
+@pytest.fixture
+def small_panels(monkeypatch):
+    """Force column panels on small LPs (production: panels of 48 MB of x,
+    i.e. only when x exceeds ~3 panels; C5 has 9)."""
+    monkeypatch.setenv("CCLP_CU_PANEL_BYTES", "16384")
+
+
+@pytest.mark.parametrize("iters", [1, 30])
+def test_column_panels_parity(small_panels, iters, oracle):
+    lp = lpgen.make_config("C5xs")  # 500k columns -> 245 panels of 2k columns
+    res = run_pdhg(lp, PdhgConfig(max_iterations=iters))
+    ref = oracle.run_pdhg(lp, config=dict(max_iterations=iters))
+    assert res.iterations == ref["iterations"]
+    assert rel(res.iterate.x, ref["x"]) <= REL_TOL
+    assert rel(res.iterate.y, ref["y"]) <= REL_TOL
+
+
+def test_column_panels_rerun_and_exact(small_panels, long_lp):
+    a = run_pdhg(long_lp, PdhgConfig(max_iterations=200))
+    b = run_pdhg(long_lp, PdhgConfig(max_iterations=200))
+    assert np.array_equal(a.iterate.x, b.iterate.x)
+    exact = run_pdhg(long_lp, PdhgConfig(max_iterations=200, exact_spmv=True))
+    assert rel(a.iterate.x, exact.iterate.x) <= 1e-9
