@@ -805,6 +805,8 @@ using SparseMatrixXd = SparseMatrix<double, ColMajor, int>;
 
 class MatrixXd;
 
+class PartialLU;
+
 class MatrixColumn : public VecBase<MatrixColumn> {
  public:
   MatrixColumn(double* p, Index n) : p_(p), n_(n) {}
@@ -861,6 +863,45 @@ class MatrixXd {
     for (auto& v : t.d_) v = std::abs(v);
     return t;
   }
+  PartialLU lu() const;
+  double maxCoeff() const {
+    if (d_.empty()) throw std::invalid_argument("Eigen shim: maxCoeff of an empty matrix");
+    double mx = d_[0];
+    for (double v : d_) mx = (mx < v) ? v : mx;
+    return mx;
+  }
+  // row(i) and row(i).tail(k): strided views (factorization.cpp:50-51)
+  class RowView : public VecBase<RowView> {
+   public:
+    RowView(double* p, Index stride, Index n) : p_(p), s_(stride), n_(n) {}
+    Index size() const { return n_; }
+    double coeff(Index i) const { return p_[i * s_]; }
+    double operator[](Index i) const { return p_[i * s_]; }
+    RowView tail(Index k) const { return RowView(p_ + (n_ - k) * s_, s_, k); }
+    RowView head(Index k) const { return RowView(p_, s_, k); }
+    template <typename E>
+    RowView& operator-=(const VecBase<E>& e) {
+      const E& d = e.derived();
+      std::vector<double> tmp(static_cast<size_t>(n_));
+      for (Index i = 0; i < n_; ++i) tmp[i] = d.coeff(i);
+      for (Index i = 0; i < n_; ++i) p_[i * s_] = p_[i * s_] - tmp[i];
+      return *this;
+    }
+    template <typename E>
+    RowView& operator=(const VecBase<E>& e) {
+      const E& d = e.derived();
+      std::vector<double> tmp(static_cast<size_t>(n_));
+      for (Index i = 0; i < n_; ++i) tmp[i] = d.coeff(i);
+      for (Index i = 0; i < n_; ++i) p_[i * s_] = tmp[i];
+      return *this;
+    }
+
+   private:
+    double* p_;
+    Index s_, n_;
+  };
+  RowView row(Index i) { return RowView(d_.data() + i, r_, c_); }
+  RowView row(Index i) const { return RowView(const_cast<double*>(d_.data()) + i, r_, c_); }
   struct Rowwise {
     const MatrixXd& m;
     VectorXd sum() const {
@@ -878,6 +919,48 @@ class MatrixXd {
   Index r_, c_;
   std::vector<double> d_;
 };
+
+// MatrixXd::lu(): partial-pivoting LU with solve (test_simplex.cpp:62-64).
+class PartialLU {
+ public:
+  explicit PartialLU(const MatrixXd& A) : n_(A.rows()), a_(A), p_(static_cast<size_t>(A.rows())) {
+    for (Index i = 0; i < n_; ++i) p_[i] = i;
+    for (Index k = 0; k < n_; ++k) {
+      Index piv = k;
+      for (Index i = k + 1; i < n_; ++i)
+        if (std::abs(a_(i, k)) > std::abs(a_(piv, k))) piv = i;
+      if (piv != k) {
+        for (Index j = 0; j < n_; ++j) std::swap(a_(k, j), a_(piv, j));
+        std::swap(p_[k], p_[piv]);
+      }
+      for (Index i = k + 1; i < n_; ++i) {
+        if (a_(k, k) == 0.0) break;
+        a_(i, k) /= a_(k, k);
+        for (Index j = k + 1; j < n_; ++j) a_(i, j) -= a_(i, k) * a_(k, j);
+      }
+    }
+  }
+  template <typename E>
+  VectorXd solve(const VecBase<E>& be) const {
+    const E& b = be.derived();
+    VectorXd x(n_);
+    for (Index i = 0; i < n_; ++i) x[i] = b.coeff(p_[i]);
+    for (Index i = 0; i < n_; ++i)
+      for (Index j = 0; j < i; ++j) x[i] -= a_(i, j) * x[j];
+    for (Index i = n_ - 1; i >= 0; --i) {
+      for (Index j = i + 1; j < n_; ++j) x[i] -= a_(i, j) * x[j];
+      x[i] /= a_(i, i);
+    }
+    return x;
+  }
+
+ private:
+  Index n_;
+  MatrixXd a_;
+  std::vector<Index> p_;
+};
+
+inline PartialLU MatrixXd::lu() const { return PartialLU(*this); }
 
 template <typename E>
 VectorXd operator*(const MatrixXd& M, const VecBase<E>& xe) {
@@ -921,10 +1004,12 @@ class FullPivLU<MatrixXd> {
       if (bi != k) {
         for (Index j = 0; j < n_; ++j) std::swap(lu_(k, j), lu_(bi, j));
         std::swap(pr_[k], pr_[bi]);
+        ++swaps_;
       }
       if (bj != k) {
         for (Index i = 0; i < n_; ++i) std::swap(lu_(i, k), lu_(i, bj));
         std::swap(pc_[k], pc_[bj]);
+        ++swaps_;
       }
       for (Index i = k + 1; i < n_; ++i) {
         lu_(i, k) /= lu_(k, k);
@@ -936,6 +1021,16 @@ class FullPivLU<MatrixXd> {
       if (p > thr * maxpivot) ++rank_;
   }
   bool isInvertible() const { return rank_ == n_; }
+  double determinant() const {
+    if (rank_ < n_ && static_cast<Index>(0) < n_) {
+      double d = 1.0;
+      for (Index i = 0; i < n_; ++i) d *= lu_(i, i);
+      return (swaps_ % 2 ? -d : d);
+    }
+    double d = 1.0;
+    for (Index i = 0; i < n_; ++i) d *= lu_(i, i);
+    return (swaps_ % 2 ? -d : d);
+  }
   Index rank() const { return rank_; }
   template <typename E>
   VectorXd solve(const VecBase<E>& be) const {
@@ -954,6 +1049,7 @@ class FullPivLU<MatrixXd> {
   }
 
  private:
+  int swaps_ = 0;
   MatrixXd lu_;
   Index n_;
   Index rank_;

@@ -1,5 +1,5 @@
 """CPU: the reference's OWN doctest suites (proj/tests/test_{kernels,scaling,
-kkt,pdhg,standard_form}.cpp), compiled unmodified against the Eigen/doctest
+kkt,pdhg,standard_form,simplex,crossover}.cpp), compiled unmodified against the Eigen/doctest
 API shims by oracle/Makefile, must pass. This pins the shim — and therefore
 oracle/_ref and the golden fixtures made from it — to the reference's own
 expectations."""
@@ -9,7 +9,8 @@ import subprocess
 import pytest
 
 REF = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref")
-SUITES = ["test_kernels", "test_scaling", "test_kkt", "test_pdhg", "test_standard_form"]
+SUITES = ["test_kernels", "test_scaling", "test_kkt", "test_pdhg", "test_standard_form",
+          "test_simplex", "test_crossover"]
 
 
 @pytest.mark.parametrize("suite", SUITES)
