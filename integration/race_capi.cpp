@@ -1,0 +1,136 @@
+// C-ABI bridge to cclp::run_race (integration/run_race.cpp) for the Python
+// tests and the time-to-basic benchmark. Built by oracle/Makefile twice from
+// the same sources: librace_gpu.so (run_pdhg = the B200 drop-in,
+// integration/run_pdhg_cuda.cpp) and librace_cpu.so (run_pdhg = the
+// reference's own CPU loop). Crossover is the reference's run_crossover in
+// both, compiled from /root/reference, so the two differ only in the PDHG.
+#include <algorithm>
+#include <cstring>
+#include <exception>
+#include <sstream>
+#include <string>
+
+#include "cclp/race.hpp"
+#include "json.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+cclp::Vector vec(const double* p, int n) {
+  cclp::Vector v(n);
+  if (n > 0) std::memcpy(v.data(), p, sizeof(double) * static_cast<size_t>(n));
+  return v;
+}
+}  // namespace
+
+extern "C" {
+
+const char* cclp_race_last_error() { return g_err.c_str(); }
+
+// mode 0 = baseline, 1 = concurrent. Writes the RaceOutcome JSON plus the
+// sorted basic column set and the event log into `out` (NUL-terminated).
+int cclp_race_run(int m, int n, const int* colptr, const int* rowind, const double* val, const double* c,
+                  const double* rl, const double* ru, const double* cl, const double* cu, int mode,
+                  double eps_rel, double eps_cross, double eps_abs, double time_limit, int pool,
+                  long long max_iterations, char* out, int cap) {
+  try {
+    cclp::LinearProgram lp;
+    lp.A = cclp::SparseMat(Eigen::Map<cclp::SparseMat>(m, n, colptr[n], colptr, rowind, val));
+    lp.c = vec(c, n);
+    lp.row_lower = vec(rl, m);
+    lp.row_upper = vec(ru, m);
+    lp.col_lower = vec(cl, n);
+    lp.col_upper = vec(cu, n);
+    lp.sense.assign(static_cast<size_t>(m), cclp::RowSense::kEq);
+    for (int i = 0; i < m; ++i)
+      if (rl[i] != ru[i]) lp.sense[static_cast<size_t>(i)] = cclp::RowSense::kLe;
+    cclp::RaceConfig cfg;
+    cfg.mode = mode ? cclp::RaceMode::kConcurrent : cclp::RaceMode::kBaseline;
+    cfg.tol.eps_rel = eps_rel;
+    cfg.tol.eps_cross = eps_cross;
+    cfg.tol.eps_abs = eps_abs;
+    cfg.time_limit = time_limit;
+    cfg.worker_pool = pool;
+    cfg.pdhg.max_iterations = max_iterations;
+    std::ostringstream events;
+    cfg.event_log = &events;
+    cclp::RaceOutcome o = cclp::run_race(lp, cfg);
+    nlohmann::json j = nlohmann::json::parse(o.to_json());
+    std::vector<long long> basic(o.final_result.basis.basic.begin(), o.final_result.basis.basic.end());
+    std::sort(basic.begin(), basic.end());
+    j["basic"] = basic;
+    j["winning_threshold"] = o.winning_threshold;
+    j["thresholds"] = o.thresholds;
+    j["events"] = events.str();
+    j["x"] = std::vector<double>(o.solution.x.data(), o.solution.x.data() + o.solution.x.size());
+    const std::string s = j.dump();
+    if (static_cast<int>(s.size()) + 1 > cap) {
+      g_err = "cclp_race_run: output buffer too small (" + std::to_string(s.size() + 1) + ")";
+      return 2;
+    }
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// Host-only helpers with the reference's semantics (race.hpp:86-100).
+int cclp_race_schedule(double eps_rel, double eps_cross, double decrement, double* out, int cap) {
+  try {
+    cclp::Tolerances t;
+    t.eps_rel = eps_rel;
+    t.eps_cross = eps_cross;
+    t.decrement = decrement;
+    const auto v = cclp::schedule_thresholds(t);
+    for (int i = 0; i < cap && i < static_cast<int>(v.size()); ++i) out[i] = v[static_cast<size_t>(i)];
+    return static_cast<int>(v.size());
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
+void cclp_race_reserve(int pool, int cores, int* pdhg, int* crossover) {
+  cclp::RaceConfig cfg;
+  cfg.worker_pool = pool;
+  const auto p = cclp::reserve_threads(cfg, cores);
+  *pdhg = p.first;
+  *crossover = p.second;
+}
+
+// run_race_simulated on a scripted trace: workers given as parallel arrays.
+int cclp_race_simulate(const double* trace, int ntrace, double sec_per_iter, const double* thr,
+                       const double* dur, const int* verifies, int nworkers, double main_dur, int main_ok,
+                       int mode, double eps_rel, double eps_cross, int pool, double time_limit, char* out,
+                       int cap) {
+  try {
+    cclp::RaceScript script;
+    script.residual_trace.assign(trace, trace + ntrace);
+    script.seconds_per_iteration = sec_per_iter;
+    for (int i = 0; i < nworkers; ++i) script.workers[thr[i]] = cclp::SimWorker{dur[i], verifies[i] != 0};
+    script.main_worker = cclp::SimWorker{main_dur, main_ok != 0};
+    cclp::RaceConfig cfg;
+    cfg.mode = mode ? cclp::RaceMode::kConcurrent : cclp::RaceMode::kBaseline;
+    cfg.tol.eps_rel = eps_rel;
+    cfg.tol.eps_cross = eps_cross;
+    cfg.worker_pool = pool;
+    cfg.time_limit = time_limit;
+    std::ostringstream events;
+    cfg.event_log = &events;
+    cclp::RaceOutcome o = cclp::run_race_simulated(script, cfg);
+    nlohmann::json j = nlohmann::json::parse(o.to_json());
+    j["winning_threshold"] = o.winning_threshold;
+    j["events"] = events.str();
+    const std::string s = j.dump();
+    if (static_cast<int>(s.size()) + 1 > cap) return 2;
+    std::memcpy(out, s.c_str(), s.size() + 1);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,65 @@
+"""CPU: cclp::run_race and friends (race.hpp:86-129, SPEC.md "[MODULE] race")
+as implemented in integration/run_race.cpp, with the SPEC's examples: the
+threshold ladder, the thread split, the deterministic simulation, and a real
+race over the reference's CPU run_pdhg + run_crossover (librace_cpu.so)."""
+import pytest
+
+from integration import race
+from paper_2510_24429_b200 import lpgen
+
+pytestmark = pytest.mark.skipif(not race.available("cpu"),
+                                reason="oracle/_ref/librace_cpu.so not built (needs /root/reference)")
+
+
+def test_schedule_thresholds_examples():
+    assert race.schedule_thresholds(1e-6, 1e-2, 0.1) == [1e-2, 1e-3, 1e-4, 1e-5]
+    assert race.schedule_thresholds(1e-8, 1e-4, 0.1) == [1e-4, 1e-5, 1e-6, 1e-7]
+    assert race.schedule_thresholds(1e-4, 1e-4, 0.1) == []
+    with pytest.raises(ValueError):
+        race.schedule_thresholds(1e-6, 1e-2, 1.5)
+
+
+def test_reserve_threads_examples():
+    assert race.reserve_threads(4, 16) == (12, 4)
+    assert race.reserve_threads(4, 2) == (1, 1)
+
+
+def test_simulated_later_faster_worker_wins():
+    # {1e-2: 100 ms, 1e-3: 10 ms launched 20 ms later} -> 1e-3 wins at 30 ms
+    trace = [5e-3] * 20 + [5e-4] * 200
+    out = race.simulate(trace, 1e-3, {1e-2: (0.100, True), 1e-3: (0.010, True)})
+    assert out["status"] == "solved"
+    assert out["winner"] == "1e-03"
+    assert out["wall_s"] == pytest.approx(0.030)
+    assert out["pdhg_stop"] == "won-by-crossover"
+    st = {w["threshold"]: w["status"] for w in out["workers"]}
+    assert st == {"1e-02": "cancelled", "1e-03": "success"}
+
+
+def test_simulated_baseline_main_wins_and_no_workers():
+    trace = [5e-3] * 10 + [1e-7]
+    out = race.simulate(trace, 1e-3, {1e-2: (0.001, True)}, main=(0.05, True), mode="baseline")
+    assert out["status"] == "solved" and out["winner"] == "main" and out["main_won"]
+    assert out["workers"] == []
+
+
+def test_simulated_failed_verification_and_pool():
+    trace = [5e-3] * 5 + [5e-4] * 5 + [5e-5] * 200
+    out = race.simulate(trace, 1e-3, {1e-2: (1.0, False), 1e-3: (1.0, True), 1e-4: (0.001, True)},
+                        pool=1)
+    # pool of one: 1e-3 and 1e-4 arrive while 1e-2 runs and are dropped; 1e-2
+    # then fails verification and PDHG never converges -> pdhg-limit
+    assert [w["threshold"] for w in out["workers"]] == ["1e-02"]
+    assert out["status"] == "pdhg-limit"
+
+
+def test_cpu_race_two_var_and_transport():
+    out = race.run_race(lpgen.two_var_lp(), kind="cpu")
+    assert out["status"] == "solved"
+    assert out["objective"] == pytest.approx(2.0, abs=1e-6)
+    lp = lpgen.transportation_lp(8, 12, seed=3)
+    base = race.run_race(lp, kind="cpu", mode="baseline")
+    conc = race.run_race(lp, kind="cpu", mode="concurrent")
+    assert base["status"] == conc["status"] == "solved"
+    assert base["winner"] == "main"
+    assert conc["objective"] == pytest.approx(base["objective"], rel=1e-9)
