@@ -209,7 +209,9 @@ int cclp_cu_sharded_solve(cclp_cu_sharded* ctx, const cclp_cu_config* cfg,
 int cclp_cu_sharded_begin(cclp_cu_sharded* ctx, const cclp_cu_config* cfg,
                           const cclp_cu_tolerances* tol);
 int cclp_cu_sharded_advance(cclp_cu_sharded* ctx, int64_t iters, double* device_ms);
-/* out: P, then row bounds [P+1], then column bounds [P+1] */
+/* out: P, row bounds [P+1], column bounds [P+1], launches, then for the x
+ * and y exchanges: halo on (1) or all-gather (0), and the halo volume in
+ * doubles per iteration summed over shards */
 int cclp_cu_sharded_describe(cclp_cu_sharded* ctx, int64_t* out, int32_t nout);
 int cclp_cu_sharded_destroy(cclp_cu_sharded* ctx);
 /* The nnz-balanced split used for the shards (host only): part b starts at

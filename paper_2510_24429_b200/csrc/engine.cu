@@ -1611,6 +1611,10 @@ int cclp_cu_sharded_describe(cclp_cu_sharded* ctx, int64_t* out, int32_t nout) {
   for (int b : S.rb) v.push_back(b);
   for (int b : S.cb) v.push_back(b);
   v.push_back(S.launches);
+  v.push_back(S.halo_x.on ? 1 : 0);
+  v.push_back(S.halo_x.volume);
+  v.push_back(S.halo_y.on ? 1 : 0);
+  v.push_back(S.halo_y.volume);
   for (int i = 0; i < nout && i < static_cast<int>(v.size()); ++i) out[i] = v[i];
   return CCLP_CU_OK;
 }

@@ -79,6 +79,32 @@ __global__ void k_slice_remap(const int* __restrict__ idx, const double* __restr
   }
 }
 
+// Halo exchange: dst[idx[i]] = src[idx[i]] (one peer's region, same device),
+// and the pack / unpack of the NCCL send / receive buffers.
+__global__ void k_halo_copy(const double* __restrict__ src, double* __restrict__ dst,
+                            const int* __restrict__ idx, int cnt) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) {
+    const int j = idx[i];
+    dst[j] = src[j];
+  }
+}
+__global__ void k_halo_pack(const double* __restrict__ src, const int* __restrict__ idx, int cnt,
+                            double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) out[i] = src[idx[i]];
+}
+__global__ void k_halo_unpack(const double* __restrict__ in, const int* __restrict__ idx, int cnt,
+                              double* __restrict__ dst) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += gridDim.x * blockDim.x) dst[idx[i]] = in[i];
+}
+// flags[col] = 1 for every column referenced by rows [r0, r1) of a CSR
+__global__ void k_mark_cols(const int* __restrict__ ptr, const int* __restrict__ idx, int r0, int r1,
+                            unsigned char* __restrict__ flags) {
+  const long long b = ptr[r0], e = ptr[r1];
+  for (long long q = b + blockIdx.x * (long long)blockDim.x + threadIdx.x; q < e;
+       q += (long long)gridDim.x * blockDim.x)
+    flags[idx[q]] = 1;
+}
+
 // ---- NCCL, resolved at run time (the library loads without NCCL) ----------
 struct NcclApi {
   bool ok = false;
@@ -87,6 +113,10 @@ struct NcclApi {
   ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
   ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 
@@ -104,7 +134,12 @@ NcclApi& nccl() {
     a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
     a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
-    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.GetErrorString;
+    a.Send = reinterpret_cast<decltype(a.Send)>(dlsym(h, "ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(dlsym(h, "ncclRecv"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.GetErrorString && a.Send &&
+           a.Recv && a.GroupStart && a.GroupEnd;
     if (!a.ok) a.err = "libnccl.so.2 lacks the needed symbols";
     return a;
   }();
@@ -215,11 +250,144 @@ struct Sharded {
   long long launches = 0;
   double *vx_full = nullptr, *vy_full = nullptr, *vz_full = nullptr, *vparts_full = nullptr;
   bool begun = false;
+  bool halo_built = false;
+
+  // Halo exchange of one side (x for the row SpMV, y for the column SpMV):
+  // need[p][q] = the sorted local offsets (in shard q's slice) of the entries
+  // shard p's SpMV gathers from shard q. Used instead of the all-gather when
+  // it moves under half the data (structured LPs: C4 needs only the
+  // neighbouring stage); every rank derives every list from the full matrix,
+  // so the send side needs no extra round of communication.
+  struct Halo {
+    bool on = false;
+    long long volume = 0;
+    std::vector<std::vector<int*>> need;  // [p][q] device lists (empty when q == p)
+    std::vector<std::vector<int>> cnt;    // [p][q]
+    double* sendbuf = nullptr;
+    double* recvbuf = nullptr;
+  } halo_x, halo_y;
+
+  void build_halo(Halo& h, bool x_side) {
+    // x side: rows of A owned by p (full CSR), columns owned by q; y side:
+    // rows of A' = columns of A owned by p (the CSC), rows of A owned by q
+    const int* ptr = x_side ? full->rowptr : full->colptr;
+    const int* idx = x_side ? full->colind : full->rowind;
+    const std::vector<int>& own = x_side ? rb : cb;     // rows of this side's matrix per shard
+    const std::vector<int>& tgt = x_side ? cb : rb;     // gathered vector's split
+    const int len = x_side ? n : m;
+    const long long S = x_side ? s0().Sn : s0().Sm;
+    const long long allgather = static_cast<long long>(P) * (P - 1) * S;
+    unsigned char* flags = full->alloc<unsigned char>(len);
+    std::vector<unsigned char> hf(static_cast<size_t>(len));
+    h.need.assign(P, std::vector<int*>(P, nullptr));
+    h.cnt.assign(P, std::vector<int>(P, 0));
+    std::vector<std::vector<std::vector<int>>> lists(P, std::vector<std::vector<int>>(P));
+    h.volume = 0;
+    for (int p = 0; p < P; ++p) {
+      CK(cudaMemsetAsync(flags, 0, std::max(1, len), stream));
+      if (own[p + 1] > own[p])
+        k_mark_cols<<<blocks_for(1 << 20), kBlock, 0, stream>>>(ptr, idx, own[p], own[p + 1], flags);
+      CKL("halo mark");
+      CK(cudaMemcpyAsync(hf.data(), flags, len, cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      for (int q = 0; q < P; ++q) {
+        if (q == p) continue;
+        for (int j = tgt[q]; j < tgt[q + 1]; ++j)
+          if (hf[j]) lists[p][q].push_back(j - tgt[q]);
+        h.cnt[p][q] = static_cast<int>(lists[p][q].size());
+        h.volume += h.cnt[p][q];
+      }
+    }
+    full->release(flags);
+    h.on = P > 1 && h.volume * 2 < allgather;
+    if (!h.on) return;
+    for (int p = 0; p < P; ++p)
+      for (int q = 0; q < P; ++q)
+        if (q != p && h.cnt[p][q] > 0) {
+          h.need[p][q] = full->alloc<int>(h.cnt[p][q]);
+          CK(cudaMemcpyAsync(h.need[p][q], lists[p][q].data(), sizeof(int) * h.cnt[p][q],
+                             cudaMemcpyHostToDevice, stream));
+        }
+    if (comm != nullptr) {
+      long long ns = 0, nr = 0;
+      for (int q = 0; q < P; ++q) {
+        ns += h.cnt[q][rank];
+        nr += h.cnt[rank][q];
+      }
+      h.sendbuf = full->alloc<double>(std::max(1LL, ns));
+      h.recvbuf = full->alloc<double>(std::max(1LL, nr));
+    }
+    CK(cudaStreamSynchronize(stream));
+  }
+
+  void release_halo(Halo& h) {
+    for (auto& row : h.need)
+      for (int* q : row) full->release(q);
+    full->release(h.sendbuf);
+    full->release(h.recvbuf);
+    h = Halo{};
+  }
+
+  // The exchange of one padded full buffer: the halo when it is on, else the
+  // in-place all-gather.
+  void exchange(double* Context::*buf, size_t S, Halo& h) {
+    if (!h.on) {
+      allgather(buf, S);
+      return;
+    }
+    if (comm == nullptr) {
+      for (auto& dst : shards)
+        for (auto& src : shards) {
+          const int p = dst->shard_rank, q = src->shard_rank;
+          if (p == q || h.cnt[p][q] == 0) continue;
+          k_halo_copy<<<blocks_for(h.cnt[p][q]), kBlock, 0, stream>>>(
+              src.get()->*buf + static_cast<size_t>(q) * S, dst.get()->*buf + static_cast<size_t>(q) * S,
+              h.need[p][q], h.cnt[p][q]);
+        }
+      CKL("halo copy");
+      return;
+    }
+    double* b = s0().*buf;
+    long long so = 0, ro = 0;
+    for (int p = 0; p < P; ++p) {  // pack what each peer needs from this rank
+      if (p == rank || h.cnt[p][rank] == 0) continue;
+      k_halo_pack<<<blocks_for(h.cnt[p][rank]), kBlock, 0, stream>>>(b + static_cast<size_t>(rank) * S,
+                                                                      h.need[p][rank], h.cnt[p][rank],
+                                                                      h.sendbuf + so);
+      so += h.cnt[p][rank];
+    }
+    CKL("halo pack");
+    nck(nccl().GroupStart(), "ncclGroupStart");
+    so = 0;
+    for (int p = 0; p < P; ++p) {
+      if (p == rank) continue;
+      if (h.cnt[p][rank] > 0) {
+        nck(nccl().Send(h.sendbuf + so, h.cnt[p][rank], ncclDouble, p, comm, stream), "ncclSend");
+        so += h.cnt[p][rank];
+      }
+      if (h.cnt[rank][p] > 0) {
+        nck(nccl().Recv(h.recvbuf + ro, h.cnt[rank][p], ncclDouble, p, comm, stream), "ncclRecv");
+        ro += h.cnt[rank][p];
+      }
+    }
+    nck(nccl().GroupEnd(), "ncclGroupEnd");
+    ro = 0;
+    for (int p = 0; p < P; ++p) {
+      if (p == rank || h.cnt[rank][p] == 0) continue;
+      k_halo_unpack<<<blocks_for(h.cnt[rank][p]), kBlock, 0, stream>>>(h.recvbuf + ro, h.need[rank][p],
+                                                                        h.cnt[rank][p],
+                                                                        b + static_cast<size_t>(p) * S);
+      ro += h.cnt[rank][p];
+    }
+    CKL("halo unpack");
+  }
 
   ~Sharded() {
     if (graph) cudaGraphExecDestroy(graph);
     shards.clear();
     if (full) {
+      release_halo(halo_x);
+      release_halo(halo_y);
       full->release(vx_full);
       full->release(vy_full);
       full->release(vz_full);
@@ -295,11 +463,19 @@ struct Sharded {
       CKL("stamp");
       shards.push_back(std::move(sh));
     }
+    if (!halo_built) {
+      const char* e = std::getenv("CCLP_CU_HALO");  // 0: always all-gather (A/B)
+      if (e == nullptr || std::atoi(e) != 0) {
+        build_halo(halo_x, true);
+        build_halo(halo_y, false);
+      }
+      halo_built = true;
+    }
   }
 
   void launch_round(bool init) {
     for (auto& s : shards) s->launch_rows_half(init);
-    allgather(&Context::y_full, static_cast<size_t>(s0().Sm));
+    exchange(&Context::y_full, static_cast<size_t>(s0().Sm), halo_y);
     for (auto& s : shards) s->launch_cols_half(init);
     allgather(&Context::xpart, kRowParts + kColParts);
     for (auto& s : shards) {
@@ -308,14 +484,14 @@ struct Sharded {
           s->params, s->x_full + static_cast<size_t>(s->shard_rank) * s->Sn);
     }
     CKL("shard finalize");
-    allgather(&Context::x_full, static_cast<size_t>(s0().Sn));
+    exchange(&Context::x_full, static_cast<size_t>(s0().Sn), halo_x);
     launches += static_cast<long long>(shards.size()) * (kKernelsPerIteration + 2);
   }
 
   void begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thr, int nthr) {
     build_shards(cfg);
     for (auto& s : shards) s->init_state(cfg, tol, thr, nthr, false);
-    allgather(&Context::x_full, static_cast<size_t>(s0().Sn));
+    allgather(&Context::x_full, static_cast<size_t>(s0().Sn));  // x_0: once, in full
     launch_round(true);
     CK(cudaStreamSynchronize(stream));
     begun = true;

@@ -508,7 +508,10 @@ class ShardedEngine:
         P = int(out[0])
         rb = list(out[1:P + 2])
         cb = list(out[P + 2:2 * P + 3])
-        return dict(shards=P, row_bounds=rb, col_bounds=cb, launches=int(out[2 * P + 3]))
+        o = 2 * P + 3
+        return dict(shards=P, row_bounds=rb, col_bounds=cb, launches=int(out[o]),
+                    halo_x=bool(out[o + 1]), halo_x_volume=int(out[o + 2]),
+                    halo_y=bool(out[o + 3]), halo_y_volume=int(out[o + 4]))
 
     def solve(self, config: Optional[PdhgConfig] = None, tol: Optional[Tolerances] = None,
               thresholds: Sequence[float] = (), sink=None, cancel=None) -> PdhgResult:

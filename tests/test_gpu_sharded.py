@@ -88,3 +88,21 @@ def test_nccl_transport_one_rank_matches_single():
     assert sh.iterations == one.iterations
     assert np.array_equal(sh.iterate.x, one.iterate.x)
     assert np.array_equal(sh.iterate.y, one.iterate.y)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+def test_halo_exchange_staircase_bit_identical(P):
+    """A staircase LP (C4's structure) needs only the neighbouring stage's x
+    and y: the halo exchange replaces the all-gathers and the iterates stay
+    bit-identical to one device."""
+    lp = lpgen.staircase_lp(stages=24, cols_per_stage=300, rows_per_stage=150, seed=6)[0]
+    cfg = PdhgConfig(max_iterations=300)
+    one = run_pdhg(lp, cfg)
+    with ShardedEngine(lp, P) as eng:
+        sh = eng.solve(cfg)
+        d = eng.describe()
+    assert d["halo_x"] and d["halo_y"]
+    assert d["halo_x_volume"] < lp.n and d["halo_y_volume"] < lp.m
+    assert sh.iterations == one.iterations and sh.restarts == one.restarts
+    assert np.array_equal(sh.iterate.x, one.iterate.x)
+    assert np.array_equal(sh.iterate.y, one.iterate.y)

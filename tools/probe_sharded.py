@@ -1,7 +1,10 @@
 """Sharded-solve probe on one GPU: the single-device engine vs P shards in one
-process (device-copy exchanges) vs the NCCL transport with one rank. With P
-shards sharing one GPU the per-iteration time is the sum of the P shards'
-kernels plus the exchanges, i.e. the compute-side cost of sharding."""
+process (device-copy exchanges: halo or all-gather) vs the NCCL transport
+with one rank. With P shards sharing one GPU the per-iteration time is the
+sum of the P shards' kernels plus the exchanges, i.e. the compute-side cost
+of sharding; `halo volume` is the per-iteration exchange in doubles (vs the
+all-gather's (P-1) x (m + n))."""
+import os
 import sys
 
 sys.path.insert(0, ".")
@@ -19,12 +22,17 @@ eng.advance(20)
 ms = eng.advance(its)
 print(f"{cfg} single: {ms/its*1e3:.1f} us/it ({B/(ms/its*1e-3)/1e9:.0f} GB/s)", flush=True)
 eng.close()
-for P in (1, 2, 4, 8):
-    with ShardedEngine(lp, P) as se:
-        se.begin(PdhgConfig())
-        se.advance(20)
-        ms = se.advance(its)
-        print(f"{cfg} local shards P={P}: {ms/its*1e3:.1f} us/it", flush=True)
+for halo in ("1", "0"):
+    os.environ["CCLP_CU_HALO"] = halo
+    for P in (2, 4, 8):
+        with ShardedEngine(lp, P) as se:
+            se.begin(PdhgConfig())
+            se.advance(20)
+            ms = se.advance(its)
+            d = se.describe()
+            print(f"{cfg} local shards P={P} halo={'on' if d['halo_x'] else 'off'}: {ms/its*1e3:.1f} us/it, "
+                  f"x/y exchange {d['halo_x_volume']}/{d['halo_y_volume']} doubles "
+                  f"(all-gather {(P-1)*(lp.n)}/{(P-1)*lp.m})", flush=True)
 with ShardedEngine(lp, 1, rank=0, nranks=1, nccl_id=nccl_unique_id()) as se:
     se.begin(PdhgConfig())
     se.advance(20)
