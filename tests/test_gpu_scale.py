@@ -1,0 +1,116 @@
+"""GPU at BASELINE.json's full sizes (C2, C3, C4, C5s) through properties
+that do not need a full CPU solve (the CPU oracle would take minutes to
+hours there), plus the loop's control paths on small LPs:
+
+* C2: equal-iteration parity against the CPU oracle itself (20 iterations).
+* C3/C4/C5s: the returned report equals the oracle's independent
+  relative_report (kkt.cpp:50-149) recomputed on the returned iterate;
+  reruns are bit-identical; C4 sharded (P = 2, halo exchange) is
+  bit-identical to one device.
+* cancel / time limit / check_interval > 1 / the iteration log.
+"""
+import re
+import threading
+import time
+
+import numpy as np
+import pytest
+
+from paper_2510_24429_b200 import lpgen
+from paper_2510_24429_b200.pdhg import (Engine, PdhgConfig, PdhgStopReason, ShardedEngine,
+                                        run_pdhg)
+
+pytestmark = pytest.mark.gpu
+
+REPORT_KEYS = ["rp_norm2", "rd_norm2", "rp_inf", "rd_inf", "primal_objective", "dual_objective",
+               "gap_abs", "rel_primal", "rel_dual", "rel_gap", "maxresid_rel", "complementarity"]
+
+
+def rel(a, b):
+    d = np.linalg.norm(np.asarray(a) - np.asarray(b))
+    return d / max(np.linalg.norm(b), 1e-300) if d > 0 else 0.0
+
+
+@pytest.fixture(scope="module")
+def lps():
+    cache = {}
+
+    def get(name):
+        if name not in cache:
+            cache[name] = lpgen.make_config(name)
+        return cache[name]
+    return get
+
+
+def test_c2_full_size_equal_iteration_parity(lps, oracle):
+    lp = lps("C2")
+    res = run_pdhg(lp, PdhgConfig(max_iterations=20))
+    ref = oracle.run_pdhg(lp, config=dict(max_iterations=20))
+    assert res.iterations == ref["iterations"] == 20
+    assert rel(res.iterate.x, ref["x"]) <= 1e-6
+    assert rel(res.iterate.y, ref["y"]) <= 1e-6
+    assert rel(res.iterate.z, ref["z"]) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["C3", "C4", "C5s"])
+def test_full_size_report_matches_independent_kkt(name, lps, oracle):
+    lp = lps(name)
+    a = run_pdhg(lp, PdhgConfig(max_iterations=300))
+    b = run_pdhg(lp, PdhgConfig(max_iterations=300))
+    assert np.array_equal(a.iterate.x, b.iterate.x) and np.array_equal(a.iterate.y, b.iterate.y)
+    kkt = oracle.relative_report(lp, a.iterate.x, a.iterate.y, a.iterate.z)
+    for k in REPORT_KEYS:
+        got = getattr(a.report, k)
+        assert got == pytest.approx(kkt[k], rel=1e-9, abs=1e-12 * (1 + abs(kkt[k]))), k
+
+
+def test_c4_full_size_sharded_bit_identical(lps):
+    lp = lps("C4")
+    cfg = PdhgConfig(max_iterations=60)
+    one = run_pdhg(lp, cfg)
+    with ShardedEngine(lp, 2) as eng:
+        sh = eng.solve(cfg)
+        assert eng.describe()["halo_x"]
+    assert np.array_equal(sh.iterate.x, one.iterate.x)
+    assert np.array_equal(sh.iterate.y, one.iterate.y)
+
+
+def test_cancel_stops_the_loop():
+    lp = lpgen.random_equality_lp(5000, 20000, 8, seed=3)[0]
+    import ctypes
+    flag = (ctypes.c_uint8 * 1)(0)
+    threading.Timer(0.3, lambda: flag.__setitem__(0, 1)).start()
+    t = time.perf_counter()
+    res = run_pdhg(lp, PdhgConfig(max_iterations=10**9), cancel=flag)
+    assert res.stop == PdhgStopReason.kCancelled
+    assert time.perf_counter() - t < 20
+    assert res.iterations > 0
+
+
+def test_time_limit_stops_the_loop():
+    lp = lpgen.random_equality_lp(5000, 20000, 8, seed=3)[0]
+    res = run_pdhg(lp, PdhgConfig(max_iterations=10**9, time_limit=0.5))
+    assert res.stop == PdhgStopReason.kTimeLimit
+    assert res.seconds < 10
+
+
+@pytest.mark.parametrize("interval", [2, 7])
+def test_check_interval_parity(interval, oracle):
+    lp = lpgen.small_equality_lp(40, 90, 0.2, 7)[0]
+    res = run_pdhg(lp, PdhgConfig(max_iterations=20000, check_interval=interval))
+    ref = oracle.run_pdhg(lp, config=dict(max_iterations=20000, check_interval=interval))
+    assert res.stop.name == {"converged": "kConverged",
+                             "iteration-limit": "kIterationLimit"}[ref["stop"]]
+    assert res.iterations == ref["iterations"]
+    assert res.iterations % interval == 0
+    assert rel(res.iterate.x, ref["x"]) <= 1e-6
+
+
+def test_iteration_log_format():
+    lines = []
+    lp = lpgen.small_equality_lp(40, 90, 0.2, 7)[0]
+    res = run_pdhg(lp, PdhgConfig(max_iterations=500, log_interval=100, log=lines.append))
+    # pdhg.cpp:332-340: "%lld\t%.6e\t%.6e\t%.6e\t%.3f\n" every log_interval checks
+    pat = re.compile(r"^(\d+)\t(\S+e[+-]\d\d)\t(\S+e[+-]\d\d)\t(\S+e[+-]\d\d)\t\d+\.\d{3}\n$")
+    its = [int(pat.match(ln).group(1)) for ln in lines]
+    assert its == [k for k in range(0, res.iterations + 1, 100)]  # check(0) included, as upstream
