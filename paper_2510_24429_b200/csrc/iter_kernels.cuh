@@ -172,39 +172,60 @@ static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied as 8-byte words");
 // (deterministic, one round of loads).
 __device__ __forceinline__ void reduce_partials(const double* rowsrc, int nrow, const double* colsrc,
                                                 int ncol, double* rowv, double* colv) {
-  const int lane = threadIdx.x & 31;
-  for (int fld = threadIdx.x >> 5; fld < kRowParts + kColParts; fld += blockDim.x / 32) {
+  // half-warp h takes field h (all 22 fields in one round with >= 11 warps);
+  // lane l of the half takes blocks l, l+16, ... with 8 loads in flight,
+  // accumulates them in order, then a fixed butterfly within the half
+  const int hl = threadIdx.x & 15;
+  for (int fld = threadIdx.x >> 4; fld - static_cast<int>(threadIdx.x >> 4) < kRowParts + kColParts;
+       fld += blockDim.x / 16) {
+    const bool live = fld < kRowParts + kColParts;
     const bool is_row = fld < kRowParts;
     const int f = is_row ? fld : fld - kRowParts;
     const bool is_max = is_row ? ((kRowMaxMask >> f) & 1u) : ((kColMaxMask >> f) & 1u);
     const double* src = is_row ? rowsrc : colsrc;
     const int stride = is_row ? kRowParts : kColParts;
-    const int nb = is_row ? nrow : ncol;
+    const int nb = live ? (is_row ? nrow : ncol) : 0;
     double a = 0.0;
-    for (int b = lane; b < nb; b += 32) {
-      const double v = __ldcg(src + b * stride + f);
-      a = is_max ? amax(a, v) : a + v;
+    for (int b0 = hl; b0 < nb; b0 += 16 * 8) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int b = b0 + 16 * k;
+        v[k] = b < nb ? __ldcg(src + b * stride + f) : 0.0;
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (b0 + 16 * k < nb) a = is_max ? amax(a, v[k]) : a + v[k];
     }
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) {
+    for (int off = 8; off > 0; off >>= 1) {
       const double o = __shfl_xor_sync(0xffffffffu, a, off);
       a = is_max ? amax(a, o) : a + o;
     }
-    if (lane == 0) (is_row ? rowv : colv)[f] = a;
+    if (hl == 0 && live) (is_row ? rowv : colv)[f] = a;
   }
   __syncthreads();
 }
 
-// decide() on a shared-memory copy of the control block (one coalesced read
-// and one write instead of a chain of dependent global round trips).
-__device__ void decide_and_store(const IterParams& p, const StepInfo& si, const double* rowv,
-                                 const double* colv) {
+// The control block's shared copy; loaded before the partial reduction so
+// the two round trips overlap.
+__device__ __forceinline__ Ctrl& ctrl_smem() {
   __shared__ Ctrl cs;
+  return cs;
+}
+__device__ __forceinline__ void load_ctrl(const IterParams& p) {
   constexpr int kWords = sizeof(Ctrl) / 8;
-  long long* csw = reinterpret_cast<long long*>(&cs);
+  long long* csw = reinterpret_cast<long long*>(&ctrl_smem());
   const long long* gw = reinterpret_cast<const long long*>(p.ctrl);
   for (int w = threadIdx.x; w < kWords; w += blockDim.x) csw[w] = __ldcg(gw + w);
-  __syncthreads();
+}
+
+// Expects load_ctrl() and a block barrier before it.
+__device__ void decide_and_store(const IterParams& p, const StepInfo& si, const double* rowv,
+                                 const double* colv) {
+  Ctrl& cs = ctrl_smem();
+  constexpr int kWords = sizeof(Ctrl) / 8;
+  long long* csw = reinterpret_cast<long long*>(&cs);
   if (threadIdx.x == 0) {
     cs.t_cols_start = globaltimer();  // debug: reuse as "partials reduced" stamp
     decide(p, si, &cs, rowv, colv);
@@ -221,7 +242,8 @@ __device__ void decide_and_store(const IterParams& p, const StepInfo& si, const 
 __device__ void finalize(const IterParams& p, const StepInfo& si) {
   __shared__ double rowv[kRowParts];
   __shared__ double colv[kColParts];
-  reduce_partials(p.rowp, p.row_grid, p.colp, p.col_grid, rowv, colv);
+  if (p.xpart_loc == nullptr) load_ctrl(p);
+  reduce_partials(p.rowp, p.row_grid, p.colp, p.col_grid, rowv, colv);  // ends with a barrier
   if (p.xpart_loc != nullptr) {
     if (threadIdx.x < kRowParts) p.xpart_loc[threadIdx.x] = rowv[threadIdx.x];
     if (threadIdx.x < kColParts) p.xpart_loc[kRowParts + threadIdx.x] = colv[threadIdx.x];
@@ -239,6 +261,7 @@ __global__ void __launch_bounds__(kEpiBlock) k_finalize_shard(const IterParams p
   if (!read_step(p, init != 0, si)) return;
   __shared__ double rowv[kRowParts];
   __shared__ double colv[kColParts];
+  load_ctrl(p);
   constexpr int W = kRowParts + kColParts;
   if (threadIdx.x < W) {
     const int f = threadIdx.x;
