@@ -5,11 +5,16 @@
 // reference's own CPU loop). Crossover is the reference's run_crossover in
 // both, compiled from /root/reference, so the two differ only in the PDHG.
 #include <algorithm>
+#include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <exception>
 #include <sstream>
 #include <string>
 
+#include <fstream>
+
+#include "cclp/mps.hpp"
 #include "cclp/race.hpp"
 #include "json.hpp"
 
@@ -70,6 +75,118 @@ int cclp_race_run(int m, int n, const int* colptr, const int* rowind, const doub
     }
     std::memcpy(out, s.c_str(), s.size() + 1);
     return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+// `solve <model.mps>` (SPEC bench_cli): read_mps_file -> run_race, then the
+// basis (write_basis, basis.hpp:92) and the solution file (objective header,
+// then "column value status" per line) when paths are given. Returns the SPEC
+// exit code: 0 solved, 2 time limit, 3 numerical failure / unsolved, 4 input
+// error; `out` receives the outcome JSON.
+int cclp_race_solve_file(const char* path, int mode, double eps_rel, double eps_cross, double eps_abs,
+                         double decrement, int pool, double time_limit, unsigned long long seed,
+                         const char* basis_out, const char* solution_out, char* out, int cap) {
+  cclp::LinearProgram lp;
+  try {
+    lp = cclp::read_mps_file(path);
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 4;
+  }
+  try {
+    cclp::RaceConfig cfg;
+    cfg.mode = mode ? cclp::RaceMode::kConcurrent : cclp::RaceMode::kBaseline;
+    cfg.tol.eps_rel = eps_rel;
+    cfg.tol.eps_cross = eps_cross;
+    cfg.tol.eps_abs = eps_abs;
+    cfg.tol.decrement = decrement;
+    cfg.worker_pool = pool;
+    cfg.time_limit = time_limit;
+    cfg.pdhg.seed = seed;
+    std::ostringstream events;
+    cfg.event_log = &events;
+    cclp::RaceOutcome o = cclp::run_race(lp, cfg);
+    nlohmann::json j = nlohmann::json::parse(o.to_json());
+    j["model"] = lp.name;
+    j["rows"] = lp.num_rows();
+    j["cols"] = lp.num_cols();
+    j["winning_threshold"] = o.winning_threshold;
+    std::int64_t pivots = o.final_result.cleanup_pivots;
+    j["pivots"] = pivots;
+    j["violation"] = o.final_result.abs_violation;
+    j["events"] = events.str();
+    if (o.status == cclp::RaceStatus::kSolved) {
+      const cclp::StandardFormMap sf = cclp::to_standard_form(lp);
+      if (basis_out && *basis_out) {
+        std::ofstream f(basis_out);
+        cclp::write_basis(cclp::EngineModel(sf.std_lp), o.final_result.basis, f);
+      }
+      if (solution_out && *solution_out) {
+        std::ofstream f(solution_out);
+        char line[256];
+        std::snprintf(line, sizeof line, "* objective %.17g\n", o.objective);
+        f << line;
+        std::vector<bool> basic(static_cast<size_t>(sf.std_lp.num_cols()), false);
+        for (auto jb : o.final_result.basis.basic)
+          if (jb < sf.std_lp.num_cols()) basic[static_cast<size_t>(jb)] = true;
+        for (cclp::Index jc = 0; jc < lp.num_cols(); ++jc) {
+          const std::string name = jc < static_cast<cclp::Index>(lp.col_names.size())
+                                       ? lp.col_names[static_cast<size_t>(jc)]
+                                       : "C" + std::to_string(jc);
+          const char* st = basic[static_cast<size_t>(jc)] ? "basic" : "nonbasic";
+          std::snprintf(line, sizeof line, "%s %.17g %s\n", name.c_str(), o.solution.x[jc], st);
+          f << line;
+        }
+      }
+    }
+    const std::string str = j.dump();
+    if (static_cast<int>(str.size()) + 1 > cap) {
+      g_err = "cclp_race_solve_file: output buffer too small";
+      return 4;
+    }
+    std::memcpy(out, str.c_str(), str.size() + 1);
+    switch (o.status) {
+      case cclp::RaceStatus::kSolved: return 0;
+      case cclp::RaceStatus::kTimeLimit: return 2;
+      default: return 3;
+    }
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return 4;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 3;
+  }
+}
+
+// write_mps (mps.hpp:50) of an LP given as arrays (rows named R<i>, columns
+// C<j>, equality rows where lower == upper): test and bench fixtures.
+int cclp_race_write_mps(int m, int n, const int* colptr, const int* rowind, const double* val,
+                        const double* c, const double* rl, const double* ru, const double* cl,
+                        const double* cu, const char* name, const char* path) {
+  try {
+    cclp::LinearProgram lp;
+    lp.name = name ? name : "LP";
+    lp.objective_name = "OBJ";
+    lp.A = cclp::SparseMat(Eigen::Map<cclp::SparseMat>(m, n, colptr[n], colptr, rowind, val));
+    lp.c = vec(c, n);
+    lp.row_lower = vec(rl, m);
+    lp.row_upper = vec(ru, m);
+    lp.col_lower = vec(cl, n);
+    lp.col_upper = vec(cu, n);
+    lp.sense.assign(static_cast<size_t>(m), cclp::RowSense::kEq);
+    for (int i = 0; i < m; ++i) {
+      if (rl[i] == ru[i]) continue;
+      lp.sense[static_cast<size_t>(i)] = std::isfinite(ru[i]) ? cclp::RowSense::kLe : cclp::RowSense::kGe;
+    }
+    for (int i = 0; i < m; ++i) lp.row_names.push_back("R" + std::to_string(i));
+    for (int j = 0; j < n; ++j) lp.col_names.push_back("C" + std::to_string(j));
+    std::ofstream f(path);
+    cclp::write_mps(lp, f);
+    return f.good() ? 0 : 1;
   } catch (const std::exception& e) {
     g_err = e.what();
     return 1;

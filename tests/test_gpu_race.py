@@ -36,3 +36,13 @@ def test_gpu_race_baseline_equals_concurrent_basis():
     assert b["winner"] == "main"
     assert b["basic"] == c["basic"]
     assert b["objective"] == pytest.approx(c["objective"], rel=1e-9)
+
+
+def test_cli_solve_on_gpu(tmp_path):
+    from integration import cli
+    lp = lpgen.transportation_lp(20, 30, seed=3)
+    cli.write_mps(lp, str(tmp_path / "t.mps"), "T")
+    rc, g = cli.solve_file(str(tmp_path / "t.mps"), "concurrent", pdhg="gpu")
+    rc2, c = cli.solve_file(str(tmp_path / "t.mps"), "concurrent", pdhg="cpu")
+    assert rc == rc2 == 0
+    assert g["objective"] == pytest.approx(c["objective"], rel=1e-9)
