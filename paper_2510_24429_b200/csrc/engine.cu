@@ -213,6 +213,9 @@ struct Context {
   };
   std::vector<Panel> panels;
   int panel_grid = 0;
+  long long panel_gn = 0;          // shards: the full matrix's column count
+  std::vector<int> panel_cb;       // shards: every shard's column bounds
+  std::vector<int> panel_G_hint;   // shards: the full matrix's per-panel G
   void build_panels(long long gather_len);
   bool use_panels() const { return !panels.empty() && !exact; }
   PanelArgs panel_args(int k) const;
@@ -579,9 +582,22 @@ SpmvPlan Context::plan(bool rows_side) const {
 void Context::build_panels(long long gather_len) {
   long long pb = static_cast<long long>(kPanelBytes);
   if (const char* e = std::getenv("CCLP_CU_PANEL_BYTES")) pb = std::max(64LL, std::atoll(e));  // tests
-  const long long K = (gather_len * 8 + pb - 1) / pb;
+  // Panels are defined on the ORIGINAL column space (a shard maps them into
+  // its padded gather space), and a shard takes each panel's G from the full
+  // matrix, so sharded sums equal the single-device sums bit for bit.
+  const long long gn = panel_gn > 0 ? panel_gn : gather_len;
+  const long long K = (gn * 8 + pb - 1) / pb;
   if (K < 3 || m == 0 || nnz == 0) return;  // x (nearly) fits the L2: one pass
-  const long long W = (gather_len + K - 1) / K;
+  const long long W = (gn + K - 1) / K;
+  auto to_gather = [&](long long c) -> long long {  // original column -> gather index
+    if (panel_cb.empty()) return std::min(c, gather_len);
+    const int P = static_cast<int>(panel_cb.size()) - 1;
+    if (c >= gn) return static_cast<long long>(P) * Sn;
+    int q = static_cast<int>(std::upper_bound(panel_cb.begin(), panel_cb.end(), static_cast<int>(c)) -
+                             panel_cb.begin()) - 1;
+    q = std::max(0, std::min(q, P - 1));
+    return static_cast<long long>(q) * Sn + (c - panel_cb[q]);
+  };
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
   panel_grid = 2 * sms;
@@ -592,8 +608,8 @@ void Context::build_panels(long long gather_len) {
   panels.resize(K);
   for (long long k = 0; k < K; ++k) {
     Panel& pn = panels[k];
-    const int lo = static_cast<int>(std::min<long long>(k * W, gather_len));
-    const int hi = static_cast<int>(std::min<long long>((k + 1) * W, gather_len));
+    const int lo = static_cast<int>(to_gather(std::min(k * W, gn)));
+    const int hi = static_cast<int>(to_gather(std::min((k + 1) * W, gn)));
     k_panel_count<<<blocks_for(m + 1), kBlock, 0, stream>>>(rowptr, colind, m, lo, hi, cnt);
     CKL("panel count");
     pn.ptr = alloc<int>(static_cast<size_t>(m) + 1);
@@ -607,7 +623,7 @@ void Context::build_panels(long long gather_len) {
     pn.val = alloc<double>(total);
     k_panel_fill<<<blocks_for(m), kBlock, 0, stream>>>(rowptr, colind, m, lo, pn.ptr, pn.idx, pn.perm);
     CKL("panel fill");
-    pn.G = pick_group(pn.nnz, m);
+    pn.G = k < static_cast<long long>(panel_G_hint.size()) ? panel_G_hint[k] : pick_group(pn.nnz, m);
     plan_side_ptr(pn.ptr, m, pn.G, pn.sp);
     pn.start = plan_starts_ptr(pn.ptr, m, pn.sp, panel_grid);
     pn.sp.wrow.clear();

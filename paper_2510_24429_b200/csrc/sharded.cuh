@@ -233,7 +233,14 @@ void Context::shard_from(Context& F, int rank, int P, const std::vector<int>& rb
   CK(cudaMemsetAsync(xpart, 0, sizeof(double) * P * (kRowParts + kColParts), stream));
   release(d_rb);
   release(d_cb);
+  panel_gn = F.n;  // column panels on the full matrix's column space
+  panel_cb = cb;
+  for (const auto& pn : F.panels) panel_G_hint.push_back(pn.G);
   partition();  // setup-kernel grids, the local SpMV plans and their tuned geometry
+  for (auto& pn : panels)  // the shard never runs setup(): its panels take the scaled values here
+    if (pn.nnz > 0)
+      k_gather_vals<<<blocks_for(pn.nnz), kBlock, 0, stream>>>(pn.perm, pn.nnz, sval_csr, pn.val);
+  CKL("shard panel values");
 }
 
 // ---- the sharded solve ---------------------------------------------------------
