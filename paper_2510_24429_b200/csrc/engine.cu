@@ -447,11 +447,9 @@ void Context::partition() {
   // blocks. The iteration's SpMV kernels run one full wave of resident
   // blocks (grid-stride over rows); the epilogues one wave of kEpiBlock-thread
   // blocks, so finalize reduces only that many partials.
-  int sms = 148, occ_r = 1, occ_c = 1, occ_d = 1, occ_p = 1;
+  int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  (void)occ_r;
-  (void)occ_c;
-  epi_grid = sms * std::max(1, std::min(occ_d, occ_p));
+  epi_grid = sms;  // one wave of kEpiBlock-thread epilogue blocks (register-limited to 1 per SM)
   const long long cap = 148 * 4;
   row_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (m + 31) / 32 + nnz / 1024)));
   col_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (n + 31) / 32 + nnz / 1024)));
