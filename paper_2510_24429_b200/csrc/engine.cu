@@ -140,6 +140,40 @@ void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t st, 
 }
 
 // Calls f(std::integral_constant<int, G>) for the runtime group size G.
+// Host <-> device copies of the caller's arrays (the LP in, the result out).
+// Pinned memory goes straight to the DMA engine; large pageable arrays are
+// staged through two pinned chunks filled (or drained) by several host
+// threads while the other chunk is in flight - the driver's own pageable path
+// is a single-threaded bounce (~8 GB/s).
+constexpr size_t kStageChunk = size_t(32) << 20;
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  if (bytes < (size_t(4) << 20) || hw == 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = (bytes + hw - 1) / hw;
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < hw && size_t(t) * per < bytes; ++t) {
+    const size_t a = size_t(t) * per;
+    th.emplace_back([=] {
+      std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, std::min(per, bytes - a));
+    });
+  }
+  std::memcpy(dst, src, std::min(per, bytes));
+  for (auto& t : th) t.join();
+}
+
 template <class F>
 void with_group(int G, F&& f) {
   switch (G) {
@@ -164,6 +198,8 @@ void with_group_long(int G, bool lng, F&& f) {
 }
 
 }  // namespace
+
+void gaussian_start(uint64_t seed, long long n, double* v);
 
 struct Context {
   int device = 0;
@@ -283,6 +319,55 @@ struct Context {
     pinned.emplace_back(p, bytes);
     return static_cast<T*>(p);
   }
+  double* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  void ensure_stage() {
+    for (int b = 0; b < 2; ++b)
+      if (!stage[b]) {
+        stage[b] = host_alloc<double>(kStageChunk / sizeof(double));
+        CK(cudaEventCreateWithFlags(&stage_ev[b], cudaEventDisableTiming));
+      }
+  }
+  void h2d(void* dst, const void* src, size_t bytes) {
+    if (bytes == 0) return;
+    if (bytes < 2 * kStageChunk || is_pinned(src)) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
+      return;
+    }
+    ensure_stage();
+    size_t k = 0;
+    for (size_t off = 0; off < bytes; off += kStageChunk, ++k) {
+      const int b = static_cast<int>(k & 1);
+      CK(cudaEventSynchronize(stage_ev[b]));  // the chunk's previous DMA (this or an earlier call)
+      const size_t len = std::min(kStageChunk, bytes - off);
+      par_memcpy(stage[b], static_cast<const char*>(src) + off, len);
+      CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, stage[b], len, cudaMemcpyHostToDevice, stream));
+      CK(cudaEventRecord(stage_ev[b], stream));
+    }
+  }
+  void d2h(void* dst, const void* src, size_t bytes) {  // synchronous on return
+    if (bytes == 0) return;
+    if (bytes < 2 * kStageChunk || is_pinned(dst)) {
+      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      return;
+    }
+    ensure_stage();
+    const size_t nch = (bytes + kStageChunk - 1) / kStageChunk;
+    auto issue = [&](size_t k) {
+      const size_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
+      CK(cudaMemcpyAsync(stage[k & 1], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
+                         stream));
+      CK(cudaEventRecord(stage_ev[k & 1], stream));
+    };
+    issue(0);
+    for (size_t k = 0; k < nch; ++k) {
+      if (k + 1 < nch) issue(k + 1);
+      CK(cudaEventSynchronize(stage_ev[k & 1]));
+      const size_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
+      par_memcpy(static_cast<char*>(dst) + off, stage[k & 1], len);
+    }
+  }
   void mark(int k) {
     CK(cudaStreamSynchronize(stream));
     const auto now = std::chrono::steady_clock::now();
@@ -302,6 +387,10 @@ struct Context {
   void ruiz(int iterations);
   double power_norm(int iterations, uint64_t seed, bool scaled, bool pregenerated = false);
   double* h_v0 = nullptr;  // pinned start vector of the power iteration
+  // h_v0 holds the start vector of seed v0_seed (a pure function of (seed, n)):
+  // the default seed's is generated on a host thread during upload / CSR build
+  std::thread v0_thread;
+  unsigned long long v0_seed = ~0ull;
   // ---- sharded mode (sharded.cuh): this context is shard `shard_rank` of
   // `shard_count`, owning rows [r0, r0 + m) of A and columns [c0, c0 + n)
   bool own_stream = true;
@@ -326,6 +415,7 @@ struct Context {
 };
 
 Context::~Context() {
+  if (v0_thread.joinable()) v0_thread.join();
   cudaSetDevice(device);
   if (graph) cudaGraphExecDestroy(graph);
   if (stream) {
@@ -352,6 +442,8 @@ Context::~Context() {
   }
   cudaGetLastError();
   for (auto& pb : pinned) pinned_release(pb.first, pb.second);
+  for (auto& e : stage_ev)
+    if (e) cudaEventDestroy(e);
   if (ev_snap) cudaEventDestroy(ev_snap);
   if (ev_a) cudaEventDestroy(ev_a);
   if (ev_b) cudaEventDestroy(ev_b);
@@ -379,12 +471,12 @@ void Context::upload(const cclp_cu_lp* lp) {
   b = alloc<double>(m);
   r = alloc<double>(m);
   s = alloc<double>(n);
-  CK(cudaMemcpyAsync(colptr, lp->colptr, sizeof(int) * (n + 1), cudaMemcpyHostToDevice, stream));
-  CK(cudaMemcpyAsync(rowind, lp->rowind, sizeof(int) * nnz, cudaMemcpyHostToDevice, stream));
-  CK(cudaMemcpyAsync(val_csc, lp->val, sizeof(double) * nnz, cudaMemcpyHostToDevice, stream));
-  CK(cudaMemcpyAsync(c, lp->c, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
-  CK(cudaMemcpyAsync(l, lp->col_lower, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
-  CK(cudaMemcpyAsync(u, lp->col_upper, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+  h2d(colptr, lp->colptr, sizeof(int) * (n + 1));
+  h2d(rowind, lp->rowind, sizeof(int) * nnz);
+  h2d(val_csc, lp->val, sizeof(double) * nnz);
+  h2d(c, lp->c, sizeof(double) * n);
+  h2d(l, lp->col_lower, sizeof(double) * n);
+  h2d(u, lp->col_upper, sizeof(double) * n);
   // equality form: b = row_lower (= row_upper); checked on the host view
   equality = true;
   for (int i = 0; i < m; ++i) {
@@ -394,7 +486,12 @@ void Context::upload(const cclp_cu_lp* lp) {
       break;
     }
   }
-  CK(cudaMemcpyAsync(b, lp->row_lower, sizeof(double) * m, cudaMemcpyHostToDevice, stream));
+  h2d(b, lp->row_lower, sizeof(double) * m);
+  if (m > 0 && n > 0 && nnz > 0) {  // the default seed's start vector, behind the ingest
+    h_v0 = host_alloc<double>(n);
+    v0_seed = 0;
+    v0_thread = std::thread(gaussian_start, 0ull, static_cast<long long>(n), h_v0);
+  }
   mark(0);
   build_csr();
   mark(1);
@@ -819,52 +916,80 @@ void Context::ruiz(int iterations) {
 }
 
 // The power iteration's start vector, v_j = normal_distribution(mt19937_64(
-// seed + 0x9e3779b97f4a7c15)) (pdhg.cpp:49-52), restated in two stages so it
-// costs ~3 ns per entry instead of the reference's ~20: (1) one thread runs the
-// engine and libstdc++'s polar-method rejection loop (generate_canonical<double,
-// 53> on a 64-bit engine is exactly u * 2^-64, clamped below 1), keeping the
-// accepted (x, y, r2); (2) all host cores apply mult = sqrt(-2 log(r2) / r2)
-// with the same libm. Entry 2k is y*mult (the returned value), 2k+1 is x*mult
-// (the saved one), then `* stddev + mean` = `* 1.0 + 0.0`. Bit-identical to
-// std::normal_distribution<double> (checked against the oracle in tests).
+// seed + 0x9e3779b97f4a7c15)) (pdhg.cpp:49-52), bit-identical to libstdc++ but
+// parallel. libstdc++'s polar method draws attempts of exactly two engine
+// outputs (generate_canonical<double, 53> on a 64-bit engine is u * 2^-64,
+// clamped below 1), accepts those with 0 < r2 <= 1, and returns y*mult then
+// x*mult per accepted attempt (mult = sqrt(-2 log(r2) / r2), then
+// `* stddev + mean` = `* 1.0 + 0.0`). Attempt boundaries are therefore fixed
+// in the raw engine stream: only the engine itself is serial. The calling
+// thread generates raw chunks while a team of host threads decides the
+// previous chunk's attempts, prefix-sums the accepted ones and writes their
+// entries (checked against the oracle's sequential restatement in tests).
 void gaussian_start(uint64_t seed, long long n, double* v) {
+  if (n <= 0) return;
   std::mt19937_64 rng(seed + 0x9e3779b97f4a7c15ull);
-  const long long pairs = n / 2;  // full pairs; an odd n leaves one tail pair
-  auto canon = [&rng]() {
-    const double r = static_cast<double>(rng()) * 0x1p-64;
+  const long long pairs = (n + 1) / 2;  // the last one half-used when n is odd
+  constexpr long long kAttempts = 1 << 19;  // per chunk
+  std::vector<uint64_t> buf[2] = {std::vector<uint64_t>(2 * kAttempts),
+                                  std::vector<uint64_t>(2 * kAttempts)};
+  const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  auto canon = [](uint64_t u) {
+    const double r = static_cast<double>(u) * 0x1p-64;
     return r >= 1.0 ? std::nextafter(1.0, 0.0) : r;
   };
-  auto draw = [&](double& x, double& y) {
-    double r2;
-    do {
-      x = 2.0 * canon() - 1.0;
-      y = 2.0 * canon() - 1.0;
-      r2 = x * x + y * y;
-    } while (r2 > 1.0 || r2 == 0.0);
+  auto attempt = [&](const uint64_t* d, long long a, double& x, double& y, double& r2) {
+    x = 2.0 * canon(d[2 * a]) - 1.0;
+    y = 2.0 * canon(d[2 * a + 1]) - 1.0;
+    r2 = x * x + y * y;
+    return !(r2 > 1.0 || r2 == 0.0);
   };
-  // stage 1 (serial): accepted (x, y) stored in place as v[2k] = y, v[2k+1] = x
-  for (long long k = 0; k < pairs; ++k) draw(v[2 * k + 1], v[2 * k]);
-  auto finish = [](double x, double y, double* out2, bool both) {
-    const double r2 = x * x + y * y;  // recomputed: the same two products and sum
-    const double mult = std::sqrt(-2 * std::log(r2) / r2);
-    out2[0] = y * mult * 1.0 + 0.0;
-    if (both) out2[1] = x * mult * 1.0 + 0.0;
+  // decides chunk d's attempts and writes its accepted pairs from pair `base`
+  auto process = [&](const uint64_t* d, long long base) -> long long {
+    std::vector<long long> cnt(T + 1, 0);
+    const long long per = (kAttempts + T - 1) / T;
+    auto run = [&](auto&& body) {
+      std::vector<std::thread> th;
+      for (int t = 1; t < T; ++t) th.emplace_back(body, t);
+      body(0);
+      for (auto& x : th) x.join();
+    };
+    run([&](int t) {
+      long long c = 0;
+      double x, y, r2;
+      for (long long a = t * per; a < std::min(kAttempts, (t + 1) * per); ++a) c += attempt(d, a, x, y, r2);
+      cnt[t + 1] = c;
+    });
+    for (int t = 0; t < T; ++t) cnt[t + 1] += cnt[t];
+    run([&](int t) {
+      long long k = base + cnt[t];
+      double x, y, r2;
+      for (long long a = t * per; a < std::min(kAttempts, (t + 1) * per) && k < pairs; ++a) {
+        if (!attempt(d, a, x, y, r2)) continue;
+        const double mult = std::sqrt(-2 * std::log(r2) / r2);
+        v[2 * k] = y * mult * 1.0 + 0.0;
+        if (2 * k + 1 < n) v[2 * k + 1] = x * mult * 1.0 + 0.0;
+        ++k;
+      }
+    });
+    return cnt[T];
   };
-  if (n & 1) {
-    double x, y;
-    draw(x, y);
-    finish(x, y, v + n - 1, false);
+  auto fill = [&](std::vector<uint64_t>& b) {
+    for (auto& w : b) w = rng();
+  };
+  long long done = 0;
+  int cur = 0;
+  fill(buf[cur]);
+  while (true) {
+    long long got = 0;
+    std::thread worker([&, cur] { got = process(buf[cur].data(), done); });
+    const bool more = true;
+    if (more) fill(buf[cur ^ 1]);  // the next chunk while this one is decided
+    worker.join();
+    done += got;
+    if (done >= pairs) break;
+    cur ^= 1;
   }
-  // stage 2 (all cores): the transcendental half
-  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
-  const long long per = std::max<long long>(1 << 16, (pairs + hw - 1) / hw);
-  auto work = [&](long long a, long long b) {
-    for (long long k = a; k < b; ++k) finish(v[2 * k + 1], v[2 * k], v + 2 * k, true);
-  };
-  std::vector<std::thread> th;
-  for (long long a = per; a < pairs; a += per) th.emplace_back(work, a, std::min(pairs, a + per));
-  work(0, std::min(pairs, per));
-  for (auto& t : th) t.join();
 }
 
 // estimate_matrix_norm (pdhg.cpp:46-65) on the scaled or unscaled matrix.
@@ -875,7 +1000,11 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
   if (m == 0 || n == 0 || nnz == 0) return 0.0;
   // start vector: mt19937_64 + normal_distribution, as the reference (:49-52)
   if (!h_v0) h_v0 = host_alloc<double>(n);
-  if (!pregenerated) gaussian_start(seed, n, h_v0);
+  if (!pregenerated) {
+    if (v0_thread.joinable()) v0_thread.join();
+    if (v0_seed != seed) gaussian_start(seed, n, h_v0);
+    v0_seed = seed;
+  }
   const double* v0 = h_v0;
   double* v = wn;
   double* u = wn2;
@@ -992,9 +1121,13 @@ void Context::setup(const cclp_cu_config& cfg) {
   phase_t0 = std::chrono::steady_clock::now();
   // the power iteration's start vector is host work: overlap it with the
   // device-side norms, Ruiz passes and value scaling
+  if (v0_thread.joinable()) v0_thread.join();
   if (!h_v0) h_v0 = host_alloc<double>(n);
   std::thread rng_thread;
-  if (m > 0 && n > 0 && nnz > 0) rng_thread = std::thread(gaussian_start, cfg.seed, (long long)n, h_v0);
+  if (m > 0 && n > 0 && nnz > 0 && v0_seed != cfg.seed) {
+    v0_seed = cfg.seed;
+    rng_thread = std::thread(gaussian_start, cfg.seed, static_cast<long long>(n), h_v0);
+  }
   struct Joiner {
     std::thread& t;
     ~Joiner() { if (t.joinable()) t.join(); }
@@ -1546,9 +1679,9 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
       if (rep_valid) std::memcpy(st.result_report, st.R ? st.avg : st.cur, sizeof(st.result_report));
     }
     C.extract_view(view, st, !rep_valid);
-    CK(cudaMemcpyAsync(x_out, C.vx, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.stream));
-    CK(cudaMemcpyAsync(y_out, C.vy, sizeof(double) * C.m, cudaMemcpyDeviceToHost, C.stream));
-    CK(cudaMemcpyAsync(z_out, C.vz, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.stream));
+    C.d2h(x_out, C.vx, sizeof(double) * C.n);
+    C.d2h(y_out, C.vy, sizeof(double) * C.m);
+    C.d2h(z_out, C.vz, sizeof(double) * C.n);
     double rep[cclp_cu::kRepN];
     CK(cudaMemcpyAsync(rep, C.vrep, sizeof(rep), cudaMemcpyDeviceToHost, C.stream));
     C.mark(10);

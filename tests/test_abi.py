@@ -105,7 +105,7 @@ def test_no_cpu_fallback_in_product():
             assert "oracle" not in src.replace("# ", ""), f
 
 
-@pytest.mark.parametrize("seed,n", [(0, 1), (0, 7), (3, 1000), (12345, 200001)])
+@pytest.mark.parametrize("seed,n", [(0, 1), (0, 7), (3, 1000), (12345, 200001), (7, 3_000_001)])
 def test_gaussian_start_matches_oracle(seed, n):
     """The engine's two-stage start vector equals the oracle's sequential
     mt19937_64 + normal_distribution restatement bit for bit (host only)."""
