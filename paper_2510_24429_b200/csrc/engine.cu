@@ -791,7 +791,9 @@ void Context::tune_spmv() {
       for (int rpg : {1, 2}) {
         if (force && std::atoi(force) != rpg) continue;
         std::vector<float> t;
-        for (int rep = 0; rep < 6; ++rep) {
+        // 5 timed samples for short SpMVs; 3 once a launch costs > 200 us
+        const int reps = (nnz > 30'000'000) ? 4 : 6;
+        for (int rep = 0; rep < reps; ++rep) {
           launch_side(!rows_side, 2, 1);
           CK(cudaEventRecord(ev_a, stream));
           launch_side(rows_side, per_sm, rpg);
