@@ -176,3 +176,34 @@ def test_rerun_bit_identical():
     assert np.array_equal(a.iterate.x, b.iterate.x)
     assert np.array_equal(a.iterate.y, b.iterate.y)
     assert a.report.maxresid_rel == b.report.maxresid_rel
+
+
+def _edge_lps():
+    from paper_2510_24429_b200.lp import csc_from_triplets
+    out = []
+    # an empty column (never touched by A) and an empty row (b = 0)
+    rows, cols, vals = [0, 1, 1, 2], [0, 0, 2, 3], [1.0, 2.0, -1.0, 1.5]
+    colptr, rowind, val = csc_from_triplets(4, 5, rows, cols, vals)
+    out.append(("empty_row_col", LinearProgram(4, 5, colptr.astype(np.int32), rowind, val,
+                                               np.array([1.0, 2.0, 0.5, 1.0, 3.0]),
+                                               np.array([1.0, 1.0, 0.0, 0.0]),
+                                               np.array([1.0, 1.0, 0.0, 0.0]), np.zeros(5),
+                                               np.full(5, INF))))
+    # boxed and free columns with negative lower bounds
+    lp = lpgen.small_equality_lp(10, 24, 0.3, 11)[0]
+    lp.col_lower = np.where(np.arange(24) % 3 == 0, -INF, -1.0)
+    lp.col_upper = np.where(np.arange(24) % 4 == 0, INF, 3.0)
+    out.append(("boxed_free_mix", lp))
+    return out
+
+
+@pytest.mark.parametrize("name,lp", _edge_lps())
+@pytest.mark.parametrize("iters", [0, 3, 500])
+def test_edge_lp_parity(name, lp, iters, oracle):
+    res = run_pdhg(lp, PdhgConfig(max_iterations=iters))
+    ref = oracle.run_pdhg(lp, config=dict(max_iterations=iters))
+    assert res.iterations == ref["iterations"]
+    assert res.restarts == ref["restarts"]
+    assert rel(res.iterate.x, ref["x"]) <= REL_TOL
+    assert rel(res.iterate.y, ref["y"]) <= REL_TOL
+    assert rel(res.iterate.z, ref["z"]) <= REL_TOL
