@@ -98,11 +98,13 @@ void pinned_release(void* p, size_t bytes) {
 
 // Lanes per row from the mean row length L. A fixed rule (never timing
 // based): G sets the per-row summation order, so it must not vary between
-// runs. Thresholds from tools/spmv_bench.cu on C1-C4 (profiles/r1_spmv_*):
-// L ~ 2 -> 2, L 9-24 -> 4, L ~ 50 -> 8, L ~ 100 -> 16, L >= 160 -> 32.
+// runs. Thresholds measured on B200 (profiles/r1/history/): L <= 8 -> 2
+// (C1 columns, C5 column panels at L ~ 5.5: G 1/2/4 = 4.40/4.22/4.69 ms),
+// L 9-24 -> 4 (C2/C4 columns, C4 rows), L ~ 50 -> 8, L ~ 100 -> 16,
+// L >= 160 -> 32.
 int pick_group(long long nnz, long long rows) {
   const double L = rows > 0 ? static_cast<double>(nnz) / static_cast<double>(rows) : 0.0;
-  if (L <= 3.0) return 2;
+  if (L <= 8.0) return 2;
   if (L <= 24.0) return 4;
   if (L <= 64.0) return 8;
   if (L <= 160.0) return 16;
@@ -719,6 +721,7 @@ void Context::build_panels(long long gather_len) {
     k_panel_fill<<<blocks_for(m), kBlock, 0, stream>>>(rowptr, colind, m, lo, pn.ptr, pn.idx, pn.perm);
     CKL("panel fill");
     pn.G = k < static_cast<long long>(panel_G_hint.size()) ? panel_G_hint[k] : pick_group(pn.nnz, m);
+    if (const char* e = std::getenv("CCLP_CU_PANEL_G")) pn.G = std::atoi(e);  // A/B experiments only
     plan_side_ptr(pn.ptr, m, pn.G, pn.sp);
     pn.start = plan_starts_ptr(pn.ptr, m, pn.sp, panel_grid);
     pn.sp.wrow.clear();
