@@ -3,7 +3,7 @@
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-A step is one batch of `--iters-per-step` PDHG iterations (reference loop
+A step is one batch of `--iters-per-step` (500) PDHG iterations (reference loop
 body, check_interval = 1: both residual reports, restart and stop decisions
 every iteration) on device-resident state. `value` = total iterations / max
 over ranks of the device time of the K timed steps (CUDA events on the engine
@@ -79,10 +79,14 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            t = time.time()  # the timed region starts once the sampler is live
+            while not self.lines and time.time() - t < 5.0:
+                time.sleep(0.01)
+            self.lines.clear()
         except Exception:
             self.proc = None
         return self
@@ -291,7 +295,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--iters-per-step", type=int, default=100)
+    ap.add_argument("--iters-per-step", type=int, default=500)
     ap.add_argument("--e2e-iters", type=int, default=2000)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-iters", type=int, default=20)
