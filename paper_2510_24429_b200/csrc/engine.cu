@@ -401,6 +401,10 @@ struct Context {
   double* y_full = nullptr;  // [P * Sm] padded full y (gather source of the column SpMV)
   double* xpart = nullptr;   // [P][kRowParts + kColParts] exchanged report sums
   double* vparts = nullptr;  // [kRowParts + kColParts] report sums of the last view
+  unsigned long long* push_flags = nullptr;  // [3][kMaxPushShards] peer epochs (push transport)
+  unsigned* push_counter = nullptr;          // [2]
+  bool ipc_buffers = false;                  // exchange buffers from cudaMalloc (CUDA IPC)
+  std::vector<void*> ipc_owned;
   void setup(const cclp_cu_config& cfg);
   void init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thresholds,
                   int nthr, bool launch_init);
@@ -421,12 +425,18 @@ Context::~Context() {
   cudaSetDevice(device);
   if (graph) cudaGraphExecDestroy(graph);
   if (stream) {
+    for (void* q : ipc_owned) {  // cudaMalloc'ed (exported over IPC): not pool memory
+      if (q == x_full) x_full = nullptr;
+      if (q == y_full) y_full = nullptr;
+      if (q == xpart) xpart = nullptr;
+      if (q == push_flags) push_flags = nullptr;
+    }
     void* ptrs[] = {colptr, rowind, rowptr, colind, val_csc, val_csr, sval_csc, sval_csr, c, l, u, b,
                     r, s, row_start, col_start, spmv_row_start, spmv_col_start, rowp, colp, work_part,
                     counter, ctrl, log, thr, t0, scalars, pctrl, iflags, amb_idx, wn, wn2, wm, vx, vy,
                     vz, vrep, plan_rows.seg, plan_rows.lr_first, plan_rows.part, plan_rows.cnt,
                     plan_cols.seg, plan_cols.lr_first, plan_cols.part, plan_cols.cnt, x_full, y_full,
-                    xpart, vparts};
+                    xpart, vparts, push_flags, push_counter};
     for (void* p : ptrs) release(p);
     for (int k = 0; k < 3; ++k)
       for (int q = 0; q < 2; ++q) release(xc[k][q]);
@@ -442,6 +452,7 @@ Context::~Context() {
     cudaStreamSynchronize(stream);
     if (side) cudaStreamSynchronize(side);
   }
+  for (void* q : ipc_owned) cudaFree(q);
   cudaGetLastError();
   for (auto& pb : pinned) pinned_release(pb.first, pb.second);
   for (auto& e : stage_ev)
@@ -1855,13 +1866,13 @@ int cclp_cu_sharded_solve(cclp_cu_sharded* ctx, const cclp_cu_config* cfg_in, co
         st.halt = 0;
       }
       if (st.stop >= 0) break;
-      if (cancel != nullptr && *cancel) {
-        cancelled = true;
-        break;
-      }
-      if (std::isfinite(cfg.time_limit) &&
-          std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count() > cfg.time_limit) {
-        timed_out = true;
+      const bool want_cancel = cancel != nullptr && *cancel;
+      const bool want_time =
+          std::isfinite(cfg.time_limit) &&
+          std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count() > cfg.time_limit;
+      if (S.agree(want_cancel || want_time)) {  // all ranks stop together
+        cancelled = want_cancel || !want_time;
+        timed_out = !cancelled;
         break;
       }
       S.run_batch(k);

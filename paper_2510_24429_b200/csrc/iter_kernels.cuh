@@ -73,6 +73,43 @@ __device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepIn
   return true;
 }
 
+// ---- push transport (PushArgs, kernels.cuh) --------------------------------
+__device__ __forceinline__ void st_release_sys(unsigned long long* a, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+// Consumer side: wait until every peer has released epoch `value` for
+// `kind` (threads < P poll; bounded: a lost peer traps instead of hanging).
+__device__ __forceinline__ void push_wait(const PushArgs& ps, int kind, unsigned long long value) {
+  if (threadIdx.x < ps.P && static_cast<int>(threadIdx.x) != ps.rank) {
+    const unsigned long long* f = ps.my_flags + kind * kMaxPushShards + threadIdx.x;
+    long long spins = 0;
+    while (ld_acquire_sys(f) < value) {
+      __nanosleep(32);
+      if (++spins > (1LL << 30)) __trap();
+    }
+  }
+  __syncthreads();
+}
+// Producer side, after every thread's stores: the grid's last block
+// releases `value` for `kind` in every peer's flag array.
+__device__ __forceinline__ void push_signal_grid(const PushArgs& ps, int kind, unsigned long long value,
+                                                 unsigned* counter) {
+  __shared__ bool last_blk;
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) last_blk = atomicAdd(counter, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last_blk || threadIdx.x != 0) return;
+  __threadfence_system();
+  for (int q = 0; q < ps.P; ++q) st_release_sys(ps.flags[q] + kind * kMaxPushShards + ps.rank, value);
+  *counter = 0u;
+}
+
 // check(t+1) and everything after the step in the reference pass
 // (pdhg.cpp:128-130 error, 301-368 next pass: time, check, limit), taken by
 // thread 0 on a shared-memory copy of the control block.
@@ -242,8 +279,22 @@ __device__ void decide_and_store(const IterParams& p, const StepInfo& si, const 
 __device__ void finalize(const IterParams& p, const StepInfo& si) {
   __shared__ double rowv[kRowParts];
   __shared__ double colv[kColParts];
-  if (p.xpart_loc == nullptr) load_ctrl(p);
+  if (p.xpart_loc == nullptr && !p.push.on) load_ctrl(p);
   reduce_partials(p.rowp, p.row_grid, p.colp, p.col_grid, rowv, colv);  // ends with a barrier
+  if (p.push.on) {  // this shard's sums into every shard's [P][22], then release
+    constexpr int W = kRowParts + kColParts;
+    for (int k = threadIdx.x; k < p.push.P * W; k += blockDim.x) {
+      const int q = k / W, f = k % W;
+      p.push.part[q][p.push.rank * W + f] = f < kRowParts ? rowv[f] : colv[f - kRowParts];
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int q = 0; q < p.push.P; ++q)
+        st_release_sys(p.push.flags[q] + kPushPart * kMaxPushShards + p.push.rank,
+                       static_cast<unsigned long long>(si.t1 + 1));
+    return;
+  }
   if (p.xpart_loc != nullptr) {
     if (threadIdx.x < kRowParts) p.xpart_loc[threadIdx.x] = rowv[threadIdx.x];
     if (threadIdx.x < kColParts) p.xpart_loc[kRowParts + threadIdx.x] = colv[threadIdx.x];
@@ -261,6 +312,7 @@ __global__ void __launch_bounds__(kEpiBlock) k_finalize_shard(const IterParams p
   if (!read_step(p, init != 0, si)) return;
   __shared__ double rowv[kRowParts];
   __shared__ double colv[kColParts];
+  if (p.push.on) push_wait(p.push, kPushPart, static_cast<unsigned long long>(si.t1 + 1));
   load_ctrl(p);
   constexpr int W = kRowParts + kColParts;
   if (threadIdx.x < W) {
@@ -282,12 +334,28 @@ __global__ void __launch_bounds__(kEpiBlock) k_finalize_shard(const IterParams p
 // Sharded mode: this shard's slice of the next iterate, x_{t+2} =
 // xc[(t+1) % 3][R] after check(t+1), into its region of the full x
 // (idempotent, so it may run after a stop or halt).
-__global__ void k_select_x(const IterParams p, double* __restrict__ x_full_loc) {
+// With the push transport it stores the slice into every shard that gathers
+// it and releases epoch t+2 (the consuming step's t1 + 1); `initial` pushes
+// x_0 for the initial products (epoch 1).
+__global__ void k_select_x(const IterParams p, double* __restrict__ x_full_loc, int initial) {
   pdl_wait();
   const Ctrl* C = p.ctrl;
-  const double* __restrict__ src = p.xc[(C->iteration + 1) % 3][C->R];
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x)
-    x_full_loc[j] = src[j];
+  const double* __restrict__ src = initial ? p.xc[0][0] : p.xc[(C->iteration + 1) % 3][C->R];
+  if (!p.push.on) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x)
+      x_full_loc[j] = src[j];
+    return;
+  }
+  const PushArgs& ps = p.push;
+  const long long off = static_cast<long long>(ps.rank) * ps.Sn;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x) {
+    const double v = src[j];
+    const unsigned mk = ps.mask_x != nullptr ? ps.mask_x[j] : 0xFFu;
+    for (int q = 0; q < ps.P; ++q)
+      if ((mk >> q) & 1u) ps.x[q][off + j] = v;
+  }
+  push_signal_grid(ps, kPushX, initial ? 1ull : static_cast<unsigned long long>(C->iteration + 2),
+                   ps.counter + 1);
 }
 
 // Lean SpMV of one half-step: out[r] = sum_k M[r,k] vec[k] over CSR M.
@@ -373,6 +441,7 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows_panel(const IterParams
                                                                 const PanelArgs a) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
+  if (p.push.on) push_wait(p.push, kPushX, static_cast<unsigned long long>(si.t1 + 1));
   spmv_block_range<G, LONG>(a.plan, a.ptr, a.idx, a.val,
                             GatherPlain{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]}, p.ax[si.s1], 1,
                             a.accumulate);
@@ -382,6 +451,7 @@ template <int G, bool LONG>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
+  if (p.push.on) push_wait(p.push, kPushX, static_cast<unsigned long long>(si.t1 + 1));
   spmv_block_range<G, LONG>(p.plan_r, p.rowptr, p.colind, p.aval,
                             GatherPlain{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]},
                       p.ax[si.s1], p.rpg_rows);
@@ -391,6 +461,7 @@ template <int G, bool LONG>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_cols(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si)) return;
+  if (p.push.on) push_wait(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1));
   spmv_block_range<G, LONG>(p.plan_c, p.colptr, p.rowind, p.atval,
                             GatherPlain{p.yg != nullptr ? p.yg : p.y[si.s1]},
                       p.aty[si.s1], p.rpg_cols);
@@ -452,7 +523,14 @@ __global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init
       const double ysn = (si.R ? 0.0 : ys[k]) + yn;
       const double axsn = (si.R ? 0.0 : axs[k]) + axn[k];
       y1[i] = yn;
-      if (p.y_full_loc != nullptr) p.y_full_loc[i] = yn;
+      if (p.push.on) {  // fused push: into every shard that gathers this row
+        const unsigned mk = p.push.mask_y != nullptr ? p.push.mask_y[i] : 0xFFu;
+        const long long off = static_cast<long long>(p.push.rank) * p.push.Sm;
+        for (int q = 0; q < p.push.P; ++q)
+          if ((mk >> q) & 1u) p.push.y[q][off + i] = yn;
+      } else if (p.y_full_loc != nullptr) {
+        p.y_full_loc[i] = yn;
+      }
       ys1[i] = ysn;
       axs1[i] = axsn;
       if (nonfinite(yn)) acc[6] += 1.0;
@@ -464,6 +542,7 @@ __global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init
   }
   block_reduce<kRowParts, kRowMaxMask, kEpiBlock>(acc, red, out);
   if (threadIdx.x < kRowParts) p.rowp[blockIdx.x * kRowParts + threadIdx.x] = out[threadIdx.x];
+  if (p.push.on) push_signal_grid(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1), p.push.counter);
 }
 
 // Primal side: sums, column-side report partials, both next-x candidates;

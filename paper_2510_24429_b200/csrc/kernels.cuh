@@ -69,6 +69,26 @@ struct PanelArgs {
   int accumulate;  // 0: out = sum; 1: out += sum (panel order)
 };
 
+// Sharded push transport (sharded.cuh): the producers store their slice of
+// y, x and the report sums straight into every peer shard's full buffers
+// (NVLink P2P stores across GPUs, plain stores between shards on one GPU),
+// then release a per-(kind, source) epoch flag in every peer's flag array;
+// the consumers acquire the flags before gathering. No collective call.
+constexpr int kMaxPushShards = 8;
+enum PushKind : int { kPushY = 0, kPushX = 1, kPushPart = 2 };
+struct PushArgs {
+  int on, P, rank;
+  long long Sm, Sn;
+  double* y[kMaxPushShards];     // every shard's padded full y
+  double* x[kMaxPushShards];     // every shard's padded full x
+  double* part[kMaxPushShards];  // every shard's [P][22] report sums
+  unsigned long long* flags[kMaxPushShards];  // every shard's flags [3][kMaxPushShards]
+  unsigned long long* my_flags;
+  const unsigned char* mask_y;   // [m_loc]: bit q = shard q gathers this row's y (null: all)
+  const unsigned char* mask_x;   // [n_loc]
+  unsigned* counter;             // [2] last-block counters (k_dual, k_select_x)
+};
+
 // ---------------------------------------------------------------------------
 // Parameters of the fused iteration kernels (passed by value, captured into
 // CUDA graphs once per solve).
@@ -121,6 +141,7 @@ struct IterParams {
   const double* yg;    // gather source of the column SpMV: the full (padded) y
   double* y_full_loc;  // this shard's region of the full y (k_dual also writes y there)
   double* xpart_loc;   // k_primal's last block writes the shard's 22 report sums here
+  PushArgs push;       // sharded push transport (push.on == 0 otherwise)
 };
 
 // ---------------------------------------------------------------------------

@@ -224,9 +224,22 @@ void Context::shard_from(Context& F, int rank, int P, const std::vector<int>& rb
   s = vec(F.s, c0, n);
   b = vec(F.b, r0, m);
   r = vec(F.r, r0, m);
-  x_full = alloc<double>(static_cast<size_t>(P) * Sn);
-  y_full = alloc<double>(static_cast<size_t>(P) * Sm);
-  xpart = alloc<double>(static_cast<size_t>(P) * (kRowParts + kColParts));
+  // the buffers peers write into: plain cudaMalloc when they are shared with
+  // other processes over CUDA IPC (pool memory cannot be exported)
+  auto xalloc = [&](size_t count) -> double* {
+    if (!ipc_buffers) return alloc<double>(count);
+    void* q = nullptr;
+    CK(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(double)));
+    ipc_owned.push_back(q);
+    return static_cast<double*>(q);
+  };
+  x_full = xalloc(static_cast<size_t>(P) * Sn);
+  y_full = xalloc(static_cast<size_t>(P) * Sm);
+  xpart = xalloc(static_cast<size_t>(P) * (kRowParts + kColParts));
+  push_flags = reinterpret_cast<unsigned long long*>(xalloc(3 * kMaxPushShards));
+  push_counter = alloc<unsigned>(2);
+  CK(cudaMemsetAsync(push_flags, 0, sizeof(unsigned long long) * 3 * kMaxPushShards, stream));
+  CK(cudaMemsetAsync(push_counter, 0, sizeof(unsigned) * 2, stream));
   vparts = alloc<double>(kRowParts + kColParts);
   CK(cudaMemsetAsync(x_full, 0, sizeof(double) * std::max<size_t>(1, size_t(P) * Sn), stream));
   CK(cudaMemsetAsync(y_full, 0, sizeof(double) * std::max<size_t>(1, size_t(P) * Sm), stream));
@@ -391,6 +404,10 @@ struct Sharded {
 
   ~Sharded() {
     if (graph) cudaGraphExecDestroy(graph);
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
+    if (full)
+      for (unsigned char* mk : masks) full->release(mk);
     shards.clear();
     if (full) {
       release_halo(halo_x);
@@ -405,6 +422,120 @@ struct Sharded {
   }
 
   Context& s0() { return *shards[0]; }
+
+  // ---- push transport ------------------------------------------------------
+  bool push = false;
+  std::vector<void*> ipc_opened;  // peers' buffers opened over CUDA IPC
+  std::vector<unsigned char*> masks;
+
+  // Per-row / per-column bitmasks of the shards that gather each entry of
+  // this shard's slice (from the halo need lists; all shards without a halo).
+  unsigned char* build_mask(const Halo& h, int owner, int len, size_t S) {
+    if (!h.on) return nullptr;
+    (void)S;
+    std::vector<unsigned char> mk(static_cast<size_t>(std::max(len, 1)), 0);
+    for (int j = 0; j < len; ++j) mk[j] = static_cast<unsigned char>(1u << owner);
+    for (int q = 0; q < P; ++q) {
+      if (q == owner || h.cnt[q][owner] == 0) continue;
+      std::vector<int> lst(h.cnt[q][owner]);
+      CK(cudaMemcpy(lst.data(), h.need[q][owner], sizeof(int) * lst.size(), cudaMemcpyDeviceToHost));
+      for (int j : lst) mk[j] |= static_cast<unsigned char>(1u << q);
+    }
+    unsigned char* d = full->alloc<unsigned char>(mk.size());
+    CK(cudaMemcpy(d, mk.data(), mk.size(), cudaMemcpyHostToDevice));
+    masks.push_back(d);
+    return d;
+  }
+
+  void barrier() { agree(false); }  // every rank past this point (multi-process only)
+
+  // Host-side stop decisions (cancel, time limit) taken by any rank apply to
+  // all ranks, so no rank is left waiting on peers that stopped launching.
+  bool agree(bool local) {
+    if (comm == nullptr) return local;
+    double* t = full->alloc<double>(P);
+    double v = local ? 1.0 : 0.0;
+    CK(cudaMemcpyAsync(t + rank, &v, sizeof(double), cudaMemcpyHostToDevice, stream));
+    nck(nccl().AllGather(t + rank, t, 1, ncclDouble, comm, stream), "ncclAllGather");
+    std::vector<double> all(P);
+    CK(cudaMemcpyAsync(all.data(), t, sizeof(double) * P, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    full->release(t);
+    for (double a : all)
+      if (a != 0.0) return true;
+    return false;
+  }
+
+  void setup_push() {
+    for (unsigned char* mk : masks) full->release(mk);
+    masks.clear();
+    for (void* q : ipc_opened) cudaIpcCloseMemHandle(q);
+    ipc_opened.clear();
+    std::vector<double*> Y(P), X(P), PT(P);
+    std::vector<unsigned long long*> F(P);
+    if (comm == nullptr) {
+      for (auto& s : shards) {
+        Y[s->shard_rank] = s->y_full;
+        X[s->shard_rank] = s->x_full;
+        PT[s->shard_rank] = s->xpart;
+        F[s->shard_rank] = s->push_flags;
+      }
+    } else {  // CUDA IPC: every rank exports its four buffers, all-gathers the handles
+      Context& me = s0();
+      cudaIpcMemHandle_t hs[4];
+      void* bufs[4] = {me.y_full, me.x_full, me.xpart, me.push_flags};
+      for (int k = 0; k < 4; ++k) CK(cudaIpcGetMemHandle(&hs[k], bufs[k]));
+      const size_t hb = sizeof(hs);
+      char* d = full->alloc<char>(hb * P);
+      CK(cudaMemcpyAsync(d + hb * rank, hs, hb, cudaMemcpyHostToDevice, stream));
+      nck(nccl().AllGather(d + hb * rank, d, hb, ncclChar, comm, stream), "ncclAllGather");
+      std::vector<char> all(hb * P);
+      CK(cudaMemcpyAsync(all.data(), d, all.size(), cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      full->release(d);
+      for (int q = 0; q < P; ++q) {
+        if (q == rank) {
+          Y[q] = me.y_full;
+          X[q] = me.x_full;
+          PT[q] = me.xpart;
+          F[q] = me.push_flags;
+          continue;
+        }
+        void* ptr[4];
+        for (int k = 0; k < 4; ++k) {
+          cudaIpcMemHandle_t h;
+          std::memcpy(&h, all.data() + hb * q + sizeof(cudaIpcMemHandle_t) * k, sizeof h);
+          CK(cudaIpcOpenMemHandle(&ptr[k], h, cudaIpcMemLazyEnablePeerAccess));
+          ipc_opened.push_back(ptr[k]);
+        }
+        Y[q] = static_cast<double*>(ptr[0]);
+        X[q] = static_cast<double*>(ptr[1]);
+        PT[q] = static_cast<double*>(ptr[2]);
+        F[q] = static_cast<unsigned long long*>(ptr[3]);
+      }
+    }
+    for (auto& s : shards) {
+      PushArgs a{};
+      a.on = 1;
+      a.P = P;
+      a.rank = s->shard_rank;
+      a.Sm = s->Sm;
+      a.Sn = s->Sn;
+      for (int q = 0; q < P; ++q) {
+        a.y[q] = Y[q];
+        a.x[q] = X[q];
+        a.part[q] = PT[q];
+        a.flags[q] = F[q];
+      }
+      a.my_flags = s->push_flags;
+      a.mask_y = build_mask(halo_y, s->shard_rank, s->m, s->Sm);
+      a.mask_x = build_mask(halo_x, s->shard_rank, s->n, s->Sn);
+      a.counter = s->push_counter;
+      s->params.push = a;
+    }
+    CK(cudaStreamSynchronize(stream));
+    barrier();  // flags are zero everywhere before anyone pushes
+  }
 
   // In-place all-gather of a padded full buffer (count doubles per shard).
   void allgather(double* Context::*buf, size_t count) {
@@ -444,6 +575,11 @@ struct Sharded {
     cb.assign(P + 1, 0);
     host_partition(rowptr_h.data(), m, P, 4, rb.data());
     host_partition(lp->colptr, n, P, 4, cb.data());
+    {  // transport: push (P2P stores fused into the producers) or NCCL / device-copy gathers
+      const char* e = std::getenv("CCLP_CU_TRANSPORT");
+      const bool want_push = e != nullptr ? std::string(e) == "push" : (id == nullptr);
+      push = want_push && P <= kMaxPushShards;
+    }
     if (id != nullptr) {  // NCCL transport (also with one rank: exercises the collective path)
       if (local_shards != 1) throw std::invalid_argument("sharded: one shard per process with NCCL");
       if (!nccl().ok) throw Error(CCLP_CU_ENCCL, nccl().err);
@@ -465,6 +601,7 @@ struct Sharded {
     const int count = comm != nullptr ? 1 : P;
     for (int q = first; q < first + count; ++q) {
       auto sh = std::make_unique<Context>();
+      sh->ipc_buffers = push && comm != nullptr;
       sh->shard_from(*full, q, P, rb, cb, stream);
       k_stamp<<<1, 1, 0, stream>>>(sh->t0);
       CKL("stamp");
@@ -480,25 +617,35 @@ struct Sharded {
     }
   }
 
+  // One iteration on every local shard. With the push transport the
+  // exchanges are inside the producers (k_dual, k_primal's last block,
+  // k_select_x) and the consumers wait on peer flags: no collective call.
   void launch_round(bool init) {
     for (auto& s : shards) s->launch_rows_half(init);
-    exchange(&Context::y_full, static_cast<size_t>(s0().Sm), halo_y);
+    if (!push) exchange(&Context::y_full, static_cast<size_t>(s0().Sm), halo_y);
     for (auto& s : shards) s->launch_cols_half(init);
-    allgather(&Context::xpart, kRowParts + kColParts);
+    if (!push) allgather(&Context::xpart, kRowParts + kColParts);
     for (auto& s : shards) {
       k_finalize_shard<<<1, kEpiBlock, 0, stream>>>(s->params, s->xpart, P, init ? 1 : 0);
       k_select_x<<<blocks_for(s->n), kBlock, 0, stream>>>(
-          s->params, s->x_full + static_cast<size_t>(s->shard_rank) * s->Sn);
+          s->params, s->x_full + static_cast<size_t>(s->shard_rank) * s->Sn, 0);
     }
     CKL("shard finalize");
-    exchange(&Context::x_full, static_cast<size_t>(s0().Sn), halo_x);
+    if (!push) exchange(&Context::x_full, static_cast<size_t>(s0().Sn), halo_x);
     launches += static_cast<long long>(shards.size()) * (kKernelsPerIteration + 2);
   }
 
   void begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thr, int nthr) {
     build_shards(cfg);
     for (auto& s : shards) s->init_state(cfg, tol, thr, nthr, false);
-    allgather(&Context::x_full, static_cast<size_t>(s0().Sn));  // x_0: once, in full
+    if (push) {
+      setup_push();
+      for (auto& s : shards)  // x_0 into every shard that gathers it (epoch 1)
+        k_select_x<<<blocks_for(s->n), kBlock, 0, stream>>>(s->params, nullptr, 1);
+      CKL("push x0");
+    } else {
+      allgather(&Context::x_full, static_cast<size_t>(s0().Sn));  // x_0: once, in full
+    }
     launch_round(true);
     CK(cudaStreamSynchronize(stream));
     begun = true;

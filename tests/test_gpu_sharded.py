@@ -14,6 +14,15 @@ from paper_2510_24429_b200.pdhg import (PdhgConfig, PdhgStopReason, ShardedEngin
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["push", "gather"], autouse=True)
+def transport(request, monkeypatch):
+    """Every sharded test runs over both transports: the fused push (P2P
+    stores inside the producing kernels + epoch flags) and the gathers
+    (device copies / NCCL)."""
+    monkeypatch.setenv("CCLP_CU_TRANSPORT", request.param)
+    return request.param
+
+
 def lps():
     return [("eq40x90", lpgen.small_equality_lp(40, 90, 0.2, 7)[0]),
             ("transport20x30", lpgen.transportation_lp(20, 30, seed=3)),
