@@ -1672,7 +1672,7 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
         cancelled = true;
         break;
       }
-      // two batches in flight: launch, copy the control block, poll
+      // launch a batch, copy the control block, poll
       CK(cudaGraphLaunch(C.graph, C.stream));
       C.launches += cclp_cu::kKernelsPerIteration * k;
       CK(cudaMemcpyAsync(&C.h_ctrl[0], C.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, C.stream));

@@ -39,9 +39,7 @@ struct StepInfo {
   bool init;
 };
 
-__device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepInfo& si) {
-  pdl_wait();  // the previous kernel of the step (or step) must be complete
-  const Ctrl* C = p.ctrl;
+__device__ __forceinline__ bool step_from(const Ctrl* C, const IterParams& p, bool init, StepInfo& si) {
   if (C->stop >= 0 || C->halt) return false;
   if (init) {
     si.t = -1;
@@ -71,6 +69,11 @@ __device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepIn
   si.check = (si.t1 % p.check_interval) == 0;
   si.init = false;
   return true;
+}
+
+__device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepInfo& si) {
+  pdl_wait();  // the previous kernel of the step (or step) must be complete
+  return step_from(p.ctrl, p, init, si);
 }
 
 // ---- push transport (PushArgs, kernels.cuh) --------------------------------
@@ -114,7 +117,7 @@ __device__ __forceinline__ void push_signal_grid(const PushArgs& ps, int kind, u
 // (pdhg.cpp:128-130 error, 301-368 next pass: time, check, limit), taken by
 // thread 0 on a shared-memory copy of the control block.
 __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, Ctrl* C,
-                                       const double* rowv, const double* colv) {
+                                       const double* rowv, const double* colv, bool write_log = true) {
   if (!si.init) {
     if (rowv[6] + colv[12] > 0.0) {  // PdhgNumericalError before commit
       C->stop = 5;
@@ -160,12 +163,14 @@ __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, 
     }
     if (C->last_restart_resid == CCLP_INF) C->last_restart_resid = C->cur[kMaxResid];
     if (p.log_interval > 0 && t1 % p.log_interval == 0) {
-      LogEntry& e = p.log[C->log_count % p.log_cap];
-      e.iteration = t1;
-      e.rel_primal = better[kRelP];
-      e.rel_dual = better[kRelD];
-      e.rel_gap = better[kRelGap];
-      e.elapsed = 1e-9 * static_cast<double>(globaltimer() - *p.t0_ns);
+      if (write_log) {
+        LogEntry& e = p.log[C->log_count % p.log_cap];
+        e.iteration = t1;
+        e.rel_primal = better[kRelP];
+        e.rel_dual = better[kRelD];
+        e.rel_gap = better[kRelGap];
+        e.elapsed = 1e-9 * static_cast<double>(globaltimer() - *p.t0_ns);
+      }
       C->log_count++;
     }
     if (better[kMaxResid] <= p.eps_rel) {
@@ -467,6 +472,74 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_cols(const IterParams p, in
                       p.aty[si.s1], p.rpg_cols);
 }
 
+// k_dual's work on rows i0 + k*stride < end (k < kDualU), loads hoisted:
+// y_{t+1}, the sums, the push of y and the row-side report partials.
+constexpr int kDualU = 2;
+__device__ __forceinline__ void dual_span(const IterParams& p, const StepInfo& si, int i0, int stride,
+                                          int end, double* acc) {
+  const double* __restrict__ axn_v = p.ax[si.s1];
+  const double* __restrict__ y0 = p.y[si.s0];
+  const double* __restrict__ ax0 = p.ax[si.s0];
+  const double* __restrict__ ys0v = p.ysum[si.s0];
+  const double* __restrict__ axs0v = p.axsum[si.s0];
+  double* __restrict__ y1 = p.y[si.s1];
+  double* __restrict__ ys1 = p.ysum[si.s1];
+  double* __restrict__ axs1 = p.axsum[si.s1];
+  constexpr int U = kDualU;
+  double r[U], b[U], axn[U], yo[U], axo[U], ys[U], axs[U];
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const int i = i0 + k * stride;
+    const bool ok = i < end;
+    r[k] = ok ? p.r[i] : 1.0;
+    b[k] = ok ? p.b[i] : 0.0;
+    axn[k] = ok ? axn_v[i] : 0.0;
+    yo[k] = ok ? y0[i] : 0.0;
+    axo[k] = ok && !si.init && !si.R ? ax0[i] : 0.0;
+    ys[k] = ok && !si.init ? ys0v[i] : 0.0;
+    axs[k] = ok && !si.init ? axs0v[i] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const int i = i0 + k * stride;
+    if (i >= end) break;
+    const double rinv = pow2_recip(r[k]);
+    if (si.init) {
+      row_report(axn[k], yo[k], r[k], rinv, b[k], acc);
+      continue;
+    }
+    double y_old = yo[k], ax_old = axo[k];
+    if (si.R) {
+      y_old = ys[k] * si.inv;
+      ax_old = axs[k] * si.inv;
+    }
+    const double bs = b[k] * r[k];  // row_lower.cwiseProduct(r)
+    double t = 2.0 * axn[k];
+    t = t - ax_old;
+    t = bs - t;
+    t = p.sigma * t;
+    const double yn = y_old + t;
+    const double ysn = (si.R ? 0.0 : ys[k]) + yn;
+    const double axsn = (si.R ? 0.0 : axs[k]) + axn[k];
+    y1[i] = yn;
+    if (p.push.on) {  // fused push: into every shard that gathers this row
+      const unsigned mk = p.push.mask_y != nullptr ? p.push.mask_y[i] : 0xFFu;
+      const long long off = static_cast<long long>(p.push.rank) * p.push.Sm;
+      for (int q = 0; q < p.push.P; ++q)
+        if ((mk >> q) & 1u) p.push.y[q][off + i] = yn;
+    } else if (p.y_full_loc != nullptr) {
+      p.y_full_loc[i] = yn;
+    }
+    ys1[i] = ysn;
+    axs1[i] = axsn;
+    if (nonfinite(yn)) acc[6] += 1.0;
+    if (si.check) {
+      row_report(axn[k], yn, r[k], rinv, b[k], acc);
+      row_report(axsn * si.inv1, ysn * si.inv1, r[k], rinv, b[k], acc + 3);
+    }
+  }
+}
+
 // Dual update + row-side report partials (one row per thread, coalesced).
 __global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init) {
   StepInfo si;
@@ -476,73 +549,66 @@ __global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init
   double acc[kRowParts];
 #pragma unroll
   for (int k = 0; k < kRowParts; ++k) acc[k] = 0.0;
-  const double* __restrict__ axn_v = p.ax[si.s1];
-  const double* __restrict__ y0 = p.y[si.s0];
-  const double* __restrict__ ax0 = p.ax[si.s0];
-  const double* __restrict__ ys0v = p.ysum[si.s0];
-  const double* __restrict__ axs0v = p.axsum[si.s0];
-  double* __restrict__ y1 = p.y[si.s1];
-  double* __restrict__ ys1 = p.ysum[si.s1];
-  double* __restrict__ axs1 = p.axsum[si.s1];
-  constexpr int U = 2;  // rows per thread per trip, loads hoisted
   const int stride = gridDim.x * kEpiBlock;
-  for (int i0 = blockIdx.x * kEpiBlock + threadIdx.x; i0 < p.m; i0 += U * stride) {
-    double r[U], b[U], axn[U], yo[U], axo[U], ys[U], axs[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int i = i0 + k * stride;
-      const bool ok = i < p.m;
-      r[k] = ok ? p.r[i] : 1.0;
-      b[k] = ok ? p.b[i] : 0.0;
-      axn[k] = ok ? axn_v[i] : 0.0;
-      yo[k] = ok ? y0[i] : 0.0;
-      axo[k] = ok && !si.init && !si.R ? ax0[i] : 0.0;
-      ys[k] = ok && !si.init ? ys0v[i] : 0.0;
-      axs[k] = ok && !si.init ? axs0v[i] : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int i = i0 + k * stride;
-      if (i >= p.m) break;
-      const double rinv = pow2_recip(r[k]);
-      if (si.init) {
-        row_report(axn[k], yo[k], r[k], rinv, b[k], acc);
-        continue;
-      }
-      double y_old = yo[k], ax_old = axo[k];
-      if (si.R) {
-        y_old = ys[k] * si.inv;
-        ax_old = axs[k] * si.inv;
-      }
-      const double bs = b[k] * r[k];  // row_lower.cwiseProduct(r)
-      double t = 2.0 * axn[k];
-      t = t - ax_old;
-      t = bs - t;
-      t = p.sigma * t;
-      const double yn = y_old + t;
-      const double ysn = (si.R ? 0.0 : ys[k]) + yn;
-      const double axsn = (si.R ? 0.0 : axs[k]) + axn[k];
-      y1[i] = yn;
-      if (p.push.on) {  // fused push: into every shard that gathers this row
-        const unsigned mk = p.push.mask_y != nullptr ? p.push.mask_y[i] : 0xFFu;
-        const long long off = static_cast<long long>(p.push.rank) * p.push.Sm;
-        for (int q = 0; q < p.push.P; ++q)
-          if ((mk >> q) & 1u) p.push.y[q][off + i] = yn;
-      } else if (p.y_full_loc != nullptr) {
-        p.y_full_loc[i] = yn;
-      }
-      ys1[i] = ysn;
-      axs1[i] = axsn;
-      if (nonfinite(yn)) acc[6] += 1.0;
-      if (si.check) {
-        row_report(axn[k], yn, r[k], rinv, b[k], acc);
-        row_report(axsn * si.inv1, ysn * si.inv1, r[k], rinv, b[k], acc + 3);
-      }
-    }
-  }
+  for (int i0 = blockIdx.x * kEpiBlock + threadIdx.x; i0 < p.m; i0 += kDualU * stride)
+    dual_span(p, si, i0, stride, p.m, acc);
   block_reduce<kRowParts, kRowMaxMask, kEpiBlock>(acc, red, out);
   if (threadIdx.x < kRowParts) p.rowp[blockIdx.x * kRowParts + threadIdx.x] = out[threadIdx.x];
   if (p.push.on) push_signal_grid(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1), p.push.counter);
+}
+
+// k_primal's work on columns j0 + k*stride < end (k < kPrimalU): the sums,
+// both next-x candidates and the column-side report partials.
+constexpr int kPrimalU = 2;
+__device__ __forceinline__ void primal_span(const IterParams& p, const StepInfo& si, int j0, int stride,
+                                            int end, double* acc) {
+  const double* __restrict__ atyn_v = p.aty[si.s1];
+  double* __restrict__ cand_c = p.xc[si.xs2][0];
+  double* __restrict__ cand_a = p.xc[si.xs2][1];
+  const double* __restrict__ xcur = p.xc[si.xs][si.R];
+  const double* __restrict__ xs0v = p.xsum[si.s0];
+  const double* __restrict__ as0v = p.atysum[si.s0];
+  double* __restrict__ xs1 = p.xsum[si.s1];
+  double* __restrict__ as1 = p.atysum[si.s1];
+  constexpr int U = kPrimalU;
+  double s[U], c[U], l[U], u[U], x1[U], atyn[U], xs0[U], as0[U];
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const int j = j0 + k * stride;
+    const bool ok = j < end;
+    s[k] = ok ? p.s[j] : 1.0;
+    c[k] = ok ? p.c[j] : 0.0;
+    l[k] = ok ? p.l[j] : 0.0;
+    u[k] = ok ? p.u[j] : 0.0;
+    x1[k] = ok ? xcur[j] : 0.0;
+    atyn[k] = ok ? atyn_v[j] : 0.0;
+    xs0[k] = ok && !si.init ? xs0v[j] : 0.0;
+    as0[k] = ok && !si.init ? as0v[j] : 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < U; ++k) {
+    const int j = j0 + k * stride;
+    if (j >= end) break;
+    const double sinv = pow2_recip(s[k]);
+    // apply_scaling: c*s, l/s, u/s (l/s == l*(1/s) exactly)
+    const double cs = c[k] * s[k], ls = l[k] * sinv, us = u[k] * sinv;
+    cand_c[j] = primal_update(x1[k], atyn[k], cs, ls, us, p.tau);
+    if (si.init) {
+      col_report(x1[k], atyn[k], s[k], sinv, c[k], l[k], u[k], acc);
+      continue;
+    }
+    const double xsn = (si.R ? 0.0 : xs0[k]) + x1[k];
+    const double asn = (si.R ? 0.0 : as0[k]) + atyn[k];
+    xs1[j] = xsn;
+    as1[j] = asn;
+    if (nonfinite(x1[k])) acc[12] += 1.0;
+    if (si.check) {
+      col_report(x1[k], atyn[k], s[k], sinv, c[k], l[k], u[k], acc);
+      const double xa = xsn * si.inv1, aa = asn * si.inv1;
+      col_report(xa, aa, s[k], sinv, c[k], l[k], u[k], acc + 6);
+      cand_a[j] = primal_update(xa, aa, cs, ls, us, p.tau);
+    }
+  }
 }
 
 // Primal side: sums, column-side report partials, both next-x candidates;
@@ -556,56 +622,9 @@ __global__ void __launch_bounds__(kEpiBlock) k_primal(const IterParams p, int in
   double acc[kColParts];
 #pragma unroll
   for (int k = 0; k < kColParts; ++k) acc[k] = 0.0;
-  const double* __restrict__ atyn_v = p.aty[si.s1];
-  double* __restrict__ cand_c = p.xc[si.xs2][0];
-  double* __restrict__ cand_a = p.xc[si.xs2][1];
-  const double* __restrict__ xcur = p.xc[si.xs][si.R];
-  const double* __restrict__ xs0v = p.xsum[si.s0];
-  const double* __restrict__ as0v = p.atysum[si.s0];
-  double* __restrict__ xs1 = p.xsum[si.s1];
-  double* __restrict__ as1 = p.atysum[si.s1];
-  constexpr int U = 2;  // columns per thread per trip, loads hoisted
   const int stride = gridDim.x * kEpiBlock;
-  for (int j0 = blockIdx.x * kEpiBlock + threadIdx.x; j0 < p.n; j0 += U * stride) {
-    double s[U], c[U], l[U], u[U], x1[U], atyn[U], xs0[U], as0[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int j = j0 + k * stride;
-      const bool ok = j < p.n;
-      s[k] = ok ? p.s[j] : 1.0;
-      c[k] = ok ? p.c[j] : 0.0;
-      l[k] = ok ? p.l[j] : 0.0;
-      u[k] = ok ? p.u[j] : 0.0;
-      x1[k] = ok ? xcur[j] : 0.0;
-      atyn[k] = ok ? atyn_v[j] : 0.0;
-      xs0[k] = ok && !si.init ? xs0v[j] : 0.0;
-      as0[k] = ok && !si.init ? as0v[j] : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int j = j0 + k * stride;
-      if (j >= p.n) break;
-      const double sinv = pow2_recip(s[k]);
-      // apply_scaling: c*s, l/s, u/s (l/s == l*(1/s) exactly)
-      const double cs = c[k] * s[k], ls = l[k] * sinv, us = u[k] * sinv;
-      cand_c[j] = primal_update(x1[k], atyn[k], cs, ls, us, p.tau);
-      if (si.init) {
-        col_report(x1[k], atyn[k], s[k], sinv, c[k], l[k], u[k], acc);
-        continue;
-      }
-      const double xsn = (si.R ? 0.0 : xs0[k]) + x1[k];
-      const double asn = (si.R ? 0.0 : as0[k]) + atyn[k];
-      xs1[j] = xsn;
-      as1[j] = asn;
-      if (nonfinite(x1[k])) acc[12] += 1.0;
-      if (si.check) {
-        col_report(x1[k], atyn[k], s[k], sinv, c[k], l[k], u[k], acc);
-        const double xa = xsn * si.inv1, aa = asn * si.inv1;
-        col_report(xa, aa, s[k], sinv, c[k], l[k], u[k], acc + 6);
-        cand_a[j] = primal_update(xa, aa, cs, ls, us, p.tau);
-      }
-    }
-  }
+  for (int j0 = blockIdx.x * kEpiBlock + threadIdx.x; j0 < p.n; j0 += kPrimalU * stride)
+    primal_span(p, si, j0, stride, p.n, acc);
   block_reduce<kColParts, kColMaxMask, kEpiBlock>(acc, red, out);
   if (threadIdx.x < kColParts) p.colp[blockIdx.x * kColParts + threadIdx.x] = out[threadIdx.x];
   __threadfence();
