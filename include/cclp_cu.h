@@ -31,6 +31,7 @@
 #ifndef CCLP_CU_H_
 #define CCLP_CU_H_
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -209,6 +210,16 @@ int cclp_cu_sharded_solve(cclp_cu_sharded* ctx, const cclp_cu_config* cfg,
                           const cclp_cu_tolerances* tol, const double* thresholds, int32_t nthr,
                           cclp_cu_sink_fn sink, void* sink_user, const volatile uint8_t* cancel,
                           double* x_out, double* y_out, double* z_out, cclp_cu_result* res);
+/* Multi-process without NCCL: the caller provides an all-gather of host
+ * bytes (e.g. over its own MPI / gloo); the iteration then runs the push
+ * transport over CUDA IPC (P <= 8 ranks, one shard each). */
+typedef struct {
+  /* in: `bytes` from this rank; out: nranks * bytes, rank order; 0 = ok */
+  int (*allgather)(const void* in, size_t bytes, void* out, void* user);
+  void* user;
+} cclp_cu_host_comm;
+int cclp_cu_sharded_create_hostcomm(const cclp_cu_lp* lp, int device, int32_t rank, int32_t nranks,
+                                    const cclp_cu_host_comm* comm, cclp_cu_sharded** out);
 /* measurement hooks, as cclp_cu_begin / cclp_cu_advance */
 int cclp_cu_sharded_begin(cclp_cu_sharded* ctx, const cclp_cu_config* cfg,
                           const cclp_cu_tolerances* tol);

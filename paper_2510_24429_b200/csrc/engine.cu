@@ -1761,6 +1761,26 @@ int cclp_cu_sharded_create(const cclp_cu_lp* lp, int device, int32_t nshards, in
   });
 }
 
+int cclp_cu_sharded_create_hostcomm(const cclp_cu_lp* lp, int device, int32_t rank, int32_t nranks,
+                                    const cclp_cu_host_comm* comm, cclp_cu_sharded** out) {
+  *out = nullptr;
+  return guarded([&] {
+    if (lp == nullptr || lp->m < 0 || lp->n < 0 || lp->colptr == nullptr || comm == nullptr)
+      throw std::invalid_argument("cclp_cu_sharded_create_hostcomm: bad arguments");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+      throw std::invalid_argument("cclp_cu_sharded_create_hostcomm: bad rank");
+    cclp_cu::ck(cudaSetDevice(device), "cudaSetDevice");
+    auto* ctx = new cclp_cu_sharded();
+    try {
+      ctx->s.create(lp, device, 1, rank, nranks, nullptr, comm);
+    } catch (...) {
+      delete ctx;
+      throw;
+    }
+    *out = ctx;
+  });
+}
+
 int cclp_cu_sharded_destroy(cclp_cu_sharded* ctx) {
   if (ctx) cudaSetDevice(ctx->s.device);
   delete ctx;

@@ -264,6 +264,12 @@ struct Sharded {
   std::vector<std::unique_ptr<Context>> shards;  // this process's shards
   std::vector<int> rb, cb;
   ncclComm_t comm = nullptr;
+  // host-callback coordination (no NCCL): handle exchange, barriers and the
+  // result gathers go through the caller's all-gather; the iteration uses the
+  // push transport over CUDA IPC
+  bool have_hcomm = false;
+  cclp_cu_host_comm hcomm{};
+  bool multi() const { return comm != nullptr || have_hcomm; }
   cudaStream_t stream = nullptr;
   cudaGraphExec_t graph = nullptr;
   int graph_k = 0;
@@ -452,18 +458,30 @@ struct Sharded {
   // Host-side stop decisions (cancel, time limit) taken by any rank apply to
   // all ranks, so no rank is left waiting on peers that stopped launching.
   bool agree(bool local) {
-    if (comm == nullptr) return local;
-    double* t = full->alloc<double>(P);
-    double v = local ? 1.0 : 0.0;
-    CK(cudaMemcpyAsync(t + rank, &v, sizeof(double), cudaMemcpyHostToDevice, stream));
-    nck(nccl().AllGather(t + rank, t, 1, ncclDouble, comm, stream), "ncclAllGather");
-    std::vector<double> all(P);
-    CK(cudaMemcpyAsync(all.data(), t, sizeof(double) * P, cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    full->release(t);
-    for (double a : all)
-      if (a != 0.0) return true;
+    if (!multi()) return local;
+    const char v = local ? 1 : 0;
+    const std::vector<char> all = gather_bytes(&v, 1);
+    for (char a : all)
+      if (a != 0) return true;
     return false;
+  }
+
+  // All-gather of `bytes` host bytes per rank, in rank order (NCCL through a
+  // device buffer, or the caller's host callback).
+  std::vector<char> gather_bytes(const void* mine, size_t bytes) {
+    std::vector<char> all(bytes * P);
+    if (have_hcomm) {
+      if (hcomm.allgather(mine, bytes, all.data(), hcomm.user) != 0)
+        throw Error(CCLP_CU_ENCCL, "host all-gather callback failed");
+      return all;
+    }
+    char* d = full->alloc<char>(std::max<size_t>(1, bytes * P));
+    CK(cudaMemcpyAsync(d + bytes * rank, mine, bytes, cudaMemcpyHostToDevice, stream));
+    nck(nccl().AllGather(d + bytes * rank, d, bytes, ncclChar, comm, stream), "ncclAllGather");
+    CK(cudaMemcpyAsync(all.data(), d, all.size(), cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    full->release(d);
+    return all;
   }
 
   void setup_push() {
@@ -473,7 +491,7 @@ struct Sharded {
     ipc_opened.clear();
     std::vector<double*> Y(P), X(P), PT(P);
     std::vector<unsigned long long*> F(P);
-    if (comm == nullptr) {
+    if (!multi()) {
       for (auto& s : shards) {
         Y[s->shard_rank] = s->y_full;
         X[s->shard_rank] = s->x_full;
@@ -486,13 +504,7 @@ struct Sharded {
       void* bufs[4] = {me.y_full, me.x_full, me.xpart, me.push_flags};
       for (int k = 0; k < 4; ++k) CK(cudaIpcGetMemHandle(&hs[k], bufs[k]));
       const size_t hb = sizeof(hs);
-      char* d = full->alloc<char>(hb * P);
-      CK(cudaMemcpyAsync(d + hb * rank, hs, hb, cudaMemcpyHostToDevice, stream));
-      nck(nccl().AllGather(d + hb * rank, d, hb, ncclChar, comm, stream), "ncclAllGather");
-      std::vector<char> all(hb * P);
-      CK(cudaMemcpyAsync(all.data(), d, all.size(), cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
-      full->release(d);
+      const std::vector<char> all = gather_bytes(hs, hb);
       for (int q = 0; q < P; ++q) {
         if (q == rank) {
           Y[q] = me.y_full;
@@ -553,11 +565,18 @@ struct Sharded {
                              cudaMemcpyDeviceToDevice, stream));
   }
 
-  void create(const cclp_cu_lp* lp, int dev, int local_shards, int rk, int nr, const ncclUniqueId* id) {
+  void create(const cclp_cu_lp* lp, int dev, int local_shards, int rk, int nr, const ncclUniqueId* id,
+              const cclp_cu_host_comm* hc = nullptr) {
     device = dev;
     rank = rk;
     nranks = nr;
-    P = (nr > 1 || id != nullptr) ? nr : local_shards;
+    if (hc != nullptr) {
+      if (hc->allgather == nullptr) throw std::invalid_argument("sharded: host comm needs an all-gather");
+      if (local_shards != 1) throw std::invalid_argument("sharded: one shard per process with a host comm");
+      have_hcomm = true;
+      hcomm = *hc;
+    }
+    P = (nr > 1 || id != nullptr || hc != nullptr) ? nr : local_shards;
     m = lp->m;
     n = lp->n;
     if (P < 1) throw std::invalid_argument("sharded: need at least one shard");
@@ -578,7 +597,8 @@ struct Sharded {
     {  // transport: push (P2P stores fused into the producers) or NCCL / device-copy gathers
       const char* e = std::getenv("CCLP_CU_TRANSPORT");
       const bool want_push = e != nullptr ? std::string(e) == "push" : (id == nullptr);
-      push = want_push && P <= kMaxPushShards;
+      push = (want_push || have_hcomm) && P <= kMaxPushShards;
+      if (have_hcomm && !push) throw std::invalid_argument("sharded: host comm needs P <= 8 (push)");
     }
     if (id != nullptr) {  // NCCL transport (also with one rank: exercises the collective path)
       if (local_shards != 1) throw std::invalid_argument("sharded: one shard per process with NCCL");
@@ -597,11 +617,11 @@ struct Sharded {
     k_stamp<<<1, 1, 0, stream>>>(full->t0);
     CKL("stamp");
     full->setup(cfg);
-    const int first = comm != nullptr ? rank : 0;
-    const int count = comm != nullptr ? 1 : P;
+    const int first = multi() ? rank : 0;
+    const int count = multi() ? 1 : P;
     for (int q = first; q < first + count; ++q) {
       auto sh = std::make_unique<Context>();
-      sh->ipc_buffers = push && comm != nullptr;
+      sh->ipc_buffers = push && multi();
       sh->shard_from(*full, q, P, rb, cb, stream);
       k_stamp<<<1, 1, 0, stream>>>(sh->t0);
       CKL("stamp");
@@ -707,6 +727,20 @@ struct Sharded {
                          cudaMemcpyDeviceToDevice, stream));
       CK(cudaMemcpyAsync(vparts_full + q * W, s->vparts, sizeof(double) * W, cudaMemcpyDeviceToDevice,
                          stream));
+    }
+    if (have_hcomm) {  // every rank ends with the full vectors, through the caller's all-gather
+      auto gather_dev = [&](double* fullbuf, size_t S) {
+        std::vector<double> mine(S);
+        CK(cudaMemcpyAsync(mine.data(), fullbuf + static_cast<size_t>(rank) * S, sizeof(double) * S,
+                           cudaMemcpyDeviceToHost, stream));
+        CK(cudaStreamSynchronize(stream));
+        const std::vector<char> all = gather_bytes(mine.data(), sizeof(double) * S);
+        CK(cudaMemcpyAsync(fullbuf, all.data(), all.size(), cudaMemcpyHostToDevice, stream));
+      };
+      gather_dev(vx_full, Sn);
+      gather_dev(vz_full, Sn);
+      gather_dev(vy_full, Sm);
+      gather_dev(vparts_full, W);
     }
     if (comm != nullptr) {  // every rank ends with the full vectors
       nck(nccl().AllGather(vx_full + static_cast<size_t>(rank) * Sn, vx_full, Sn, ncclDouble, comm, stream),

@@ -81,6 +81,11 @@ class _Result(C.Structure):
 
 
 _SINK = C.CFUNCTYPE(None, C.POINTER(_Snapshot), C.c_void_p)
+_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+
+
+class _HostComm(C.Structure):
+    _fields_ = [("allgather", _ALLGATHER), ("user", C.c_void_p)]
 _LOG = C.CFUNCTYPE(None, C.c_char_p, C.c_void_p)
 
 _lib = None
@@ -130,6 +135,8 @@ def load_library(path: str = LIB_PATH):
         L.cclp_cu_sharded_advance.argtypes = [C.c_void_p, C.c_int64, _dp]
         L.cclp_cu_sharded_describe.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]
         L.cclp_cu_sharded_destroy.argtypes = [C.c_void_p]
+        L.cclp_cu_sharded_create_hostcomm.argtypes = [C.POINTER(_LP), C.c_int, C.c_int32, C.c_int32,
+                                                      C.POINTER(_HostComm), C.POINTER(C.c_void_p)]
         _lib = L
         return L
 
@@ -142,7 +149,7 @@ EXPORTED_SYMBOLS = [
     "cclp_cu_stream", "cclp_cu_describe", "cclp_cu_gaussian_start", "cclp_cu_partition",
     "cclp_cu_nccl_unique_id", "cclp_cu_sharded_create", "cclp_cu_sharded_solve",
     "cclp_cu_sharded_begin", "cclp_cu_sharded_advance", "cclp_cu_sharded_describe",
-    "cclp_cu_sharded_destroy",
+    "cclp_cu_sharded_destroy", "cclp_cu_sharded_create_hostcomm",
 ]
 
 
@@ -459,10 +466,12 @@ class ShardedEngine:
 
     nranks == 1: `nshards` shards in this process on `device` (exchanges by
     device copies); nranks > 1: one shard per process over NCCL, `nccl_id`
-    from rank 0's nccl_unique_id()."""
+    from rank 0's nccl_unique_id(); or, with `host_allgather(bytes) -> [bytes
+    per rank]` (e.g. over torch.distributed gloo), one shard per process with
+    the push transport over CUDA IPC and no NCCL."""
 
     def __init__(self, lp: LinearProgram, nshards: int = 1, device: int = 0, rank: int = 0,
-                 nranks: int = 1, nccl_id: Optional[bytes] = None):
+                 nranks: int = 1, nccl_id: Optional[bytes] = None, host_allgather=None):
         self.L = load_library()
         self.lp = lp
         self._keep = dict(colptr=np.ascontiguousarray(lp.colptr, np.int32),
@@ -482,6 +491,21 @@ class ShardedEngine:
         if nccl_id is not None:
             idbuf = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
         self.ctx = C.c_void_p()
+        if host_allgather is not None:
+            # host_allgather(bytes) -> list of bytes objects, one per rank (rank order)
+            def _ag(inp, nbytes, out, _u):
+                try:
+                    parts = host_allgather(C.string_at(inp, nbytes))
+                    blob = b"".join(parts)
+                    C.memmove(out, blob, len(blob))
+                    return 0
+                except Exception:
+                    return 1
+            self._ag = _ALLGATHER(_ag)
+            self._hc = _HostComm(self._ag, None)
+            _check(self.L, self.L.cclp_cu_sharded_create_hostcomm(
+                C.byref(self._lp), device, rank, nranks, C.byref(self._hc), C.byref(self.ctx)))
+            return
         _check(self.L, self.L.cclp_cu_sharded_create(C.byref(self._lp), device, nshards, rank,
                                                      nranks, idbuf, C.byref(self.ctx)))
 
