@@ -198,10 +198,10 @@ int cclp_cu_describe(cclp_cu_ctx* ctx, int64_t* out, int32_t nout);
  *                (nranks may be 1: the collective path on one GPU).
  * Every rank passes the full LP and receives the full result. The run_pdhg
  * setup (Ruiz, ||A||) is replicated per rank; the iteration is sharded.
- * Exchanges: gathers (device copies in-process, NCCL all-gather or halo
- * send/recv across processes) or, with CCLP_CU_TRANSPORT=push (the default
- * in-process), stores fused into the producing kernels plus epoch flags
- * (CUDA IPC peers across processes). */
+ * Exchanges: by default (P <= 8) stores fused into the producing kernels
+ * plus epoch flags (CUDA IPC peers across processes, opened at setup); with
+ * CCLP_CU_TRANSPORT=gather, device copies in-process or NCCL all-gathers /
+ * halo send/recv across processes. */
 typedef struct cclp_cu_sharded cclp_cu_sharded;
 int cclp_cu_nccl_unique_id(uint8_t* out128);
 int cclp_cu_sharded_create(const cclp_cu_lp* lp, int device, int32_t nshards, int32_t rank,

@@ -596,7 +596,7 @@ struct Sharded {
     host_partition(lp->colptr, n, P, 4, cb.data());
     {  // transport: push (P2P stores fused into the producers) or NCCL / device-copy gathers
       const char* e = std::getenv("CCLP_CU_TRANSPORT");
-      const bool want_push = e != nullptr ? std::string(e) == "push" : (id == nullptr);
+      const bool want_push = e == nullptr || std::string(e) != "gather";  // push unless asked
       push = (want_push || have_hcomm) && P <= kMaxPushShards;
       if (have_hcomm && !push) throw std::invalid_argument("sharded: host comm needs P <= 8 (push)");
     }
