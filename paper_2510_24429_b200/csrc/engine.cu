@@ -417,7 +417,7 @@ struct Context {
   void launch_cols_half(bool init);  // k_spmv_cols + k_primal
   void build_graph(int k);
   void fetch_ctrl(Ctrl* dst);
-  void extract_view(int view, const Ctrl& st, bool need_report);
+  void extract_view(int view, const Ctrl& st);
 };
 
 Context::~Context() {
@@ -881,22 +881,15 @@ void Context::ruiz(int iterations) {
   double* rmax = wm;
   double* cmax = wn;
   for (int t = 0; t < iterations; ++t) {
-    const int gr = blocks_for(m, kBlock / Grow, 148 * 8);
-    const int gc = blocks_for(n, kBlock / Gcol, 148 * 8);
+    // max over each row / column of |a_ij| r_i s_j (exact, order-free)
     auto absmax = [&](int G, int grid, const int* ptr, const int* idx, const double* val,
                       const double* self, const double* other, int is_row, const int* start,
                       double* out) {
-      switch (G) {
-        case 1: k_scaled_absmax<1><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
-        case 2: k_scaled_absmax<2><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
-        case 4: k_scaled_absmax<4><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
-        case 8: k_scaled_absmax<8><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
-        case 16: k_scaled_absmax<16><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
-        default: k_scaled_absmax<32><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row, start, out); break;
-      }
+      with_group(G, [&](auto g) {
+        k_scaled_absmax<decltype(g)::value><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row,
+                                                                          start, out);
+      });
     };
-    (void)gr;
-    (void)gc;
     absmax(Grow, row_grid, rowptr, colind, val_csr, r, s, 1, row_start, rmax);
     absmax(Gcol, col_grid, colptr, rowind, val_csc, s, r, 0, col_start, cmax);
     CK(cudaMemsetAsync(iflags, 0, sizeof(int) * 4, stream));
@@ -1270,7 +1263,7 @@ void Context::fetch_ctrl(Ctrl* dst) {
 
 // Unscaled x, y, z (and a report) of a view of the current state into vx,
 // vy, vz, vrep.
-void Context::extract_view(int view, const Ctrl& st, bool need_report) {
+void Context::extract_view(int view, const Ctrl& st) {
   if (!vx) {
     vx = alloc<double>(n);
     vz = alloc<double>(n);
@@ -1298,7 +1291,6 @@ void Context::extract_view(int view, const Ctrl& st, bool need_report) {
   k_view_rows<<<gr, kBlock, 0, stream>>>(v);
   k_view_cols<<<gc, kBlock, 0, stream>>>(v, gr);
   CKL("view");
-  (void)need_report;
 }
 
 }  // namespace cclp_cu
@@ -1625,7 +1617,7 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
     };
     auto emit_snapshot = [&](const Ctrl& q) {
       // PdhgSnapshot of the better view (pdhg.cpp:346-358)
-      C.extract_view(q.snap_use_avg ? cclp_cu::kViewAvg : cclp_cu::kViewCur, q, false);
+      C.extract_view(q.snap_use_avg ? cclp_cu::kViewAvg : cclp_cu::kViewCur, q);
       if (!C.h_sx) {
         C.h_sx = C.host_alloc<double>(C.n);
         C.h_sz = C.host_alloc<double>(C.n);
@@ -1694,7 +1686,7 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
       rep_valid = st.checked != 0;
       if (rep_valid) std::memcpy(st.result_report, st.R ? st.avg : st.cur, sizeof(st.result_report));
     }
-    C.extract_view(view, st, !rep_valid);
+    C.extract_view(view, st);
     C.d2h(x_out, C.vx, sizeof(double) * C.n);
     C.d2h(y_out, C.vy, sizeof(double) * C.m);
     C.d2h(z_out, C.vz, sizeof(double) * C.n);

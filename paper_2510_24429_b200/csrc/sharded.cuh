@@ -436,9 +436,8 @@ struct Sharded {
 
   // Per-row / per-column bitmasks of the shards that gather each entry of
   // this shard's slice (from the halo need lists; all shards without a halo).
-  unsigned char* build_mask(const Halo& h, int owner, int len, size_t S) {
+  unsigned char* build_mask(const Halo& h, int owner, int len) {
     if (!h.on) return nullptr;
-    (void)S;
     std::vector<unsigned char> mk(static_cast<size_t>(std::max(len, 1)), 0);
     for (int j = 0; j < len; ++j) mk[j] = static_cast<unsigned char>(1u << owner);
     for (int q = 0; q < P; ++q) {
@@ -540,8 +539,8 @@ struct Sharded {
         a.flags[q] = F[q];
       }
       a.my_flags = s->push_flags;
-      a.mask_y = build_mask(halo_y, s->shard_rank, s->m, s->Sm);
-      a.mask_x = build_mask(halo_x, s->shard_rank, s->n, s->Sn);
+      a.mask_y = build_mask(halo_y, s->shard_rank, s->m);
+      a.mask_x = build_mask(halo_x, s->shard_rank, s->n);
       a.counter = s->push_counter;
       s->params.push = a;
     }
@@ -717,7 +716,7 @@ struct Sharded {
     }
     constexpr int W = kRowParts + kColParts;
     for (auto& s : shards) {
-      s->extract_view(view, st, true);
+      s->extract_view(view, st);
       const int q = s->shard_rank;
       CK(cudaMemcpyAsync(vx_full + static_cast<size_t>(q) * Sn, s->vx, sizeof(double) * s->n,
                          cudaMemcpyDeviceToDevice, stream));
