@@ -136,6 +136,12 @@ void cclp_cu_default_tolerances(cclp_cu_tolerances* t); /* kkt.hpp:33-36 */
 
 /* Uploads the CSC and bounds to `device` and builds CSR(A) on the device. */
 int cclp_cu_create(const cclp_cu_lp* lp, int device, cclp_cu_ctx** out);
+/* LP ingest from a binary CSC file (layout in paper_2510_24429_b200/lp.py,
+ * magic "CCLPCSC1"): the file is memory-mapped and streamed to the device
+ * through the multi-threaded pinned staging, then as cclp_cu_create.
+ * m_out / n_out (optional) receive the dimensions. */
+int cclp_cu_create_from_file(const char* path, int device, cclp_cu_ctx** out, int32_t* m_out,
+                             int32_t* n_out);
 int cclp_cu_destroy(cclp_cu_ctx* ctx);
 
 /* run_pdhg on a context (pdhg.cpp:230-378): Ruiz scaling, ||A|| estimate,

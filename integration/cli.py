@@ -1,7 +1,7 @@
 """Command-line front end (SPEC.md "[MODULE] bench_cli") over
 cclp::run_race with the B200 run_pdhg:
 
-  python -m integration.cli solve <model.mps[.gz]> [--mode baseline|concurrent]
+  python -m integration.cli solve <model.mps[.gz]|model.cscb> [--mode baseline|concurrent]
       [--eps-rel 1e-6] [--eps-cross 1e-2] [--eps-abs 1e-6] [--decrement 0.1]
       [--workers 4] [--time-limit 3600] [--seed S] [--write-basis FILE]
       [--write-solution FILE] [--json] [--pdhg gpu|cpu]
@@ -182,9 +182,9 @@ def main(argv=None) -> int:
                   f"winner {out['winner']} in {out['cli_wall_s']:.3f} s "
                   f"({out['pdhg_iterations']} PDHG iterations)")
         return rc
-    files = sorted(f for f in os.listdir(a.dir) if f.endswith((".mps", ".mps.gz")))
+    files = sorted(f for f in os.listdir(a.dir) if f.endswith((".mps", ".mps.gz", ".cscb")))
     if not files:
-        print(f"input error: no .mps files in {a.dir}", file=sys.stderr)
+        print(f"input error: no .mps or .cscb files in {a.dir}", file=sys.stderr)
         return EXIT_INPUT
     records = []
     for f in files:

@@ -11,6 +11,7 @@
 #include <exception>
 #include <sstream>
 #include <string>
+#include <vector>
 
 #include <fstream>
 
@@ -25,6 +26,65 @@ cclp::Vector vec(const double* p, int n) {
   cclp::Vector v(n);
   if (n > 0) std::memcpy(v.data(), p, sizeof(double) * static_cast<size_t>(n));
   return v;
+}
+
+// Binary CSC ingest (layout: paper_2510_24429_b200/lp.py, magic "CCLPCSC1"):
+// the general-form LP with row activity bounds; the row sense (only used by
+// write_mps, mps.cpp:465) follows the bounds.
+cclp::LinearProgram read_cscb_file(const std::string& path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) throw std::invalid_argument("cannot open " + path);
+  char head[32];
+  if (!f.read(head, 32) || std::memcmp(head, "CCLPCSC1", 8) != 0)
+    throw std::invalid_argument(path + ": not a CCLPCSC1 file");
+  int32_t mn[2];
+  int64_t nnz;
+  std::memcpy(mn, head + 8, sizeof mn);
+  std::memcpy(&nnz, head + 16, sizeof nnz);
+  const int m = mn[0], n = mn[1];
+  if (m < 0 || n < 0 || nnz < 0) throw std::invalid_argument(path + ": bad header");
+  long long off = 32;
+  auto read = [&](void* dst, size_t bytes) {
+    f.seekg(off);
+    if (bytes && !f.read(static_cast<char*>(dst), static_cast<std::streamsize>(bytes)))
+      throw std::invalid_argument(path + ": truncated file");
+    off = (off + static_cast<long long>(bytes) + 7) / 8 * 8;
+  };
+  std::vector<int> colptr(static_cast<size_t>(n) + 1), rowind(static_cast<size_t>(nnz));
+  std::vector<double> val(static_cast<size_t>(nnz));
+  cclp::LinearProgram lp;
+  lp.c.resize(n);
+  lp.row_lower.resize(m);
+  lp.row_upper.resize(m);
+  lp.col_lower.resize(n);
+  lp.col_upper.resize(n);
+  read(colptr.data(), sizeof(int) * colptr.size());
+  read(rowind.data(), sizeof(int) * rowind.size());
+  read(val.data(), sizeof(double) * val.size());
+  read(lp.c.data(), sizeof(double) * n);
+  read(lp.row_lower.data(), sizeof(double) * m);
+  read(lp.row_upper.data(), sizeof(double) * m);
+  read(lp.col_lower.data(), sizeof(double) * n);
+  read(lp.col_upper.data(), sizeof(double) * n);
+  if (colptr[static_cast<size_t>(n)] != nnz) throw std::invalid_argument(path + ": colptr[n] != nnz");
+  lp.A = cclp::SparseMat(Eigen::Map<cclp::SparseMat>(m, n, static_cast<int>(nnz), colptr.data(),
+                                                     rowind.data(), val.data()));
+  lp.sense.resize(static_cast<size_t>(m));
+  for (int i = 0; i < m; ++i) {
+    const double l = lp.row_lower[i], u = lp.row_upper[i];
+    lp.sense[static_cast<size_t>(i)] =
+        l == u ? cclp::RowSense::kEq : (std::isfinite(u) ? cclp::RowSense::kLe : cclp::RowSense::kGe);
+  }
+  const size_t slash = path.find_last_of('/');
+  lp.name = path.substr(slash == std::string::npos ? 0 : slash + 1);
+  lp.objective_name = "OBJ";
+  lp.validate();
+  return lp;
+}
+
+bool ends_with(const std::string& s, const char* suf) {
+  const size_t k = std::strlen(suf);
+  return s.size() >= k && s.compare(s.size() - k, k, suf) == 0;
 }
 }  // namespace
 
@@ -91,7 +151,7 @@ int cclp_race_solve_file(const char* path, int mode, double eps_rel, double eps_
                          const char* basis_out, const char* solution_out, char* out, int cap) {
   cclp::LinearProgram lp;
   try {
-    lp = cclp::read_mps_file(path);
+    lp = ends_with(path, ".cscb") ? read_cscb_file(path) : cclp::read_mps_file(path);
   } catch (const std::exception& e) {
     g_err = e.what();
     return 4;

@@ -7,6 +7,11 @@
 // batch. Snapshots are extracted on the device and copied out on a side
 // stream into pinned memory; the sink is called on the caller's thread.
 // Reference: run_pdhg, proj/src/pdhg.cpp:230-378.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
@@ -1418,6 +1423,58 @@ int cclp_cu_create(const cclp_cu_lp* lp, int device, cclp_cu_ctx** out) {
     }
     *out = ctx;
   });
+}
+
+int cclp_cu_create_from_file(const char* path, int device, cclp_cu_ctx** out, int32_t* m_out,
+                             int32_t* n_out) {
+  *out = nullptr;
+  int fd = -1;
+  void* map = MAP_FAILED;
+  size_t len = 0;
+  const int rc = guarded([&] {
+    fd = open(path, O_RDONLY);
+    if (fd < 0) throw std::invalid_argument(std::string("cclp_cu_create_from_file: cannot open ") + path);
+    struct stat st;
+    if (fstat(fd, &st) != 0 || st.st_size < 32) throw std::invalid_argument("cclp_cu_create_from_file: short file");
+    len = static_cast<size_t>(st.st_size);
+    map = mmap(nullptr, len, PROT_READ, MAP_SHARED, fd, 0);
+    if (map == MAP_FAILED) throw std::invalid_argument("cclp_cu_create_from_file: mmap failed");
+    const char* base = static_cast<const char*>(map);
+    if (std::memcmp(base, "CCLPCSC1", 8) != 0) throw std::invalid_argument("cclp_cu_create_from_file: bad magic");
+    int32_t mn[2];
+    int64_t nnz;
+    std::memcpy(mn, base + 8, sizeof mn);
+    std::memcpy(&nnz, base + 16, sizeof nnz);
+    const int32_t m = mn[0], n = mn[1];
+    if (m < 0 || n < 0 || nnz < 0) throw std::invalid_argument("cclp_cu_create_from_file: bad header");
+    size_t off = 32;
+    auto take = [&](size_t bytes) {
+      const char* p = base + off;
+      off += bytes;
+      off = (off + 7) / 8 * 8;
+      if (off > len + 7) throw std::invalid_argument("cclp_cu_create_from_file: truncated file");
+      return p;
+    };
+    cclp_cu_lp lp;
+    lp.m = m;
+    lp.n = n;
+    lp.colptr = reinterpret_cast<const int32_t*>(take(sizeof(int32_t) * (static_cast<size_t>(n) + 1)));
+    lp.rowind = reinterpret_cast<const int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(nnz)));
+    lp.val = reinterpret_cast<const double*>(take(sizeof(double) * static_cast<size_t>(nnz)));
+    lp.c = reinterpret_cast<const double*>(take(sizeof(double) * n));
+    lp.row_lower = reinterpret_cast<const double*>(take(sizeof(double) * m));
+    lp.row_upper = reinterpret_cast<const double*>(take(sizeof(double) * m));
+    lp.col_lower = reinterpret_cast<const double*>(take(sizeof(double) * n));
+    lp.col_upper = reinterpret_cast<const double*>(take(sizeof(double) * n));
+    if (lp.colptr[n] != nnz) throw std::invalid_argument("cclp_cu_create_from_file: colptr[n] != nnz");
+    if (m_out) *m_out = m;
+    if (n_out) *n_out = n;
+    const int rc2 = cclp_cu_create(&lp, device, out);
+    if (rc2 != CCLP_CU_OK) throw Error(rc2, g_err);
+  });
+  if (map != MAP_FAILED) munmap(map, len);
+  if (fd >= 0) close(fd);
+  return rc;
 }
 
 int cclp_cu_destroy(cclp_cu_ctx* ctx) {

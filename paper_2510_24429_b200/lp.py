@@ -132,3 +132,50 @@ def to_standard_form(lp: LinearProgram, maximize: bool = False) -> LinearProgram
     return LinearProgram(m, n_std, colptr.astype(np.int32), rowind.astype(np.int32), val, c,
                          b.astype(np.float64).copy(), b.astype(np.float64).copy(), cl, cu,
                          name=lp.name)
+
+
+# ---- binary CSC ingest -----------------------------------
+# A flat file the engine maps and uploads directly (cclp_cu_create_from_file):
+#   bytes 0-7   magic b"CCLPCSC1"
+#   bytes 8-31  int32 m, int32 n, int64 nnz, int64 reserved (0)
+#   then, each starting on an 8-byte boundary: colptr int32[n+1], rowind
+#   int32[nnz], val f64[nnz], c f64[n], row_lower f64[m], row_upper f64[m],
+#   col_lower f64[n], col_upper f64[n]
+CSCB_MAGIC = b"CCLPCSC1"
+
+
+def _cscb_layout(m: int, n: int, nnz: int):
+    out, off = [], 32
+    for name, dt, cnt in (("colptr", np.int32, n + 1), ("rowind", np.int32, nnz),
+                          ("val", np.float64, nnz), ("c", np.float64, n),
+                          ("row_lower", np.float64, m), ("row_upper", np.float64, m),
+                          ("col_lower", np.float64, n), ("col_upper", np.float64, n)):
+        out.append((name, dt, cnt, off))
+        off += cnt * np.dtype(dt).itemsize
+        off = (off + 7) // 8 * 8
+    return out, off
+
+
+def write_cscb(lp: LinearProgram, path: str) -> None:
+    layout, total = _cscb_layout(lp.m, lp.n, lp.nnz)
+    with open(path, "wb") as f:
+        f.write(CSCB_MAGIC + np.array([lp.m, lp.n], np.int32).tobytes() +
+                np.array([lp.nnz, 0], np.int64).tobytes())
+        for name, dt, cnt, off in layout:
+            f.seek(off)
+            f.write(np.ascontiguousarray(getattr(lp, name), dt).tobytes())
+        f.truncate(total)
+
+
+def read_cscb(path: str) -> LinearProgram:
+    """Memory-mapped view of a .cscb file (no copy until touched)."""
+    with open(path, "rb") as f:
+        head = f.read(32)
+    if head[:8] != CSCB_MAGIC:
+        raise ValueError(f"{path}: not a CCLPCSC1 file")
+    m, n = np.frombuffer(head[8:16], np.int32)
+    nnz = int(np.frombuffer(head[16:24], np.int64)[0])
+    layout, _ = _cscb_layout(int(m), int(n), nnz)
+    arrs = {name: np.memmap(path, dtype=dt, mode="r", offset=off, shape=(cnt,))
+            for name, dt, cnt, off in layout}
+    return LinearProgram(int(m), int(n), **arrs, name=path)

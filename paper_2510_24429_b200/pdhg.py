@@ -109,6 +109,8 @@ def load_library(path: str = LIB_PATH):
         L.cclp_cu_default_tolerances.argtypes = [C.POINTER(_Tol)]
         L.cclp_cu_create.argtypes = [C.POINTER(_LP), C.c_int, C.POINTER(C.c_void_p)]
         L.cclp_cu_destroy.argtypes = [C.c_void_p]
+        L.cclp_cu_create_from_file.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p),
+                                               C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.cclp_cu_solve.argtypes = [C.c_void_p, C.POINTER(_Config), C.POINTER(_Tol), _dp, C.c_int32,
                                     _SINK, C.c_void_p, C.POINTER(C.c_uint8), _LOG, C.c_void_p,
                                     _dp, _dp, _dp, C.POINTER(_Result)]
@@ -149,7 +151,7 @@ EXPORTED_SYMBOLS = [
     "cclp_cu_stream", "cclp_cu_describe", "cclp_cu_gaussian_start", "cclp_cu_partition",
     "cclp_cu_nccl_unique_id", "cclp_cu_sharded_create", "cclp_cu_sharded_solve",
     "cclp_cu_sharded_begin", "cclp_cu_sharded_advance", "cclp_cu_sharded_describe",
-    "cclp_cu_sharded_destroy", "cclp_cu_sharded_create_hostcomm",
+    "cclp_cu_sharded_destroy", "cclp_cu_sharded_create_hostcomm", "cclp_cu_create_from_file",
 ]
 
 
@@ -314,6 +316,21 @@ class Engine:
                        d(k["rl"]), d(k["ru"]), d(k["cl"]), d(k["cu"]))
         self.ctx = C.c_void_p()
         _check(self.L, self.L.cclp_cu_create(C.byref(self._lp), device, C.byref(self.ctx)))
+
+    @classmethod
+    def from_file(cls, path: str, device: int = 0) -> "Engine":
+        """LP ingest from a binary CSC file (lp.write_cscb): mapped and streamed
+        to the device by the engine; the host keeps only a memory map."""
+        from .lp import read_cscb
+        self = cls.__new__(cls)
+        self.L = load_library()
+        self.lp = read_cscb(path)
+        self._keep = {}
+        self.ctx = C.c_void_p()
+        m, n = C.c_int32(), C.c_int32()
+        _check(self.L, self.L.cclp_cu_create_from_file(path.encode(), device, C.byref(self.ctx),
+                                                       C.byref(m), C.byref(n)))
+        return self
 
     def close(self) -> None:
         if self.ctx:

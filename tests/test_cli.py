@@ -65,3 +65,22 @@ def test_solve_and_bench_end_to_end(tmp_path):
     rep = json.loads(out.read_text())
     assert rep["models"] == 2 and len(rep["records"]) == 4
     assert all(r["status"] == "solved" for r in rep["records"])
+
+
+def test_solve_cscb_matches_mps(tmp_path, capsys):
+    """`solve model.cscb` (binary CSC ingest) reaches the same optimum and
+    basis as `solve model.mps` of the same LP."""
+    from paper_2510_24429_b200.lp import write_cscb
+    lp = lpgen.transportation_lp(8, 12, seed=5)
+    cli.write_mps(lp, str(tmp_path / "t.mps"), "T")
+    write_cscb(lp, str(tmp_path / "t.cscb"))
+    outs = []
+    for f in ("t.mps", "t.cscb"):
+        assert cli.main(["solve", str(tmp_path / f), "--pdhg", "cpu", "--json"]) == 0
+        outs.append(json.loads(capsys.readouterr().out.strip().splitlines()[-1]))
+    a, b = outs
+    assert a["status"] == b["status"] == "solved"
+    assert (a["rows"], a["cols"]) == (b["rows"], b["cols"])
+    assert math.isclose(a["objective"], b["objective"], rel_tol=1e-9, abs_tol=1e-9)
+    (tmp_path / "bad.cscb").write_bytes(b"CCLPCSC1" + bytes(8))
+    assert cli.main(["solve", str(tmp_path / "bad.cscb"), "--pdhg", "cpu"]) == 4
