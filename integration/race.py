@@ -36,8 +36,31 @@ def lib(kind: str):
         L.cclp_race_simulate.argtypes = [_dp, C.c_int, C.c_double, _dp, _dp, _ip, C.c_int, C.c_double,
                                          C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
                                          C.c_double, C.c_char_p, C.c_int]
+        L.cclp_race_standard_form_check.argtypes = [C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp, _dp,
+                                                    _dp, _dp, C.c_int, C.c_int, _dp]
         _cache[kind] = L
     return _cache[kind]
+
+
+def standard_form_check(lp, maximize: bool = False, named: bool = False, kind: str = "cpu",
+                        timings: bool = False):
+    """(equal, reason[, (t_reference_s, t_direct_s)]): the race's O(nnz)
+    standard form against the reference's to_standard_form
+    (standard_form.cpp:23-104) on `lp`."""
+    import numpy as np
+    L = lib(kind)
+    a = [np.ascontiguousarray(x, t) for x, t in (
+        (lp.colptr, np.int32), (lp.rowind, np.int32), (lp.val, np.float64), (lp.c, np.float64),
+        (lp.row_lower, np.float64), (lp.row_upper, np.float64), (lp.col_lower, np.float64),
+        (lp.col_upper, np.float64))]
+    ptr = [x.ctypes.data_as(_ip if x.dtype == np.int32 else _dp) for x in a]
+    t = np.zeros(2)
+    rc = L.cclp_race_standard_form_check(lp.m, lp.n, *ptr, int(maximize), int(named),
+                                         t.ctypes.data_as(_dp))
+    if rc == 2:
+        raise ValueError(L.cclp_race_last_error().decode())
+    out = (rc == 0, L.cclp_race_last_error().decode())
+    return out + ((float(t[0]), float(t[1])),) if timings else out
 
 
 def run_race(lp, kind: str = "gpu", mode: str = "concurrent", eps_rel: float = 1e-6,

@@ -5,6 +5,7 @@
 // reference's own CPU loop). Crossover is the reference's run_crossover in
 // both, compiled from /root/reference, so the two differ only in the PDHG.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -87,6 +88,10 @@ bool ends_with(const std::string& s, const char* suf) {
   return s.size() >= k && s.compare(s.size() - k, k, suf) == 0;
 }
 }  // namespace
+
+namespace cclp {
+StandardFormMap to_standard_form_direct(const LinearProgram& lp);
+}
 
 extern "C" {
 
@@ -179,7 +184,7 @@ int cclp_race_solve_file(const char* path, int mode, double eps_rel, double eps_
     j["violation"] = o.final_result.abs_violation;
     j["events"] = events.str();
     if (o.status == cclp::RaceStatus::kSolved) {
-      const cclp::StandardFormMap sf = cclp::to_standard_form(lp);
+      const cclp::StandardFormMap sf = cclp::to_standard_form_direct(lp);
       if (basis_out && *basis_out) {
         std::ofstream f(basis_out);
         cclp::write_basis(cclp::EngineModel(sf.std_lp), o.final_result.basis, f);
@@ -307,6 +312,76 @@ int cclp_race_simulate(const double* trace, int ntrace, double sec_per_iter, con
   } catch (const std::exception& e) {
     g_err = e.what();
     return 1;
+  }
+}
+
+
+// Test hook: the race's O(nnz) standard form against the reference's
+// to_standard_form on the same LP (row senses from the bounds, optional max
+// objective). 0 = identical in every field, 1 = differs (reason in
+// cclp_race_last_error), 2 = error. seconds (optional) receives the two
+// wall times {reference, direct}.
+int cclp_race_standard_form_check(int m, int n, const int* colptr, const int* rowind, const double* val,
+                                  const double* c, const double* rl, const double* ru, const double* cl,
+                                  const double* cu, int maximize, int named, double* seconds) {
+  try {
+    cclp::LinearProgram lp;
+    lp.A = cclp::SparseMat(Eigen::Map<cclp::SparseMat>(m, n, colptr[n], colptr, rowind, val));
+    lp.c = vec(c, n);
+    lp.row_lower = vec(rl, m);
+    lp.row_upper = vec(ru, m);
+    lp.col_lower = vec(cl, n);
+    lp.col_upper = vec(cu, n);
+    lp.obj_sense = maximize ? cclp::ObjSense::kMax : cclp::ObjSense::kMin;
+    lp.obj_offset = 1.25;
+    lp.sense.resize(static_cast<size_t>(m));
+    for (int i = 0; i < m; ++i)
+      lp.sense[static_cast<size_t>(i)] =
+          rl[i] == ru[i] ? cclp::RowSense::kEq : (std::isfinite(ru[i]) ? cclp::RowSense::kLe : cclp::RowSense::kGe);
+    if (named) {
+      for (int i = 0; i < m; ++i) lp.row_names.push_back("row" + std::to_string(i));
+      for (int j = 0; j < n; ++j) lp.col_names.push_back("col" + std::to_string(j));
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    const cclp::StandardFormMap a = cclp::to_standard_form(lp);
+    const auto t1 = std::chrono::steady_clock::now();
+    const cclp::StandardFormMap b = cclp::to_standard_form_direct(lp);
+    const auto t2 = std::chrono::steady_clock::now();
+    if (seconds) {
+      seconds[0] = std::chrono::duration<double>(t1 - t0).count();
+      seconds[1] = std::chrono::duration<double>(t2 - t1).count();
+    }
+    auto vec_eq = [](const cclp::Vector& x, const cclp::Vector& y) {
+      if (x.size() != y.size()) return false;
+      for (cclp::Index i = 0; i < x.size(); ++i)
+        if (std::memcmp(x.data() + i, y.data() + i, sizeof(double)) != 0) return false;
+      return true;
+    };
+    const auto& A = a.std_lp.A;
+    const auto& B = b.std_lp.A;
+    std::string why;
+    if (A.rows() != B.rows() || A.cols() != B.cols() || A.nonZeros() != B.nonZeros()) why = "A shape";
+    else if (!std::equal(A.outerIndexPtr(), A.outerIndexPtr() + A.cols() + 1, B.outerIndexPtr())) why = "A colptr";
+    else if (!std::equal(A.innerIndexPtr(), A.innerIndexPtr() + A.nonZeros(), B.innerIndexPtr())) why = "A rowind";
+    else if (std::memcmp(A.valuePtr(), B.valuePtr(), sizeof(double) * static_cast<size_t>(A.nonZeros())) != 0)
+      why = "A values";
+    else if (!vec_eq(a.std_lp.c, b.std_lp.c)) why = "c";
+    else if (!vec_eq(a.std_lp.row_lower, b.std_lp.row_lower) || !vec_eq(a.std_lp.row_upper, b.std_lp.row_upper))
+      why = "row bounds";
+    else if (!vec_eq(a.std_lp.col_lower, b.std_lp.col_lower) || !vec_eq(a.std_lp.col_upper, b.std_lp.col_upper))
+      why = "column bounds";
+    else if (a.std_lp.col_names != b.std_lp.col_names || a.std_lp.row_names != b.std_lp.row_names) why = "names";
+    else if (a.std_lp.sense != b.std_lp.sense || a.std_lp.obj_sense != b.std_lp.obj_sense ||
+             a.std_lp.obj_offset != b.std_lp.obj_offset || a.std_lp.name != b.std_lp.name)
+      why = "senses / offset";
+    else if (a.slack_col_of_row != b.slack_col_of_row || a.negated != b.negated || a.orig_cols != b.orig_cols ||
+             a.orig_rows != b.orig_rows)
+      why = "map";
+    g_err = why;
+    return why.empty() ? 0 : 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 2;
   }
 }
 

@@ -32,6 +32,9 @@
 
 namespace cclp {
 
+// integration/standard_form_direct.cpp: the same map in O(nnz).
+StandardFormMap to_standard_form_direct(const LinearProgram& lp);
+
 const char* to_string(RaceStatus status) {
   switch (status) {
     case RaceStatus::kSolved: return "solved";
@@ -215,7 +218,7 @@ RaceOutcome run_race(const LinearProgram& lp, const RaceConfig& config) {
   S.config = &config;
   S.out = &out;
   S.t0 = Clock::now();
-  const StandardFormMap sf = to_standard_form(lp);
+  const StandardFormMap sf = to_standard_form_direct(lp);
   S.std_lp = &sf.std_lp;
   const bool concurrent = config.mode == RaceMode::kConcurrent;
   out.thresholds = concurrent ? schedule_thresholds(config.tol) : std::vector<Scalar>{};

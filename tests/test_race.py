@@ -63,3 +63,45 @@ def test_cpu_race_two_var_and_transport():
     assert base["status"] == conc["status"] == "solved"
     assert base["winner"] == "main"
     assert conc["objective"] == pytest.approx(base["objective"], rel=1e-9)
+
+
+def _general_lp(m, n, seed, density=0.2):
+    """Mixed row types: equality, <=, >=, ranged; a few empty columns."""
+    import numpy as np
+    from paper_2510_24429_b200.lp import INF, LinearProgram, csc_from_triplets
+    rng = np.random.default_rng(seed)
+    mask = rng.random((m, n)) < density
+    mask[:, ::7] = False  # empty columns
+    r, c = np.nonzero(mask)
+    cp, ri, v = csc_from_triplets(m, n, r, c, rng.uniform(0.5, 2.0, r.size))
+    kind = rng.integers(0, 4, m)
+    b = rng.uniform(-1, 1, m)
+    rl = np.where(kind == 2, -INF, b)
+    ru = np.where(kind == 1, INF, np.where(kind == 3, b + 1.0, b))
+    return LinearProgram(m, n, cp, ri, v, rng.normal(size=n), rl, ru,
+                         np.zeros(n), np.where(rng.random(n) < 0.3, 4.0, INF))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+@pytest.mark.parametrize("maximize,named", [(False, False), (True, False), (False, True)])
+def test_direct_standard_form_equals_reference(seed, maximize, named):
+    """The race's O(nnz) to_standard_form_direct (integration/
+    standard_form_direct.cpp) is field-for-field the reference's
+    to_standard_form (standard_form.cpp:23-104)."""
+    lp = _general_lp(23 + seed, 41 + 3 * seed, seed)
+    ok, why = race.standard_form_check(lp, maximize, named)
+    assert ok, why
+    eq = lpgen.transportation_lp(5, 7, seed=seed)  # slack-free too
+    ok, why = race.standard_form_check(eq, maximize, named)
+    assert ok, why
+
+
+def test_direct_standard_form_rejects_free_row():
+    import numpy as np
+    from paper_2510_24429_b200.lp import INF
+    lp = _general_lp(10, 20, 3)
+    lp.row_lower = lp.row_lower.copy()
+    lp.row_upper = lp.row_upper.copy()
+    lp.row_lower[4], lp.row_upper[4] = -INF, INF
+    with pytest.raises(ValueError):
+        race.standard_form_check(lp)
