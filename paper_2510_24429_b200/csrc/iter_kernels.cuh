@@ -208,14 +208,14 @@ __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, 
 
 static_assert(sizeof(Ctrl) % 8 == 0, "Ctrl is copied as 8-byte words");
 
-// Reduces every epilogue block's partials into rowv[kRowParts] and
-// colv[kColParts] (shared memory): warp w takes fields w, w+nwarps, ...; lane
-// l takes blocks l, l+32, ... in order, then a fixed butterfly
-// (deterministic, one round of loads).
+// Reduces every epilogue block's partials (field-major: field f of block b at
+// src[f * nblocks + b]) into rowv[kRowParts] and colv[kColParts] (shared
+// memory), deterministically.
 __device__ __forceinline__ void reduce_partials(const double* rowsrc, int nrow, const double* colsrc,
                                                 int ncol, double* rowv, double* colv) {
   // half-warp h takes field h (all 22 fields in one round with >= 11 warps);
-  // lane l of the half takes blocks l, l+16, ... with 8 loads in flight,
+  // lane l of the half takes blocks l, l+16, ... with 16 loads in flight (one
+  // round up to 256 blocks; consecutive lanes read consecutive blocks),
   // accumulates them in order, then a fixed butterfly within the half
   const int hl = threadIdx.x & 15;
   for (int fld = threadIdx.x >> 4; fld - static_cast<int>(threadIdx.x >> 4) < kRowParts + kColParts;
@@ -224,19 +224,18 @@ __device__ __forceinline__ void reduce_partials(const double* rowsrc, int nrow, 
     const bool is_row = fld < kRowParts;
     const int f = is_row ? fld : fld - kRowParts;
     const bool is_max = is_row ? ((kRowMaxMask >> f) & 1u) : ((kColMaxMask >> f) & 1u);
-    const double* src = is_row ? rowsrc : colsrc;
-    const int stride = is_row ? kRowParts : kColParts;
     const int nb = live ? (is_row ? nrow : ncol) : 0;
+    const double* src = (is_row ? rowsrc : colsrc) + static_cast<long long>(f) * nb;
     double a = 0.0;
-    for (int b0 = hl; b0 < nb; b0 += 16 * 8) {
-      double v[8];
+    for (int b0 = hl; b0 < nb; b0 += 16 * 16) {
+      double v[16];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
+      for (int k = 0; k < 16; ++k) {
         const int b = b0 + 16 * k;
-        v[k] = b < nb ? __ldcg(src + b * stride + f) : 0.0;
+        v[k] = b < nb ? __ldcg(src + b) : 0.0;
       }
 #pragma unroll
-      for (int k = 0; k < 8; ++k)
+      for (int k = 0; k < 16; ++k)
         if (b0 + 16 * k < nb) a = is_max ? amax(a, v[k]) : a + v[k];
     }
 #pragma unroll
@@ -553,7 +552,7 @@ __global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init
   for (int i0 = blockIdx.x * kEpiBlock + threadIdx.x; i0 < p.m; i0 += kDualU * stride)
     dual_span(p, si, i0, stride, p.m, acc);
   block_reduce<kRowParts, kRowMaxMask, kEpiBlock>(acc, red, out);
-  if (threadIdx.x < kRowParts) p.rowp[blockIdx.x * kRowParts + threadIdx.x] = out[threadIdx.x];
+  if (threadIdx.x < kRowParts) p.rowp[threadIdx.x * gridDim.x + blockIdx.x] = out[threadIdx.x];  // field-major
   if (p.push.on) push_signal_grid(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1), p.push.counter);
 }
 
@@ -626,7 +625,7 @@ __global__ void __launch_bounds__(kEpiBlock) k_primal(const IterParams p, int in
   for (int j0 = blockIdx.x * kEpiBlock + threadIdx.x; j0 < p.n; j0 += kPrimalU * stride)
     primal_span(p, si, j0, stride, p.n, acc);
   block_reduce<kColParts, kColMaxMask, kEpiBlock>(acc, red, out);
-  if (threadIdx.x < kColParts) p.colp[blockIdx.x * kColParts + threadIdx.x] = out[threadIdx.x];
+  if (threadIdx.x < kColParts) p.colp[threadIdx.x * gridDim.x + blockIdx.x] = out[threadIdx.x];  // field-major
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
