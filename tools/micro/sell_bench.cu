@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <numeric>
 #include <vector>
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s line %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
@@ -97,6 +98,57 @@ __global__ void __launch_bounds__(1024) v_sell(int nsl, const long long* __restr
   }
 }
 
+// SELL-G: 32/G rows per slice, G lanes per row; lane gl of row r takes the
+// row's elements gl, gl+G, ... (stored at off + k*32 + r*G + gl), then the
+// same xor butterfly as the CSR-G kernel: bit-identical to it.
+template <int G, int U, bool PIPE>
+__global__ void __launch_bounds__(1024) v_sellg(int nsl, const long long* __restrict__ soff, const int* __restrict__ swid,
+    const int* __restrict__ plen, const int* __restrict__ sidx, const double* __restrict__ sval,
+    const double* __restrict__ x, double* __restrict__ y, int m) {
+  constexpr int R = 32 / G;
+  const int lane = threadIdx.x & 31, r = lane / G, gl = lane % G;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int s = gw; s < nsl; s += nw) {
+    const long long off = soff[s];
+    const int w = swid[s];
+    const int row = s * R + r;
+    const int len = row < m ? __ldg(plen + row) : 0;
+    const int* ib = sidx + off + lane;
+    const double* vb = sval + off + lane;
+    double acc = 0.0;
+    if (!PIPE) {
+      for (int k = 0; k < w; k += U) {
+        int ii[U]; double vv[U], xx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) { const bool ok = (k + u) * G + gl < len; ii[u] = ok ? __ldcs(ib + (k + u) * 32) : -1; vv[u] = ok ? __ldcs(vb + (k + u) * 32) : 0.0; }
+#pragma unroll
+        for (int u = 0; u < U; ++u) xx[u] = ii[u] >= 0 ? __ldg(x + ii[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; ++u) if (ii[u] >= 0) acc = acc + vv[u] * xx[u];
+      }
+    } else {
+      int ii[U]; double vv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) { const bool ok = u * G + gl < len; ii[u] = ok ? __ldcs(ib + u * 32) : -1; vv[u] = ok ? __ldcs(vb + u * 32) : 0.0; }
+      for (int k = 0; k < w; k += U) {
+        double xx[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) xx[u] = ii[u] >= 0 ? __ldg(x + ii[u]) : 0.0;
+        int in[U]; double vn[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) { const bool ok = (k + U + u) * G + gl < len; in[u] = ok ? __ldcs(ib + (k + U + u) * 32) : -1; vn[u] = ok ? __ldcs(vb + (k + U + u) * 32) : 0.0; }
+#pragma unroll
+        for (int u = 0; u < U; ++u) if (ii[u] >= 0) acc = acc + vv[u] * xx[u];
+#pragma unroll
+        for (int u = 0; u < U; ++u) { ii[u] = in[u]; vv[u] = vn[u]; }
+      }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(~0u, acc, o);
+    if (gl == 0 && row < m) y[row] = acc;
+  }
+}
+
 int main(int argc, char** argv) {
   char path[512];
   snprintf(path, sizeof path, "%s.meta", argv[1]);
@@ -153,6 +205,56 @@ int main(int argc, char** argv) {
       if (G == 16) run(nm, f, [&] { v_csr2<16, 2><<<grid, 1024>>>(dst, dp, di, dv, dx, dy); });
     }
   }
+  {
+    // SELL-G in natural row order (no sorting), same G as the CSR kernel
+    const int R = 32 / G;
+    const int nsl = (m + R - 1) / R;
+    std::vector<long long> soff(nsl + 1); std::vector<int> swid(nsl), plen(m);
+    for (int i = 0; i < m; ++i) plen[i] = hp[i + 1] - hp[i];
+    soff[0] = 0;
+    for (int s = 0; s < nsl; ++s) {
+      int w = 0; for (int r = 0; r < R && s * R + r < m; ++r) w = std::max(w, (plen[s * R + r] + G - 1) / G);
+      swid[s] = w; soff[s + 1] = soff[s] + 32LL * w;
+    }
+    const long long tot = soff[nsl];
+    std::vector<int> si(tot, -1); std::vector<double> sv(tot, 0.0);
+    for (int i = 0; i < m; ++i) {
+      const int s = i / R, r = i % R;
+      for (int e = 0; e < plen[i]; ++e) { const long long q = soff[s] + 32LL * (e / G) + r * G + e % G; si[q] = hi[hp[i] + e]; sv[q] = hv[hp[i] + e]; }
+    }
+    long long *d_off; int *d_w, *d_plen, *d_si; double* d_sv;
+    CK(cudaMalloc(&d_off, 8 * (nsl + 1))); CK(cudaMalloc(&d_w, 4 * nsl)); CK(cudaMalloc(&d_plen, 4 * m));
+    CK(cudaMalloc(&d_si, 4 * tot)); CK(cudaMalloc(&d_sv, 8 * tot));
+    CK(cudaMemcpy(d_off, soff.data(), 8 * (nsl + 1), cudaMemcpyHostToDevice)); CK(cudaMemcpy(d_w, swid.data(), 4 * nsl, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_plen, plen.data(), 4 * m, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_si, si.data(), 4 * tot, cudaMemcpyHostToDevice)); CK(cudaMemcpy(d_sv, sv.data(), 8 * tot, cudaMemcpyHostToDevice));
+    printf("SELL-G%d: padding %.2f%%\n", G, 100.0 * (tot - nnz) / nnz);
+    std::vector<double> csr_y(m), sg_y(m);
+    for (int bs : {256, 1024}) for (int per : {1, 2}) {
+      const int grid = bs == 256 ? sms * per * 4 : sms * per;
+      char nm[80];
+#define SG(GG, UU, PP) \
+      if (G == GG) { snprintf(nm, sizeof nm, "sellG%d U%d%s bs%d g%d", GG, UU, PP ? " pipe" : "", bs, grid); \
+        run(nm, false, [&] { v_sellg<GG, UU, PP><<<grid, bs>>>(nsl, d_off, d_w, d_plen, d_si, d_sv, dx, dy, m); }); }
+      SG(4, 2, false) SG(4, 4, false) SG(4, 2, true) SG(4, 4, true)
+      SG(8, 2, false) SG(8, 4, false) SG(8, 2, true)
+      SG(16, 2, false) SG(16, 2, true)
+    }
+    CK(cudaMemcpy(sg_y.data(), dy, 8 * m, cudaMemcpyDeviceToHost));
+    cudaFree(d_off); cudaFree(d_w); cudaFree(d_plen); cudaFree(d_si); cudaFree(d_sv);
+    // bit-identity against the CSR-G kernel
+    int* dst; const int grid = sms; std::vector<int> st(grid + 1);
+    for (int b = 0; b <= grid; ++b) st[b] = (int)((long long)m * b / grid);
+    CK(cudaMalloc(&dst, 4 * (grid + 1))); CK(cudaMemcpy(dst, st.data(), 4 * (grid + 1), cudaMemcpyHostToDevice));
+    if (G == 4) v_csr2<4, 2><<<grid, 1024>>>(dst, dp, di, dv, dx, dy);
+    if (G == 8) v_csr2<8, 2><<<grid, 1024>>>(dst, dp, di, dv, dx, dy);
+    if (G == 16) v_csr2<16, 2><<<grid, 1024>>>(dst, dp, di, dv, dx, dy);
+    CK(cudaMemcpy(csr_y.data(), dy, 8 * m, cudaMemcpyDeviceToHost));
+    int same = 0; for (int i = 0; i < m; ++i) same += memcmp(&csr_y[i], &sg_y[i], 8) == 0;
+    printf("SELL-G%d vs CSR-G%d bit-identical rows: %d/%d\n", G, G, same, m);
+    cudaFree(dst);
+  }
+  if (argc > 3) return 0;
   for (int sigma : {32, 256, 4096}) {
     std::vector<int> perm(m); std::iota(perm.begin(), perm.end(), 0);
     for (int w0 = 0; w0 < m; w0 += sigma) {
