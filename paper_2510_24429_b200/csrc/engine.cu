@@ -28,6 +28,7 @@
 #include <type_traits>
 #include <random>
 #include <stdexcept>
+#include <memory>
 #include <thread>
 #include <string>
 #include <vector>
@@ -387,6 +388,20 @@ struct Context {
   void build_csr();
   void partition();
   void tune_spmv();
+  // SpMV geometry tuning folded into the first power iterations (results are
+  // geometry-independent, so the candidates can do real work): both start
+  // tables stay alive until the choice is made.
+  bool tune_pending = false;
+  int* tune_rows_st[3] = {nullptr, nullptr, nullptr};
+  int* tune_cols_st[3] = {nullptr, nullptr, nullptr};
+  int tune_sms = 148;
+  cudaEvent_t tune_ev[96] = {};
+  void set_geometry(bool rows_side, int per_sm, int rpg);
+  void choose_geometry(const std::vector<float> (&ms)[2][4]);
+  void explicit_tune();
+  void ensure_tuned() {
+    if (tune_pending) explicit_tune();
+  }
   int grow() const { return exact ? 1 : Grow; }
   int gcol() const { return exact ? 1 : Gcol; }
   void launch_spmv(bool transpose, const double* vec, double* out, bool scaled, const int* stop);
@@ -453,6 +468,10 @@ Context::~Context() {
       void* pp[] = {pn.ptr, pn.idx, pn.perm, pn.val, pn.start, pn.sp.seg, pn.sp.lr_first, pn.sp.part, pn.sp.cnt};
       for (void* q : pp) release(q);
     }
+    for (int k = 1; k < 3; ++k) {  // start tables not already owned as spmv_*_start
+      if (tune_rows_st[k] != spmv_row_start) release(tune_rows_st[k]);
+      if (tune_cols_st[k] != spmv_col_start) release(tune_cols_st[k]);
+    }
     // pinned buffers may still be targets of queued copies
     cudaStreamSynchronize(stream);
     if (side) cudaStreamSynchronize(side);
@@ -463,6 +482,8 @@ Context::~Context() {
   for (auto& e : stage_ev)
     if (e) cudaEventDestroy(e);
   if (ev_snap) cudaEventDestroy(ev_snap);
+  for (auto& e : tune_ev)
+    if (e) cudaEventDestroy(e);
   if (ev_a) cudaEventDestroy(ev_a);
   if (ev_b) cudaEventDestroy(ev_b);
   if (stream && own_stream) cudaStreamDestroy(stream);
@@ -776,17 +797,78 @@ PanelArgs Context::panel_args(int k) const {
 void Context::tune_spmv() {
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  tune_sms = sms;
   CK(cudaMemsetAsync(wn, 0, sizeof(double) * std::max(n, 1), stream));
   CK(cudaMemsetAsync(wm, 0, sizeof(double) * std::max(m, 1), stream));
   plan_side(true, Grow, plan_rows);
   plan_side(false, Gcol, plan_cols);
-  int* rows_st[3] = {nullptr, plan_starts(true, plan_rows, sms), plan_starts(true, plan_rows, 2 * sms)};
-  int* cols_st[3] = {nullptr, plan_starts(false, plan_cols, sms), plan_starts(false, plan_cols, 2 * sms)};
+  tune_rows_st[1] = plan_starts(true, plan_rows, sms);
+  tune_rows_st[2] = plan_starts(true, plan_rows, 2 * sms);
+  tune_cols_st[1] = plan_starts(false, plan_cols, sms);
+  tune_cols_st[2] = plan_starts(false, plan_cols, 2 * sms);
+  build_panels(x_full ? static_cast<long long>(shard_count) * Sn : n);
+  plan_rows.wrow.clear();
+  plan_rows.wrow.shrink_to_fit();
+  plan_rows.wseg.clear();
+  plan_rows.wseg.shrink_to_fit();
+  plan_cols.wrow.clear();
+  plan_cols.wrow.shrink_to_fit();
+  plan_cols.wseg.clear();
+  plan_cols.wseg.shrink_to_fit();
+  set_geometry(true, 2, 1);
+  set_geometry(false, 2, 1);
+  tune_pending = true;
+  // A device-wide context (not a shard) without column panels tunes inside
+  // its first power iterations (power_norm); everything else now.
+  const bool defer = x_full == nullptr && !use_panels() && std::getenv("CCLP_CU_TUNE_EAGER") == nullptr;
+  if (!defer) explicit_tune();
+}
+
+void Context::set_geometry(bool rows_side, int per_sm, int rpg) {
+  if (rows_side) {
+    spmv_grid_r = tune_sms * per_sm;
+    spmv_row_start = tune_rows_st[per_sm];
+    rpg_r = rpg;
+  } else {
+    spmv_grid_c = tune_sms * per_sm;
+    spmv_col_start = tune_cols_st[per_sm];
+    rpg_c = rpg;
+  }
+}
+
+// Candidates in the order (1,1), (1,2), (2,1), (2,2) = (blocks per SM, rows
+// per group in flight); a later one replaces the best only when its median
+// is 3% faster (prefer the simpler geometry). ms[side][cand] = samples.
+void Context::choose_geometry(const std::vector<float> (&ms)[2][4]) {
+  for (int side = 0; side < 2; ++side) {
+    float best = 1e30f;
+    int best_ps = 2, best_rpg = 1;
+    for (int c = 0; c < 4; ++c) {
+      std::vector<float> t = ms[side][c];
+      if (t.empty()) continue;
+      std::sort(t.begin(), t.end());
+      const float med = t[t.size() / 2];
+      if (med < 0.97f * best) {
+        best = med;
+        best_ps = 1 + c / 2;
+        best_rpg = 1 + c % 2;
+      }
+    }
+    set_geometry(side == 0, best_ps, best_rpg);
+  }
+  release(tune_rows_st[3 - spmv_grid_r / tune_sms]);
+  release(tune_cols_st[3 - spmv_grid_c / tune_sms]);
+  tune_rows_st[3 - spmv_grid_r / tune_sms] = nullptr;
+  tune_cols_st[3 - spmv_grid_c / tune_sms] = nullptr;
+  tune_pending = false;
+}
+
+// Stand-alone tuning: each candidate timed between launches of the other
+// side's SpMV (the cache state of the iteration), first sample discarded.
+void Context::explicit_tune() {
   auto launch_side = [&](bool rows_side, int per_sm, int rpg) {
-    const int grid = sms * per_sm;
-    spmv_grid_r = spmv_grid_c = grid;
-    spmv_row_start = rows_st[per_sm];
-    spmv_col_start = cols_st[per_sm];
+    set_geometry(rows_side, per_sm, rpg);
+    const int grid = rows_side ? spmv_grid_r : spmv_grid_c;
     const SpmvPlan P = plan(rows_side);
     const bool lng = P.thr != 0x7fffffff;
     if (rows_side) {
@@ -803,56 +885,26 @@ void Context::tune_spmv() {
     CKL("tune spmv");
   };
   const char* force = std::getenv("CCLP_CU_RPG");
-  auto tune_one = [&](bool rows_side, int* per_sm_out, int* rpg_out) {
-    float best = 1e30f;
-    int best_ps = 2, best_rpg = 1;
-    for (int per_sm : {1, 2}) {
-      for (int rpg : {1, 2}) {
-        if (force && std::atoi(force) != rpg) continue;
-        std::vector<float> t;
-        // 5 timed samples for short SpMVs; 3 once a launch costs > 200 us
-        const int reps = (nnz > 30'000'000) ? 4 : 6;
-        for (int rep = 0; rep < reps; ++rep) {
-          launch_side(!rows_side, 2, 1);
-          CK(cudaEventRecord(ev_a, stream));
-          launch_side(rows_side, per_sm, rpg);
-          CK(cudaEventRecord(ev_b, stream));
-          CK(cudaEventSynchronize(ev_b));
-          float ms = 0;
-          CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
-          if (rep > 0) t.push_back(ms);
-        }
-        std::sort(t.begin(), t.end());
-        const float med = t[t.size() / 2];
-        // prefer the simpler candidate unless the other is clearly faster
-        if (med < 0.97f * best) {
-          best = med;
-          best_ps = per_sm;
-          best_rpg = rpg;
-        }
+  std::vector<float> ms[2][4];
+  const int reps = (nnz > 30'000'000) ? 4 : 6;
+  for (int side = 0; side < 2; ++side) {
+    const bool rows_side = side == 0;
+    for (int c = 0; c < 4; ++c) {
+      const int per_sm = 1 + c / 2, rpg = 1 + c % 2;
+      if (force && std::atoi(force) != rpg) continue;
+      for (int rep = 0; rep < reps; ++rep) {
+        launch_side(!rows_side, 2, 1);
+        CK(cudaEventRecord(ev_a, stream));
+        launch_side(rows_side, per_sm, rpg);
+        CK(cudaEventRecord(ev_b, stream));
+        CK(cudaEventSynchronize(ev_b));
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, ev_a, ev_b));
+        if (rep > 0) ms[side][c].push_back(t);
       }
     }
-    *per_sm_out = best_ps;
-    *rpg_out = best_rpg;
-  };
-  int ps_r = 2, ps_c = 2;
-  tune_one(true, &ps_r, &rpg_r);
-  tune_one(false, &ps_c, &rpg_c);
-  spmv_grid_r = sms * ps_r;
-  spmv_grid_c = sms * ps_c;
-  spmv_row_start = rows_st[ps_r];
-  spmv_col_start = cols_st[ps_c];
-  release(rows_st[3 - ps_r]);
-  release(cols_st[3 - ps_c]);
-  build_panels(x_full ? static_cast<long long>(shard_count) * Sn : n);
-  plan_rows.wrow.clear();
-  plan_rows.wrow.shrink_to_fit();
-  plan_rows.wseg.clear();
-  plan_rows.wseg.shrink_to_fit();
-  plan_cols.wrow.clear();
-  plan_cols.wrow.shrink_to_fit();
-  plan_cols.wseg.clear();
-  plan_cols.wseg.shrink_to_fit();
+  }
+  choose_geometry(ms);
 }
 
 void Context::launch_spmv(bool transpose, const double* vec, double* out, bool scaled,
@@ -945,8 +997,9 @@ void gaussian_start(uint64_t seed, long long n, double* v) {
   std::mt19937_64 rng(seed + 0x9e3779b97f4a7c15ull);
   const long long pairs = (n + 1) / 2;  // the last one half-used when n is odd
   constexpr long long kAttempts = 1 << 19;  // per chunk
-  std::vector<uint64_t> buf[2] = {std::vector<uint64_t>(2 * kAttempts),
-                                  std::vector<uint64_t>(2 * kAttempts)};
+  // raw engine outputs, two chunks (uninitialized: filled before use)
+  std::unique_ptr<uint64_t[]> buf[2];
+  long long buf_cap[2] = {0, 0};
   const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
   auto canon = [](uint64_t u) {
     const double r = static_cast<double>(u) * 0x1p-64;
@@ -959,9 +1012,9 @@ void gaussian_start(uint64_t seed, long long n, double* v) {
     return !(r2 > 1.0 || r2 == 0.0);
   };
   // decides chunk d's attempts and writes its accepted pairs from pair `base`
-  auto process = [&](const uint64_t* d, long long base) -> long long {
+  auto process = [&](const uint64_t* d, long long na, long long base) -> long long {
     std::vector<long long> cnt(T + 1, 0);
-    const long long per = (kAttempts + T - 1) / T;
+    const long long per = (na + T - 1) / T;
     auto run = [&](auto&& body) {
       std::vector<std::thread> th;
       for (int t = 1; t < T; ++t) th.emplace_back(body, t);
@@ -971,14 +1024,14 @@ void gaussian_start(uint64_t seed, long long n, double* v) {
     run([&](int t) {
       long long c = 0;
       double x, y, r2;
-      for (long long a = t * per; a < std::min(kAttempts, (t + 1) * per); ++a) c += attempt(d, a, x, y, r2);
+      for (long long a = t * per; a < std::min(na, (t + 1) * per); ++a) c += attempt(d, a, x, y, r2);
       cnt[t + 1] = c;
     });
     for (int t = 0; t < T; ++t) cnt[t + 1] += cnt[t];
     run([&](int t) {
       long long k = base + cnt[t];
       double x, y, r2;
-      for (long long a = t * per; a < std::min(kAttempts, (t + 1) * per) && k < pairs; ++a) {
+      for (long long a = t * per; a < std::min(na, (t + 1) * per) && k < pairs; ++a) {
         if (!attempt(d, a, x, y, r2)) continue;
         const double mult = std::sqrt(-2 * std::log(r2) / r2);
         v[2 * k] = y * mult * 1.0 + 0.0;
@@ -988,21 +1041,45 @@ void gaussian_start(uint64_t seed, long long n, double* v) {
     });
     return cnt[T];
   };
-  auto fill = [&](std::vector<uint64_t>& b) {
-    for (auto& w : b) w = rng();
+  // Attempts to draw for `r` more pairs: the expected count (acceptance pi/4)
+  // plus six standard deviations, capped at one chunk. Drawing more than
+  // needed only discards engine outputs; drawing fewer costs another chunk.
+  auto want = [&](long long r) {
+    const double p = 0.78539816339744831;
+    const double a = r / p + 6.0 * std::sqrt(r * (1.0 - p)) / p + 64.0;
+    return std::min<long long>(kAttempts, static_cast<long long>(a));
+  };
+  auto fill = [&](int b, long long na) {
+    if (buf_cap[b] < na) {
+      buf[b].reset(new uint64_t[2 * na]);
+      buf_cap[b] = na;
+    }
+    uint64_t* d = buf[b].get();
+    for (long long i = 0; i < 2 * na; ++i) d[i] = rng();
   };
   long long done = 0;
   int cur = 0;
-  fill(buf[cur]);
+  long long na = want(pairs);
+  fill(cur, na);
   while (true) {
     long long got = 0;
-    std::thread worker([&, cur] { got = process(buf[cur].data(), done); });
-    const bool more = true;
-    if (more) fill(buf[cur ^ 1]);  // the next chunk while this one is decided
+    std::thread worker([&, cur, na] { got = process(buf[cur].get(), na, done); });
+    // the next chunk is drawn while this one is decided, only when this one
+    // cannot be expected to finish the vector
+    long long na_next = 0;
+    if (na == kAttempts && done + static_cast<long long>(0.78 * na) < pairs) {
+      na_next = want(pairs - done - static_cast<long long>(0.78 * na));
+      fill(cur ^ 1, na_next);
+    }
     worker.join();
     done += got;
     if (done >= pairs) break;
     cur ^= 1;
+    if (na_next == 0) {  // short (rare): draw the remainder now
+      na_next = want(pairs - done);
+      fill(cur, na_next);
+    }
+    na = na_next;
   }
 }
 
@@ -1011,7 +1088,10 @@ void gaussian_start(uint64_t seed, long long n, double* v) {
 // geometry (G lanes per row), nu = ||u|| and lambda = v.u in one reduction,
 // then v = u / nu materialized (the reference's `v = u / norm`, :62).
 double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool pregenerated) {
-  if (m == 0 || n == 0 || nnz == 0) return 0.0;
+  if (m == 0 || n == 0 || nnz == 0) {
+    ensure_tuned();
+    return 0.0;
+  }
   // start vector: mt19937_64 + normal_distribution, as the reference (:49-52)
   if (!h_v0) h_v0 = host_alloc<double>(n);
   if (!pregenerated) {
@@ -1034,7 +1114,40 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
   const double* aval = scaled ? sval_csr : val_csr;
   const double* atval = scaled ? sval_csc : val_csc;
   const int rgrid = blocks_for(n, kBlock, 148 * 4);
+  // Deferred geometry tuning: the first K iterations cycle through the four
+  // candidates (one warm-up round, then `reps` timed rounds) with events
+  // around each product; one host sync after them picks the geometry.
+  const bool rows_panels = scaled && use_panels();
+  const int reps = (nnz > 30'000'000) ? 3 : 5;
+  int K = 0;
+  if (tune_pending && !rows_panels && iterations >= 4 * (reps + 1) && 4 * (reps + 1) * 3 <= 96) {
+    K = 4 * (reps + 1);
+    for (int e = 0; e < 3 * K; ++e)
+      if (!tune_ev[e]) CK(cudaEventCreate(&tune_ev[e]));
+  } else {
+    ensure_tuned();
+  }
+  const char* force = std::getenv("CCLP_CU_RPG");
   for (int t = 0; t < iterations; ++t) {
+    const int cand = t % 4;
+    if (t < K) {
+      set_geometry(true, 1 + cand / 2, 1 + cand % 2);
+      set_geometry(false, 1 + cand / 2, 1 + cand % 2);
+      CK(cudaEventRecord(tune_ev[3 * t], stream));
+    } else if (t == K && K > 0) {
+      CK(cudaEventSynchronize(tune_ev[3 * K - 1]));
+      std::vector<float> ms[2][4];
+      for (int q = 4; q < K; ++q) {  // round 0 is the warm-up
+        const int c = q % 4;
+        if (force && std::atoi(force) != 1 + c % 2) continue;
+        float a = 0, b = 0;
+        CK(cudaEventElapsedTime(&a, tune_ev[3 * q], tune_ev[3 * q + 1]));
+        CK(cudaEventElapsedTime(&b, tune_ev[3 * q + 1], tune_ev[3 * q + 2]));
+        ms[0][c].push_back(a);
+        ms[1][c].push_back(b);
+      }
+      choose_geometry(ms);
+    }
     const SpmvPlan Pr = plan(true), Pc = plan(false);
     if (scaled && use_panels()) {  // w = A v (:57), panel by panel
       for (int k = 0; k < static_cast<int>(panels.size()); ++k) {
@@ -1050,14 +1163,17 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
             Pr, rowptr, colind, aval, GatherPlain{v}, wm, rpg_r);
       });
     }
+    if (t < K) CK(cudaEventRecord(tune_ev[3 * t + 1], stream));
     with_group_long(gcol(), Pc.thr != 0x7fffffff, [&](auto g, auto l) {  // u = A' w (:58)
       k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(
           Pc, colptr, rowind, atval, GatherPlain{wm}, u, rpg_c);
     });
+    if (t < K) CK(cudaEventRecord(tune_ev[3 * t + 2], stream));
     k_power_reduce<<<rgrid, kBlock, 0, stream>>>(u, v, n, work_part, counter + 2, pctrl);
     k_div_scalar<<<blocks_for(n), kBlock, 0, stream>>>(u, &pctrl->nu, v, n);  // v = u / norm
     CKL("power");
   }
+  if (tune_pending) ensure_tuned();  // fewer iterations than the tuning rounds
   CK(cudaMemcpyAsync(&pc, pctrl, sizeof(pc), cudaMemcpyDeviceToHost, stream));
   CK(cudaStreamSynchronize(stream));
   if (pc.zero) return 0.0;
@@ -1135,7 +1251,9 @@ void Context::setup(const cclp_cu_config& cfg) {
   phase_t0 = std::chrono::steady_clock::now();
   // the power iteration's start vector is host work: overlap it with the
   // device-side norms, Ruiz passes and value scaling
-  if (v0_thread.joinable()) v0_thread.join();
+  // (the default seed's vector may still be in the making since upload: it
+  // is joined only right before the power iteration)
+  if (v0_thread.joinable() && v0_seed != cfg.seed) v0_thread.join();
   if (!h_v0) h_v0 = host_alloc<double>(n);
   std::thread rng_thread;
   if (m > 0 && n > 0 && nnz > 0 && v0_seed != cfg.seed) {
@@ -1165,6 +1283,7 @@ void Context::setup(const cclp_cu_config& cfg) {
   CKL("panel values");
   mark(5);
   if (rng_thread.joinable()) rng_thread.join();
+  if (v0_thread.joinable()) v0_thread.join();
   norm_est = power_norm(cfg.norm_iterations, cfg.seed, true, true);
   mark(6);
   const double a_norm = norm_est > 0.0 ? norm_est : 1.0;
@@ -1645,6 +1764,18 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
     validate_inputs(ctx, cfg, *tol, thresholds, nthr);
     const auto wall0 = std::chrono::steady_clock::now();
     C.launches = 0;
+    // First-touch the caller's result arrays on a host thread while the
+    // device works, so the final device-to-host copies do not take page
+    // faults (fresh pageable arrays cost ~4 ms on C2 otherwise).
+    std::thread prefault([=, &C] {
+      if (x_out) std::memset(x_out, 0, sizeof(double) * C.n);
+      if (y_out) std::memset(y_out, 0, sizeof(double) * C.m);
+      if (z_out) std::memset(z_out, 0, sizeof(double) * C.n);
+    });
+    struct JoinOnExit {
+      std::thread& t;
+      ~JoinOnExit() { if (t.joinable()) t.join(); }
+    } prefault_join{prefault};
     C.begin(cfg, *tol, thresholds, nthr);
     const double setup_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
@@ -1744,6 +1875,7 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
       if (rep_valid) std::memcpy(st.result_report, st.R ? st.avg : st.cur, sizeof(st.result_report));
     }
     C.extract_view(view, st);
+    if (prefault.joinable()) prefault.join();
     C.d2h(x_out, C.vx, sizeof(double) * C.n);
     C.d2h(y_out, C.vy, sizeof(double) * C.m);
     C.d2h(z_out, C.vz, sizeof(double) * C.n);
