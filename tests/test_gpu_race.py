@@ -46,3 +46,17 @@ def test_cli_solve_on_gpu(tmp_path):
     rc2, c = cli.solve_file(str(tmp_path / "t.mps"), "concurrent", pdhg="cpu")
     assert rc == rc2 == 0
     assert g["objective"] == pytest.approx(c["objective"], rel=1e-9)
+
+
+def test_cli_solve_cscb_on_gpu(tmp_path):
+    """Binary CSC ingest through the CLI with the B200 PDHG: same objective as
+    the MPS file of the same LP with the reference CPU PDHG."""
+    from integration import cli
+    from paper_2510_24429_b200.lp import write_cscb
+    lp = lpgen.transportation_lp(20, 30, seed=4)
+    cli.write_mps(lp, str(tmp_path / "t.mps"), "T")
+    write_cscb(lp, str(tmp_path / "t.cscb"))
+    rc, g = cli.solve_file(str(tmp_path / "t.cscb"), "concurrent", pdhg="gpu")
+    rc2, c = cli.solve_file(str(tmp_path / "t.mps"), "concurrent", pdhg="cpu")
+    assert rc == rc2 == 0
+    assert g["objective"] == pytest.approx(c["objective"], rel=1e-9)
