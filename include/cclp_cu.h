@@ -163,6 +163,12 @@ int cclp_cu_run_pdhg(const cclp_cu_lp* lp, const cclp_cu_config* cfg, const cclp
 /* matvec / matvec_transpose (kernels.hpp:27-40). Host in, host out. */
 int cclp_cu_matvec(cclp_cu_ctx* ctx, const double* x, double* out);
 int cclp_cu_matvec_transpose(cclp_cu_ctx* ctx, const double* y, double* out);
+/* relative_report and absolute_violation (kkt.hpp:76,84; kkt.cpp:106-149) of
+ * the iterate (x[n], y[m], z[n]) on the context's unscaled LP, which must be
+ * in equality form (as run_pdhg requires). abs_violation may be NULL. Sums are
+ * reduced in a fixed order (within rounding of the reference's); maxima exact. */
+int cclp_cu_relative_report(cclp_cu_ctx* ctx, const double* x, const double* y, const double* z,
+                            cclp_cu_report* out, double* abs_violation);
 /* ruiz_scale factors (scaling.cpp:46-90): row_scale[m], col_scale[n]. */
 int cclp_cu_ruiz(cclp_cu_ctx* ctx, int32_t iterations, double* row_scale, double* col_scale);
 /* estimate_matrix_norm (pdhg.cpp:46-65) on the unscaled A. */

@@ -388,6 +388,8 @@ struct Context {
   void build_csr();
   void partition();
   void tune_spmv();
+  bool rows_equality = false;
+  void relative_report(const double* x, const double* y, const double* z, double* rep, double* abs_viol);
   // SpMV geometry tuning folded into the first power iterations (results are
   // geometry-independent, so the candidates can do real work): both start
   // tables stay alive until the choice is made.
@@ -526,6 +528,9 @@ void Context::upload(const cclp_cu_lp* lp) {
     }
   }
   h2d(b, lp->row_lower, sizeof(double) * m);
+  rows_equality = true;  // kkt entry points need the equality form (b = row bounds)
+  for (int i = 0; i < m && rows_equality; ++i)
+    rows_equality = lp->row_lower[i] == lp->row_upper[i] && std::isfinite(lp->row_lower[i]);
   if (m > 0 && n > 0 && nnz > 0) {  // the default seed's start vector, behind the ingest
     h_v0 = host_alloc<double>(n);
     v0_seed = 0;
@@ -905,6 +910,53 @@ void Context::explicit_tune() {
     }
   }
   choose_geometry(ms);
+}
+
+// relative_report + absolute_violation (kkt.cpp:106-149) of a host iterate
+// on the unscaled equality-form LP; `rep` in cclp_cu_report order.
+void Context::relative_report(const double* x, const double* y, const double* z, double* rep,
+                              double* abs_viol) {
+  if (!rows_equality) throw std::invalid_argument("relative_report: LP must be in equality form");
+  if (!vx) {  // the view buffers (extract_view allocates the same set)
+    vx = alloc<double>(n);
+    vz = alloc<double>(n);
+    vy = alloc<double>(m);
+    vrep = alloc<double>(kRepN);
+  }
+  h2d(vx, x, sizeof(double) * n);
+  h2d(vy, y, sizeof(double) * m);
+  h2d(vz, z, sizeof(double) * n);
+  launch_spmv(false, vx, wm, false, nullptr);  // ax = A x, reference order
+  launch_spmv(true, vy, wn, false, nullptr);   // aty = A' y
+  const int rb = static_cast<int>(std::max<long long>(1, std::min<long long>(148 * 4, (m + kBlock - 1) / kBlock)));
+  const int cb = static_cast<int>(std::max<long long>(1, std::min<long long>(148 * 4, (n + kBlock - 1) / kBlock)));
+  double* part = alloc<double>(static_cast<size_t>(rb) * kKktRowF + static_cast<size_t>(cb) * kKktColF + 16);
+  double* rpart = part;
+  double* cpart = part + static_cast<size_t>(rb) * kKktRowF;
+  double* fin = cpart + static_cast<size_t>(cb) * kKktColF;
+  k_kkt_rows<<<rb, kBlock, 0, stream>>>(m, wm, vy, b, rpart);
+  k_kkt_cols<<<cb, kBlock, 0, stream>>>(n, vx, vz, wn, c, l, u, cpart);
+  k_kkt_finish<<<1, 32, 0, stream>>>(rpart, m > 0 ? rb : 0, cpart, n > 0 ? cb : 0, fin);
+  CKL("kkt");
+  double f[kKktRowF + kKktColF];
+  CK(cudaMemcpyAsync(f, fin, sizeof(f), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  release(part);
+  const double* rw = f;
+  const double* cl = f + kKktRowF;
+  rep[kRpNorm2] = std::sqrt(rw[0]);
+  rep[kRdNorm2] = std::sqrt(cl[0]);
+  rep[kRpInf] = std::max(rw[1], cl[2]);
+  rep[kRdInf] = cl[1];
+  rep[kPobj] = cl[4];
+  rep[kDobj] = rw[2] + cl[5];
+  rep[kGap] = std::abs(rep[kPobj] - rep[kDobj]);
+  rep[kRelP] = rep[kRpNorm2] / (1.0 + std::sqrt(rw[3]));
+  rep[kRelD] = rep[kRdNorm2] / (1.0 + std::sqrt(cl[6]));
+  rep[kRelGap] = rep[kGap] / (1.0 + std::abs(rep[kPobj]) + std::abs(rep[kDobj]));
+  rep[kMaxResid] = std::max({rep[kRelP], rep[kRelD], rep[kRelGap]});
+  rep[kCompl] = cl[3];
+  if (abs_viol) *abs_viol = std::max({rw[1], cl[2], cl[1], cl[3]});  // absolute_violation (:141-149)
 }
 
 void Context::launch_spmv(bool transpose, const double* vec, double* out, bool scaled,
@@ -1720,6 +1772,17 @@ int cclp_cu_matvec(cclp_cu_ctx* ctx, const double* x, double* out) {
     C.launch_spmv(false, C.wn, C.wm, false, nullptr);
     CK(cudaMemcpyAsync(out, C.wm, sizeof(double) * C.m, cudaMemcpyDeviceToHost, C.stream));
     CK(cudaStreamSynchronize(C.stream));
+  });
+}
+
+int cclp_cu_relative_report(cclp_cu_ctx* ctx, const double* x, const double* y, const double* z,
+                            cclp_cu_report* out, double* abs_violation) {
+  return guarded([&] {
+    Context& C = ctx->c;
+    CK(cudaSetDevice(C.device));
+    double rep[cclp_cu::kRepN];
+    C.relative_report(x, y, z, rep, abs_violation);
+    copy_report(rep, out);
   });
 }
 

@@ -386,3 +386,90 @@ __global__ void k_init_x(const double* __restrict__ l, const double* __restrict_
 __global__ void k_stamp(unsigned long long* t) { *t = globaltimer(); }
 
 }  // namespace cclp_cu
+
+// ---------------------------------------------------------------------------
+// Verification side (kkt.cpp:37-149): relative_report / absolute_violation
+// of a given iterate (x, y, z) on the unscaled equality-form LP, from
+// ax = A x and aty = A' y of the reference-order (G = 1) SpMV. Per-row and
+// per-column terms go to block partials (field-major); one block then sums
+// each field over the blocks in block order (deterministic).
+// ---------------------------------------------------------------------------
+namespace cclp_cu {
+
+constexpr int kKktRowF = 4;   // 0 sum r^2, 1 max |r|, 2 b.y, 3 sum b^2   (r = b - ax, kkt.cpp:37-52)
+constexpr int kKktColF = 7;   // 0 sum rd^2, 1 max |rd|, 2 max bound violation, 3 complementarity,
+                              // 4 c.x, 5 dual bound terms, 6 sum c^2
+constexpr unsigned kKktRowMax = (1u << 1);
+constexpr unsigned kKktColMax = (1u << 1) | (1u << 2) | (1u << 3);
+
+__global__ void __launch_bounds__(kBlock) k_kkt_rows(int m, const double* __restrict__ ax,
+                                                     const double* __restrict__ y,
+                                                     const double* __restrict__ b, double* part) {
+  __shared__ double red[(kBlock / 32) * kKktRowF];
+  __shared__ double out[kKktRowF];
+  double acc[kKktRowF] = {0.0, 0.0, 0.0, 0.0};
+  for (int i = blockIdx.x * kBlock + threadIdx.x; i < m; i += gridDim.x * kBlock) {
+    const double r = b[i] - ax[i];  // equality row: rl - ax (kkt.cpp:42-43)
+    acc[0] += r * r;
+    acc[1] = amax(acc[1], fabs(r));
+    acc[2] += b[i] * y[i];
+    acc[3] += b[i] * b[i];
+  }
+  block_reduce<kKktRowF, kKktRowMax>(acc, red, out);
+  if (threadIdx.x < kKktRowF) part[threadIdx.x * gridDim.x + blockIdx.x] = out[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kBlock) k_kkt_cols(int n, const double* __restrict__ x,
+                                                     const double* __restrict__ z,
+                                                     const double* __restrict__ aty,
+                                                     const double* __restrict__ c,
+                                                     const double* __restrict__ l,
+                                                     const double* __restrict__ u, double* part) {
+  __shared__ double red[(kBlock / 32) * kKktColF];
+  __shared__ double out[kKktColF];
+  double acc[kKktColF] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+  for (int j = blockIdx.x * kBlock + threadIdx.x; j < n; j += gridDim.x * kBlock) {
+    const double xj = x[j], zj = z[j], cj = c[j], lj = l[j], uj = u[j];
+    const double rd = (aty[j] + zj) - cj;  // dual_residual (kkt.cpp:66-69)
+    acc[0] += rd * rd;
+    acc[1] = amax(acc[1], fabs(rd));
+    double bv = lj - xj;  // bound_violations: max({l - x, x - u, 0}) (:55-63)
+    if (bv < xj - uj) bv = xj - uj;
+    if (bv < 0.0) bv = 0.0;
+    acc[2] = amax(acc[2], bv);
+    const bool lf = isfin(lj), uf = isfin(uj);  // complementarity_inf (:90-104)
+    double dist = CCLP_INF;
+    if (lf) dist = fmin(dist, fabs(xj - lj));
+    if (uf) dist = fmin(dist, fabs(xj - uj));
+    if (isfin(dist)) acc[3] = amax(acc[3], dist * fabs(zj));  // free column: skipped
+    acc[4] += cj * xj;  // objective_gap (:71-86)
+    if (zj > 0.0 && lf) {
+      acc[5] += lj * zj;
+    } else if (zj < 0.0 && uf) {
+      acc[5] += uj * zj;
+    }
+    acc[6] += cj * cj;
+  }
+  block_reduce<kKktColF, kKktColMax>(acc, red, out);
+  if (threadIdx.x < kKktColF) part[threadIdx.x * gridDim.x + blockIdx.x] = out[threadIdx.x];
+}
+
+// One block: field f (thread f) sums / maxes its blocks in block order.
+__global__ void k_kkt_finish(const double* __restrict__ rpart, int rblocks, const double* __restrict__ cpart,
+                             int cblocks, double* out) {
+  const int f = threadIdx.x;
+  if (f < kKktRowF) {
+    const bool mx = (kKktRowMax >> f) & 1u;
+    double a = 0.0;
+    for (int k = 0; k < rblocks; ++k) a = mx ? amax(a, rpart[f * rblocks + k]) : a + rpart[f * rblocks + k];
+    out[f] = a;
+  } else if (f < kKktRowF + kKktColF) {
+    const int g = f - kKktRowF;
+    const bool mx = (kKktColMax >> g) & 1u;
+    double a = 0.0;
+    for (int k = 0; k < cblocks; ++k) a = mx ? amax(a, cpart[g * cblocks + k]) : a + cpart[g * cblocks + k];
+    out[f] = a;
+  }
+}
+
+}  // namespace cclp_cu

@@ -109,6 +109,8 @@ def load_library(path: str = LIB_PATH):
         L.cclp_cu_default_tolerances.argtypes = [C.POINTER(_Tol)]
         L.cclp_cu_create.argtypes = [C.POINTER(_LP), C.c_int, C.POINTER(C.c_void_p)]
         L.cclp_cu_destroy.argtypes = [C.c_void_p]
+        L.cclp_cu_relative_report.argtypes = [C.c_void_p, _dp, _dp, _dp, C.POINTER(_Report),
+                                               C.POINTER(C.c_double)]
         L.cclp_cu_create_from_file.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p),
                                                C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         L.cclp_cu_solve.argtypes = [C.c_void_p, C.POINTER(_Config), C.POINTER(_Tol), _dp, C.c_int32,
@@ -152,6 +154,7 @@ EXPORTED_SYMBOLS = [
     "cclp_cu_nccl_unique_id", "cclp_cu_sharded_create", "cclp_cu_sharded_solve",
     "cclp_cu_sharded_begin", "cclp_cu_sharded_advance", "cclp_cu_sharded_describe",
     "cclp_cu_sharded_destroy", "cclp_cu_sharded_create_hostcomm", "cclp_cu_create_from_file",
+    "cclp_cu_relative_report",
 ]
 
 
@@ -331,6 +334,16 @@ class Engine:
         _check(self.L, self.L.cclp_cu_create_from_file(path.encode(), device, C.byref(self.ctx),
                                                        C.byref(m), C.byref(n)))
         return self
+
+    def relative_report(self, x, y, z):
+        """relative_report and absolute_violation (kkt.cpp:106-149) of the
+        iterate on this (equality-form, unscaled) LP, computed on the device.
+        Returns (ResidualReport, absolute_violation)."""
+        xs = [np.ascontiguousarray(a, np.float64) for a in (x, y, z)]
+        rep, av = _Report(), C.c_double()
+        _check(self.L, self.L.cclp_cu_relative_report(self.ctx, *(a.ctypes.data_as(_dp) for a in xs),
+                                                      C.byref(rep), C.byref(av)))
+        return ResidualReport(**{f: getattr(rep, f) for f in REPORT_FIELDS}), av.value
 
     def close(self) -> None:
         if self.ctx:

@@ -62,6 +62,11 @@ def test_full_size_report_matches_independent_kkt(name, lps, oracle):
     for k in REPORT_KEYS:
         got = getattr(a.report, k)
         assert got == pytest.approx(kkt[k], rel=1e-9, abs=1e-12 * (1 + abs(kkt[k]))), k
+    # the device verification entry point (cclp_cu_relative_report) on the same iterate
+    with Engine(lp) as eng:
+        dev, _ = eng.relative_report(a.iterate.x, a.iterate.y, a.iterate.z)
+    for k in REPORT_KEYS:
+        assert getattr(dev, k) == pytest.approx(kkt[k], rel=1e-11, abs=1e-12 * (1 + abs(kkt[k]))), k
 
 
 def test_c4_full_size_sharded_bit_identical(lps):
