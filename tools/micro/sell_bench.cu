@@ -51,6 +51,31 @@ __global__ void __launch_bounds__(1024) v_csr2(const int* __restrict__ st, const
   }
 }
 
+// rpg = 1 CSR-G kernel with U loads in flight per lane (engine's group_dot<G, U>)
+template <int G, int U>
+__global__ void __launch_bounds__(1024) v_csr1(const int* __restrict__ st, const int* __restrict__ ptr,
+    const int* __restrict__ idx, const double* __restrict__ val, const double* __restrict__ x, double* __restrict__ y) {
+  const int gl = threadIdx.x % G, gpb = blockDim.x / G;
+  const int rb = st[blockIdx.x], re = st[blockIdx.x + 1];
+  for (int row = rb + (int)(threadIdx.x / G); row - (int)(threadIdx.x / G) < re; row += gpb) {
+    const bool ok = row < re;
+    const int b = ok ? __ldg(ptr + row) : 0, e = ok ? __ldg(ptr + row + 1) : 0;
+    double acc = 0.0;
+    for (int p = b + gl; p < e; p += G * U) {
+      int ii[U]; double vv[U], xx[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) { const int q = p + k * G; ii[k] = q < e ? __ldcs(idx + q) : -1; vv[k] = q < e ? __ldcs(val + q) : 0.0; }
+#pragma unroll
+      for (int k = 0; k < U; ++k) xx[k] = ii[k] >= 0 ? __ldg(x + ii[k]) : 0.0;
+#pragma unroll
+      for (int k = 0; k < U; ++k) if (ii[k] >= 0) acc = acc + vv[k] * xx[k];
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) acc += __shfl_xor_sync(~0u, acc, off);
+    if (gl == 0 && ok) y[row] = acc;
+  }
+}
+
 // SELL: warp per slice (grid-stride over slices); lane = row; U elements per round.
 template <int U, bool PIPE>
 __global__ void __launch_bounds__(1024) v_sell(int nsl, const long long* __restrict__ soff, const int* __restrict__ swid,
@@ -198,6 +223,9 @@ int main(int argc, char** argv) {
     }
     int* dst; CK(cudaMalloc(&dst, 4 * (grid + 1))); CK(cudaMemcpy(dst, st.data(), 4 * (grid + 1), cudaMemcpyHostToDevice));
     char nm[64];
+#define C1(GG, UU) if (G == GG) { snprintf(nm, sizeof nm, "csr1 G%d U%d x%d", GG, UU, per); \
+      run(nm, false, [&] { v_csr1<GG, UU><<<grid, 1024>>>(dst, dp, di, dv, dx, dy); }); }
+    C1(4, 2) C1(4, 3) C1(4, 4) C1(4, 6) C1(4, 8) C1(8, 2) C1(8, 4) C1(8, 6) C1(8, 7) C1(8, 8) C1(16, 2) C1(16, 3) C1(16, 4)
     for (bool f : {false, true}) {
       snprintf(nm, sizeof nm, "csr G%d U2 rpg2 x%d", G, per);
       if (G == 4) run(nm, f, [&] { v_csr2<4, 2><<<grid, 1024>>>(dst, dp, di, dv, dx, dy); });
