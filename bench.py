@@ -135,16 +135,22 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# Test mode for the N > 1 code paths on a single-GPU box: every rank on
+# device 0, the process group over gloo, and the sharded arm's control
+# exchange through it (host all-gather) instead of NCCL.
+ONE_DEVICE = os.environ.get("CCLP_BENCH_ONE_DEVICE") == "1"
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if ONE_DEVICE else int(os.environ.get("LOCAL_RANK", "0"))
     pg = None
     if world > 1 and args.impl != "reference":
         import torch.distributed as dist
         import torch
         torch.cuda.set_device(local)
-        dist.init_process_group(backend="nccl")
+        dist.init_process_group(backend="gloo" if ONE_DEVICE else "nccl")
         pg = dist
     return world, rank, local, pg
 
@@ -158,7 +164,7 @@ def allreduce_max(pg, v: float, device) -> float:
     if pg is None:
         return v
     import torch
-    t = torch.tensor([v], dtype=torch.float64, device=device)
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if ONE_DEVICE else device)
     pg.all_reduce(t, op=pg.ReduceOp.MAX)
     return float(t.item())
 
@@ -167,7 +173,7 @@ def allreduce_sum(pg, v: float, device) -> float:
     if pg is None:
         return v
     import torch
-    t = torch.tensor([v], dtype=torch.float64, device=device)
+    t = torch.tensor([v], dtype=torch.float64, device="cpu" if ONE_DEVICE else device)
     pg.all_reduce(t, op=pg.ReduceOp.SUM)
     return float(t.item())
 
@@ -251,6 +257,17 @@ def metric_for(workload: str) -> str:
     return f"PDHG iterations/s ({workload} synthetic LP, fp64, check every iteration)"
 
 
+def _fresh_nccl_id(pg, rank, dev):
+    """A new NCCL unique id from rank 0, broadcast over the process group."""
+    import torch
+    from paper_2510_24429_b200.pdhg import nccl_unique_id
+    idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        idt.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+    pg.broadcast(idt, src=0)
+    return bytes(idt.cpu().numpy().tobytes())
+
+
 def run_sharded_arm(args, world, rank, local, pg):
     """N ranks, one row-block shard each (cclp_cu_sharded over NCCL)."""
     import torch
@@ -258,13 +275,23 @@ def run_sharded_arm(args, world, rank, local, pg):
     from paper_2510_24429_b200.pdhg import PdhgConfig, ShardedEngine, nccl_unique_id
 
     dev = torch.device("cuda", local)
-    idt = torch.zeros(128, dtype=torch.uint8, device=dev)
-    if rank == 0:
-        idt.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
-    pg.broadcast(idt, src=0)
-    nccl_id = bytes(idt.cpu().numpy().tobytes())
     lp = lpgen.make_config(args.workload)
-    eng = ShardedEngine(lp, 1, device=local, rank=rank, nranks=world, nccl_id=nccl_id)
+    if ONE_DEVICE:
+        def host_allgather(blob: bytes):
+            parts = [None] * world
+            pg.all_gather_object(parts, blob)
+            return parts
+        make = lambda src: ShardedEngine(src, 1, device=local, rank=rank, nranks=world,  # noqa: E731
+                                         host_allgather=host_allgather)
+    else:
+        idt = torch.zeros(128, dtype=torch.uint8, device=dev)
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(nccl_unique_id()), dtype=torch.uint8))
+        pg.broadcast(idt, src=0)
+        nccl_id = bytes(idt.cpu().numpy().tobytes())
+        make = lambda src: ShardedEngine(src, 1, device=local, rank=rank, nranks=world,  # noqa: E731
+                                         nccl_id=nccl_id if src is lp else _fresh_nccl_id(pg, rank, dev))
+    eng = make(lp)
     eng.begin(PdhgConfig())
     K, W, I = args.steps, args.warmup, args.iters_per_step
     for _ in range(W):
@@ -278,6 +305,17 @@ def run_sharded_arm(args, world, rank, local, pg):
     d = eng.describe()
     eng.close()
     value = K * I / (t_max * 1e-3)
+    # e2e: every rank builds its shard engine from the LP in pinned host
+    # memory and solves `--e2e-iters` iterations, result gathered to every
+    # rank (upload, slicing, setup, loop, download); max over ranks
+    plp, _keep = pinned_copy(lp)
+    cfg = PdhgConfig(max_iterations=args.e2e_iters)
+    barrier(pg)
+    t = time.perf_counter()
+    with make(plp) as e2:
+        res = e2.solve(cfg)
+    e2e_t = allreduce_max(pg, time.perf_counter() - t, dev)
+    e2e_value = res.iterations / e2e_t
     B = 24 * lp.nnz + 20 * (lp.m + lp.n) + 8
     peak, peak_kind = measured_peak_gbs()
     if rank == 0:
@@ -296,9 +334,17 @@ def run_sharded_arm(args, world, rank, local, pg):
                          "unit": "GB/s", "frac": B * value / 1e9 / world / peak,
                          "traffic": None, "kernel": "whole iteration, per GPU",
                          "bytes_per_launch": B, "peak_kind": peak_kind},
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": sum(a.nbytes for a in (plp.colptr, plp.rowind, plp.val, plp.c,
+                                                                 plp.row_lower, plp.row_upper,
+                                                                 plp.col_lower, plp.col_upper)),
+                    "d2h_bytes_per_step": 8 * (2 * lp.n + lp.m), "iters_per_step": args.e2e_iters,
+                    "includes": "per rank: shard engine from pinned host LP, setup, loop, full result"},
             "gpu_launches": int(d["launches"]),
             "clocks": clk.summary(),
         }
+        if ONE_DEVICE:
+            line["config"]["parallelism"] = f"row-block sharded x{world} on ONE device (test mode)"
         print(json.dumps(line), flush=True)
 
 
