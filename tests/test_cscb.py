@@ -75,3 +75,20 @@ def test_solve_from_file_matches_arrays(tmp_path, name, lp):
     assert ra.iterations == rb.iterations and ra.stop == rb.stop
     assert np.array_equal(ra.iterate.x, rb.iterate.x)
     assert np.array_equal(ra.iterate.y, rb.iterate.y)
+
+
+def test_round_trip_empty_matrix(tmp_path):
+    """A matrix with no nonzeros (and an LP with no rows) survives the format."""
+    from paper_2510_24429_b200.lp import INF, LinearProgram
+    lp = LinearProgram(3, 4, np.zeros(5, np.int32), np.zeros(0, np.int32), np.zeros(0),
+                       np.arange(4.0), np.ones(3), np.ones(3), np.zeros(4), np.full(4, INF))
+    p = str(tmp_path / "empty.cscb")
+    write_cscb(lp, p)
+    back = read_cscb(p)
+    assert (back.m, back.n, back.nnz) == (3, 4, 0)
+    assert np.array_equal(back.c, lp.c) and np.all(np.isinf(back.col_upper))
+    norows = LinearProgram(0, 2, np.zeros(3, np.int32), np.zeros(0, np.int32), np.zeros(0),
+                           np.ones(2), np.zeros(0), np.zeros(0), np.zeros(2), np.ones(2))
+    write_cscb(norows, p)
+    back = read_cscb(p)
+    assert (back.m, back.n, back.nnz) == (0, 2, 0) and np.array_equal(back.col_upper, np.ones(2))
