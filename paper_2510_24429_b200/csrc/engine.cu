@@ -389,6 +389,17 @@ struct Context {
   void partition();
   void tune_spmv();
   bool rows_equality = false;
+  // SELL-32 copy of A' for the column product (k_spmv_cols_sell): structure
+  // per long-row threshold, block ranges per column grid, values per solve.
+  bool sell_on = false;
+  static constexpr double kSellMaxPad = 1.25;
+  int sell_thr = -1, sell_grid = 0, sell_nsl = 0, sell_bs = kSpmvBlock;
+  long long* sell_off = nullptr;
+  int* sell_start = nullptr;
+  int* sell_idx = nullptr;
+  double* sell_val = nullptr;
+  std::vector<long long> sell_cum;  // host: slots before each slice
+  void build_sell_cols();
   void relative_report(const double* x, const double* y, const double* z, double* rep, double* abs_viol);
   // SpMV geometry tuning folded into the first power iterations (results are
   // geometry-independent, so the candidates can do real work): both start
@@ -458,7 +469,7 @@ Context::~Context() {
                     counter, ctrl, log, thr, t0, scalars, pctrl, iflags, amb_idx, wn, wn2, wm, vx, vy,
                     vz, vrep, plan_rows.seg, plan_rows.lr_first, plan_rows.part, plan_rows.cnt,
                     plan_cols.seg, plan_cols.lr_first, plan_cols.part, plan_cols.cnt, x_full, y_full,
-                    xpart, vparts, push_flags, push_counter};
+                    xpart, vparts, push_flags, push_counter, sell_off, sell_start, sell_idx, sell_val};
     for (void* p : ptrs) release(p);
     for (int k = 0; k < 3; ++k)
       for (int q = 0; q < 2; ++q) release(xc[k][q]);
@@ -912,6 +923,123 @@ void Context::explicit_tune() {
   choose_geometry(ms);
 }
 
+// SELL-32 layout of A' (SellPlan): per-slice widths ignore the columns the
+// long-row segments sum; each block of the column grid gets a contiguous
+// slice range of about equal slots + per-column overhead. CCLP_CU_SELL=0
+// keeps the G-lane CSR column kernel (A/B).
+void Context::build_sell_cols() {
+  const char* e = std::getenv("CCLP_CU_SELL");
+  sell_on = false;
+  if ((e != nullptr && std::atoi(e) == 0) || n == 0 || nnz == 0 || !sval_csc) return;
+  // Measured (profiles/r1/history/r1_spmv_experiments.txt): SELL wins where
+  // the gathered y is large (C3 m = 0.4M: -12 us, C4 m = 5M: -40 us per
+  // column product) and loses slightly when y is cache-resident (C2 m = 0.1M:
+  // +0.5 us); the threshold depends on the matrix only (CCLP_CU_SELL=1 forces).
+  const bool force = e != nullptr && std::atoi(e) == 1;
+  if (!force && static_cast<long long>(m) * 8 < (2LL << 20)) return;
+  const SpmvPlan P = plan(false);
+  const int thr = P.thr;
+  const int nsl = (n + 31) / 32;
+  if (sell_thr == thr && sell_nsl < 0) return;  // padding too high (decided once)
+  if (!sell_off || sell_thr != thr) {
+    int* w = alloc<int>(nsl);
+    k_sell_width<<<blocks_for(nsl), kBlock, 0, stream>>>(colptr, n, thr, nsl, w);
+    CKL("sell width");
+    std::vector<int> hw(nsl);
+    CK(cudaMemcpyAsync(hw.data(), w, sizeof(int) * nsl, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    release(w);
+    sell_cum.assign(static_cast<size_t>(nsl) + 1, 0);
+    for (int q = 0; q < nsl; ++q) sell_cum[q + 1] = sell_cum[q] + 32LL * hw[q];
+    // Slices pad every column to the slice's longest: worth it only when the
+    // column lengths are near-uniform (C2, C3, C4: <= 1.25x the nonzeros;
+    // Poisson-like lengths as in C5 pad ~2x and lose). A property of the
+    // matrix alone, so the choice (and the summation order) is deterministic.
+    if (static_cast<double>(sell_cum[nsl]) > kSellMaxPad * static_cast<double>(nnz)) {
+      sell_thr = thr;
+      sell_nsl = -1;  // remembered: no SELL for this threshold
+      return;
+    }
+    release(sell_off);
+    release(sell_idx);
+    release(sell_val);
+    sell_off = alloc<long long>(static_cast<size_t>(nsl) + 1);
+    CK(cudaMemcpyAsync(sell_off, sell_cum.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, stream));
+    sell_idx = alloc<int>(static_cast<size_t>(std::max<long long>(sell_cum[nsl], 1)));
+    sell_val = alloc<double>(static_cast<size_t>(std::max<long long>(sell_cum[nsl], 1)));
+    sell_thr = thr;
+    sell_nsl = nsl;
+    sell_grid = 0;
+  }
+  k_sell_fill<<<blocks_for(static_cast<long long>(nsl) * 32), kBlock, 0, stream>>>(
+      colptr, rowind, sval_csc, n, thr, nsl, sell_off, sell_idx, sell_val);
+  CKL("sell fill");
+  // block slice ranges for `grid` blocks: equal slots + per-column overhead
+  auto starts = [&](int grid) {
+    auto weight = [&](long long q) { return sell_cum[q] + 16LL * 32 * q; };
+    const long long total = weight(nsl);
+    std::vector<int> st(static_cast<size_t>(grid) + 1);
+    for (int b = 0; b <= grid; ++b) {
+      const long long target = total * b / grid;
+      int lo = 0, hi = nsl;
+      while (lo < hi) {
+        const int mid = (lo + hi) / 2;
+        if (weight(mid) >= target) hi = mid; else lo = mid + 1;
+      }
+      st[b] = b == grid ? nsl : lo;
+    }
+    int* d = alloc<int>(static_cast<size_t>(grid) + 1);
+    CK(cudaMemcpyAsync(d, st.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice, stream));
+    CK(cudaStreamSynchronize(stream));  // st is a host temporary
+    return d;
+  };
+  if (sell_grid == 0 || (thr != 0x7fffffff && sell_grid != spmv_grid_c)) {
+    release(sell_start);
+    sell_bs = kSpmvBlock;
+    sell_grid = spmv_grid_c;
+    sell_start = starts(sell_grid);
+    // Without long columns the block shape is free (every shape sums each
+    // column in the same order): time 1024-thread blocks on the column grid
+    // against 256-thread blocks on four times as many, keep the faster.
+    if (thr == 0x7fffffff) {
+      int* alt = starts(4 * spmv_grid_c);
+      SellPlan S{sell_off, sell_start, colptr, sell_idx, sell_val, n, thr};
+      const double* gy = y_full ? y_full : wm;  // shards gather from the padded full y
+      auto time_it = [&](int bs) {
+        std::vector<float> t;
+        for (int rep = 0; rep < 4; ++rep) {
+          CK(cudaEventRecord(ev_a, stream));
+          if (bs == kSpmvBlock) {
+            S.start = sell_start;
+            k_sell_range<kSpmvBlock><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(S, GatherPlain{gy}, wn);
+          } else {
+            S.start = alt;
+            k_sell_range<256><<<4 * spmv_grid_c, 256, 0, stream>>>(S, GatherPlain{gy}, wn);
+          }
+          CK(cudaEventRecord(ev_b, stream));
+          CK(cudaEventSynchronize(ev_b));
+          float ms = 0;
+          CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+          if (rep > 0) t.push_back(ms);
+        }
+        std::sort(t.begin(), t.end());
+        return t[t.size() / 2];
+      };
+      CKL("sell tune");
+      const float t_big = time_it(kSpmvBlock), t_small = time_it(256);
+      if (t_small < 0.97f * t_big) {
+        release(sell_start);
+        sell_start = alt;
+        sell_bs = 256;
+        sell_grid = 4 * spmv_grid_c;
+      } else {
+        release(alt);
+      }
+    }
+  }
+  sell_on = true;
+}
+
 // relative_report + absolute_violation (kkt.cpp:106-149) of a host iterate
 // on the unscaled equality-form LP; `rep` in cclp_cu_report order.
 void Context::relative_report(const double* x, const double* y, const double* z, double* rep,
@@ -1170,7 +1298,7 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
   // candidates (one warm-up round, then `reps` timed rounds) with events
   // around each product; one host sync after them picks the geometry.
   const bool rows_panels = scaled && use_panels();
-  const int reps = (nnz > 30'000'000) ? 3 : 5;
+  const int reps = (nnz > 30'000'000) ? 4 : 7;
   int K = 0;
   if (tune_pending && !rows_panels && iterations >= 4 * (reps + 1) && 4 * (reps + 1) * 3 <= 96) {
     K = 4 * (reps + 1);
@@ -1256,9 +1384,18 @@ void Context::launch_rows_half(bool init) {
 void Context::launch_cols_half(bool init) {
   const IterParams& p = params;
   const int ii = init ? 1 : 0;
-  with_group_long(gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
-    launch_pdl(k_spmv_cols<decltype(g)::value, decltype(l)::value>, spmv_grid_c, kSpmvBlock, stream, p, ii);
-  });
+  if (p.use_sell_c) {
+    if (p.plan_c.thr != 0x7fffffff)
+      launch_pdl(k_spmv_cols_sell<true, kSpmvBlock>, spmv_grid_c, kSpmvBlock, stream, p, ii);
+    else if (sell_bs == 256)
+      launch_pdl(k_spmv_cols_sell<false, 256>, sell_grid, 256, stream, p, ii);
+    else
+      launch_pdl(k_spmv_cols_sell<false, kSpmvBlock>, sell_grid, kSpmvBlock, stream, p, ii);
+  } else {
+    with_group_long(gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
+      launch_pdl(k_spmv_cols<decltype(g)::value, decltype(l)::value>, spmv_grid_c, kSpmvBlock, stream, p, ii);
+    });
+  }
   launch_pdl(k_primal, epi_grid, kEpiBlock, stream, p, ii);
 }
 
@@ -1398,6 +1535,9 @@ void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& to
   p.row_grid = epi_grid; p.col_grid = epi_grid;  // partial counts for finalize
   p.plan_r = plan(true); p.plan_c = plan(false);
   p.rpg_rows = rpg_r; p.rpg_cols = rpg_c;
+  build_sell_cols();
+  p.use_sell_c = sell_on ? 1 : 0;
+  p.sell_c = SellPlan{sell_off, sell_start, colptr, sell_idx, sell_val, n, sell_thr};
   p.c = c; p.l = l; p.u = u; p.b = b; p.r = r; p.s = s;
   for (int k = 0; k < 3; ++k)
     for (int q = 0; q < 2; ++q) p.xc[k][q] = xc[k][q];
@@ -1719,10 +1859,21 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
       CK(cudaEventRecord(e[1], C.stream));
       cclp_cu::k_dual<<<C.epi_grid, cclp_cu::kEpiBlock, 0, C.stream>>>(p, 0);
       CK(cudaEventRecord(e[2], C.stream));
-      cclp_cu::with_group_long(C.gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
-        cclp_cu::k_spmv_cols<decltype(g)::value, decltype(l)::value>
-            <<<C.spmv_grid_c, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
-      });
+      if (p.use_sell_c) {
+        if (p.plan_c.thr != 0x7fffffff)
+          cclp_cu::k_spmv_cols_sell<true, cclp_cu::kSpmvBlock>
+              <<<C.spmv_grid_c, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
+        else if (C.sell_bs == 256)
+          cclp_cu::k_spmv_cols_sell<false, 256><<<C.sell_grid, 256, 0, C.stream>>>(p, 0);
+        else
+          cclp_cu::k_spmv_cols_sell<false, cclp_cu::kSpmvBlock>
+              <<<C.sell_grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
+      } else {
+        cclp_cu::with_group_long(C.gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
+          cclp_cu::k_spmv_cols<decltype(g)::value, decltype(l)::value>
+              <<<C.spmv_grid_c, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
+        });
+      }
       CK(cudaEventRecord(e[3], C.stream));
       cclp_cu::k_primal<<<C.epi_grid, cclp_cu::kEpiBlock, 0, C.stream>>>(p, 0);
       CK(cudaEventRecord(e[4], C.stream));

@@ -369,6 +369,11 @@ __global__ void k_select_x(const IterParams p, double* __restrict__ x_full_loc, 
 // depends only on G, never on the launch geometry, so the geometry can be
 // autotuned without changing a bit of the result; G = 1 sums each row in the
 // reference's own order.
+template <class Gather>
+__device__ __forceinline__ void spmv_long_segments(const SpmvPlan& P, const int* __restrict__ idx,
+                                                   const double* __restrict__ val, const Gather& g,
+                                                   double* __restrict__ out, int accumulate);
+
 template <int G, bool LONG, class Gather>
 __device__ __forceinline__ void spmv_block_range(const SpmvPlan& P, const int* __restrict__ ptr,
                                                  const int* __restrict__ idx,
@@ -403,8 +408,15 @@ __device__ __forceinline__ void spmv_block_range(const SpmvPlan& P, const int* _
       if (gl == 0 && ok) out[row] = (accumulate ? out[row] : 0.0) + s;
     }
   }
-  if (!LONG) return;
-  // long-row segments: one warp per segment, 32 lanes strided, then combine
+  if (LONG) spmv_long_segments(P, idx, val, g, out, accumulate);
+}
+
+// Long-row segments of block blockIdx.x: one warp per segment, 32 lanes
+// strided, then the last segment of a row to finish combines them in order.
+template <class Gather>
+__device__ __forceinline__ void spmv_long_segments(const SpmvPlan& P, const int* __restrict__ idx,
+                                                   const double* __restrict__ val, const Gather& g,
+                                                   double* __restrict__ out, int accumulate) {
   const int lane = threadIdx.x & 31;
   const int sb = P.start[P.grid + 1 + blockIdx.x], se = P.start[P.grid + 2 + blockIdx.x];
   for (int k = sb + static_cast<int>(threadIdx.x >> 5); k < se; k += static_cast<int>(blockDim.x >> 5)) {
@@ -459,6 +471,75 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows(const IterParams p, in
   spmv_block_range<G, LONG>(p.plan_r, p.rowptr, p.colind, p.aval,
                             GatherPlain{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]},
                       p.ax[si.s1], p.rpg_rows);
+}
+
+// SELL-32 column product of block blockIdx.x's slices: lane = column, its
+// elements in ascending position with one accumulator (the reference's
+// sequential order, as the G = 1 path), 4 gathers in flight and the next 4
+// idx/val already loading. Columns longer than S.thr are written by the
+// long-row segments instead.
+template <class Gather>
+__device__ __forceinline__ void sell_block(const SellPlan& S, const Gather& g, double* __restrict__ out) {
+  constexpr int U = 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int sb = S.start[blockIdx.x], se = S.start[blockIdx.x + 1];
+  for (int s = sb + warp; s < se; s += nw) {
+    const long long off = S.off[s];
+    const int w = static_cast<int>((S.off[s + 1] - off) >> 5);
+    const int j = s * 32 + lane;
+    int len = j < S.n ? __ldg(S.ptr + j + 1) - __ldg(S.ptr + j) : 0;
+    const bool seg = len > S.thr;
+    if (seg) len = 0;
+    const int* __restrict__ ib = S.idx + off + lane;
+    const double* __restrict__ vb = S.val + off + lane;
+    int ii[U];
+    double vv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const bool ok = u < len;
+      ii[u] = ok ? __ldcs(ib + 32 * u) : 0;
+      vv[u] = ok ? __ldcs(vb + 32 * u) : 0.0;
+    }
+    double acc = 0.0;
+    for (int k = 0; k < w; k += U) {
+      double xx[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) xx[u] = k + u < len ? g(ii[u]) : 0.0;
+      int in[U];
+      double vn[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = k + U + u < len;
+        in[u] = ok ? __ldcs(ib + 32 * (k + U + u)) : 0;
+        vn[u] = ok ? __ldcs(vb + 32 * (k + U + u)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k + u < len) acc = acc + vv[u] * xx[u];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ii[u] = in[u];
+        vv[u] = vn[u];
+      }
+    }
+    if (j < S.n && !seg) out[j] = acc;
+  }
+}
+
+// Stand-alone SELL product (geometry tuning in Context::build_sell_cols).
+template <int BS>
+__global__ void __launch_bounds__(BS) k_sell_range(const SellPlan S, GatherPlain g, double* __restrict__ out) {
+  sell_block(S, g, out);
+}
+
+template <bool LONG, int BS>
+__global__ void __launch_bounds__(BS) k_spmv_cols_sell(const IterParams p, int init) {
+  StepInfo si;
+  if (!read_step(p, init != 0, si)) return;
+  if (p.push.on) push_wait(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1));
+  const GatherPlain g{p.yg != nullptr ? p.yg : p.y[si.s1]};
+  sell_block(p.sell_c, g, p.aty[si.s1]);
+  if (LONG) spmv_long_segments(p.plan_c, p.rowind, p.atval, g, p.aty[si.s1], 0);
 }
 
 template <int G, bool LONG>

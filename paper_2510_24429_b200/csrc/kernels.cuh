@@ -60,6 +60,20 @@ struct SpmvPlan {
   int grid;
 };
 
+// SELL-32 layout of one SpMV side (engine.cu, Context::build_sell_cols):
+// 32 consecutive rows per slice, slice s holding 32 * width_s slots, slot k
+// of lane l at off[s] + 32k + l (row s*32 + l's k-th element). Rows longer
+// than `thr` are left to the long-row segments of the side's SpmvPlan.
+struct SellPlan {
+  const long long* off;  // [nsl + 1]
+  const int* start;      // [grid + 1] slice range of each block
+  const int* ptr;        // the side's row pointer (lengths)
+  const int* idx;
+  const double* val;
+  int n;                 // rows of the side
+  int thr;
+};
+
 // One column panel of the row SpMV (engine.cu, Context::build_panels).
 struct PanelArgs {
   SpmvPlan plan;
@@ -109,6 +123,8 @@ struct IterParams {
   int row_grid, col_grid;
   // work plans of the iteration SpMV kernels (autotuned grids)
   SpmvPlan plan_r, plan_c;
+  SellPlan sell_c;     // SELL-32 copy of A' for the column product
+  int use_sell_c;      // k_spmv_cols_sell instead of k_spmv_cols
   // unscaled problem data and Ruiz factors
   const double *c, *l, *u, *b, *r, *s;
   // state

@@ -473,3 +473,47 @@ __global__ void k_kkt_finish(const double* __restrict__ rpart, int rblocks, cons
 }
 
 }  // namespace cclp_cu
+
+// SELL-32 build (Context::build_sell_cols): slice widths, then the slots.
+namespace cclp_cu {
+
+__global__ void k_sell_width(const int* __restrict__ ptr, int n, int thr, int nsl, int* __restrict__ width) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsl; s += gridDim.x * blockDim.x) {
+    int w = 0;
+    for (int l = 0; l < 32; ++l) {
+      const int j = s * 32 + l;
+      if (j >= n) break;
+      const int len = ptr[j + 1] - ptr[j];
+      if (len <= thr && len > w) w = len;
+    }
+    width[s] = w;
+  }
+}
+
+// warp per slice: lane l writes row s*32+l's elements (zero padding) into
+// slots off + 32k + l — coalesced stores, strided loads (setup only)
+__global__ void k_sell_fill(const int* __restrict__ ptr, const int* __restrict__ idx,
+                            const double* __restrict__ val, int n, int thr, int nsl,
+                            const long long* __restrict__ off, int* __restrict__ sidx,
+                            double* __restrict__ sval) {
+  const int lane = threadIdx.x & 31;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nsl; s += nwarps) {
+    const long long o = off[s];
+    const int w = static_cast<int>((off[s + 1] - o) >> 5);
+    const int j = s * 32 + lane;
+    int b = 0, len = 0;
+    if (j < n) {
+      b = ptr[j];
+      len = ptr[j + 1] - b;
+      if (len > thr) len = 0;
+    }
+    for (int k = 0; k < w; ++k) {
+      const bool ok = k < len;
+      sidx[o + 32LL * k + lane] = ok ? idx[b + k] : 0;
+      sval[o + 32LL * k + lane] = ok ? val[b + k] : 0.0;
+    }
+  }
+}
+
+}  // namespace cclp_cu
