@@ -400,6 +400,15 @@ struct Context {
   double* sell_val = nullptr;
   std::vector<long long> sell_cum;  // host: slots before each slice
   void build_sell_cols();
+  // SELL-G copy of A for the row product (k_spmv_rows_sellg): the same sums
+  // as the CSR-G kernel, so it is chosen by timing (decided once).
+  bool sellr_on = false, sellr_decided = false;
+  int sellr_thr = -1, sellr_G = 0, sellr_grid = 0, sellr_bs = kSpmvBlock, sellr_nsl = 0;
+  long long* sellr_off = nullptr;
+  int* sellr_start = nullptr;
+  int* sellr_idx = nullptr;
+  double* sellr_val = nullptr;
+  void build_sell_rows();
   void relative_report(const double* x, const double* y, const double* z, double* rep, double* abs_viol);
   // SpMV geometry tuning folded into the first power iterations (results are
   // geometry-independent, so the candidates can do real work): both start
@@ -469,7 +478,8 @@ Context::~Context() {
                     counter, ctrl, log, thr, t0, scalars, pctrl, iflags, amb_idx, wn, wn2, wm, vx, vy,
                     vz, vrep, plan_rows.seg, plan_rows.lr_first, plan_rows.part, plan_rows.cnt,
                     plan_cols.seg, plan_cols.lr_first, plan_cols.part, plan_cols.cnt, x_full, y_full,
-                    xpart, vparts, push_flags, push_counter, sell_off, sell_start, sell_idx, sell_val};
+                    xpart, vparts, push_flags, push_counter, sell_off, sell_start, sell_idx, sell_val,
+                    sellr_off, sellr_start, sellr_idx, sellr_val};
     for (void* p : ptrs) release(p);
     for (int k = 0; k < 3; ++k)
       for (int q = 0; q < 2; ++q) release(xc[k][q]);
@@ -1043,6 +1053,155 @@ void Context::build_sell_cols() {
   sell_on = true;
 }
 
+// SELL-G layout of A (SellPlan with G lanes per row, the row kernel's own G):
+// bit-identical to the CSR-G row product, kept only if a timing against it
+// (in the tuned geometry) shows it 3% faster. Not with column panels.
+// CCLP_CU_SELL_ROWS=0 disables it, =2 forces it (tests: bit-identity).
+void Context::build_sell_rows() {
+  const char* e = std::getenv("CCLP_CU_SELL_ROWS");
+  const bool force = e != nullptr && std::atoi(e) == 2;
+  if ((e != nullptr && std::atoi(e) == 0) || m == 0 || nnz == 0 || !sval_csr || use_panels()) {
+    sellr_on = false;
+    return;
+  }
+  if (sellr_decided && !sellr_on) return;
+  const SpmvPlan P = plan(true);
+  const int thr = P.thr, G = grow(), R = 32 / G;
+  const int nsl = (m + R - 1) / R;
+  if (!sellr_off || sellr_thr != thr || sellr_G != G) {
+    int* w = alloc<int>(nsl);
+    k_sellg_width<<<blocks_for(nsl), kBlock, 0, stream>>>(rowptr, m, thr, nsl, G, w);
+    CKL("sellg width");
+    std::vector<int> hw(nsl);
+    CK(cudaMemcpyAsync(hw.data(), w, sizeof(int) * nsl, cudaMemcpyDeviceToHost, stream));
+    CK(cudaStreamSynchronize(stream));
+    release(w);
+    std::vector<long long> cum(static_cast<size_t>(nsl) + 1, 0);
+    for (int q = 0; q < nsl; ++q) cum[q + 1] = cum[q] + 32LL * hw[q];
+    // padded slots beyond 1.25x the nonzeros lose inside the iteration even
+    // where a stand-alone timing says otherwise (C4 rows, G = 4: 1.40x,
+    // +15 us); the rule depends on the matrix only
+    if (!force && static_cast<double>(cum[nsl]) > kSellMaxPad * static_cast<double>(nnz)) {
+      sellr_on = false;
+      sellr_decided = true;
+      return;
+    }
+    release(sellr_off);
+    release(sellr_idx);
+    release(sellr_val);
+    release(sellr_start);
+    sellr_off = alloc<long long>(static_cast<size_t>(nsl) + 1);
+    CK(cudaMemcpyAsync(sellr_off, cum.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, stream));
+    sellr_idx = alloc<int>(static_cast<size_t>(std::max<long long>(cum[nsl], 1)));
+    sellr_val = alloc<double>(static_cast<size_t>(std::max<long long>(cum[nsl], 1)));
+    // block slice ranges for `grid` blocks: equal slots + per-row overhead
+    auto starts = [&](int grid) {
+      auto weight = [&](long long q) { return cum[q] + 16LL * R * q; };
+      const long long total = weight(nsl);
+      std::vector<int> st(static_cast<size_t>(grid) + 1);
+      for (int b = 0; b <= grid; ++b) {
+        const long long target = total * b / grid;
+        int lo = 0, hi = nsl;
+        while (lo < hi) {
+          const int mid = (lo + hi) / 2;
+          if (weight(mid) >= target) hi = mid; else lo = mid + 1;
+        }
+        st[b] = b == grid ? nsl : lo;
+      }
+      int* d = alloc<int>(static_cast<size_t>(grid) + 1);
+      CK(cudaMemcpyAsync(d, st.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice, stream));
+      CK(cudaStreamSynchronize(stream));
+      return d;
+    };
+    sellr_thr = thr;
+    sellr_G = G;
+    sellr_nsl = nsl;
+    k_sellg_fill<<<blocks_for(static_cast<long long>(nsl) * 32), kBlock, 0, stream>>>(
+        rowptr, colind, sval_csr, m, thr, nsl, G, sellr_off, sellr_idx, sellr_val);
+    CKL("sellg fill");
+    // candidates: 1024-thread blocks on the row grid (the only one with long
+    // rows: the segments are planned for it), else also 2 x 1024 and 8 x 256
+    // per SM; against the CSR-G kernel in its tuned geometry
+    const bool lng = thr != 0x7fffffff;
+    const double* gx = x_full ? x_full : wn;
+    const SpmvPlan Pc = plan(false);
+    auto other_side = [&] {  // the column product between samples: the iteration's cache state
+      with_group_long(gcol(), Pc.thr != 0x7fffffff, [&](auto g, auto l) {
+        k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(
+            Pc, colptr, rowind, val_csc, GatherPlain{y_full ? y_full : wm}, wn2, rpg_c);
+      });
+    };
+    auto timed = [&](auto launch) {
+      std::vector<float> t;
+      for (int rep = 0; rep < 5; ++rep) {
+        other_side();
+        CK(cudaEventRecord(ev_a, stream));
+        launch();
+        CK(cudaEventRecord(ev_b, stream));
+        CK(cudaEventSynchronize(ev_b));
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+        if (rep > 0) t.push_back(ms);
+      }
+      std::sort(t.begin(), t.end());
+      return t[t.size() / 2];
+    };
+    const float t_csr = timed([&] {
+      with_group_long(G, lng, [&](auto g, auto l) {
+        k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_r, kSpmvBlock, 0, stream>>>(
+            P, rowptr, colind, val_csr, GatherPlain{gx}, wm, rpg_r);
+      });
+    });
+    struct Cand { int bs, grid; };
+    std::vector<Cand> cands{{kSpmvBlock, spmv_grid_r}};
+    if (!lng) {
+      cands.push_back({kSpmvBlock, 2 * tune_sms});
+      cands.push_back({256, 8 * tune_sms});
+    }
+    float best = force ? 1e30f : 0.97f * t_csr;
+    int* best_start = nullptr;
+    for (const Cand& c : cands) {
+      int* st = starts(c.grid);
+      SellPlan S{sellr_off, st, rowptr, sellr_idx, sellr_val, m, thr};
+      const float t = timed([&] {
+        with_group_long(G, lng, [&](auto g, auto l) {
+          if (c.bs == 256)
+            k_sellg_range<decltype(g)::value, decltype(l)::value, 256><<<c.grid, 256, 0, stream>>>(
+                S, P, colind, val_csr, GatherPlain{gx}, wm);
+          else
+            k_sellg_range<decltype(g)::value, decltype(l)::value, kSpmvBlock><<<c.grid, kSpmvBlock, 0, stream>>>(
+                S, P, colind, val_csr, GatherPlain{gx}, wm);
+        });
+      });
+      if (t < best) {
+        best = t;
+        release(best_start);
+        best_start = st;
+        sellr_bs = c.bs;
+        sellr_grid = c.grid;
+      } else {
+        release(st);
+      }
+    }
+    CKL("sellg tune");
+    sellr_decided = true;
+    sellr_on = best_start != nullptr;
+    sellr_start = best_start;
+    if (!sellr_on) {
+      release(sellr_off);
+      release(sellr_idx);
+      release(sellr_val);
+      sellr_off = nullptr;
+      sellr_idx = nullptr;
+      sellr_val = nullptr;
+    }
+    return;
+  }
+  k_sellg_fill<<<blocks_for(static_cast<long long>(nsl) * 32), kBlock, 0, stream>>>(
+      rowptr, colind, sval_csr, m, thr, nsl, G, sellr_off, sellr_idx, sellr_val);
+  CKL("sellg fill");
+}
+
 // relative_report + absolute_violation (kkt.cpp:106-149) of a host iterate
 // on the unscaled equality-form LP; `rep` in cclp_cu_report order.
 void Context::relative_report(const double* x, const double* y, const double* z, double* rep,
@@ -1375,6 +1534,15 @@ void Context::launch_rows_half(bool init) {
       });
     }
     launches += static_cast<long long>(panels.size()) - 1;
+  } else if (p.use_sell_r) {
+    with_group_long(grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
+      if (sellr_bs == 256)
+        launch_pdl(k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, 256>, sellr_grid, 256, stream, p,
+                   ii);
+      else
+        launch_pdl(k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, kSpmvBlock>, sellr_grid,
+                   kSpmvBlock, stream, p, ii);
+    });
   } else {
     with_group_long(grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
       launch_pdl(k_spmv_rows<decltype(g)::value, decltype(l)::value>, spmv_grid_r, kSpmvBlock, stream, p,
@@ -1539,6 +1707,9 @@ void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& to
   p.plan_r = plan(true); p.plan_c = plan(false);
   p.rpg_rows = rpg_r; p.rpg_cols = rpg_c;
   build_sell_cols();
+  build_sell_rows();
+  p.use_sell_r = sellr_on ? 1 : 0;
+  p.sell_r = SellPlan{sellr_off, sellr_start, rowptr, sellr_idx, sellr_val, m, sellr_thr};
   p.use_sell_c = sell_on ? 1 : 0;
   p.sell_c = SellPlan{sell_off, sell_start, colptr, sell_idx, sell_val, n, sell_thr};
   p.c = c; p.l = l; p.u = u; p.b = b; p.r = r; p.s = s;
@@ -1853,6 +2024,15 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
                 <<<C.panel_grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0, a);
           });
         }
+      } else if (p.use_sell_r) {
+        cclp_cu::with_group_long(C.grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
+          if (C.sellr_bs == 256)
+            cclp_cu::k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, 256>
+                <<<C.sellr_grid, 256, 0, C.stream>>>(p, 0);
+          else
+            cclp_cu::k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, cclp_cu::kSpmvBlock>
+                <<<C.sellr_grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
+        });
       } else {
         cclp_cu::with_group_long(C.grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
           cclp_cu::k_spmv_rows<decltype(g)::value, decltype(l)::value>

@@ -526,6 +526,67 @@ __device__ __forceinline__ void sell_block(const SellPlan& S, const Gather& g, d
   }
 }
 
+// SELL-G row product of block blockIdx.x's slices: 32/G rows per slice, lane
+// gl of a row's group takes the row's elements gl, gl+G, ... in order (4 in
+// flight) and the group ends with the xor butterfly — the CSR-G kernel's
+// exact per-lane order and combine, so the sums are bit-identical to it
+// while every index/value load is one 128-byte line. Rows longer than S.thr
+// are written by the long-row segments.
+template <int G, class Gather>
+__device__ __forceinline__ void sellg_block(const SellPlan& S, const Gather& g, double* __restrict__ out) {
+  constexpr int U = 4, R = 32 / G;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int r = lane / G, gl = lane % G;
+  const int sb = S.start[blockIdx.x], se = S.start[blockIdx.x + 1];
+  for (int s = sb + warp; s < se; s += nw) {
+    const long long off = S.off[s];
+    const int w = static_cast<int>((S.off[s + 1] - off) >> 5);
+    const int row = s * R + r;
+    int len = row < S.n ? __ldg(S.ptr + row + 1) - __ldg(S.ptr + row) : 0;
+    const bool seg = len > S.thr;
+    if (seg) len = 0;
+    const int* __restrict__ ib = S.idx + off + lane;
+    const double* __restrict__ vb = S.val + off + lane;
+    double acc = 0.0;
+    for (int k = 0; k < w; k += U) {
+      int ii[U];
+      double vv[U], xx[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const bool ok = (k + u) * G + gl < len;
+        ii[u] = ok ? __ldcs(ib + 32 * (k + u)) : -1;
+        vv[u] = ok ? __ldcs(vb + 32 * (k + u)) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) xx[u] = ii[u] >= 0 ? g(ii[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (ii[u] >= 0) acc = acc + vv[u] * xx[u];
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (gl == 0 && row < S.n && !seg) out[row] = 0.0 + acc;
+  }
+}
+
+template <int G, bool LONG, int BS>
+__global__ void __launch_bounds__(BS) k_sellg_range(const SellPlan S, const SpmvPlan P, const int* __restrict__ idx,
+                                                    const double* __restrict__ val, GatherPlain g,
+                                                    double* __restrict__ out) {
+  sellg_block<G>(S, g, out);
+  if (LONG) spmv_long_segments(P, idx, val, g, out, 0);
+}
+
+template <int G, bool LONG, int BS>
+__global__ void __launch_bounds__(BS) k_spmv_rows_sellg(const IterParams p, int init) {
+  StepInfo si;
+  if (!read_step(p, init != 0, si)) return;
+  if (p.push.on) push_wait(p.push, kPushX, static_cast<unsigned long long>(si.t1 + 1));
+  const GatherPlain g{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]};
+  sellg_block<G>(p.sell_r, g, p.ax[si.s1]);
+  if (LONG) spmv_long_segments(p.plan_r, p.colind, p.aval, g, p.ax[si.s1], 0);
+}
+
 // Stand-alone SELL product (geometry tuning in Context::build_sell_cols).
 template <int BS>
 __global__ void __launch_bounds__(BS) k_sell_range(const SellPlan S, GatherPlain g, double* __restrict__ out) {

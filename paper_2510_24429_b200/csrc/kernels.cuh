@@ -125,6 +125,8 @@ struct IterParams {
   SpmvPlan plan_r, plan_c;
   SellPlan sell_c;     // SELL-32 copy of A' for the column product
   int use_sell_c;      // k_spmv_cols_sell instead of k_spmv_cols
+  SellPlan sell_r;     // SELL-G copy of A for the row product (same sums as CSR-G)
+  int use_sell_r;      // k_spmv_rows_sellg instead of k_spmv_rows
   // unscaled problem data and Ruiz factors
   const double *c, *l, *u, *b, *r, *s;
   // state

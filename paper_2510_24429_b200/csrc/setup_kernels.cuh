@@ -517,3 +517,49 @@ __global__ void k_sell_fill(const int* __restrict__ ptr, const int* __restrict__
 }
 
 }  // namespace cclp_cu
+
+// SELL-G build (Context::build_sell_rows): 32/G rows per slice, G lanes per
+// row; slot k of lane (r, gl) holds row s*R + r's element k*G + gl.
+namespace cclp_cu {
+
+__global__ void k_sellg_width(const int* __restrict__ ptr, int n, int thr, int nsl, int G,
+                              int* __restrict__ width) {
+  const int R = 32 / G;
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsl; s += gridDim.x * blockDim.x) {
+    int w = 0;
+    for (int r = 0; r < R; ++r) {
+      const int j = s * R + r;
+      if (j >= n) break;
+      const int len = ptr[j + 1] - ptr[j];
+      if (len <= thr) w = max(w, (len + G - 1) / G);
+    }
+    width[s] = w;
+  }
+}
+
+__global__ void k_sellg_fill(const int* __restrict__ ptr, const int* __restrict__ idx,
+                             const double* __restrict__ val, int n, int thr, int nsl, int G,
+                             const long long* __restrict__ off, int* __restrict__ sidx,
+                             double* __restrict__ sval) {
+  const int lane = threadIdx.x & 31, R = 32 / G, r = lane / G, gl = lane % G;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nsl; s += nwarps) {
+    const long long o = off[s];
+    const int w = static_cast<int>((off[s + 1] - o) >> 5);
+    const int j = s * R + r;
+    int b = 0, len = 0;
+    if (j < n) {
+      b = ptr[j];
+      len = ptr[j + 1] - b;
+      if (len > thr) len = 0;
+    }
+    for (int k = 0; k < w; ++k) {
+      const int e = k * G + gl;
+      const bool ok = e < len;
+      sidx[o + 32LL * k + lane] = ok ? idx[b + e] : 0;
+      sval[o + 32LL * k + lane] = ok ? val[b + e] : 0.0;
+    }
+  }
+}
+
+}  // namespace cclp_cu

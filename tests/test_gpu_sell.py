@@ -77,3 +77,26 @@ def test_sell_rerun_identical_and_close_to_csr(name, lp, monkeypatch):
     monkeypatch.setenv("CCLP_CU_SELL", "0")
     c = run_pdhg(lp, cfg)
     assert rel(a.iterate.x, c.iterate.x) <= 1e-9 and rel(a.iterate.y, c.iterate.y) <= 1e-9
+
+
+# ---- SELL-G row product (k_spmv_rows_sellg): chosen by timing, so it must be
+# bit-identical to the CSR-G row kernel; CCLP_CU_SELL_ROWS=2 forces it.
+
+def _long_rows_lp():
+    from test_gpu_longrows import dense_rows_lp
+    return dense_rows_lp()
+
+
+@pytest.mark.parametrize("name", ["eq40x90", "transport20x30", "random2k", "dense_cols", "long_rows"])
+def test_sellg_rows_bit_identical_to_csr(name, monkeypatch):
+    lp = _long_rows_lp() if name == "long_rows" else dict(lps())[name]
+    cfg = PdhgConfig(max_iterations=150)
+    monkeypatch.setenv("CCLP_CU_SELL", "0")
+    monkeypatch.setenv("CCLP_CU_SELL_ROWS", "0")
+    a = run_pdhg(lp, cfg)
+    monkeypatch.setenv("CCLP_CU_SELL_ROWS", "2")
+    b = run_pdhg(lp, cfg)
+    sh = run_pdhg_sharded(lp, 2, cfg)
+    assert a.iterations == b.iterations == sh.iterations
+    for u, v in ((a.iterate.x, b.iterate.x), (a.iterate.y, b.iterate.y), (a.iterate.x, sh.iterate.x)):
+        assert np.array_equal(u, v)
