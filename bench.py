@@ -54,14 +54,14 @@ def algorithmic_bytes(m: int, n: int, nnz: int) -> dict:
                 cols=12 * nnz + 4 * (n + 1) + 8 * m + 8 * n)
 
 
-def l2_roofline(lp, dom: str, dom_ms: float, clocks: dict) -> dict:
+def l2_roofline(lp, dom: str, dom_ms: float, clocks: dict, kernel: str = "") -> dict:
     rows = dom == "rows"
     out_len, vec_len = (lp.m, lp.n) if rows else (lp.n, lp.m)
     traffic = 44.0 * lp.nnz + 4.0 * (out_len + 1) + 8.0 * out_len
     mhz = clocks.get("sm_mhz") or 1965.0
     cap = 6300.0 * mhz * 1e6 / 1e9  # GB/s
     achieved = traffic / (dom_ms * 1e-3) / 1e9
-    return {"bound": "l2_sectors", "kernel": f"k_spmv_{dom}", "bytes_per_launch": traffic,
+    return {"bound": "l2_sectors", "kernel": kernel or f"k_spmv_{dom}", "bytes_per_launch": traffic,
             "achieved": achieved, "peak": cap, "unit": "GB/s", "frac": achieved / cap,
             "model": "12 B stream + 32 B L2 sector per gathered nonzero + row pointers + output; "
                      "cap 6300 B/clk x SM clock"}
@@ -412,12 +412,16 @@ def main():
     ab = algorithmic_bytes(lp.m, lp.n, lp.nnz)
     dom = "rows" if pk["spmv_rows"] >= pk["spmv_cols"] else "cols"
     dom_ms = pk["spmv_" + dom]
+    dsc = eng.describe()
+    # the kernel that actually ran for that product (SELL layouts: engine.cu)
+    dom_kernel = {"rows": "k_spmv_rows_sellg" if dsc.get("sell_rows_block") else "k_spmv_rows",
+                  "cols": "k_spmv_cols_sell" if dsc.get("sell_cols_block") else "k_spmv_cols"}[dom]
     achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peak_gbs()
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(args.workload, {}).get("k_spmv_" + dom)
+            traffic = json.load(f).get(args.workload, {}).get(dom_kernel)
     except Exception:
         pass
     iter_us = dev_ms * 1e3 / (K * I)
@@ -477,7 +481,7 @@ def main():
                        "l2": "working set ~180 MB > 126 MB L2, no flush"},
             "us_per_iteration": iter_us,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": f"k_spmv_{dom}",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": dom_kernel,
                          "kernel_us": dom_ms * 1e3, "bytes_per_launch": ab[dom],
                          "peak_kind": peak_kind,
                          "iteration": {"bytes": ab["iteration"],
@@ -488,7 +492,7 @@ def main():
             # 12 B stream + one 32 B sector per gathered nonzero (+ the vectors),
             # against the LTS throughput cap (~6,300 B/clk, B300_MICROARCH.md) at
             # the sampled SM clock
-            "l2_roofline": l2_roofline(lp, dom, dom_ms, clk.summary()),
+            "l2_roofline": l2_roofline(lp, dom, dom_ms, clk.summary(), dom_kernel),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "iters_per_step": args.e2e_iters,
                     "includes": "upload, CSR build, Ruiz, ||A|| power iteration, loop, download"},
