@@ -360,6 +360,7 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=20)
     ap.add_argument("--cpu-iters", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance solves (profiling runs)")
     ap.add_argument("--workload", default=CONFIG_NAME,
                     help="C2 (default, configs[1]); C3/C4/C5/C5s: with N>1 the sharded solve")
     args = ap.parse_args()
@@ -447,7 +448,7 @@ def main():
 
     # time to tolerance (one solve, rank 0)
     ttt = None
-    if rank == 0 and lp.nnz <= 25_000_000:  # ~1 s on C2; C4/C5 would take minutes
+    if rank == 0 and lp.nnz <= 25_000_000 and not args.no_ttt:  # ~1 s on C2; C4/C5 would take minutes
         t = time.perf_counter()
         r4 = run_pdhg(plp, PdhgConfig(max_iterations=200000),
                       tol=Tolerances(eps_rel=1e-4),
