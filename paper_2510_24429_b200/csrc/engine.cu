@@ -402,13 +402,17 @@ struct Context {
   void build_sell_cols();
   // SELL-G copy of A for the row product (k_spmv_rows_sellg): the same sums
   // as the CSR-G kernel, so it is chosen by timing (decided once).
-  bool sellr_on = false, sellr_decided = false;
-  int sellr_thr = -1, sellr_G = 0, sellr_grid = 0, sellr_bs = kSpmvBlock, sellr_nsl = 0;
-  long long* sellr_off = nullptr;
-  int* sellr_start = nullptr;
-  int* sellr_idx = nullptr;
-  double* sellr_val = nullptr;
+  struct SellG {
+    bool on = false, decided = false;
+    int thr = -1, G = 0, grid = 0, bs = kSpmvBlock, nsl = 0;
+    long long* off = nullptr;
+    int* start = nullptr;
+    int* idx = nullptr;
+    double* val = nullptr;
+  };
+  SellG sgr, sgc;  // rows (k_spmv_rows_sellg), columns (k_spmv_cols_sellg)
   void build_sell_rows();
+  void build_sellg(bool rows_side);
   void relative_report(const double* x, const double* y, const double* z, double* rep, double* abs_viol);
   // SpMV geometry tuning folded into the first power iterations (results are
   // geometry-independent, so the candidates can do real work): both start
@@ -479,7 +483,7 @@ Context::~Context() {
                     vz, vrep, plan_rows.seg, plan_rows.lr_first, plan_rows.part, plan_rows.cnt,
                     plan_cols.seg, plan_cols.lr_first, plan_cols.part, plan_cols.cnt, x_full, y_full,
                     xpart, vparts, push_flags, push_counter, sell_off, sell_start, sell_idx, sell_val,
-                    sellr_off, sellr_start, sellr_idx, sellr_val};
+                    sgr.off, sgr.start, sgr.idx, sgr.val, sgc.off, sgc.start, sgc.idx, sgc.val};
     for (void* p : ptrs) release(p);
     for (int k = 0; k < 3; ++k)
       for (int q = 0; q < 2; ++q) release(xc[k][q]);
@@ -1057,20 +1061,34 @@ void Context::build_sell_cols() {
 // bit-identical to the CSR-G row product, kept only if a timing against it
 // (in the tuned geometry) shows it 3% faster. Not with column panels.
 // CCLP_CU_SELL_ROWS=0 disables it, =2 forces it (tests: bit-identity).
-void Context::build_sell_rows() {
-  const char* e = std::getenv("CCLP_CU_SELL_ROWS");
+void Context::build_sell_rows() { build_sellg(true); }
+
+void Context::build_sellg(bool rows_side) {
+  SellG& S = rows_side ? sgr : sgc;
+  const char* e = std::getenv(rows_side ? "CCLP_CU_SELL_ROWS" : "CCLP_CU_SELLG_COLS");
   const bool force = e != nullptr && std::atoi(e) == 2;
-  if ((e != nullptr && std::atoi(e) == 0) || m == 0 || nnz == 0 || !sval_csr || use_panels()) {
-    sellr_on = false;
+  const int cnt = rows_side ? m : n;
+  const int* ptr = rows_side ? rowptr : colptr;
+  const int* idx = rows_side ? colind : rowind;
+  const double* sval = rows_side ? sval_csr : sval_csc;
+  const double* uval = rows_side ? val_csr : val_csc;
+  // the column side takes SELL-G only where the SELL-32 layout was not chosen
+  // The column side measured slower inside the iteration than its stand-alone
+  // timing suggested (C2: 31.4 vs 30.6 us), so it is opt-in there
+  // (CCLP_CU_SELLG_COLS=1: timed, =2: forced).
+  const bool opted = rows_side || (e != nullptr && std::atoi(e) >= 1);
+  if ((e != nullptr && std::atoi(e) == 0) || !opted || cnt == 0 || nnz == 0 || !sval ||
+      (rows_side && use_panels()) || (!rows_side && sell_on)) {
+    S.on = false;
     return;
   }
-  if (sellr_decided && !sellr_on) return;
-  const SpmvPlan P = plan(true);
-  const int thr = P.thr, G = grow(), R = 32 / G;
-  const int nsl = (m + R - 1) / R;
-  if (!sellr_off || sellr_thr != thr || sellr_G != G) {
+  if (S.decided && !S.on) return;
+  const SpmvPlan P = plan(rows_side);
+  const int thr = P.thr, G = rows_side ? grow() : gcol(), R = 32 / G;
+  const int nsl = (cnt + R - 1) / R;
+  if (!S.off || S.thr != thr || S.G != G) {
     int* w = alloc<int>(nsl);
-    k_sellg_width<<<blocks_for(nsl), kBlock, 0, stream>>>(rowptr, m, thr, nsl, G, w);
+    k_sellg_width<<<blocks_for(nsl), kBlock, 0, stream>>>(ptr, cnt, thr, nsl, G, w);
     CKL("sellg width");
     std::vector<int> hw(nsl);
     CK(cudaMemcpyAsync(hw.data(), w, sizeof(int) * nsl, cudaMemcpyDeviceToHost, stream));
@@ -1082,18 +1100,18 @@ void Context::build_sell_rows() {
     // where a stand-alone timing says otherwise (C4 rows, G = 4: 1.40x,
     // +15 us); the rule depends on the matrix only
     if (!force && static_cast<double>(cum[nsl]) > kSellMaxPad * static_cast<double>(nnz)) {
-      sellr_on = false;
-      sellr_decided = true;
+      S.on = false;
+      S.decided = true;
       return;
     }
-    release(sellr_off);
-    release(sellr_idx);
-    release(sellr_val);
-    release(sellr_start);
-    sellr_off = alloc<long long>(static_cast<size_t>(nsl) + 1);
-    CK(cudaMemcpyAsync(sellr_off, cum.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, stream));
-    sellr_idx = alloc<int>(static_cast<size_t>(std::max<long long>(cum[nsl], 1)));
-    sellr_val = alloc<double>(static_cast<size_t>(std::max<long long>(cum[nsl], 1)));
+    release(S.off);
+    release(S.idx);
+    release(S.val);
+    release(S.start);
+    S.off = alloc<long long>(static_cast<size_t>(nsl) + 1);
+    CK(cudaMemcpyAsync(S.off, cum.data(), sizeof(long long) * (nsl + 1), cudaMemcpyHostToDevice, stream));
+    S.idx = alloc<int>(static_cast<size_t>(std::max<long long>(cum[nsl], 1)));
+    S.val = alloc<double>(static_cast<size_t>(std::max<long long>(cum[nsl], 1)));
     // block slice ranges for `grid` blocks: equal slots + per-row overhead
     auto starts = [&](int grid) {
       auto weight = [&](long long q) { return cum[q] + 16LL * R * q; };
@@ -1113,23 +1131,34 @@ void Context::build_sell_rows() {
       CK(cudaStreamSynchronize(stream));
       return d;
     };
-    sellr_thr = thr;
-    sellr_G = G;
-    sellr_nsl = nsl;
+    S.thr = thr;
+    S.G = G;
+    S.nsl = nsl;
     k_sellg_fill<<<blocks_for(static_cast<long long>(nsl) * 32), kBlock, 0, stream>>>(
-        rowptr, colind, sval_csr, m, thr, nsl, G, sellr_off, sellr_idx, sellr_val);
+        ptr, idx, sval, cnt, thr, nsl, G, S.off, S.idx, S.val);
     CKL("sellg fill");
-    // candidates: 1024-thread blocks on the row grid (the only one with long
-    // rows: the segments are planned for it), else also 2 x 1024 and 8 x 256
-    // per SM; against the CSR-G kernel in its tuned geometry
+    // candidates: 1024-thread blocks on the side's grid (the only one with
+    // long rows: the segments are planned for it), else also 2 x 1024 and
+    // 8 x 256 per SM; against the CSR-G kernel in its tuned geometry, the
+    // other side's product run between samples (the iteration's cache state)
     const bool lng = thr != 0x7fffffff;
-    const double* gx = x_full ? x_full : wn;
-    const SpmvPlan Pc = plan(false);
-    auto other_side = [&] {  // the column product between samples: the iteration's cache state
-      with_group_long(gcol(), Pc.thr != 0x7fffffff, [&](auto g, auto l) {
-        k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(
-            Pc, colptr, rowind, val_csc, GatherPlain{y_full ? y_full : wm}, wn2, rpg_c);
-      });
+    const int side_grid = rows_side ? spmv_grid_r : spmv_grid_c;
+    const int side_rpg = rows_side ? rpg_r : rpg_c;
+    const double* gv = rows_side ? (x_full ? x_full : wn) : (y_full ? y_full : wm);
+    double* outv = rows_side ? wm : wn2;
+    const SpmvPlan Po = plan(!rows_side);
+    auto other_side = [&] {
+      if (rows_side) {
+        with_group_long(gcol(), Po.thr != 0x7fffffff, [&](auto g, auto l) {
+          k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(
+              Po, colptr, rowind, val_csc, GatherPlain{y_full ? y_full : wm}, wn2, rpg_c);
+        });
+      } else {
+        with_group_long(grow(), Po.thr != 0x7fffffff, [&](auto g, auto l) {
+          k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_r, kSpmvBlock, 0, stream>>>(
+              Po, rowptr, colind, val_csr, GatherPlain{x_full ? x_full : wn}, wm, rpg_r);
+        });
+      }
     };
     auto timed = [&](auto launch) {
       std::vector<float> t;
@@ -1148,57 +1177,59 @@ void Context::build_sell_rows() {
     };
     const float t_csr = timed([&] {
       with_group_long(G, lng, [&](auto g, auto l) {
-        k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_r, kSpmvBlock, 0, stream>>>(
-            P, rowptr, colind, val_csr, GatherPlain{gx}, wm, rpg_r);
+        k_spmv_range<decltype(g)::value, decltype(l)::value><<<side_grid, kSpmvBlock, 0, stream>>>(
+            P, ptr, idx, uval, GatherPlain{gv}, outv, side_rpg);
       });
     });
     struct Cand { int bs, grid; };
-    std::vector<Cand> cands{{kSpmvBlock, spmv_grid_r}};
+    std::vector<Cand> cands{{kSpmvBlock, side_grid}};
     if (!lng) {
       cands.push_back({kSpmvBlock, 2 * tune_sms});
       cands.push_back({256, 8 * tune_sms});
     }
-    float best = force ? 1e30f : 0.97f * t_csr;
+    // rows: SELL-G whenever the timing does not find it slower (inside the
+    // iteration it won on every matrix that passes the padding rule)
+    float best = force ? 1e30f : (rows_side ? 1.0f : 0.97f) * t_csr;
     int* best_start = nullptr;
     for (const Cand& c : cands) {
       int* st = starts(c.grid);
-      SellPlan S{sellr_off, st, rowptr, sellr_idx, sellr_val, m, thr};
+      SellPlan SP{S.off, st, ptr, S.idx, S.val, cnt, thr};
       const float t = timed([&] {
         with_group_long(G, lng, [&](auto g, auto l) {
           if (c.bs == 256)
             k_sellg_range<decltype(g)::value, decltype(l)::value, 256><<<c.grid, 256, 0, stream>>>(
-                S, P, colind, val_csr, GatherPlain{gx}, wm);
+                SP, P, idx, uval, GatherPlain{gv}, outv);
           else
             k_sellg_range<decltype(g)::value, decltype(l)::value, kSpmvBlock><<<c.grid, kSpmvBlock, 0, stream>>>(
-                S, P, colind, val_csr, GatherPlain{gx}, wm);
+                SP, P, idx, uval, GatherPlain{gv}, outv);
         });
       });
       if (t < best) {
         best = t;
         release(best_start);
         best_start = st;
-        sellr_bs = c.bs;
-        sellr_grid = c.grid;
+        S.bs = c.bs;
+        S.grid = c.grid;
       } else {
         release(st);
       }
     }
     CKL("sellg tune");
-    sellr_decided = true;
-    sellr_on = best_start != nullptr;
-    sellr_start = best_start;
-    if (!sellr_on) {
-      release(sellr_off);
-      release(sellr_idx);
-      release(sellr_val);
-      sellr_off = nullptr;
-      sellr_idx = nullptr;
-      sellr_val = nullptr;
+    S.decided = true;
+    S.on = best_start != nullptr;
+    S.start = best_start;
+    if (!S.on) {
+      release(S.off);
+      release(S.idx);
+      release(S.val);
+      S.off = nullptr;
+      S.idx = nullptr;
+      S.val = nullptr;
     }
     return;
   }
   k_sellg_fill<<<blocks_for(static_cast<long long>(nsl) * 32), kBlock, 0, stream>>>(
-      rowptr, colind, sval_csr, m, thr, nsl, G, sellr_off, sellr_idx, sellr_val);
+      ptr, idx, sval, cnt, thr, nsl, G, S.off, S.idx, S.val);
   CKL("sellg fill");
 }
 
@@ -1536,11 +1567,11 @@ void Context::launch_rows_half(bool init) {
     launches += static_cast<long long>(panels.size()) - 1;
   } else if (p.use_sell_r) {
     with_group_long(grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
-      if (sellr_bs == 256)
-        launch_pdl(k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, 256>, sellr_grid, 256, stream, p,
+      if (sgr.bs == 256)
+        launch_pdl(k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, 256>, sgr.grid, 256, stream, p,
                    ii);
       else
-        launch_pdl(k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, kSpmvBlock>, sellr_grid,
+        launch_pdl(k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, kSpmvBlock>, sgr.grid,
                    kSpmvBlock, stream, p, ii);
     });
   } else {
@@ -1555,7 +1586,15 @@ void Context::launch_rows_half(bool init) {
 void Context::launch_cols_half(bool init) {
   const IterParams& p = params;
   const int ii = init ? 1 : 0;
-  if (p.use_sell_c) {
+  if (p.use_sell_cg) {
+    with_group_long(gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
+      if (sgc.bs == 256)
+        launch_pdl(k_spmv_cols_sellg<decltype(g)::value, decltype(l)::value, 256>, sgc.grid, 256, stream, p, ii);
+      else
+        launch_pdl(k_spmv_cols_sellg<decltype(g)::value, decltype(l)::value, kSpmvBlock>, sgc.grid, kSpmvBlock,
+                   stream, p, ii);
+    });
+  } else if (p.use_sell_c) {
     if (p.plan_c.thr != 0x7fffffff)
       launch_pdl(k_spmv_cols_sell<true, kSpmvBlock>, spmv_grid_c, kSpmvBlock, stream, p, ii);
     else if (sell_bs == 256)
@@ -1707,9 +1746,12 @@ void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& to
   p.plan_r = plan(true); p.plan_c = plan(false);
   p.rpg_rows = rpg_r; p.rpg_cols = rpg_c;
   build_sell_cols();
-  build_sell_rows();
-  p.use_sell_r = sellr_on ? 1 : 0;
-  p.sell_r = SellPlan{sellr_off, sellr_start, rowptr, sellr_idx, sellr_val, m, sellr_thr};
+  build_sellg(true);
+  build_sellg(false);
+  p.use_sell_r = sgr.on ? 1 : 0;
+  p.sell_r = SellPlan{sgr.off, sgr.start, rowptr, sgr.idx, sgr.val, m, sgr.thr};
+  p.use_sell_cg = sgc.on ? 1 : 0;
+  p.sell_cg = SellPlan{sgc.off, sgc.start, colptr, sgc.idx, sgc.val, n, sgc.thr};
   p.use_sell_c = sell_on ? 1 : 0;
   p.sell_c = SellPlan{sell_off, sell_start, colptr, sell_idx, sell_val, n, sell_thr};
   p.c = c; p.l = l; p.u = u; p.b = b; p.r = r; p.s = s;
@@ -2026,12 +2068,12 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
         }
       } else if (p.use_sell_r) {
         cclp_cu::with_group_long(C.grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
-          if (C.sellr_bs == 256)
+          if (C.sgr.bs == 256)
             cclp_cu::k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, 256>
-                <<<C.sellr_grid, 256, 0, C.stream>>>(p, 0);
+                <<<C.sgr.grid, 256, 0, C.stream>>>(p, 0);
           else
             cclp_cu::k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, cclp_cu::kSpmvBlock>
-                <<<C.sellr_grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
+                <<<C.sgr.grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
         });
       } else {
         cclp_cu::with_group_long(C.grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
@@ -2042,7 +2084,16 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
       CK(cudaEventRecord(e[1], C.stream));
       cclp_cu::k_dual<<<C.epi_grid, cclp_cu::kEpiBlock, 0, C.stream>>>(p, 0);
       CK(cudaEventRecord(e[2], C.stream));
-      if (p.use_sell_c) {
+      if (p.use_sell_cg) {
+        cclp_cu::with_group_long(C.gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
+          if (C.sgc.bs == 256)
+            cclp_cu::k_spmv_cols_sellg<decltype(g)::value, decltype(l)::value, 256>
+                <<<C.sgc.grid, 256, 0, C.stream>>>(p, 0);
+          else
+            cclp_cu::k_spmv_cols_sellg<decltype(g)::value, decltype(l)::value, cclp_cu::kSpmvBlock>
+                <<<C.sgc.grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
+        });
+      } else if (p.use_sell_c) {
         if (p.plan_c.thr != 0x7fffffff)
           cclp_cu::k_spmv_cols_sell<true, cclp_cu::kSpmvBlock>
               <<<C.spmv_grid_c, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
@@ -2095,7 +2146,7 @@ int cclp_cu_describe(cclp_cu_ctx* ctx, int64_t* out, int32_t nout) {
                        static_cast<int64_t>(1e9 * C.phase[8]), static_cast<int64_t>(1e9 * C.phase[9]),
                        static_cast<int64_t>(1e9 * C.phase[10]),
                        // 21, 22: block size of the SELL row / column product (0: CSR-G kernel)
-                       C.sellr_on ? C.sellr_bs : 0, C.sell_on ? C.sell_bs : 0};
+                       C.sgr.on ? C.sgr.bs : 0, C.sell_on ? C.sell_bs : (C.sgc.on ? C.sgc.bs : 0)};
   for (int i = 0; i < nout && i < static_cast<int>(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
   return CCLP_CU_OK;
 }

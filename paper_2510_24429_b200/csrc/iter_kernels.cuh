@@ -587,6 +587,16 @@ __global__ void __launch_bounds__(BS) k_spmv_rows_sellg(const IterParams p, int 
   if (LONG) spmv_long_segments(p.plan_r, p.colind, p.aval, g, p.ax[si.s1], 0);
 }
 
+template <int G, bool LONG, int BS>
+__global__ void __launch_bounds__(BS) k_spmv_cols_sellg(const IterParams p, int init) {
+  StepInfo si;
+  if (!read_step(p, init != 0, si)) return;
+  if (p.push.on) push_wait(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1));
+  const GatherPlain g{p.yg != nullptr ? p.yg : p.y[si.s1]};
+  sellg_block<G>(p.sell_cg, g, p.aty[si.s1]);
+  if (LONG) spmv_long_segments(p.plan_c, p.rowind, p.atval, g, p.aty[si.s1], 0);
+}
+
 // Stand-alone SELL product (geometry tuning in Context::build_sell_cols).
 template <int BS>
 __global__ void __launch_bounds__(BS) k_sell_range(const SellPlan S, GatherPlain g, double* __restrict__ out) {

@@ -127,6 +127,8 @@ struct IterParams {
   int use_sell_c;      // k_spmv_cols_sell instead of k_spmv_cols
   SellPlan sell_r;     // SELL-G copy of A for the row product (same sums as CSR-G)
   int use_sell_r;      // k_spmv_rows_sellg instead of k_spmv_rows
+  SellPlan sell_cg;    // SELL-G copy of A' (same sums as CSR-G), when SELL-32 is not used
+  int use_sell_cg;     // k_spmv_cols_sellg
   // unscaled problem data and Ruiz factors
   const double *c, *l, *u, *b, *r, *s;
   // state

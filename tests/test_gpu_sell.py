@@ -79,8 +79,9 @@ def test_sell_rerun_identical_and_close_to_csr(name, lp, monkeypatch):
     assert rel(a.iterate.x, c.iterate.x) <= 1e-9 and rel(a.iterate.y, c.iterate.y) <= 1e-9
 
 
-# ---- SELL-G row product (k_spmv_rows_sellg): chosen by timing, so it must be
-# bit-identical to the CSR-G row kernel; CCLP_CU_SELL_ROWS=2 forces it.
+# ---- SELL-G products (k_spmv_rows_sellg, k_spmv_cols_sellg): chosen by
+# timing, so they must be bit-identical to the CSR-G kernels;
+# CCLP_CU_SELL_ROWS=2 / CCLP_CU_SELLG_COLS=2 force them.
 
 def _long_rows_lp():
     from test_gpu_longrows import dense_rows_lp
@@ -93,8 +94,10 @@ def test_sellg_rows_bit_identical_to_csr(name, monkeypatch):
     cfg = PdhgConfig(max_iterations=150)
     monkeypatch.setenv("CCLP_CU_SELL", "0")
     monkeypatch.setenv("CCLP_CU_SELL_ROWS", "0")
+    monkeypatch.setenv("CCLP_CU_SELLG_COLS", "0")
     a = run_pdhg(lp, cfg)
     monkeypatch.setenv("CCLP_CU_SELL_ROWS", "2")
+    monkeypatch.setenv("CCLP_CU_SELLG_COLS", "2")  # both sides in SELL-G slices
     b = run_pdhg(lp, cfg)
     sh = run_pdhg_sharded(lp, 2, cfg)
     assert a.iterations == b.iterations == sh.iterations
