@@ -169,6 +169,16 @@ int cclp_cu_matvec_transpose(cclp_cu_ctx* ctx, const double* y, double* out);
  * reduced in a fixed order (within rounding of the reference's); maxima exact. */
 int cclp_cu_relative_report(cclp_cu_ctx* ctx, const double* x, const double* y, const double* z,
                             cclp_cu_report* out, double* abs_violation);
+/* Crossover pricing (simplex.cpp:266-296, price()) on the device for the
+ * EngineModel of the context's equality-form LP: n structural columns then
+ * m logical ones (basis.hpp:30-58). status[n+m] holds ColStatus chars
+ * ('B','L','U','X','Z'), skip[n+m] (optional) nonzero for the skip set,
+ * y[m] the duals. d_j = cost_j - column_dot(j, y) in column_dot's own order;
+ * returns the reference's pick: entering column (-1: none), direction (+1 /
+ * -1) and violation (Dantzig: largest, first index on ties; bland != 0:
+ * first violating index). */
+int cclp_cu_price(cclp_cu_ctx* ctx, const double* y, const char* status, const uint8_t* skip, int32_t phase1,
+                  double dtol, int32_t bland, int64_t* entering, int32_t* direction, double* violation);
 /* ruiz_scale factors (scaling.cpp:46-90): row_scale[m], col_scale[n]. */
 int cclp_cu_ruiz(cclp_cu_ctx* ctx, int32_t iterations, double* row_scale, double* col_scale);
 /* estimate_matrix_norm (pdhg.cpp:46-65) on the unscaled A. */

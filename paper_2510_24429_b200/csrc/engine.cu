@@ -414,6 +414,8 @@ struct Context {
   void build_sell_rows();
   void build_sellg(bool rows_side);
   void relative_report(const double* x, const double* y, const double* z, double* rep, double* abs_viol);
+  void price(const double* y, const char* status, const unsigned char* skip, int phase1, double dtol, int bland,
+             long long* entering, int* direction, double* violation);
   // SpMV geometry tuning folded into the first power iterations (results are
   // geometry-independent, so the candidates can do real work): both start
   // tables stay alive until the choice is made.
@@ -1232,6 +1234,33 @@ void Context::build_sellg(bool rows_side) {
   k_sellg_fill<<<blocks_for(static_cast<long long>(nsl) * 32), kBlock, 0, stream>>>(
       ptr, idx, sval, cnt, thr, nsl, G, S.off, S.idx, S.val);
   CKL("sellg fill");
+}
+
+// price() (simplex.cpp:266-296) on the device: see k_price.
+void Context::price(const double* y_in, const char* status, const unsigned char* skip, int phase1, double dtol,
+                    int bland, long long* entering, int* direction, double* violation) {
+  if (!rows_equality) throw std::invalid_argument("price: LP must be in equality form");
+  const long long total = static_cast<long long>(n) + m;
+  const int grid = static_cast<int>(std::max<long long>(1, std::min<long long>(148 * 8, (total + kBlock - 1) / kBlock)));
+  char* d_status = alloc<char>(static_cast<size_t>(std::max<long long>(total, 1)));
+  unsigned char* d_skip = skip ? alloc<unsigned char>(static_cast<size_t>(std::max<long long>(total, 1))) : nullptr;
+  PriceCand* part = alloc<PriceCand>(static_cast<size_t>(grid) + 1);
+  h2d(wm, y_in, sizeof(double) * m);
+  h2d(d_status, status, static_cast<size_t>(total));
+  if (skip) h2d(d_skip, skip, static_cast<size_t>(total));
+  k_price<<<grid, kBlock, 0, stream>>>(n, m, colptr, rowind, val_csc, c, wm, d_status, d_skip, phase1, dtol,
+                                       bland, part);
+  k_price_finish<<<1, 1, 0, stream>>>(part, grid, bland, part + grid);
+  CKL("price");
+  PriceCand out;
+  CK(cudaMemcpyAsync(&out, part + grid, sizeof(out), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  release(d_status);
+  release(d_skip);
+  release(part);
+  *entering = out.j;
+  *direction = out.dir;
+  *violation = out.viol;
 }
 
 // relative_report + absolute_violation (kkt.cpp:106-149) of a host iterate
@@ -2171,6 +2200,19 @@ int cclp_cu_relative_report(cclp_cu_ctx* ctx, const double* x, const double* y, 
     double rep[cclp_cu::kRepN];
     C.relative_report(x, y, z, rep, abs_violation);
     copy_report(rep, out);
+  });
+}
+
+int cclp_cu_price(cclp_cu_ctx* ctx, const double* y, const char* status, const uint8_t* skip, int32_t phase1,
+                  double dtol, int32_t bland, int64_t* entering, int32_t* direction, double* violation) {
+  return guarded([&] {
+    Context& C = ctx->c;
+    CK(cudaSetDevice(C.device));
+    long long e = -1;
+    int d = 0;
+    C.price(y, status, skip, phase1, dtol, bland, &e, &d, violation);
+    *entering = e;
+    *direction = d;
   });
 }
 

@@ -563,3 +563,94 @@ __global__ void k_sellg_fill(const int* __restrict__ ptr, const int* __restrict_
 }
 
 }  // namespace cclp_cu
+
+// ---------------------------------------------------------------------------
+// Crossover pricing on the device: the reference's price()
+// (simplex.cpp:266-296) over the EngineModel's n structural + m logical
+// columns. d_j = cost_j - column_dot(j, y) with column_dot's own sequential
+// order (basis.cpp:35-42; a logical column j >= n has column_dot = y[j-n]),
+// then the same status tests; the pick is the largest violation, first
+// index on ties (the reference's strict '>'), or with Bland's rule the first
+// violating index. Block candidates are combined by the same total order, so
+// the pick is the reference's.
+// ---------------------------------------------------------------------------
+namespace cclp_cu {
+
+struct PriceCand {
+  double viol;
+  long long j;  // -1: none
+  int dir;
+};
+
+__device__ __forceinline__ bool price_better(const PriceCand& a, const PriceCand& b, int bland) {
+  if (a.j < 0) return false;
+  if (b.j < 0) return true;
+  if (bland) return a.j < b.j;
+  return a.viol > b.viol || (a.viol == b.viol && a.j < b.j);
+}
+
+__global__ void __launch_bounds__(kBlock) k_price(int n, int m, const int* __restrict__ colptr,
+                                                  const int* __restrict__ rowind, const double* __restrict__ val,
+                                                  const double* __restrict__ c, const double* __restrict__ y,
+                                                  const char* __restrict__ status, const unsigned char* __restrict__ skip,
+                                                  int phase1, double dtol, int bland, PriceCand* part) {
+  PriceCand best{0.0, -1, 0};
+  const long long total = static_cast<long long>(n) + m;
+  for (long long j = blockIdx.x * static_cast<long long>(kBlock) + threadIdx.x; j < total;
+       j += static_cast<long long>(gridDim.x) * kBlock) {
+    const char st = status[j];
+    if (st == 'B' || st == 'X') continue;
+    if (skip != nullptr && skip[j]) continue;
+    double dot;
+    if (j >= n) {
+      dot = y[j - n];
+    } else {
+      dot = 0.0;  // column_dot: acc += value * v[row], ascending position
+      for (int p = colptr[j]; p < colptr[j + 1]; ++p) dot = dot + val[p] * y[rowind[p]];
+    }
+    const double cost = phase1 ? 0.0 : (j < n ? c[j] : 0.0);
+    const double d = cost - dot;
+    double viol = 0.0;
+    int dir = 0;
+    if (st == 'L' && d < -dtol) {
+      viol = -d;
+      dir = 1;
+    } else if (st == 'U' && d > dtol) {
+      viol = d;
+      dir = -1;
+    } else if (st == 'Z' && fabs(d) > dtol) {
+      viol = fabs(d);
+      dir = d < 0.0 ? 1 : -1;
+    } else {
+      continue;
+    }
+    const PriceCand cand{viol, j, dir};
+    if (price_better(cand, best, bland)) best = cand;
+  }
+  // block: warp shuffles, then warp 0 over the warps (the order is total)
+  for (int off = 16; off > 0; off >>= 1) {
+    PriceCand o;
+    o.viol = __shfl_down_sync(0xffffffffu, best.viol, off);
+    o.j = __shfl_down_sync(0xffffffffu, best.j, off);
+    o.dir = __shfl_down_sync(0xffffffffu, best.dir, off);
+    if (price_better(o, best, bland)) best = o;
+  }
+  __shared__ PriceCand wb[kBlock / 32];
+  if ((threadIdx.x & 31) == 0) wb[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    PriceCand b = wb[0];
+    for (int w = 1; w < kBlock / 32; ++w)
+      if (price_better(wb[w], b, bland)) b = wb[w];
+    part[blockIdx.x] = b;
+  }
+}
+
+__global__ void k_price_finish(const PriceCand* __restrict__ part, int nblocks, int bland, PriceCand* out) {
+  PriceCand b{0.0, -1, 0};
+  for (int k = 0; k < nblocks; ++k)
+    if (price_better(part[k], b, bland)) b = part[k];
+  *out = b;
+}
+
+}  // namespace cclp_cu

@@ -109,6 +109,9 @@ def load_library(path: str = LIB_PATH):
         L.cclp_cu_default_tolerances.argtypes = [C.POINTER(_Tol)]
         L.cclp_cu_create.argtypes = [C.POINTER(_LP), C.c_int, C.POINTER(C.c_void_p)]
         L.cclp_cu_destroy.argtypes = [C.c_void_p]
+        L.cclp_cu_price.argtypes = [C.c_void_p, _dp, C.c_char_p, C.c_void_p, C.c_int32, C.c_double,
+                                     C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_double)]
         L.cclp_cu_relative_report.argtypes = [C.c_void_p, _dp, _dp, _dp, C.POINTER(_Report),
                                                C.POINTER(C.c_double)]
         L.cclp_cu_create_from_file.argtypes = [C.c_char_p, C.c_int, C.POINTER(C.c_void_p),
@@ -154,7 +157,7 @@ EXPORTED_SYMBOLS = [
     "cclp_cu_nccl_unique_id", "cclp_cu_sharded_create", "cclp_cu_sharded_solve",
     "cclp_cu_sharded_begin", "cclp_cu_sharded_advance", "cclp_cu_sharded_describe",
     "cclp_cu_sharded_destroy", "cclp_cu_sharded_create_hostcomm", "cclp_cu_create_from_file",
-    "cclp_cu_relative_report",
+    "cclp_cu_relative_report", "cclp_cu_price",
 ]
 
 
@@ -344,6 +347,21 @@ class Engine:
         _check(self.L, self.L.cclp_cu_relative_report(self.ctx, *(a.ctypes.data_as(_dp) for a in xs),
                                                       C.byref(rep), C.byref(av)))
         return ResidualReport(**{f: getattr(rep, f) for f in REPORT_FIELDS}), av.value
+
+    def price(self, y, status, skip=None, phase1: bool = False, dtol: float = 1e-9, bland: bool = False):
+        """price() of the reference's simplex (simplex.cpp:266-296) on the
+        device. `status`: n+m ColStatus chars (bytes or str) over the
+        structural then logical columns; `skip`: optional n+m booleans.
+        Returns (entering or -1, direction, violation)."""
+        yv = np.ascontiguousarray(y, np.float64)
+        st = status.encode() if isinstance(status, str) else bytes(status)
+        sk = None if skip is None else np.ascontiguousarray(skip, np.uint8)
+        e, d, v = C.c_int64(), C.c_int32(), C.c_double()
+        _check(self.L, self.L.cclp_cu_price(self.ctx, yv.ctypes.data_as(_dp), st,
+                                            None if sk is None else sk.ctypes.data_as(C.c_void_p),
+                                            int(phase1), dtol, int(bland), C.byref(e), C.byref(d),
+                                            C.byref(v)))
+        return int(e.value), int(d.value), float(v.value)
 
     def close(self) -> None:
         if self.ctx:
