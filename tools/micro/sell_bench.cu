@@ -225,7 +225,7 @@ int main(int argc, char** argv) {
     char nm[64];
 #define C1(GG, UU) if (G == GG) { snprintf(nm, sizeof nm, "csr1 G%d U%d x%d", GG, UU, per); \
       run(nm, false, [&] { v_csr1<GG, UU><<<grid, 1024>>>(dst, dp, di, dv, dx, dy); }); }
-    C1(4, 2) C1(4, 3) C1(4, 4) C1(4, 6) C1(4, 8) C1(8, 2) C1(8, 4) C1(8, 6) C1(8, 7) C1(8, 8) C1(16, 2) C1(16, 3) C1(16, 4)
+    C1(2, 4) C1(2, 8) C1(4, 2) C1(4, 3) C1(4, 4) C1(4, 6) C1(4, 8) C1(8, 2) C1(8, 4) C1(8, 6) C1(8, 7) C1(8, 8) C1(16, 2) C1(16, 3) C1(16, 4)
     for (bool f : {false, true}) {
       snprintf(nm, sizeof nm, "csr G%d U2 rpg2 x%d", G, per);
       if (G == 4) run(nm, f, [&] { v_csr2<4, 2><<<grid, 1024>>>(dst, dp, di, dv, dx, dy); });
@@ -264,6 +264,7 @@ int main(int argc, char** argv) {
 #define SG(GG, UU, PP) \
       if (G == GG) { snprintf(nm, sizeof nm, "sellG%d U%d%s bs%d g%d", GG, UU, PP ? " pipe" : "", bs, grid); \
         run(nm, false, [&] { v_sellg<GG, UU, PP><<<grid, bs>>>(nsl, d_off, d_w, d_plen, d_si, d_sv, dx, dy, m); }); }
+      SG(2, 2, false) SG(2, 4, false) SG(2, 8, false)
       SG(4, 2, false) SG(4, 4, false) SG(4, 2, true) SG(4, 4, true)
       SG(8, 2, false) SG(8, 4, false) SG(8, 2, true)
       SG(16, 2, false) SG(16, 2, true)
@@ -274,6 +275,7 @@ int main(int argc, char** argv) {
     int* dst; const int grid = sms; std::vector<int> st(grid + 1);
     for (int b = 0; b <= grid; ++b) st[b] = (int)((long long)m * b / grid);
     CK(cudaMalloc(&dst, 4 * (grid + 1))); CK(cudaMemcpy(dst, st.data(), 4 * (grid + 1), cudaMemcpyHostToDevice));
+    if (G == 2) v_csr2<2, 2><<<grid, 1024>>>(dst, dp, di, dv, dx, dy);
     if (G == 4) v_csr2<4, 2><<<grid, 1024>>>(dst, dp, di, dv, dx, dy);
     if (G == 8) v_csr2<8, 2><<<grid, 1024>>>(dst, dp, di, dv, dx, dy);
     if (G == 16) v_csr2<16, 2><<<grid, 1024>>>(dst, dp, di, dv, dx, dy);
