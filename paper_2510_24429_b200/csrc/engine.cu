@@ -1046,11 +1046,44 @@ void Context::build_sell_cols() {
       };
       CKL("sell tune");
       const float t_big = time_it(kSpmvBlock), t_small = time_it(256);
-      if (t_small < 0.97f * t_big) {
-        release(sell_start);
+      // and the grid-stride deal (no start table) on 1024-thread blocks
+      int* keep_big = sell_start;
+      S.start = nullptr;
+      float t_gs;
+      {
+        std::vector<float> t;
+        for (int rep = 0; rep < 4; ++rep) {
+          CK(cudaEventRecord(ev_a, stream));
+          k_sell_range<kSpmvBlock><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(S, GatherPlain{gy}, wn);
+          CK(cudaEventRecord(ev_b, stream));
+          CK(cudaEventSynchronize(ev_b));
+          float ms = 0;
+          CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
+          if (rep > 0) t.push_back(ms);
+        }
+        std::sort(t.begin(), t.end());
+        t_gs = t[t.size() / 2];
+      }
+      const char* fm = std::getenv("CCLP_CU_SELL_MODE");  // A/B: contig | small | gs
+      int mode = 0;  // 0 contiguous 1024, 1 contiguous 256, 2 grid-stride 1024
+      if (fm != nullptr) {
+        mode = std::string(fm) == "small" ? 1 : (std::string(fm) == "gs" ? 2 : 0);
+      } else {
+        float best = t_big;
+        if (t_small < 0.97f * best) { mode = 1; best = t_small; }
+        if (t_gs < 0.97f * best) mode = 2;
+      }
+      if (mode == 1) {
+        release(keep_big);
         sell_start = alt;
         sell_bs = 256;
         sell_grid = 4 * spmv_grid_c;
+      } else if (mode == 2) {
+        release(keep_big);
+        release(alt);
+        sell_start = nullptr;
+        sell_bs = kSpmvBlock;
+        sell_grid = spmv_grid_c;
       } else {
         release(alt);
       }

@@ -481,9 +481,20 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows(const IterParams p, in
 template <class Gather>
 __device__ __forceinline__ void sell_block(const SellPlan& S, const Gather& g, double* __restrict__ out) {
   constexpr int U = 4;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int sb = S.start[blockIdx.x], se = S.start[blockIdx.x + 1];
-  for (int s = sb + warp; s < se; s += nw) {
+  const int lane = threadIdx.x & 31;
+  // block-contiguous slice ranges (S.start), or, with S.start == nullptr,
+  // slices dealt round-robin over every warp of the grid
+  int s0, se, step;
+  if (S.start != nullptr) {
+    s0 = S.start[blockIdx.x] + static_cast<int>(threadIdx.x >> 5);
+    se = S.start[blockIdx.x + 1];
+    step = static_cast<int>(blockDim.x >> 5);
+  } else {
+    s0 = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    se = (S.n + 31) / 32;
+    step = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+  }
+  for (int s = s0; s < se; s += step) {
     const long long off = S.off[s];
     const int w = static_cast<int>((S.off[s + 1] - off) >> 5);
     const int j = s * 32 + lane;

@@ -59,7 +59,11 @@ def test_sell_equal_iteration_parity(name, lp, iters, oracle):
 
 @pytest.mark.parametrize("name,lp", lps())
 @pytest.mark.parametrize("P", [2, 3])
-def test_sell_sharded_bit_identical(name, lp, P):
+@pytest.mark.parametrize("mode", ["contig", "small", "gs"])
+def test_sell_sharded_bit_identical(name, lp, P, mode, monkeypatch):
+    """Every slice-to-warp deal (block-contiguous 1024 / 256, grid-stride)
+    gives the same sums: shards and one device agree bit for bit."""
+    monkeypatch.setenv("CCLP_CU_SELL_MODE", mode)
     cfg = PdhgConfig(max_iterations=200)
     one = run_pdhg(lp, cfg)
     sh = run_pdhg_sharded(lp, P, cfg)
