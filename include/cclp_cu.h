@@ -22,11 +22,16 @@
  *    std::invalid_argument (pdhg.cpp:235-244); CCLP_CU_ECUDA / CCLP_CU_ENOMEM on
  *    device failure. A non-finite iterate is NOT an error: it is stop reason
  *    CCLP_CU_STOP_NUMERICAL_ERROR with error_iteration set (pdhg.cpp:369-376).
- *  - The snapshot sink runs synchronously on the calling thread with pointers
- *    valid only for the duration of the call (pdhg.cpp:346-358).
- *  - cancel is polled (relaxed) between device batches, so a cancel is seen
- *    within `poll_interval` iterations (reference: every iteration).
- *  - One context per host thread; a context is not thread-safe.
+ *  - The snapshot sink runs on the calling thread with pointers valid only
+ *    for the duration of the call (pdhg.cpp:346-358). The snapshot is the
+ *    reference's (same iterate, threshold, maxresid, iteration); it is taken
+ *    by the iteration kernels into a device slot and copied out on a side
+ *    stream, so the device keeps iterating while the sink runs.
+ *  - cancel is polled every iteration (pdhg.cpp:301): the host loop mirrors
+ *    the caller's byte into device-mapped memory that the kernels read, so the
+ *    loop stops within one iteration of the host seeing the flag.
+ *  - One context per host thread; a context is not thread-safe (except
+ *    cclp_cu_request_cancel).
  */
 #ifndef CCLP_CU_H_
 #define CCLP_CU_H_
@@ -152,6 +157,12 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg, const cclp_cu_tol
                   const volatile uint8_t* cancel, cclp_cu_log_fn log, void* log_user,
                   double* x_out, double* y_out, double* z_out, cclp_cu_result* res);
 
+/* Asks a running cclp_cu_solve on `ctx` to stop (stop reason CANCELLED) at
+ * the next iteration, exactly as setting its cancel byte would. Safe to call
+ * from any thread, including from inside the snapshot sink (the C++ drop-in
+ * uses it to stop the loop when the sink throws, then rethrows). */
+int cclp_cu_request_cancel(cclp_cu_ctx* ctx);
+
 /* One-shot drop-in: create + solve + destroy. */
 int cclp_cu_run_pdhg(const cclp_cu_lp* lp, const cclp_cu_config* cfg, const cclp_cu_tolerances* tol,
                      const double* thresholds, int32_t nthr, cclp_cu_sink_fn sink, void* sink_user,
@@ -251,6 +262,9 @@ int cclp_cu_sharded_advance(cclp_cu_sharded* ctx, int64_t iters, double* device_
  * doubles per iteration summed over shards */
 int cclp_cu_sharded_describe(cclp_cu_sharded* ctx, int64_t* out, int32_t nout);
 int cclp_cu_sharded_destroy(cclp_cu_sharded* ctx);
+/* As cclp_cu_request_cancel for a running cclp_cu_sharded_solve (seen at the
+ * next batch boundary, agreed by every rank). */
+int cclp_cu_sharded_request_cancel(cclp_cu_sharded* ctx);
 /* The nnz-balanced split used for the shards (host only): part b starts at
  * the first i with ptr[i] + 4 i >= (ptr[rows] + 4 rows) b / parts. */
 int cclp_cu_partition(const int32_t* ptr, int32_t rows, int32_t parts, int32_t* bounds);

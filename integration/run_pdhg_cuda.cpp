@@ -10,15 +10,18 @@
 //     non-decreasing thresholds (pdhg.cpp:235-244);
 //   * a non-finite iterate is stop reason kNumericalError with
 //     error_iteration, not an exception (pdhg.cpp:369-376);
-//   * the sink runs synchronously on the calling thread (pdhg.cpp:346-358);
-//   * cancel is polled with a relaxed load (pdhg.cpp:301), here between
-//     device batches.
+//   * the sink runs on the calling thread (pdhg.cpp:346-358) while the device
+//     keeps iterating; an exception it throws stops the loop at the next
+//     iteration (cclp_cu_request_cancel) and propagates unchanged out of
+//     run_pdhg, as the reference's synchronous call would;
+//   * cancel is polled with a relaxed load every iteration (pdhg.cpp:301).
 // oracle/Makefile's `dropin` target builds the reference's own test_pdhg.cpp
 // against this file (tests/test_dropin.py runs it on the GPU).
 #include <atomic>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <ostream>
 #include <stdexcept>
 #include <string>
@@ -34,11 +37,24 @@ namespace {
 struct SinkBridge {
   const SnapshotSink* sink;
   Index m, n;
+  cclp_cu_ctx* ctx = nullptr;
+  std::exception_ptr error;  // the sink's exception, rethrown after the solve
 };
+
+void sink_call(SinkBridge* b, const cclp_cu_snapshot* s);
 
 void sink_trampoline(const cclp_cu_snapshot* s, void* user) {
   auto* b = static_cast<SinkBridge*>(user);
-  if (b->sink == nullptr || !*b->sink) return;
+  if (b->sink == nullptr || !*b->sink || b->error) return;
+  try {
+    sink_call(b, s);
+  } catch (...) {  // never unwind through the C ABI
+    b->error = std::current_exception();
+    cclp_cu_request_cancel(b->ctx);
+  }
+}
+
+void sink_call(SinkBridge* b, const cclp_cu_snapshot* s) {
   PdhgSnapshot snap;
   snap.iterate.x = Vector(b->n);
   snap.iterate.y = Vector(b->m);
@@ -107,12 +123,14 @@ PdhgResult run_pdhg(const LinearProgram& std_lp, const PdhgConfig& config, const
   cclp_cu_ctx* ctx = nullptr;
   int rc = cclp_cu_create(&lp, device, &ctx);
   if (rc == CCLP_CU_OK) {
+    bridge.ctx = ctx;
     rc = cclp_cu_solve(ctx, &cfg, &t, thresholds.data(), static_cast<int32_t>(thresholds.size()),
                        &sink_trampoline, &bridge, cancel_byte,
                        config.log != nullptr ? &log_trampoline : nullptr, config.log, x.data(),
                        y.data(), z.data(), &res);
     cclp_cu_destroy(ctx);
   }
+  if (bridge.error) std::rethrow_exception(bridge.error);
   if (rc == CCLP_CU_EINVAL) throw std::invalid_argument(cclp_cu_last_error());
   if (rc != CCLP_CU_OK) throw std::runtime_error(std::string("cclp_cu: ") + cclp_cu_last_error());
 

@@ -17,6 +17,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <climits>
+#include <condition_variable>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -182,6 +185,41 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
   for (auto& t : th) t.join();
 }
 
+// The CSC checks of LinearProgram::validate (lp.cpp:71-83) that guard memory
+// safety: colptr[0] == 0, non-decreasing offsets, 0 <= row < m, rows strictly
+// ascending within a column. Same messages; host threads over column ranges.
+void validate_csc(const cclp_cu_lp* lp) {
+  const int m = lp->m, n = lp->n;
+  const int32_t* cp = lp->colptr;
+  const int32_t* ri = lp->rowind;
+  if (cp[0] != 0) throw std::invalid_argument("colptr[0] != 0");
+  for (int j = 0; j < n; ++j)
+    if (cp[j] > cp[j + 1]) throw std::invalid_argument("decreasing column offsets");
+  const long long nnz = cp[n];
+  if (nnz > 0 && ri == nullptr) throw std::invalid_argument("null row indices");
+  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  const unsigned T = nnz < (1LL << 20) ? 1u : hw;
+  std::vector<int> bad(T, 0);
+  auto work = [&](unsigned t) {
+    const int j0 = static_cast<int>(static_cast<long long>(n) * t / T);
+    const int j1 = static_cast<int>(static_cast<long long>(n) * (t + 1) / T);
+    for (int j = j0; j < j1 && !bad[t]; ++j)
+      for (int q = cp[j]; q < cp[j + 1]; ++q) {
+        const int i = ri[q];
+        if (i < 0 || i >= m) { bad[t] = 1; break; }
+        if (q > cp[j] && i <= ri[q - 1]) { bad[t] = 2; break; }
+      }
+  };
+  std::vector<std::thread> th;
+  for (unsigned t = 1; t < T; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  for (int b : bad) {
+    if (b == 1) throw std::invalid_argument("row index out of range");
+    if (b == 2) throw std::invalid_argument("unsorted or duplicate row indices");
+  }
+}
+
 template <class F>
 void with_group(int G, F&& f) {
   switch (G) {
@@ -293,6 +331,23 @@ struct Context {
   // outputs (device views) + pinned staging for snapshots
   double *vx = nullptr, *vy = nullptr, *vz = nullptr, *vrep = nullptr;
   double *h_sx = nullptr, *h_sy = nullptr, *h_sz = nullptr;
+  // inline ladder snapshots: kSnapSlots device slots of x | z (n each) | y (m)
+  double* snap_buf[kSnapSlots] = {};
+  // host flags in pinned, device-mapped memory: [0] cancel request (mirrored
+  // from the caller's flag by the host loop, read by the kernels every
+  // iteration), [1] snapshots copied out by the host
+  unsigned* h_flags = nullptr;
+  const unsigned* d_flags = nullptr;
+  unsigned* cancel_dev = nullptr;
+  std::atomic<int> abort_req{0};  // cclp_cu_request_cancel (any thread)
+  void ensure_flags() {
+    if (h_flags) return;
+    h_flags = host_alloc<unsigned>(16);
+    std::memset(h_flags, 0, 16 * sizeof(unsigned));
+    void* dp = nullptr;
+    CK(cudaHostGetDevicePointer(&dp, h_flags, 0));
+    d_flags = static_cast<const unsigned*>(dp);
+  }
   cudaEvent_t ev_snap = nullptr, ev_a = nullptr, ev_b = nullptr;
   // graph
   cudaGraphExec_t graph = nullptr;
@@ -485,7 +540,9 @@ Context::~Context() {
                     vz, vrep, plan_rows.seg, plan_rows.lr_first, plan_rows.part, plan_rows.cnt,
                     plan_cols.seg, plan_cols.lr_first, plan_cols.part, plan_cols.cnt, x_full, y_full,
                     xpart, vparts, push_flags, push_counter, sell_off, sell_start, sell_idx, sell_val,
-                    sgr.off, sgr.start, sgr.idx, sgr.val, sgc.off, sgc.start, sgc.idx, sgc.val};
+                    sgr.off, sgr.start, sgr.idx, sgr.val, sgc.off, sgc.start, sgc.idx, sgc.val,
+                    cancel_dev, snap_buf[0], snap_buf[1]};
+    static_assert(kSnapSlots == 2, "release list");
     for (void* p : ptrs) release(p);
     for (int k = 0; k < 3; ++k)
       for (int q = 0; q < 2; ++q) release(xc[k][q]);
@@ -1841,6 +1898,29 @@ void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& to
     CK(cudaMemcpyAsync(x_full + static_cast<size_t>(shard_rank) * Sn, xc[0][0], sizeof(double) * n,
                        cudaMemcpyDeviceToDevice, stream));
   }
+  // inline snapshots and the per-iteration cancel (single device only: the
+  // sharded solve halts for snapshots and agrees on stops on the host)
+  const bool single = !(shard_count > 1 || x_full != nullptr);
+  p.snap_inline = 0;
+  p.host_flags = nullptr;
+  p.cancel_dev = nullptr;
+  for (int k = 0; k < kSnapSlots; ++k) p.snap_x[k] = p.snap_y[k] = p.snap_z[k] = nullptr;
+  if (single) {
+    ensure_flags();
+    if (!cancel_dev) cancel_dev = alloc<unsigned>(1);
+    CK(cudaMemsetAsync(cancel_dev, 0, sizeof(unsigned), stream));
+    p.host_flags = d_flags;
+    p.cancel_dev = cancel_dev;
+    if (nthr > 0) {
+      for (int k = 0; k < kSnapSlots; ++k) {
+        if (!snap_buf[k]) snap_buf[k] = alloc<double>(2 * static_cast<size_t>(n) + m);
+        p.snap_x[k] = snap_buf[k];
+        p.snap_z[k] = snap_buf[k] + n;
+        p.snap_y[k] = snap_buf[k] + 2 * static_cast<size_t>(n);
+      }
+      p.snap_inline = 1;
+    }
+  }
   // initial products and check(0)
   if (launch_init) launch_iteration(true);
   if (graph) {
@@ -2002,6 +2082,7 @@ int cclp_cu_create(const cclp_cu_lp* lp, int device, cclp_cu_ctx** out) {
   return guarded([&] {
     if (lp == nullptr || lp->m < 0 || lp->n < 0 || lp->colptr == nullptr)
       throw std::invalid_argument("cclp_cu_create: bad LP");
+    cclp_cu::validate_csc(lp);  // before any device work
     cclp_cu::ck(cudaSetDevice(device), "cudaSetDevice");
     auto* ctx = new cclp_cu_ctx();
     ctx->c.device = device;
@@ -2038,11 +2119,11 @@ int cclp_cu_create_from_file(const char* path, int device, cclp_cu_ctx** out, in
     const int32_t m = mn[0], n = mn[1];
     if (m < 0 || n < 0 || nnz < 0) throw std::invalid_argument("cclp_cu_create_from_file: bad header");
     size_t off = 32;
-    auto take = [&](size_t bytes) {
+    auto take = [&](size_t bytes) {  // exact bound: the array ends inside the file
       const char* p = base + off;
+      if (off + bytes > len) throw std::invalid_argument("cclp_cu_create_from_file: truncated file");
       off += bytes;
       off = (off + 7) / 8 * 8;
-      if (off > len + 7) throw std::invalid_argument("cclp_cu_create_from_file: truncated file");
       return p;
     };
     cclp_cu_lp lp;
@@ -2077,6 +2158,8 @@ int cclp_cu_begin(cclp_cu_ctx* ctx, const cclp_cu_config* cfg, const cclp_cu_tol
     cclp_cu::ck(cudaSetDevice(ctx->c.device), "cudaSetDevice");
     validate_inputs(ctx, *cfg, *tol, nullptr, 0);
     cclp_cu_tolerances t = *tol;
+    ctx->c.ensure_flags();
+    ctx->c.h_flags[0] = ctx->c.h_flags[1] = 0u;
     ctx->c.begin(*cfg, t, nullptr, 0);
     // measurement mode: never converge, never hit the limit
     ctx->c.params.eps_rel = -1.0;
@@ -2302,104 +2385,236 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
       std::thread& t;
       ~JoinOnExit() { if (t.joinable()) t.join(); }
     } prefault_join{prefault};
+    const int k = cfg.poll_interval > 0 ? cfg.poll_interval : 64;
+    // the log ring holds two batches in flight (at most one line per iteration)
+    if (cfg.log_interval > 0 && C.log_cap < 4 * k) {
+      C.release(C.log);
+      C.log = nullptr;
+      C.log_cap = 4 * k;
+      C.h_log = C.host_alloc<cclp_cu::LogEntry>(C.log_cap);
+      C.log = C.alloc<cclp_cu::LogEntry>(C.log_cap);
+    }
+    // cancel: the caller's flag (and cclp_cu_request_cancel) mirrored into
+    // mapped memory that k_primal reads every iteration (pdhg.cpp:301)
+    C.ensure_flags();
+    C.abort_req.store(0);
+    volatile unsigned* hf = C.h_flags;
+    auto mirror_cancel = [&]() {
+      if ((cancel != nullptr && *cancel) || C.abort_req.load(std::memory_order_relaxed)) hf[0] = 1u;
+    };
+    hf[0] = 0u;
+    hf[1] = 0u;
+    mirror_cancel();
     C.begin(cfg, *tol, thresholds, nthr);
     const double setup_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
-    const int k = cfg.poll_interval > 0 ? cfg.poll_interval : 64;
     C.build_graph(k);
     C.mark(8);
     CK(cudaEventRecord(C.ev_a, C.stream));
 
+    // ---- host side of the loop ------------------------------------------
+    // A launcher thread keeps two graph batches in flight (the device never
+    // waits for the host between batches), mirrors the cancel flag, and
+    // copies ladder snapshots out of their device slots on the side stream;
+    // the calling thread receives log lines and snapshots through a queue, in
+    // iteration order, and runs the caller's log and sink callbacks
+    // (pdhg.cpp:332-358) while the device keeps iterating.
+    struct Event {
+      int kind;  // 0 log line, 1 snapshot (staging set `set`), 2 end of loop
+      long long iteration;
+      std::string line;
+      int set = 0, thr_idx = 0, use_avg = 0;
+      double maxresid = 0.0;
+    };
+    std::mutex mu;
+    std::condition_variable cv;
+    std::deque<Event> events;
+    bool staging_busy[3] = {false, false, false};  // 0,1: slot snapshots; 2: host-extracted
+    std::exception_ptr launcher_error;
     Ctrl st;
-    C.fetch_ctrl(&st);
-    long long log_seen = 0;
-    auto flush_log = [&](const Ctrl& q) {
-      if (!logfn || cfg.log_interval <= 0) {
-        log_seen = q.log_count;
-        return;
-      }
-      if (q.log_count == log_seen) return;
-      CK(cudaMemcpy(C.h_log, C.log, sizeof(cclp_cu::LogEntry) * C.log_cap, cudaMemcpyDeviceToHost));
-      for (long long i = std::max(log_seen, q.log_count - C.log_cap); i < q.log_count; ++i) {
-        const auto& e = C.h_log[i % C.log_cap];
-        char line[160];
-        std::snprintf(line, sizeof line, "%lld\t%.6e\t%.6e\t%.6e\t%.3f\n", e.iteration,
-                      e.rel_primal, e.rel_dual, e.rel_gap, e.elapsed);
-        logfn(line, log_user);
-      }
-      log_seen = q.log_count;
+    auto push = [&](Event e) {
+      std::lock_guard<std::mutex> g(mu);
+      events.push_back(std::move(e));
+      cv.notify_all();
     };
-    auto emit_snapshot = [&](const Ctrl& q) {
-      // PdhgSnapshot of the better view (pdhg.cpp:346-358)
-      C.extract_view(q.snap_use_avg ? cclp_cu::kViewAvg : cclp_cu::kViewCur, q);
-      if (!C.h_sx) {
-        C.h_sx = C.host_alloc<double>(C.n);
-        C.h_sz = C.host_alloc<double>(C.n);
-        C.h_sy = C.host_alloc<double>(C.m);
-      }
-      CK(cudaEventRecord(C.ev_snap, C.stream));
-      CK(cudaStreamWaitEvent(C.side, C.ev_snap, 0));
-      CK(cudaMemcpyAsync(C.h_sx, C.vx, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.side));
-      CK(cudaMemcpyAsync(C.h_sy, C.vy, sizeof(double) * C.m, cudaMemcpyDeviceToHost, C.side));
-      CK(cudaMemcpyAsync(C.h_sz, C.vz, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.side));
-      CK(cudaStreamSynchronize(C.side));
-      if (sink) {
-        cclp_cu_snapshot sp;
-        sp.x = C.h_sx;
-        sp.y = C.h_sy;
-        sp.z = C.h_sz;
-        sp.m = C.m;
-        sp.n = C.n;
-        sp.threshold = thresholds[q.snap_thr_idx];
-        sp.maxresid = q.snap_maxresid;
-        sp.from_average = q.snap_use_avg;
-        sp.iteration = q.snap_iteration;
-        sink(&sp, sink_user);
-      }
-    };
-    auto clear_halt = [&]() {
-      const int zero[2] = {0, 0};
-      CK(cudaMemcpyAsync(&C.ctrl->halt, &zero[0], sizeof(int), cudaMemcpyHostToDevice, C.stream));
-      CK(cudaMemcpyAsync(&C.ctrl->snap_pending, &zero[1], sizeof(int), cudaMemcpyHostToDevice, C.stream));
-      CK(cudaStreamSynchronize(C.stream));
+    if (nthr > 0 && !C.h_sx) {  // three pinned staging sets of x | z (n) | y (m)
+      C.h_sx = C.host_alloc<double>(3 * (2 * static_cast<size_t>(C.n) + C.m));
+    }
+    auto set_ptr = [&](int set) { return C.h_sx + static_cast<size_t>(set) * (2 * static_cast<size_t>(C.n) + C.m); };
+    auto acquire_set = [&](int set) {  // launcher: wait until the sink released it
+      std::unique_lock<std::mutex> g(mu);
+      cv.wait(g, [&] { return !staging_busy[set]; });
+      staging_busy[set] = true;
     };
 
-    // the initial check may already stop or snapshot
-    bool cancelled = false;
+    std::thread launcher([&] {
+      try {
+        CK(cudaSetDevice(C.device));
+        long long log_seen = 0;
+        int snaps_copied = 0;
+        auto emit_logs_upto = [&](const Ctrl& q, long long upto) {
+          if (!logfn || cfg.log_interval <= 0) {
+            log_seen = q.log_count;
+            return;
+          }
+          for (long long i = std::max(log_seen, q.log_count - C.log_cap); i < q.log_count; ++i) {
+            const auto& e = C.h_log[i % C.log_cap];
+            if (e.iteration > upto) return;
+            char line[160];
+            std::snprintf(line, sizeof line, "%lld\t%.6e\t%.6e\t%.6e\t%.3f\n", e.iteration, e.rel_primal,
+                          e.rel_dual, e.rel_gap, e.elapsed);
+            push(Event{0, e.iteration, line});
+            log_seen = i + 1;
+          }
+        };
+        auto fetch_log = [&](const Ctrl& q) {
+          if (!logfn || cfg.log_interval <= 0 || q.log_count == log_seen) return;
+          CK(cudaMemcpyAsync(C.h_log, C.log, sizeof(cclp_cu::LogEntry) * C.log_cap, cudaMemcpyDeviceToHost,
+                             C.side));
+          CK(cudaStreamSynchronize(C.side));
+        };
+        // snapshot `idx`, extracted by the kernels into slot idx % kSnapSlots
+        auto copy_inline = [&](const Ctrl& q, int idx) {
+          const cclp_cu::SnapMeta& mt = q.snap_meta[idx % cclp_cu::kSnapSlots];
+          const int set = idx % cclp_cu::kSnapSlots;
+          acquire_set(set);
+          CK(cudaMemcpyAsync(set_ptr(set), C.snap_buf[set], sizeof(double) * (2 * static_cast<size_t>(C.n) + C.m),
+                             cudaMemcpyDeviceToHost, C.side));
+          CK(cudaStreamSynchronize(C.side));
+          hf[1] = static_cast<unsigned>(idx + 1);  // the device slot is free again
+          emit_logs_upto(q, mt.iteration);
+          push(Event{1, mt.iteration, {}, set, mt.thr_idx, mt.use_avg, mt.maxresid});
+        };
+        // a snapshot the loop halted for, or one requested at the final check
+        auto copy_extracted = [&](const Ctrl& q) {
+          acquire_set(2);
+          C.extract_view(q.snap_use_avg ? cclp_cu::kViewAvg : cclp_cu::kViewCur, q);
+          double* h = set_ptr(2);
+          CK(cudaEventRecord(C.ev_snap, C.stream));
+          CK(cudaStreamWaitEvent(C.side, C.ev_snap, 0));
+          CK(cudaMemcpyAsync(h, C.vx, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.side));
+          CK(cudaMemcpyAsync(h + C.n, C.vz, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.side));
+          CK(cudaMemcpyAsync(h + 2 * static_cast<size_t>(C.n), C.vy, sizeof(double) * C.m, cudaMemcpyDeviceToHost,
+                             C.side));
+          CK(cudaStreamSynchronize(C.side));
+          emit_logs_upto(q, q.snap_iteration);
+          push(Event{1, q.snap_iteration, {}, 2, q.snap_thr_idx, q.snap_use_avg, q.snap_maxresid});
+        };
+        auto clear_halt = [&]() {
+          const int zero[2] = {0, 0};
+          CK(cudaMemcpyAsync(&C.ctrl->halt, &zero[0], sizeof(int), cudaMemcpyHostToDevice, C.stream));
+          CK(cudaMemcpyAsync(&C.ctrl->snap_pending, &zero[1], sizeof(int), cudaMemcpyHostToDevice, C.stream));
+          CK(cudaStreamSynchronize(C.stream));
+        };
+        auto process = [&](const Ctrl& q) {  // everything a finished batch reported
+          fetch_log(q);
+          while (snaps_copied < q.snaps_done) copy_inline(q, snaps_copied++);
+          if (q.halt && q.snap_pending) {
+            copy_extracted(q);
+            clear_halt();
+          }
+          emit_logs_upto(q, LLONG_MAX);
+        };
+        cudaEvent_t evb[2];
+        for (auto& e : evb) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        struct EvGuard {
+          cudaEvent_t* e;
+          ~EvGuard() { for (int i = 0; i < 2; ++i) cudaEventDestroy(e[i]); }
+        } evguard{evb};
+        auto launch_batch = [&](int slot) {
+          CK(cudaGraphLaunch(C.graph, C.stream));
+          C.launches += cclp_cu::kKernelsPerIteration * k;
+          CK(cudaMemcpyAsync(&C.h_ctrl[slot], C.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, C.stream));
+          CK(cudaEventRecord(evb[slot], C.stream));
+        };
+        auto wait_batch = [&](int slot) {  // polls, mirroring the cancel flag meanwhile
+          while (true) {
+            const cudaError_t e = cudaEventQuery(evb[slot]);
+            if (e == cudaSuccess) return;
+            if (e != cudaErrorNotReady) CK(e);
+            mirror_cancel();
+            std::this_thread::sleep_for(std::chrono::microseconds(20));
+          }
+        };
+        Ctrl q;
+        C.fetch_ctrl(&q);  // after the initial check
+        process(q);
+        if (q.stop < 0) {
+          int cur = 0;
+          launch_batch(cur);
+          bool ahead = false;
+          while (true) {
+            if (!ahead) launch_batch(cur ^ 1);  // one batch ahead of the one waited for
+            ahead = false;
+            wait_batch(cur);
+            q = C.h_ctrl[cur];
+            const bool drained = q.stop >= 0 || q.halt;
+            if (drained) wait_batch(cur ^ 1);  // exits at once: the device state is q
+            process(q);
+            if (q.stop >= 0) break;
+            if (drained) {  // the halt was served: restart the pipeline
+              launch_batch(cur);
+              continue;
+            }
+            cur ^= 1;
+          }
+        }
+        if (q.snap_pending && !q.halt) copy_extracted(q);  // the step that would extract it never ran
+        emit_logs_upto(q, LLONG_MAX);
+        st = q;
+      } catch (...) {
+        launcher_error = std::current_exception();
+      }
+      push(Event{2, 0, {}});
+    });
+    struct JoinLauncher {
+      std::thread& t;
+      ~JoinLauncher() { if (t.joinable()) t.join(); }
+    } launcher_join{launcher};
+
+    // calling thread: callbacks in order
     while (true) {
-      flush_log(st);
-      if (st.halt && st.snap_pending) {
-        emit_snapshot(st);
-        clear_halt();
-        st.halt = 0;
+      Event e;
+      {
+        std::unique_lock<std::mutex> g(mu);
+        cv.wait(g, [&] { return !events.empty(); });
+        e = std::move(events.front());
+        events.pop_front();
       }
-      if (st.stop >= 0) break;
-      if (cancel != nullptr && *cancel) {
-        cancelled = true;
-        break;
+      if (e.kind == 2) break;
+      if (e.kind == 0) {
+        logfn(e.line.c_str(), log_user);
+        continue;
       }
-      // launch a batch, copy the control block, poll
-      CK(cudaGraphLaunch(C.graph, C.stream));
-      C.launches += cclp_cu::kKernelsPerIteration * k;
-      CK(cudaMemcpyAsync(&C.h_ctrl[0], C.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, C.stream));
-      CK(cudaStreamSynchronize(C.stream));
-      st = C.h_ctrl[0];
+      if (sink) {
+        const double* h = set_ptr(e.set);
+        cclp_cu_snapshot sp;
+        sp.x = h;
+        sp.z = h + C.n;
+        sp.y = h + 2 * static_cast<size_t>(C.n);
+        sp.m = C.m;
+        sp.n = C.n;
+        sp.threshold = thresholds[e.thr_idx];
+        sp.maxresid = e.maxresid;
+        sp.from_average = e.use_avg;
+        sp.iteration = e.iteration;
+        sink(&sp, sink_user);
+      }
+      std::lock_guard<std::mutex> g(mu);
+      staging_busy[e.set] = false;
+      cv.notify_all();
     }
+    launcher.join();
+    if (launcher_error) std::rethrow_exception(launcher_error);
     CK(cudaEventRecord(C.ev_b, C.stream));
     CK(cudaEventSynchronize(C.ev_b));
     float loop_ms = 0;
     CK(cudaEventElapsedTime(&loop_ms, C.ev_a, C.ev_b));
     C.mark(9);
 
-    int view = st.result_view;
-    int stop = st.stop;
-    bool rep_valid = st.result_report_valid != 0;
-    if (cancelled) {
-      stop = CCLP_CU_STOP_CANCELLED;
-      view = cclp_cu::kViewCurEff;
-      rep_valid = st.checked != 0;
-      if (rep_valid) std::memcpy(st.result_report, st.R ? st.avg : st.cur, sizeof(st.result_report));
-    }
+    const int view = st.result_view;
+    const int stop = st.stop;
+    const bool rep_valid = st.result_report_valid != 0;
     C.extract_view(view, st);
     if (prefault.joinable()) prefault.join();
     C.d2h(x_out, C.vx, sizeof(double) * C.n);
@@ -2407,6 +2622,7 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
     C.d2h(z_out, C.vz, sizeof(double) * C.n);
     double rep[cclp_cu::kRepN];
     CK(cudaMemcpyAsync(rep, C.vrep, sizeof(rep), cudaMemcpyDeviceToHost, C.stream));
+    CK(cudaStreamSynchronize(C.stream));
     C.mark(10);
     res->stop = stop;
     res->iterations = st.iteration;
@@ -2423,6 +2639,18 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
     res->kernel_launches = C.launches;
     C.begun = false;
   });
+}
+
+int cclp_cu_sharded_request_cancel(cclp_cu_sharded* ctx) {
+  if (ctx == nullptr) return CCLP_CU_EINVAL;
+  ctx->s.abort_req.store(1);
+  return CCLP_CU_OK;
+}
+
+int cclp_cu_request_cancel(cclp_cu_ctx* ctx) {
+  if (ctx == nullptr) return CCLP_CU_EINVAL;
+  ctx->c.abort_req.store(1);
+  return CCLP_CU_OK;
 }
 
 int cclp_cu_partition(const int32_t* ptr, int32_t rows, int32_t parts, int32_t* bounds) {
@@ -2561,6 +2789,7 @@ int cclp_cu_sharded_solve(cclp_cu_sharded* ctx, const cclp_cu_config* cfg_in, co
     validate_inputs_eq(S.full->equality, cfg, *tol, thresholds, nthr);
     const auto wall0 = std::chrono::steady_clock::now();
     S.launches = 0;
+    S.abort_req.store(0);
     S.begin(cfg, *tol, thresholds, nthr);
     const double setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
     const int k = cfg.poll_interval > 0 ? cfg.poll_interval : 32;
@@ -2593,13 +2822,15 @@ int cclp_cu_sharded_solve(cclp_cu_sharded* ctx, const cclp_cu_config* cfg_in, co
         st.halt = 0;
       }
       if (st.stop >= 0) break;
-      const bool want_cancel = cancel != nullptr && *cancel;
+      const bool want_cancel = (cancel != nullptr && *cancel) || S.abort_req.load(std::memory_order_relaxed);
       const bool want_time =
           std::isfinite(cfg.time_limit) &&
           std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count() > cfg.time_limit;
-      if (S.agree(want_cancel || want_time)) {  // all ranks stop together
-        cancelled = want_cancel || !want_time;
-        timed_out = !cancelled;
+      using Req = cclp_cu::Sharded::StopReq;
+      const Req req = S.agree(want_cancel ? Req::kStopCancel : want_time ? Req::kStopTime : Req::kStopNone);
+      if (req != Req::kStopNone) {  // all ranks stop together, with the same reason
+        cancelled = req == Req::kStopCancel;
+        timed_out = req == Req::kStopTime;
         break;
       }
       S.run_batch(k);

@@ -33,6 +33,18 @@ enum Rep : int {
   kCompl, kRepN
 };
 
+// Ladder snapshots are extracted by the iteration kernels themselves into one
+// of kSnapSlots device slots (the step after the check that fired reads the
+// checked state anyway) and copied out by the host on a side stream while
+// the loop runs on; only when every slot still waits for the host does the
+// loop fall back to halting.
+constexpr int kSnapSlots = 2;
+struct SnapMeta {
+  long long iteration;
+  double maxresid;
+  int thr_idx, use_avg;
+};
+
 struct LogEntry {
   long long iteration;
   double rel_primal, rel_dual, rel_gap, elapsed;
@@ -58,9 +70,13 @@ struct Ctrl {
   int result_report_valid;
   int use_avg;
   int checked;           // cur/avg reports belong to the current iteration
-  int pad;
+  int snaps_done;        // snapshots extracted into slots (slot = index % kSnapSlots)
+  int snap_rprev;        // x of the pending snapshot's state: xc[it % 3][snap_rprev]
+  int pad2;
   double last_restart_resid;
   double snap_maxresid;
+  double snap_inv;       // 1/window of the pending snapshot's state (average view)
+  SnapMeta snap_meta[kSnapSlots];
   // timing probes (globaltimer ns) of the last step: column-kernel start
   // (block 0), finalize start and end
   unsigned long long t_cols_start, t_fin_start, t_fin_end;

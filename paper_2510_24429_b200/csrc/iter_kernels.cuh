@@ -37,6 +37,10 @@ struct StepInfo {
   double inv1;   // 1/window_{t+1} (average view at check(t+1))
   bool check;    // check(t+1) happens
   bool init;
+  // the pending ladder snapshot of state t (inline extraction, decide())
+  bool snap;
+  int snap_slot, snap_avg, snap_rprev;
+  double snap_inv;
 };
 
 __device__ __forceinline__ bool step_from(const Ctrl* C, const IterParams& p, bool init, StepInfo& si) {
@@ -53,6 +57,7 @@ __device__ __forceinline__ bool step_from(const Ctrl* C, const IterParams& p, bo
     si.inv1 = 0.0;
     si.check = true;
     si.init = true;
+    si.snap = false;
     return true;
   }
   si.t = C->iteration;
@@ -68,7 +73,20 @@ __device__ __forceinline__ bool step_from(const Ctrl* C, const IterParams& p, bo
   si.xs2 = static_cast<int>((si.t1 + 1) % 3);
   si.check = (si.t1 % p.check_interval) == 0;
   si.init = false;
+  si.snap = p.snap_inline && C->snap_pending;
+  if (si.snap) {
+    si.snap_slot = C->snaps_done % kSnapSlots;
+    si.snap_avg = C->snap_use_avg;
+    si.snap_rprev = C->snap_rprev;
+    si.snap_inv = C->snap_inv;
+  }
   return true;
+}
+
+__device__ __forceinline__ unsigned ld_relaxed_sys(const volatile unsigned* a) {
+  unsigned v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
 }
 
 __device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepInfo& si) {
@@ -118,6 +136,15 @@ __device__ __forceinline__ void push_signal_grid(const PushArgs& ps, int kind, u
 // thread 0 on a shared-memory copy of the control block.
 __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, Ctrl* C,
                                        const double* rowv, const double* colv, bool write_log = true) {
+  if (!si.init && p.snap_inline && C->snap_pending) {  // this step extracted the pending snapshot
+    SnapMeta& mt = C->snap_meta[C->snaps_done % kSnapSlots];
+    mt.iteration = C->snap_iteration;
+    mt.maxresid = C->snap_maxresid;
+    mt.thr_idx = C->snap_thr_idx;
+    mt.use_avg = C->snap_use_avg;
+    C->snaps_done++;
+    C->snap_pending = 0;
+  }
   if (!si.init) {
     if (rowv[6] + colv[12] > 0.0) {  // PdhgNumericalError before commit
       C->stop = 5;
@@ -141,6 +168,16 @@ __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, 
   if (si.check) {
     make_report(rowv, colv, p.b_norm, p.c_norm, C->cur);
     if (win > 0) make_report(rowv + 3, colv + 6, p.b_norm, p.c_norm, C->avg);
+  }
+  // cancel poll at the top of the pass (pdhg.cpp:301-305): the request the
+  // host mirrored into mapped memory, read by k_primal's block 0 this step
+  if (p.cancel_dev != nullptr && *reinterpret_cast<volatile unsigned*>(p.cancel_dev) != 0u) {
+    C->stop = 3;
+    C->result_view = kViewCur;
+    C->result_report_valid = C->checked;
+    if (C->checked)
+      for (int k = 0; k < kRepN; ++k) C->result_report[k] = C->cur[k];
+    return;
   }
   if (isfin(p.time_limit)) {  // pdhg.cpp:306-310
     const double el = 1e-9 * static_cast<double>(globaltimer() - *p.t0_ns);
@@ -181,7 +218,13 @@ __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, 
       return;
     }
     if (C->next_threshold < p.nthr && better[kMaxResid] <= p.thr[C->next_threshold]) {
-      C->halt = 1;
+      // a free slot: the next step extracts the view and the loop runs on;
+      // else halt and let the host extract it (pdhg.cpp:346-358)
+      const int copied = p.host_flags != nullptr ? static_cast<int>(ld_relaxed_sys(p.host_flags + 1)) : 0;
+      const bool inl = p.snap_inline && p.host_flags != nullptr && C->snaps_done - copied < kSnapSlots;
+      if (!inl) C->halt = 1;
+      C->snap_rprev = C->R_prev;
+      C->snap_inv = win > 0 ? 1.0 / static_cast<double>(win) : 0.0;
       C->snap_pending = 1;
       C->snap_use_avg = use_avg ? 1 : 0;
       C->snap_thr_idx = C->next_threshold;
@@ -702,6 +745,37 @@ __device__ __forceinline__ void dual_span(const IterParams& p, const StepInfo& s
   }
 }
 
+// Unscaled y of the pending snapshot's state t (view_of, pdhg.cpp:271-283;
+// the same operations as k_view_rows) into its slot.
+__device__ __noinline__ void snap_rows(const IterParams& p, const StepInfo& si) {
+  const double* __restrict__ src = si.snap_avg ? p.ysum[si.s0] : p.y[si.s0];
+  double* __restrict__ out = p.snap_y[si.snap_slot];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.m; i += gridDim.x * blockDim.x) {
+    const double ys = si.snap_avg ? src[i] * si.snap_inv : src[i];
+    out[i] = ys * p.r[i];
+  }
+}
+
+// Unscaled x and clipped z of the pending snapshot's state t (k_view_cols).
+__device__ __noinline__ void snap_cols(const IterParams& p, const StepInfo& si) {
+  const double* __restrict__ xsrc = si.snap_avg ? p.xsum[si.s0] : p.xc[si.t % 3][si.snap_rprev];
+  const double* __restrict__ asrc = si.snap_avg ? p.atysum[si.s0] : p.aty[si.s0];
+  double* __restrict__ xo = p.snap_x[si.snap_slot];
+  double* __restrict__ zo = p.snap_z[si.snap_slot];
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x) {
+    double xs = xsrc[j], as = asrc[j];
+    if (si.snap_avg) {
+      xs = xs * si.snap_inv;
+      as = as * si.snap_inv;
+    }
+    const double sj = p.s[j];
+    const double sinv = pow2_recip(sj);
+    const double x = xs * sj;
+    xo[j] = x;
+    zo[j] = clip_z(p.c[j], as * sinv, x, p.l[j], p.u[j]);
+  }
+}
+
 // Dual update + row-side report partials (one row per thread, coalesced).
 __global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init) {
   StepInfo si;
@@ -714,6 +788,7 @@ __global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init
   const int stride = gridDim.x * kEpiBlock;
   for (int i0 = blockIdx.x * kEpiBlock + threadIdx.x; i0 < p.m; i0 += kDualU * stride)
     dual_span(p, si, i0, stride, p.m, acc);
+  if (si.snap) snap_rows(p, si);
   block_reduce<kRowParts, kRowMaxMask, kEpiBlock>(acc, red, out);
   if (threadIdx.x < kRowParts) p.rowp[threadIdx.x * gridDim.x + blockIdx.x] = out[threadIdx.x];  // field-major
   if (p.push.on) push_signal_grid(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1), p.push.counter);
@@ -784,11 +859,17 @@ __global__ void __launch_bounds__(kEpiBlock) k_primal(const IterParams p, int in
   double acc[kColParts];
 #pragma unroll
   for (int k = 0; k < kColParts; ++k) acc[k] = 0.0;
+  // block 0 samples the host's cancel request early (a PCIe read that
+  // completes behind the column stream) for this step's decide()
+  const bool sampler = blockIdx.x == 0 && threadIdx.x == 0 && p.host_flags != nullptr;
+  const unsigned cancel_req = sampler ? ld_relaxed_sys(p.host_flags) : 0u;
   const int stride = gridDim.x * kEpiBlock;
   for (int j0 = blockIdx.x * kEpiBlock + threadIdx.x; j0 < p.n; j0 += kPrimalU * stride)
     primal_span(p, si, j0, stride, p.n, acc);
+  if (si.snap) snap_cols(p, si);
   block_reduce<kColParts, kColMaxMask, kEpiBlock>(acc, red, out);
   if (threadIdx.x < kColParts) p.colp[threadIdx.x * gridDim.x + blockIdx.x] = out[threadIdx.x];  // field-major
+  if (sampler && p.cancel_dev != nullptr) *p.cancel_dev = cancel_req;
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -162,6 +162,17 @@ struct IterParams {
   double* y_full_loc;  // this shard's region of the full y (k_dual also writes y there)
   double* xpart_loc;   // k_primal's last block writes the shard's 22 report sums here
   PushArgs push;       // sharded push transport (push.on == 0 otherwise)
+  // ladder snapshots extracted by the step after the check (single device;
+  // 0: halt the loop and let the host extract, as the sharded solve does)
+  int snap_inline;
+  double* snap_x[kSnapSlots];
+  double* snap_y[kSnapSlots];
+  double* snap_z[kSnapSlots];
+  // host flags in mapped pinned memory ([0] cancel request, [1] snapshots the
+  // host has copied out), read by block 0 of k_primal / by decide(); null:
+  // none. cancel_dev: block 0's copy of the cancel request for decide().
+  const volatile unsigned* host_flags;
+  unsigned* cancel_dev;
 };
 
 // ---------------------------------------------------------------------------

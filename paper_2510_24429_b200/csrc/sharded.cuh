@@ -277,6 +277,7 @@ struct Sharded {
   double *vx_full = nullptr, *vy_full = nullptr, *vz_full = nullptr, *vparts_full = nullptr;
   bool begun = false;
   bool halo_built = false;
+  std::atomic<int> abort_req{0};  // cclp_cu_sharded_request_cancel
 
   // Halo exchange of one side (x for the row SpMV, y for the column SpMV):
   // need[p][q] = the sorted local offsets (in shard q's slice) of the entries
@@ -452,17 +453,21 @@ struct Sharded {
     return d;
   }
 
-  void barrier() { agree(false); }  // every rank past this point (multi-process only)
+  void barrier() { agree(kStopNone); }  // every rank past this point (multi-process only)
 
-  // Host-side stop decisions (cancel, time limit) taken by any rank apply to
+  // Host-side stop requests (cancel, time limit) taken by any rank apply to
   // all ranks, so no rank is left waiting on peers that stopped launching.
-  bool agree(bool local) {
+  // Every rank all-gathers its request code and takes the same decision with
+  // a fixed priority (cancel over time limit), so all shards also report the
+  // same stop reason although their wall clocks differ.
+  enum StopReq : char { kStopNone = 0, kStopTime = 1, kStopCancel = 2 };
+  StopReq agree(StopReq local) {
     if (!multi()) return local;
-    const char v = local ? 1 : 0;
+    const char v = static_cast<char>(local);
     const std::vector<char> all = gather_bytes(&v, 1);
-    for (char a : all)
-      if (a != 0) return true;
-    return false;
+    char best = kStopNone;
+    for (char a : all) best = a > best ? a : best;
+    return static_cast<StopReq>(best);
   }
 
   // All-gather of `bytes` host bytes per rank, in rank order (NCCL through a
@@ -566,6 +571,9 @@ struct Sharded {
 
   void create(const cclp_cu_lp* lp, int dev, int local_shards, int rk, int nr, const ncclUniqueId* id,
               const cclp_cu_host_comm* hc = nullptr) {
+    if (lp == nullptr || lp->m < 0 || lp->n < 0 || lp->colptr == nullptr)
+      throw std::invalid_argument("sharded: bad LP");
+    validate_csc(lp);
     device = dev;
     rank = rk;
     nranks = nr;

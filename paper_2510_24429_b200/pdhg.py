@@ -109,6 +109,8 @@ def load_library(path: str = LIB_PATH):
         L.cclp_cu_default_tolerances.argtypes = [C.POINTER(_Tol)]
         L.cclp_cu_create.argtypes = [C.POINTER(_LP), C.c_int, C.POINTER(C.c_void_p)]
         L.cclp_cu_destroy.argtypes = [C.c_void_p]
+        L.cclp_cu_request_cancel.argtypes = [C.c_void_p]
+        L.cclp_cu_sharded_request_cancel.argtypes = [C.c_void_p]
         L.cclp_cu_price.argtypes = [C.c_void_p, _dp, C.c_char_p, C.c_void_p, C.c_int32, C.c_double,
                                      C.c_int32, C.POINTER(C.c_int64), C.POINTER(C.c_int32),
                                      C.POINTER(C.c_double)]
@@ -157,7 +159,8 @@ EXPORTED_SYMBOLS = [
     "cclp_cu_nccl_unique_id", "cclp_cu_sharded_create", "cclp_cu_sharded_solve",
     "cclp_cu_sharded_begin", "cclp_cu_sharded_advance", "cclp_cu_sharded_describe",
     "cclp_cu_sharded_destroy", "cclp_cu_sharded_create_hostcomm", "cclp_cu_create_from_file",
-    "cclp_cu_relative_report", "cclp_cu_price",
+    "cclp_cu_relative_report", "cclp_cu_price", "cclp_cu_request_cancel",
+    "cclp_cu_sharded_request_cancel",
 ]
 
 
@@ -426,8 +429,9 @@ class Engine:
                 if sink is not None:
                     sink(PdhgSnapshot(it, s.threshold, s.maxresid, bool(s.from_average),
                                       int(s.iteration)))
-            except Exception as e:  # surfaced after the solve
+            except BaseException as e:  # stop the loop now, re-raise after the solve
                 errors.append(e)
+                self.L.cclp_cu_request_cancel(self.ctx)
 
         def _log(line, _u):
             if config.log is not None:
@@ -607,8 +611,9 @@ class ShardedEngine:
                 if sink is not None:
                     sink(PdhgSnapshot(it, s.threshold, s.maxresid, bool(s.from_average),
                                       int(s.iteration)))
-            except Exception as e:  # surfaced after the solve
+            except BaseException as e:  # stop the loop now, re-raise after the solve
                 errors.append(e)
+                self.L.cclp_cu_sharded_request_cancel(self.ctx)
 
         cb = _SINK(_sink)
         flag = cancel if cancel is not None else (C.c_uint8 * 1)(0)

@@ -116,3 +116,46 @@ def test_gaussian_start_matches_oracle(seed, n):
     ours = gaussian_start(seed, n)
     ref = Restatement().gaussian_start(seed, n)
     assert np.array_equal(ours.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("case,msg", [
+    ("colptr0", "colptr[0] != 0"),
+    ("decreasing", "decreasing column offsets"),
+    ("range", "row index out of range"),
+    ("negative", "row index out of range"),
+    ("unsorted", "unsorted or duplicate row indices"),
+    ("duplicate", "unsorted or duplicate row indices"),
+])
+def test_create_rejects_malformed_csc_before_touching_the_device(lib, case, msg):
+    """LinearProgram::validate's CSC checks (lp.cpp:71-83) run on the host in
+    cclp_cu_create, so a bad matrix is EINVAL (no GPU needed) instead of an
+    out-of-bounds gather on the device."""
+    import numpy as np
+
+    from paper_2510_24429_b200.pdhg import _LP
+    colptr = np.array([0, 2, 3], np.int32)
+    rowind = np.array([0, 1, 1], np.int32)
+    if case == "colptr0":
+        colptr = np.array([1, 2, 3], np.int32)
+    elif case == "decreasing":
+        colptr = np.array([0, 3, 2], np.int32)
+    elif case == "range":
+        rowind = np.array([0, 2, 1], np.int32)
+    elif case == "negative":
+        rowind = np.array([0, -1, 1], np.int32)
+    elif case == "unsorted":
+        rowind = np.array([1, 0, 1], np.int32)
+    elif case == "duplicate":
+        rowind = np.array([1, 1, 1], np.int32)
+    val = np.ones(3)
+    v2, v1 = np.zeros(2), np.zeros(2)
+    dp = C.POINTER(C.c_double)
+    ip = C.POINTER(C.c_int32)
+    lp = _LP(2, 2, colptr.ctypes.data_as(ip), rowind.ctypes.data_as(ip), val.ctypes.data_as(dp),
+             v2.ctypes.data_as(dp), v1.ctypes.data_as(dp), v1.ctypes.data_as(dp),
+             v2.ctypes.data_as(dp), v2.ctypes.data_as(dp))
+    ctx = C.c_void_p()
+    lib.cclp_cu_last_error.restype = C.c_char_p
+    assert lib.cclp_cu_create(C.byref(lp), 0, C.byref(ctx)) == 1  # CCLP_CU_EINVAL
+    assert msg in lib.cclp_cu_last_error().decode()
+    assert not ctx.value
