@@ -747,7 +747,7 @@ __device__ __forceinline__ void dual_span(const IterParams& p, const StepInfo& s
 
 // Unscaled y of the pending snapshot's state t (view_of, pdhg.cpp:271-283;
 // the same operations as k_view_rows) into its slot.
-__device__ __noinline__ void snap_rows(const IterParams& p, const StepInfo& si) {
+__device__ __forceinline__ void snap_rows(const IterParams& p, const StepInfo& si) {
   const double* __restrict__ src = si.snap_avg ? p.ysum[si.s0] : p.y[si.s0];
   double* __restrict__ out = p.snap_y[si.snap_slot];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < p.m; i += gridDim.x * blockDim.x) {
@@ -757,7 +757,7 @@ __device__ __noinline__ void snap_rows(const IterParams& p, const StepInfo& si) 
 }
 
 // Unscaled x and clipped z of the pending snapshot's state t (k_view_cols).
-__device__ __noinline__ void snap_cols(const IterParams& p, const StepInfo& si) {
+__device__ __forceinline__ void snap_cols(const IterParams& p, const StepInfo& si) {
   const double* __restrict__ xsrc = si.snap_avg ? p.xsum[si.s0] : p.xc[si.t % 3][si.snap_rprev];
   const double* __restrict__ asrc = si.snap_avg ? p.atysum[si.s0] : p.aty[si.s0];
   double* __restrict__ xo = p.snap_x[si.snap_slot];

@@ -159,3 +159,21 @@ def test_create_rejects_malformed_csc_before_touching_the_device(lib, case, msg)
     assert lib.cclp_cu_create(C.byref(lp), 0, C.byref(ctx)) == 1  # CCLP_CU_EINVAL
     assert msg in lib.cclp_cu_last_error().decode()
     assert not ctx.value
+
+
+def test_iteration_kernels_keep_no_stack_frame():
+    """The per-iteration kernels take IterParams (~2 KB) by value; a helper that
+    is not inlined copies it into a per-thread stack frame on every launch (a
+    50% slowdown of the epilogues, measured). Guard it from the cubin."""
+    import shutil
+    import subprocess
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(LIB) or not os.path.exists(tool):
+        pytest.skip("library or cuobjdump missing")
+    out = subprocess.run([tool, "-res-usage", LIB], capture_output=True, text=True).stdout
+    seen = 0
+    for fn, stack in re.findall(r"Function (\S+):\s*\n\s*REG:\d+ STACK:(\d+)", out):
+        if re.search(r"k_(spmv_rows|spmv_cols|dual|primal|finalize)", fn):
+            seen += 1
+            assert int(stack) <= 16, (fn, stack)
+    assert seen >= 6
