@@ -67,6 +67,41 @@ def l2_roofline(lp, dom: str, dom_ms: float, clocks: dict, kernel: str = "") -> 
                      "cap 6300 B/clk x SM clock"}
 
 
+def bench_config(lp, workload: str, world: int, sharded: bool = False) -> dict:
+    """The workload description both arms print (identical keys and values)."""
+    return {"workload": workload, "m": lp.m, "n": lp.n, "nnz": lp.nnz, "check_interval": 1,
+            "parallelism": (f"row-block sharded x{world}" if sharded else
+                            ("replicas" if world > 1 else "single")),
+            "l2": "working set > 126 MB L2, no flush"}
+
+
+def pinned_core():
+    """Run the CPU baselines on ONE host core (the reference loop is
+    single-threaded; 1 pinned core). Returns (core, host_cores)."""
+    host = os.cpu_count() or 1
+    try:
+        allowed = sorted(os.sched_getaffinity(0))
+        return allowed[-1], host, allowed
+    except Exception:
+        return None, host, None
+
+
+class OneCore:
+    def __enter__(self):
+        self.core, self.host, self.allowed = pinned_core()
+        if self.core is not None:
+            os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *a):
+        if self.allowed is not None:
+            os.sched_setaffinity(0, set(self.allowed))
+
+
+CPU_NOTE = ("the reference's own sources (proj/src/*.cpp, unmodified) compiled against the "
+            "repo's Eigen-API subset (oracle/eigen_shim: Eigen 3.4 is not installed on the box)")
+
+
 def measured_peak_gbs():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -197,18 +232,20 @@ def pinned_copy(lp):
 
 
 def cpu_reference_rate(lp, iters: int, use_ref: bool = True):
-    """Loop-only iterations/s of the reference run_pdhg: (T(S) - T(0)) / S."""
+    """Loop-only iterations/s of the reference run_pdhg: (T(S) - T(0)) / S, on
+    one pinned host core."""
     from oracle.pyoracle import Reference, Restatement, reference_available
     kind = "reference" if (use_ref and reference_available()) else "port"
     impl = Reference() if kind == "reference" else Restatement()
-    t = time.perf_counter()
-    impl.run_pdhg(lp, config=dict(max_iterations=0))
-    t0 = time.perf_counter() - t
-    t = time.perf_counter()
-    r = impl.run_pdhg(lp, config=dict(max_iterations=iters))
-    ts = time.perf_counter() - t
+    with OneCore() as oc:
+        t = time.perf_counter()
+        impl.run_pdhg(lp, config=dict(max_iterations=0))
+        t0 = time.perf_counter() - t
+        t = time.perf_counter()
+        r = impl.run_pdhg(lp, config=dict(max_iterations=iters))
+        ts = time.perf_counter() - t
     return dict(value=r["iterations"] / max(ts - t0, 1e-9), setup_s=t0, total_s=ts,
-                iterations=r["iterations"], kind=kind)
+                iterations=r["iterations"], kind=kind, core=oc.core, host_cores=oc.host)
 
 
 def run_reference_arm(args, world, rank, pg):
@@ -220,29 +257,32 @@ def run_reference_arm(args, world, rank, pg):
     kind = "reference" if reference_available() else "port"
     impl = Reference() if kind == "reference" else Restatement()
     S = args.ref_iters
-    t = time.perf_counter()
-    impl.run_pdhg(lp, config=dict(max_iterations=0))  # setup only: Ruiz + ||A|| + check(0)
-    t_setup = time.perf_counter() - t
-    for _ in range(max(args.warmup - 1, 0)):
-        impl.run_pdhg(lp, config=dict(max_iterations=1))
-    loop_s, iters = 0.0, 0
-    for _ in range(args.steps):
+    with OneCore() as oc:
         t = time.perf_counter()
-        r = impl.run_pdhg(lp, config=dict(max_iterations=S))
-        loop_s += max(time.perf_counter() - t - t_setup, 1e-9)
-        iters += r["iterations"]
+        impl.run_pdhg(lp, config=dict(max_iterations=0))  # setup only: Ruiz + ||A|| + check(0)
+        t_setup = time.perf_counter() - t
+        for _ in range(max(args.warmup - 1, 0)):
+            impl.run_pdhg(lp, config=dict(max_iterations=1))
+        loop_s, iters = 0.0, 0
+        for _ in range(args.steps):
+            t = time.perf_counter()
+            r = impl.run_pdhg(lp, config=dict(max_iterations=S))
+            loop_s += max(time.perf_counter() - t - t_setup, 1e-9)
+            iters += r["iterations"]
     v = iters / loop_s
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * loop_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded generator, paper_2510_24429_b200/lpgen.py)",
-        "config": {"workload": CONFIG_NAME, "m": lp.m, "n": lp.n, "nnz": lp.nnz,
-                   "iters_per_step": S, "check_interval": 1},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": kind,
+        "config": bench_config(lp, CONFIG_NAME, world),
+        "iters_per_step": S,
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "host_cores": oc.host,
+                         "kind": kind,
                          "sample": f"C2, {args.steps} x run_pdhg(max_iterations={S}) minus its "
-                                   f"setup ({t_setup:.2f} s: Ruiz + power iteration), "
-                                   "single-threaded (reference has no threading)"},
+                                   f"setup ({t_setup:.2f} s: Ruiz + power iteration), on 1 of "
+                                   f"{oc.host} host cores (sched_setaffinity to core {oc.core}; "
+                                   f"the reference has no threading); {CPU_NOTE}"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -348,6 +388,47 @@ def run_sharded_arm(args, world, rank, local, pg):
         print(json.dumps(line), flush=True)
 
 
+def per_config_line(name: str, args, local: int) -> dict:
+    """The >= 10M-nnz configs (north_star's 50 % target) in the same run:
+    device-resident iterations/s through the same loop, the in-graph kernel
+    split, the dominant kernel's and the iteration's fraction of the measured
+    HBM peak, and the clocks sampled during that timed region."""
+    import torch
+    from paper_2510_24429_b200 import lpgen
+    from paper_2510_24429_b200.pdhg import Engine, PdhgConfig
+    lp = lpgen.make_config(name)
+    I = max(20, int(args.iters_per_step * 5_000_000 / lp.nnz))
+    K = 5
+    peak, peak_kind = measured_peak_gbs()
+    with Engine(lp, device=local) as eng:
+        eng.begin(PdhgConfig())
+        for _ in range(3):
+            eng.advance(I)
+        torch.cuda.synchronize(local)
+        with ClockSampler(local) as clk:
+            ms = sum(eng.advance(I) for _ in range(K))
+        ph = eng.phase_profile()
+        dsc = eng.describe()
+    ab = algorithmic_bytes(lp.m, lp.n, lp.nnz)
+    iter_us = ms * 1e3 / (K * I)
+    dom = "rows" if ph["spmv_rows"] >= ph["spmv_cols"] else "cols"
+    dom_kernel = {"rows": "k_spmv_rows_sellg" if dsc.get("sell_rows_block") else
+                  ("k_spmv_rows_panel" if False else "k_spmv_rows"),
+                  "cols": "k_spmv_cols_sell" if dsc.get("sell_cols_block") else "k_spmv_cols"}[dom]
+    dom_gbs = ab[dom] / (ph["spmv_" + dom] * 1e-6) / 1e9
+    it_gbs = ab["iteration"] / (iter_us * 1e-6) / 1e9
+    del lp
+    return {"m": dsc.get("m"), "n": dsc.get("n"), "nnz": dsc.get("nnz"),
+            "iters_per_s": K * I / (ms * 1e-3), "us_per_iteration": iter_us,
+            "iters_timed": K * I,
+            "kernels_us": {k: ph[k] for k in ("spmv_rows", "dual", "spmv_cols", "primal")},
+            "kernels_timing": f"in-graph stamps, median of {ph['steps']} steps",
+            "dominant": {"kernel": dom_kernel, "bytes_per_launch": ab[dom], "achieved": dom_gbs,
+                         "frac": dom_gbs / peak},
+            "iteration": {"bytes": ab["iteration"], "achieved": it_gbs, "frac": it_gbs / peak},
+            "peak": peak, "peak_kind": peak_kind, "clocks": clk.summary()}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -360,6 +441,8 @@ def main():
     ap.add_argument("--ref-iters", type=int, default=20)
     ap.add_argument("--cpu-iters", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--per-config", default="C3,C4",
+                    help="extra configs timed in the same N=1 run ('' to skip)")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance solves (profiling runs)")
     ap.add_argument("--workload", default=CONFIG_NAME,
                     help="C2 (default, configs[1]); C3/C4/C5/C5s: with N>1 the sharded solve")
@@ -408,8 +491,12 @@ def main():
     total_iters = allreduce_sum(pg, float(K * I), dev)
     value = total_iters / (t_max * 1e-3)
 
-    # per-kernel device time for the roofline (eager launches, events between)
-    pk = eng.profile_kernels(100)
+    # per-kernel device time for the roofline: the split of the timed graph
+    # iterations themselves (in-kernel %globaltimer stamps, median over the
+    # last 128 steps); the eager per-kernel event timing is kept beside it
+    ph = eng.phase_profile()
+    pk_eager = eng.profile_kernels(100)
+    pk = {k: ph[k] * 1e-3 for k in ("spmv_rows", "dual", "spmv_cols", "primal")}
     ab = algorithmic_bytes(lp.m, lp.n, lp.nnz)
     dom = "rows" if pk["spmv_rows"] >= pk["spmv_cols"] else "cols"
     dom_ms = pk["spmv_" + dom]
@@ -461,14 +548,20 @@ def main():
         ttt = [ttt, {"eps_rel": 1e-6, "seconds": time.perf_counter() - t,
                      "iterations": r6.iterations, "stop": r6.stop.name, "restarts": r6.restarts}]
 
+    per_config = None
+    if rank == 0 and world == 1 and args.per_config:
+        per_config = {c: per_config_line(c, args, local) for c in args.per_config.split(",") if c}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu_iters = max(3, int(args.cpu_iters * 5_000_000 / max(lp.nnz, 1)))
         cb = cpu_reference_rate(lp, cpu_iters)
-        cpu = {"value": cb["value"], "unit": UNIT, "cores": 1, "kind": cb["kind"],
+        cpu = {"value": cb["value"], "unit": UNIT, "cores": 1, "host_cores": cb["host_cores"],
+               "kind": cb["kind"],
                "sample": f"{args.workload}, run_pdhg(max_iterations={cpu_iters}) minus "
-                         f"run_pdhg(max_iterations=0) ({cb['setup_s']:.2f} s setup), 1 thread "
-                         "(the reference loop is single-threaded)"}
+                         f"run_pdhg(max_iterations=0) ({cb['setup_s']:.2f} s setup), on 1 of "
+                         f"{cb['host_cores']} host cores (sched_setaffinity to core {cb['core']}; "
+                         f"the reference loop is single-threaded); {CPU_NOTE}"}
 
     if rank == 0:
         line = {
@@ -476,10 +569,8 @@ def main():
             "warmup": W, "ms_per_step": t_max / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, paper_2510_24429_b200/lpgen.py)",
-            "config": {"workload": args.workload, "m": lp.m, "n": lp.n, "nnz": lp.nnz,
-                       "iters_per_step": I, "check_interval": 1,
-                       "parallelism": "replicas" if world > 1 else "single",
-                       "l2": "working set ~180 MB > 126 MB L2, no flush"},
+            "config": bench_config(lp, args.workload, world),
+            "iters_per_step": I,
             "us_per_iteration": iter_us,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": dom_kernel,
@@ -488,7 +579,10 @@ def main():
                          "iteration": {"bytes": ab["iteration"],
                                        "achieved": ab["iteration"] / (iter_us * 1e-6) / 1e9,
                                        "frac": ab["iteration"] / (iter_us * 1e-6) / 1e9 / peak},
-                         "kernels_us": {k: v * 1e3 for k, v in pk.items()}},
+                         "kernels_us": {k: v * 1e3 for k, v in pk.items()},
+                         "kernels_timing": f"in-graph: block-0 %globaltimer stamps after each "
+                                           f"kernel's PDL wait, median of {ph['steps']} steps",
+                         "kernels_us_eager": {k: v * 1e3 for k, v in pk_eager.items()}},
             # the bound the SpMV actually meets on gather-heavy LPs: L2 traffic of
             # 12 B stream + one 32 B sector per gathered nonzero (+ the vectors),
             # against the LTS throughput cap (~6,300 B/clk, B300_MICROARCH.md) at
@@ -502,6 +596,8 @@ def main():
             "time_to_tolerance": ttt,
             "cpu_baseline": cpu,
         }
+        if per_config:
+            line["per_config"] = per_config
         print(json.dumps(line), flush=True)
     if pg is not None:
         pg.destroy_process_group()

@@ -213,6 +213,12 @@ int cclp_cu_advance(cclp_cu_ctx* ctx, int64_t iters, double* device_ms);
  * k_dual (dual update + row reports), k_spmv_cols (A'y) and k_primal (primal
  * update + column reports + candidates + on-device decisions). */
 int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out);
+/* The same split as it runs inside the CUDA graphs of the loop: block 0 of
+ * each kernel stamps %globaltimer after its PDL wait (= the previous kernel's
+ * completion), over the last 128 steps; out[0..3] = median microseconds of
+ * rows / dual / cols / primal+decisions per step, *steps = steps used.
+ * Single-device contexts after cclp_cu_begin/cclp_cu_advance. */
+int cclp_cu_phase_profile(cclp_cu_ctx* ctx, double* out, int64_t* steps);
 /* The engine's CUDA stream (cudaStream_t) for external event timing. */
 void* cclp_cu_stream(cclp_cu_ctx* ctx);
 /* Static description: nnz, CSR/CSC group sizes, grid sizes, bytes/iteration. */

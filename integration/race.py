@@ -1,8 +1,9 @@
 """ctypes bridge to cclp::run_race (integration/run_race.cpp via
-integration/race_capi.cpp), built by `make -C oracle race` into
-oracle/_ref/librace_gpu.so (run_pdhg = the B200 engine) and
-oracle/_ref/librace_cpu.so (run_pdhg = the reference's CPU loop); the
-crossover is the reference's run_crossover in both. Used by tests/ and
+integration/race_capi.cpp), built by `make -C integration` into
+integration/lib/librace_gpu.so (run_pdhg = the B200 engine) and
+integration/lib/librace_cpu.so (run_pdhg = the reference's CPU loop); the
+crossover is the reference's run_crossover in both, over the product's sparse
+LU (third_party/eigen_subset). Used by tests/ and
 tools/time_to_basic.py."""
 from __future__ import annotations
 
@@ -13,8 +14,8 @@ import os
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIBS = {"gpu": os.path.join(ROOT, "oracle", "_ref", "librace_gpu.so"),
-        "cpu": os.path.join(ROOT, "oracle", "_ref", "librace_cpu.so")}
+LIBS = {"gpu": os.path.join(ROOT, "integration", "lib", "librace_gpu.so"),
+        "cpu": os.path.join(ROOT, "integration", "lib", "librace_cpu.so")}
 _dp = C.POINTER(C.c_double)
 _ip = C.POINTER(C.c_int32)
 _cache = {}

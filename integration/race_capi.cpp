@@ -1,5 +1,5 @@
 // C-ABI bridge to cclp::run_race (integration/run_race.cpp) for the Python
-// tests and the time-to-basic benchmark. Built by oracle/Makefile twice from
+// tests, the CLI and the time-to-basic benchmark. Built by integration/Makefile twice from
 // the same sources: librace_gpu.so (run_pdhg = the B200 drop-in,
 // integration/run_pdhg_cuda.cpp) and librace_cpu.so (run_pdhg = the
 // reference's own CPU loop). Crossover is the reference's run_crossover in

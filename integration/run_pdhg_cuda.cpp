@@ -15,7 +15,8 @@
 //     iteration (cclp_cu_request_cancel) and propagates unchanged out of
 //     run_pdhg, as the reference's synchronous call would;
 //   * cancel is polled with a relaxed load every iteration (pdhg.cpp:301).
-// oracle/Makefile's `dropin` target builds the reference's own test_pdhg.cpp
+// integration/Makefile links it into librace_gpu.so; oracle/Makefile's `dropin`
+// target builds the reference's own test_pdhg.cpp
 // against this file (tests/test_dropin.py runs it on the GPU).
 #include <atomic>
 #include <cstdint>

@@ -339,6 +339,7 @@ struct Context {
   unsigned* h_flags = nullptr;
   const unsigned* d_flags = nullptr;
   unsigned* cancel_dev = nullptr;
+  unsigned long long* stamps = nullptr;  // in-graph phase stamps (stamp_phase)
   std::atomic<int> abort_req{0};  // cclp_cu_request_cancel (any thread)
   void ensure_flags() {
     if (h_flags) return;
@@ -541,7 +542,7 @@ Context::~Context() {
                     plan_cols.seg, plan_cols.lr_first, plan_cols.part, plan_cols.cnt, x_full, y_full,
                     xpart, vparts, push_flags, push_counter, sell_off, sell_start, sell_idx, sell_val,
                     sgr.off, sgr.start, sgr.idx, sgr.val, sgc.off, sgc.start, sgc.idx, sgc.val,
-                    cancel_dev, snap_buf[0], snap_buf[1]};
+                    cancel_dev, stamps, snap_buf[0], snap_buf[1]};
     static_assert(kSnapSlots == 2, "release list");
     for (void* p : ptrs) release(p);
     for (int k = 0; k < 3; ++k)
@@ -1902,6 +1903,7 @@ void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& to
   // sharded solve halts for snapshots and agrees on stops on the host)
   const bool single = !(shard_count > 1 || x_full != nullptr);
   p.snap_inline = 0;
+  p.stamps = nullptr;
   p.host_flags = nullptr;
   p.cancel_dev = nullptr;
   for (int k = 0; k < kSnapSlots; ++k) p.snap_x[k] = p.snap_y[k] = p.snap_z[k] = nullptr;
@@ -1911,6 +1913,9 @@ void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& to
     CK(cudaMemsetAsync(cancel_dev, 0, sizeof(unsigned), stream));
     p.host_flags = d_flags;
     p.cancel_dev = cancel_dev;
+    if (!stamps) stamps = alloc<unsigned long long>(cclp_cu::kStampRing * 4);
+    CK(cudaMemsetAsync(stamps, 0, sizeof(unsigned long long) * cclp_cu::kStampRing * 4, stream));
+    p.stamps = stamps;
     if (nthr > 0) {
       for (int k = 0; k < kSnapSlots; ++k) {
         if (!snap_buf[k]) snap_buf[k] = alloc<double>(2 * static_cast<size_t>(n) + m);
@@ -2269,6 +2274,38 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
       }
     for (auto& e : ev) cudaEventDestroy(e);
     for (int k = 0; k < K; ++k) out[k] = iters ? acc[k] / iters : 0.0;
+  });
+}
+
+int cclp_cu_phase_profile(cclp_cu_ctx* ctx, double* out, int64_t* steps) {
+  return guarded([&] {
+    Context& C = ctx->c;
+    if (!C.begun || C.stamps == nullptr)
+      throw std::invalid_argument("cclp_cu_phase_profile: call cclp_cu_begin/advance first (single device)");
+    constexpr int R = cclp_cu::kStampRing;
+    std::vector<unsigned long long> st(R * 4);
+    Ctrl ctl;
+    CK(cudaStreamSynchronize(C.stream));
+    CK(cudaMemcpy(st.data(), C.stamps, sizeof(unsigned long long) * R * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&ctl, C.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
+    // steps t and t+1 both still in the ring: t in [it - R + 1, it - 2]
+    std::vector<double> d[4];
+    const long long it = ctl.iteration;
+    for (long long t = std::max<long long>(1, it - R + 1); t + 1 < it; ++t) {
+      const unsigned long long* a = &st[(t % R) * 4];
+      const unsigned long long nxt = st[((t + 1) % R) * 4];
+      const unsigned long long e[5] = {a[0], a[1], a[2], a[3], nxt};
+      bool ok = true;
+      for (int k = 0; k < 4; ++k) ok = ok && e[k] != 0 && e[k + 1] > e[k];
+      if (!ok) continue;
+      for (int k = 0; k < 4; ++k) d[k].push_back(1e-3 * static_cast<double>(e[k + 1] - e[k]));
+    }
+    for (int k = 0; k < 4; ++k) {
+      if (d[k].empty()) { out[k] = 0.0; continue; }
+      std::nth_element(d[k].begin(), d[k].begin() + d[k].size() / 2, d[k].end());
+      out[k] = d[k][d[k].size() / 2];
+    }
+    if (steps) *steps = static_cast<int64_t>(d[0].size());
   });
 }
 

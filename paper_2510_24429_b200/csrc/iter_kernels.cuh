@@ -89,9 +89,21 @@ __device__ __forceinline__ unsigned ld_relaxed_sys(const volatile unsigned* a) {
   return v;
 }
 
-__device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepInfo& si) {
+// In-graph phase stamps: block 0 of each of the step's four kernels records
+// %globaltimer once the previous kernel has completed (after the PDL wait),
+// into a ring of kStampRing steps; consecutive stamps split the iteration
+// into rows / dual / cols / primal+decide as they run inside the CUDA graph
+// (cclp_cu_phase_profile). A store by one thread per kernel: no load, no wait.
+__device__ __forceinline__ void stamp_phase(const IterParams& p, const StepInfo& si, int phase) {
+  if (phase >= 0 && p.stamps != nullptr && !si.init && blockIdx.x == 0 && threadIdx.x == 0)
+    p.stamps[(si.t % kStampRing) * 4 + phase] = globaltimer();
+}
+
+__device__ __forceinline__ bool read_step(const IterParams& p, bool init, StepInfo& si, int phase = -1) {
   pdl_wait();  // the previous kernel of the step (or step) must be complete
-  return step_from(p.ctrl, p, init, si);
+  const bool go = step_from(p.ctrl, p, init, si);
+  if (go) stamp_phase(p, si, phase);
+  return go;
 }
 
 // ---- push transport (PushArgs, kernels.cuh) --------------------------------
@@ -499,7 +511,7 @@ template <int G, bool LONG>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows_panel(const IterParams p, int init,
                                                                 const PanelArgs a) {
   StepInfo si;
-  if (!read_step(p, init != 0, si)) return;
+  if (!read_step(p, init != 0, si, a.accumulate ? -1 : 0)) return;
   if (p.push.on) push_wait(p.push, kPushX, static_cast<unsigned long long>(si.t1 + 1));
   spmv_block_range<G, LONG>(a.plan, a.ptr, a.idx, a.val,
                             GatherPlain{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]}, p.ax[si.s1], 1,
@@ -509,7 +521,7 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows_panel(const IterParams
 template <int G, bool LONG>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows(const IterParams p, int init) {
   StepInfo si;
-  if (!read_step(p, init != 0, si)) return;
+  if (!read_step(p, init != 0, si, 0)) return;
   if (p.push.on) push_wait(p.push, kPushX, static_cast<unsigned long long>(si.t1 + 1));
   spmv_block_range<G, LONG>(p.plan_r, p.rowptr, p.colind, p.aval,
                             GatherPlain{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]},
@@ -634,7 +646,7 @@ __global__ void __launch_bounds__(BS) k_sellg_range(const SellPlan S, const Spmv
 template <int G, bool LONG, int BS>
 __global__ void __launch_bounds__(BS) k_spmv_rows_sellg(const IterParams p, int init) {
   StepInfo si;
-  if (!read_step(p, init != 0, si)) return;
+  if (!read_step(p, init != 0, si, 0)) return;
   if (p.push.on) push_wait(p.push, kPushX, static_cast<unsigned long long>(si.t1 + 1));
   const GatherPlain g{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]};
   sellg_block<G>(p.sell_r, g, p.ax[si.s1]);
@@ -644,7 +656,7 @@ __global__ void __launch_bounds__(BS) k_spmv_rows_sellg(const IterParams p, int 
 template <int G, bool LONG, int BS>
 __global__ void __launch_bounds__(BS) k_spmv_cols_sellg(const IterParams p, int init) {
   StepInfo si;
-  if (!read_step(p, init != 0, si)) return;
+  if (!read_step(p, init != 0, si, 2)) return;
   if (p.push.on) push_wait(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1));
   const GatherPlain g{p.yg != nullptr ? p.yg : p.y[si.s1]};
   sellg_block<G>(p.sell_cg, g, p.aty[si.s1]);
@@ -660,7 +672,7 @@ __global__ void __launch_bounds__(BS) k_sell_range(const SellPlan S, GatherPlain
 template <bool LONG, int BS>
 __global__ void __launch_bounds__(BS) k_spmv_cols_sell(const IterParams p, int init) {
   StepInfo si;
-  if (!read_step(p, init != 0, si)) return;
+  if (!read_step(p, init != 0, si, 2)) return;
   if (p.push.on) push_wait(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1));
   const GatherPlain g{p.yg != nullptr ? p.yg : p.y[si.s1]};
   sell_block(p.sell_c, g, p.aty[si.s1]);
@@ -670,7 +682,7 @@ __global__ void __launch_bounds__(BS) k_spmv_cols_sell(const IterParams p, int i
 template <int G, bool LONG>
 __global__ void __launch_bounds__(kSpmvBlock) k_spmv_cols(const IterParams p, int init) {
   StepInfo si;
-  if (!read_step(p, init != 0, si)) return;
+  if (!read_step(p, init != 0, si, 2)) return;
   if (p.push.on) push_wait(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1));
   spmv_block_range<G, LONG>(p.plan_c, p.colptr, p.rowind, p.atval,
                             GatherPlain{p.yg != nullptr ? p.yg : p.y[si.s1]},
@@ -779,7 +791,7 @@ __device__ __forceinline__ void snap_cols(const IterParams& p, const StepInfo& s
 // Dual update + row-side report partials (one row per thread, coalesced).
 __global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init) {
   StepInfo si;
-  if (!read_step(p, init != 0, si)) return;
+  if (!read_step(p, init != 0, si, 1)) return;
   __shared__ double red[(kEpiBlock / 32) * kRowParts];
   __shared__ double out[kRowParts];
   double acc[kRowParts];
@@ -852,7 +864,7 @@ __device__ __forceinline__ void primal_span(const IterParams& p, const StepInfo&
 // the last block to finish runs finalize().
 __global__ void __launch_bounds__(kEpiBlock) k_primal(const IterParams p, int init) {
   StepInfo si;
-  if (!read_step(p, init != 0, si)) return;
+  if (!read_step(p, init != 0, si, 3)) return;
   __shared__ double red[(kEpiBlock / 32) * kColParts];
   __shared__ double out[kColParts];
   __shared__ bool last;

@@ -107,6 +107,8 @@ struct PushArgs {
 // Parameters of the fused iteration kernels (passed by value, captured into
 // CUDA graphs once per solve).
 // ---------------------------------------------------------------------------
+constexpr int kStampRing = 128;
+
 struct IterParams {
   int m, n;
   // CSR(A), scaled values
@@ -173,6 +175,8 @@ struct IterParams {
   // none. cancel_dev: block 0's copy of the cancel request for decide().
   const volatile unsigned* host_flags;
   unsigned* cancel_dev;
+  // in-graph phase stamps (stamp_phase): u64[kStampRing * 4] or null
+  unsigned long long* stamps;
 };
 
 // ---------------------------------------------------------------------------

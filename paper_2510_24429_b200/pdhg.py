@@ -128,6 +128,7 @@ def load_library(path: str = LIB_PATH):
         L.cclp_cu_begin.argtypes = [C.c_void_p, C.POINTER(_Config), C.POINTER(_Tol)]
         L.cclp_cu_advance.argtypes = [C.c_void_p, C.c_int64, _dp]
         L.cclp_cu_profile_kernels.argtypes = [C.c_void_p, C.c_int64, _dp]
+        L.cclp_cu_phase_profile.argtypes = [C.c_void_p, _dp, C.POINTER(C.c_int64)]
         L.cclp_cu_stream.restype = C.c_void_p
         L.cclp_cu_stream.argtypes = [C.c_void_p]
         L.cclp_cu_describe.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.c_int32]
@@ -154,7 +155,7 @@ EXPORTED_SYMBOLS = [
     "cclp_cu_last_error", "cclp_cu_stop_string", "cclp_cu_default_config",
     "cclp_cu_default_tolerances", "cclp_cu_create", "cclp_cu_destroy", "cclp_cu_solve",
     "cclp_cu_run_pdhg", "cclp_cu_matvec", "cclp_cu_matvec_transpose", "cclp_cu_ruiz",
-    "cclp_cu_estimate_norm", "cclp_cu_begin", "cclp_cu_advance", "cclp_cu_profile_kernels",
+    "cclp_cu_estimate_norm", "cclp_cu_begin", "cclp_cu_advance", "cclp_cu_profile_kernels", "cclp_cu_phase_profile",
     "cclp_cu_stream", "cclp_cu_describe", "cclp_cu_gaussian_start", "cclp_cu_partition",
     "cclp_cu_nccl_unique_id", "cclp_cu_sharded_create", "cclp_cu_sharded_solve",
     "cclp_cu_sharded_begin", "cclp_cu_sharded_advance", "cclp_cu_sharded_describe",
@@ -472,6 +473,17 @@ class Engine:
         out = (C.c_double * 4)()
         _check(self.L, self.L.cclp_cu_profile_kernels(self.ctx, iters, out))
         return dict(zip(["spmv_rows", "dual", "spmv_cols", "primal"], list(out)))
+
+    def phase_profile(self) -> dict:
+        """Median microseconds per step of rows / dual / cols / primal as they
+        ran inside the loop's CUDA graphs (in-kernel %globaltimer stamps of the
+        last 128 steps), plus the number of steps they cover."""
+        out = (C.c_double * 4)()
+        steps = C.c_int64()
+        _check(self.L, self.L.cclp_cu_phase_profile(self.ctx, out, C.byref(steps)))
+        d = dict(zip(["spmv_rows", "dual", "spmv_cols", "primal"], list(out)))
+        d["steps"] = steps.value
+        return d
 
     def stream_ptr(self) -> int:
         return int(self.L.cclp_cu_stream(self.ctx) or 0)

@@ -8,7 +8,7 @@ from integration import race
 from paper_2510_24429_b200 import lpgen
 
 pytestmark = pytest.mark.skipif(not race.available("cpu"),
-                                reason="oracle/_ref/librace_cpu.so not built (needs /root/reference)")
+                                reason="integration/lib/librace_cpu.so not built (needs /root/reference at build time)")
 
 
 def test_schedule_thresholds_examples():
