@@ -442,6 +442,8 @@ struct Context {
   ~Context();
   void upload(const cclp_cu_lp* lp);
   void build_csr();
+  void build_csr_from(const int* cptr, const int* ridx, const double* cval, int ncols, long long cnt);
+  void init_aux(int dev);
   void partition();
   void tune_spmv();
   bool rows_equality = false;
@@ -489,8 +491,19 @@ struct Context {
   int grow() const { return exact ? 1 : Grow; }
   int gcol() const { return exact ? 1 : Gcol; }
   void launch_spmv(bool transpose, const double* vec, double* out, bool scaled, const int* stop);
-  double reduce(const double* a, const double* bvec, long long len, int mode);
+  double reduce(const double* a, const double* bvec, long long len, int mode);  // reproducible
+  void launch_repro_max(int mode, const double* a, const double* bvec, long long len);
+  void launch_repro_sum(int mode, const double* a, const double* bvec, long long len, const double* Mdev,
+                        long long N);
+  void repro_local_max(int mode, const double* a, const double* bvec, long long len, double* M);
+  void repro_local_sums(int mode, const double* a, const double* bvec, long long len, const double* M,
+                        long long N, double* S);
   void ruiz(int iterations);
+  void ruiz_init();
+  bool ruiz_maxima(const double* s_g, const double* r_g);
+  void ruiz_update();
+  void power_rows(const double* vg, double* w, bool scaled);
+  void power_cols(const double* wg, double* u, bool scaled);
   double power_norm(int iterations, uint64_t seed, bool scaled, bool pregenerated = false);
   double* h_v0 = nullptr;  // pinned start vector of the power iteration
   // h_v0 holds the start vector of seed v0_seed (a pure function of (seed, n)):
@@ -512,8 +525,8 @@ struct Context {
   void setup(const cclp_cu_config& cfg);
   void init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thresholds,
                   int nthr, bool launch_init);
-  void shard_from(Context& F, int rank, int P, const std::vector<int>& rb, const std::vector<int>& cb,
-                  cudaStream_t shared);
+  void shard_from_host(const cclp_cu_lp* lp, int rank, int P, const std::vector<int>& rb,
+                       const std::vector<int>& cb, cudaStream_t shared, const std::vector<int>& panel_G);
   void begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thresholds,
              int nthr);
   void launch_iteration(bool init);
@@ -577,6 +590,19 @@ Context::~Context() {
   if (side) cudaStreamDestroy(side);
 }
 
+// A context without a matrix: the device's pool, a stream and scratch
+// allocation (the sharded coordinator's helper buffers).
+void Context::init_aux(int dev) {
+  device = dev;
+  phase_t0 = std::chrono::steady_clock::now();
+  ensure_pool(device);
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&ev_snap, cudaEventDisableTiming));
+  CK(cudaEventCreate(&ev_a));
+  CK(cudaEventCreate(&ev_b));
+}
+
 void Context::upload(const cclp_cu_lp* lp) {
   m = lp->m;
   n = lp->n;
@@ -628,33 +654,36 @@ void Context::upload(const cclp_cu_lp* lp) {
   mark(2);
 }
 
-void Context::build_csr() {
+void Context::build_csr() { build_csr_from(colptr, rowind, val_csc, n, nnz); }
+
+// CSR of the m x ncols matrix given by a device CSC (rows local, ascending
+// within each column): a stable radix sort of the entries by row, so within
+// a row the entries keep CSC order, i.e. ascending column.
+void Context::build_csr_from(const int* cptr, const int* ridx, const double* cval, int ncols, long long cnt) {
   rowptr = alloc<int>(m + 1);
-  colind = alloc<int>(nnz);
-  val_csr = alloc<double>(nnz);
-  if (nnz == 0) {
+  colind = alloc<int>(cnt);
+  val_csr = alloc<double>(cnt);
+  if (cnt == 0) {
     CK(cudaMemsetAsync(rowptr, 0, sizeof(int) * (m + 1), stream));
     return;
   }
-  // Stable radix sort of the CSC entries by row: within a row the entries
-  // keep CSC order, i.e. ascending column, as a CSR requires.
-  int* col_of = alloc<int>(nnz);
-  int* keys_out = alloc<int>(nnz);
-  int* perm_in = alloc<int>(nnz);
-  int* perm_out = alloc<int>(nnz);
-  k_expand_major<<<blocks_for(n), kBlock, 0, stream>>>(colptr, n, col_of);
-  k_iota<<<blocks_for(nnz), kBlock, 0, stream>>>(perm_in, nnz);
+  int* col_of = alloc<int>(cnt);
+  int* keys_out = alloc<int>(cnt);
+  int* perm_in = alloc<int>(cnt);
+  int* perm_out = alloc<int>(cnt);
+  k_expand_major<<<blocks_for(ncols), kBlock, 0, stream>>>(cptr, ncols, col_of);
+  k_iota<<<blocks_for(cnt), kBlock, 0, stream>>>(perm_in, cnt);
   CKL("expand");
   int bits = 1;
   while ((1LL << bits) < m) ++bits;
   size_t tmp_bytes = 0;
-  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, rowind, keys_out, perm_in, perm_out,
-                                     static_cast<int>(nnz), 0, bits, stream));
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, ridx, keys_out, perm_in, perm_out,
+                                     static_cast<int>(cnt), 0, bits, stream));
   void* tmp = alloc<char>(tmp_bytes);
-  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, rowind, keys_out, perm_in, perm_out,
-                                     static_cast<int>(nnz), 0, bits, stream));
-  k_offsets_from_sorted<<<blocks_for(m + 1), kBlock, 0, stream>>>(keys_out, nnz, m, rowptr);
-  k_gather_csr<<<blocks_for(nnz), kBlock, 0, stream>>>(perm_out, nnz, col_of, val_csc, colind, val_csr);
+  CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, ridx, keys_out, perm_in, perm_out,
+                                     static_cast<int>(cnt), 0, bits, stream));
+  k_offsets_from_sorted<<<blocks_for(m + 1), kBlock, 0, stream>>>(keys_out, cnt, m, rowptr);
+  k_gather_csr<<<blocks_for(cnt), kBlock, 0, stream>>>(perm_out, cnt, col_of, cval, colind, val_csr);
   CKL("csr");
   CK(cudaStreamSynchronize(stream));
   release(tmp);
@@ -687,7 +716,7 @@ void Context::partition() {
   rowp = alloc<double>(static_cast<size_t>(std::max(epi_grid, 148 * 8)) * kRowParts);
   colp = alloc<double>(static_cast<size_t>(std::max(epi_grid, 148 * 8)) * kColParts);
   // view kernels reuse rowp/colp with up to 148*4 blocks
-  work_part = alloc<double>(148 * 8 * 2);
+  work_part = alloc<double>(148 * 8 * 6);  // up to 148*4 blocks x 6 level sums
   counter = alloc<unsigned>(4);
   CK(cudaMemsetAsync(counter, 0, sizeof(unsigned) * 4, stream));
   scalars = alloc<double>(16);
@@ -1414,64 +1443,128 @@ void Context::launch_spmv(bool transpose, const double* vec, double* out, bool s
   CKL("spmv");
 }
 
-double Context::reduce(const double* a, const double* bvec, long long len, int mode) {
-  const int grid = blocks_for(len, kBlock, 148 * 4);
-  k_reduce<<<grid, kBlock, 0, stream>>>(a, bvec, len, mode, work_part, counter + 1, scalars);
-  CKL("reduce");
-  CK(cudaMemcpyAsync(h_scalars, scalars, sizeof(double), cudaMemcpyDeviceToHost, stream));
+// Reproducible reductions (repro_consts, setup_kernels.cuh): pass 1 the
+// per-term maxima into scalars[0..K), pass 2 the exact level sums into
+// scalars[2..2 + 3K), both on the stream. `N` is the GLOBAL term count (a
+// shard passes the full length), `Mdev` the global maxima on the device.
+void Context::launch_repro_max(int mode, const double* a, const double* bvec, long long len) {
+  const int grid = blocks_for(std::max(len, 1LL), kBlock, 148 * 4);
+  switch (mode) {
+    case 0: k_repro_max<0><<<grid, kBlock, 0, stream>>>(a, bvec, len, work_part, counter + 1, scalars); break;
+    case 1: k_repro_max<1><<<grid, kBlock, 0, stream>>>(a, bvec, len, work_part, counter + 1, scalars); break;
+    case 2: k_repro_max<2><<<grid, kBlock, 0, stream>>>(a, bvec, len, work_part, counter + 1, scalars); break;
+    default: k_repro_max<3><<<grid, kBlock, 0, stream>>>(a, bvec, len, work_part, counter + 1, scalars); break;
+  }
+  CKL("repro max");
+}
+void Context::launch_repro_sum(int mode, const double* a, const double* bvec, long long len, const double* Mdev,
+                               long long N) {
+  const int grid = blocks_for(std::max(len, 1LL), kBlock, 148 * 4);
+  double* out = scalars + 2;
+  switch (mode) {
+    case 0: k_repro_sum<0><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out); break;
+    case 1: k_repro_sum<1><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out); break;
+    case 2: k_repro_sum<2><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out); break;
+    default: k_repro_sum<3><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out); break;
+  }
+  CKL("repro sum");
+}
+// Host-synced halves for the sharded setup: the local maxima, then (given
+// the global maxima) the local exact level sums.
+void Context::repro_local_max(int mode, const double* a, const double* bvec, long long len, double* M) {
+  const int K = mode == 3 ? 2 : 1;
+  launch_repro_max(mode, a, bvec, len);
+  CK(cudaMemcpyAsync(h_scalars, scalars, sizeof(double) * K, cudaMemcpyDeviceToHost, stream));
   CK(cudaStreamSynchronize(stream));
-  return h_scalars[0];
+  for (int k = 0; k < K; ++k) M[k] = h_scalars[k];
+}
+void Context::repro_local_sums(int mode, const double* a, const double* bvec, long long len, const double* M,
+                               long long N, double* S) {
+  const int K = mode == 3 ? 2 : 1;
+  std::memcpy(h_scalars + 8, M, sizeof(double) * K);
+  CK(cudaMemcpyAsync(scalars + 8, h_scalars + 8, sizeof(double) * K, cudaMemcpyHostToDevice, stream));
+  launch_repro_sum(mode, a, bvec, len, scalars + 8, N);
+  CK(cudaMemcpyAsync(h_scalars, scalars + 2, sizeof(double) * 3 * K, cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  for (int k = 0; k < 3 * K; ++k) S[k] = h_scalars[k];
+}
+double Context::reduce(const double* a, const double* bvec, long long len, int mode) {
+  launch_repro_max(mode, a, bvec, len);
+  launch_repro_sum(mode, a, bvec, len, scalars, len);
+  CK(cudaMemcpyAsync(h_scalars, scalars + 2, sizeof(double) * 3, cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  return repro_final(h_scalars);
 }
 
 // Ruiz factors into r, s (scaling.cpp:46-90); ambiguous pow2_sqrt cases are
 // evaluated with the host libm exactly as the reference does.
-void Context::ruiz(int iterations) {
+void Context::ruiz_init() {
   k_fill<<<blocks_for(m), kBlock, 0, stream>>>(r, m, 1.0);
   k_fill<<<blocks_for(n), kBlock, 0, stream>>>(s, n, 1.0);
   CKL("ruiz init");
+}
+
+// One pass's row / column maxima of |a_ij| r_i s_j (exact, order-free) into
+// wm / wn; s_g and r_g are the gathered scales (this context's own r, s, or a
+// shard's padded full copies). Returns whether any factor is outside [1/2, 2).
+bool Context::ruiz_maxima(const double* s_g, const double* r_g) {
   double* rmax = wm;
   double* cmax = wn;
-  for (int t = 0; t < iterations; ++t) {
-    // max over each row / column of |a_ij| r_i s_j (exact, order-free)
-    auto absmax = [&](int G, int grid, const int* ptr, const int* idx, const double* val,
-                      const double* self, const double* other, int is_row, const int* start,
-                      double* out) {
-      with_group(G, [&](auto g) {
-        k_scaled_absmax<decltype(g)::value><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row,
-                                                                          start, out);
-      });
-    };
-    absmax(Grow, row_grid, rowptr, colind, val_csr, r, s, 1, row_start, rmax);
-    absmax(Gcol, col_grid, colptr, rowind, val_csc, s, r, 0, col_start, cmax);
-    CK(cudaMemsetAsync(iflags, 0, sizeof(int) * 4, stream));
-    k_ruiz_notdone<<<blocks_for(m), kBlock, 0, stream>>>(rmax, m, iflags);
-    k_ruiz_notdone<<<blocks_for(n), kBlock, 0, stream>>>(cmax, n, iflags);
-    CKL("ruiz max");
-    int hf[4];
-    CK(cudaMemcpyAsync(hf, iflags, sizeof(hf), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    if (!hf[0]) break;
-    k_ruiz_update<<<blocks_for(m), kBlock, 0, stream>>>(rmax, m, r, iflags + 1, amb_idx, 256);
-    k_ruiz_update<<<blocks_for(n), kBlock, 0, stream>>>(cmax, n, s, iflags + 2, amb_idx + 256, 256);
-    CKL("ruiz update");
-    CK(cudaMemcpyAsync(hf, iflags, sizeof(hf), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    for (int side_k = 0; side_k < 2; ++side_k) {
-      const int cnt = hf[1 + side_k];
-      if (cnt == 0) continue;
-      if (cnt > 256) throw Error(CCLP_CU_ECUDA, "ruiz: too many ambiguous pow2_sqrt cases");
-      std::vector<int> idx(cnt);
-      CK(cudaMemcpy(idx.data(), amb_idx + 256 * side_k, sizeof(int) * cnt, cudaMemcpyDeviceToHost));
-      double* mx = side_k == 0 ? rmax : cmax;
-      double* sc = side_k == 0 ? r : s;
-      for (int q = 0; q < cnt; ++q) {
-        double v, cur;
-        CK(cudaMemcpy(&v, mx + idx[q], sizeof(double), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(&cur, sc + idx[q], sizeof(double), cudaMemcpyDeviceToHost));
-        cur /= std::exp2(std::round(0.5 * std::log2(v)));  // pow2_sqrt, scaling.cpp:23-25
-        CK(cudaMemcpy(sc + idx[q], &cur, sizeof(double), cudaMemcpyHostToDevice));
-      }
+  auto absmax = [&](int G, int grid, const int* ptr, const int* idx, const double* val, const double* self,
+                    const double* other, int is_row, const int* start, double* out) {
+    with_group(G, [&](auto g) {
+      k_scaled_absmax<decltype(g)::value><<<grid, kBlock, 0, stream>>>(ptr, idx, val, self, other, is_row,
+                                                                        start, out);
+    });
+  };
+  absmax(Grow, row_grid, rowptr, colind, val_csr, r, s_g, 1, row_start, rmax);
+  absmax(Gcol, col_grid, colptr, rowind, val_csc, s, r_g, 0, col_start, cmax);
+  CK(cudaMemsetAsync(iflags, 0, sizeof(int) * 4, stream));
+  k_ruiz_notdone<<<blocks_for(m), kBlock, 0, stream>>>(rmax, m, iflags);
+  k_ruiz_notdone<<<blocks_for(n), kBlock, 0, stream>>>(cmax, n, iflags);
+  CKL("ruiz max");
+  int hf[4];
+  CK(cudaMemcpyAsync(hf, iflags, sizeof(hf), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  return hf[0] != 0;
+}
+
+// r_i /= pow2_sqrt(rowmax_i), s_j /= pow2_sqrt(colmax_j) (scaling.cpp:23-25,
+// :75-86); ambiguous pow2_sqrt cases are evaluated with the host libm
+// exactly as the reference does.
+void Context::ruiz_update() {
+  double* rmax = wm;
+  double* cmax = wn;
+  k_ruiz_update<<<blocks_for(m), kBlock, 0, stream>>>(rmax, m, r, iflags + 1, amb_idx, 256);
+  k_ruiz_update<<<blocks_for(n), kBlock, 0, stream>>>(cmax, n, s, iflags + 2, amb_idx + 256, 256);
+  CKL("ruiz update");
+  int hf[4];
+  CK(cudaMemcpyAsync(hf, iflags, sizeof(hf), cudaMemcpyDeviceToHost, stream));
+  CK(cudaStreamSynchronize(stream));
+  for (int side_k = 0; side_k < 2; ++side_k) {
+    const int cnt = hf[1 + side_k];
+    if (cnt == 0) continue;
+    if (cnt > 256) throw Error(CCLP_CU_ECUDA, "ruiz: too many ambiguous pow2_sqrt cases");
+    std::vector<int> idx(cnt);
+    CK(cudaMemcpy(idx.data(), amb_idx + 256 * side_k, sizeof(int) * cnt, cudaMemcpyDeviceToHost));
+    double* mx = side_k == 0 ? rmax : cmax;
+    double* sc = side_k == 0 ? r : s;
+    for (int q = 0; q < cnt; ++q) {
+      double v, cur;
+      CK(cudaMemcpy(&v, mx + idx[q], sizeof(double), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(&cur, sc + idx[q], sizeof(double), cudaMemcpyDeviceToHost));
+      cur /= std::exp2(std::round(0.5 * std::log2(v)));  // pow2_sqrt, scaling.cpp:23-25
+      CK(cudaMemcpy(sc + idx[q], &cur, sizeof(double), cudaMemcpyHostToDevice));
     }
+  }
+}
+
+// Ruiz factors into r, s (scaling.cpp:46-90).
+void Context::ruiz(int iterations) {
+  ruiz_init();
+  for (int t = 0; t < iterations; ++t) {
+    if (!ruiz_maxima(s, r)) break;
+    ruiz_update();
   }
 }
 
@@ -1605,9 +1698,6 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
   PowerCtrl pc{std::sqrt(nv), 0.0, 0, 0};
   CK(cudaMemcpyAsync(pctrl, &pc, sizeof(pc), cudaMemcpyHostToDevice, stream));
   k_div_scalar<<<blocks_for(n), kBlock, 0, stream>>>(v, &pctrl->nu, v, n);  // v /= v.norm()
-  const double* aval = scaled ? sval_csr : val_csr;
-  const double* atval = scaled ? sval_csc : val_csc;
-  const int rgrid = blocks_for(n, kBlock, 148 * 4);
   // Deferred geometry tuning: the first K iterations cycle through the four
   // candidates (one warm-up round, then `reps` timed rounds) with events
   // around each product; one host sync after them picks the geometry.
@@ -1642,28 +1732,15 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
       }
       choose_geometry(ms);
     }
-    const SpmvPlan Pr = plan(true), Pc = plan(false);
-    if (scaled && use_panels()) {  // w = A v (:57), panel by panel
-      for (int k = 0; k < static_cast<int>(panels.size()); ++k) {
-        const PanelArgs a = panel_args(k);
-        with_group_long(panels[k].G, a.plan.thr != 0x7fffffff, [&](auto g, auto l) {
-          k_spmv_range<decltype(g)::value, decltype(l)::value><<<panel_grid, kSpmvBlock, 0, stream>>>(
-              a.plan, a.ptr, a.idx, a.val, GatherPlain{v}, wm, 1, a.accumulate);
-        });
-      }
-    } else {
-      with_group_long(grow(), Pr.thr != 0x7fffffff, [&](auto g, auto l) {  // w = A v (:57)
-        k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_r, kSpmvBlock, 0, stream>>>(
-            Pr, rowptr, colind, aval, GatherPlain{v}, wm, rpg_r);
-      });
-    }
+    power_rows(v, wm, scaled);  // w = A v (:57)
     if (t < K) CK(cudaEventRecord(tune_ev[3 * t + 1], stream));
-    with_group_long(gcol(), Pc.thr != 0x7fffffff, [&](auto g, auto l) {  // u = A' w (:58)
-      k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(
-          Pc, colptr, rowind, atval, GatherPlain{wm}, u, rpg_c);
-    });
+    power_cols(wm, u, scaled);  // u = A' w (:58)
     if (t < K) CK(cudaEventRecord(tune_ev[3 * t + 2], stream));
-    k_power_reduce<<<rgrid, kBlock, 0, stream>>>(u, v, n, work_part, counter + 2, pctrl);
+    // nu = ||u||, lambda = v.u with the partition-free sums (sharded setups
+    // reproduce them bit for bit)
+    launch_repro_max(3, u, v, n);
+    launch_repro_sum(3, u, v, n, scalars, n);
+    k_power_finish<<<1, 1, 0, stream>>>(scalars + 2, pctrl);
     k_div_scalar<<<blocks_for(n), kBlock, 0, stream>>>(u, &pctrl->nu, v, n);  // v = u / norm
     CKL("power");
   }
@@ -1672,6 +1749,35 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
   CK(cudaStreamSynchronize(stream));
   if (pc.zero) return 0.0;
   return std::sqrt(std::max(pc.lambda, 0.0));
+}
+
+// The power iteration's products on the tuned SpMV plans (sharded: the
+// gathered vector is the padded full one).
+void Context::power_rows(const double* vg, double* w, bool scaled) {
+  const double* aval = scaled ? sval_csr : val_csr;
+  if (scaled && use_panels()) {  // panel by panel
+    for (int k = 0; k < static_cast<int>(panels.size()); ++k) {
+      const PanelArgs a = panel_args(k);
+      with_group_long(panels[k].G, a.plan.thr != 0x7fffffff, [&](auto g, auto l) {
+        k_spmv_range<decltype(g)::value, decltype(l)::value><<<panel_grid, kSpmvBlock, 0, stream>>>(
+            a.plan, a.ptr, a.idx, a.val, GatherPlain{vg}, w, 1, a.accumulate);
+      });
+    }
+  } else {
+    const SpmvPlan Pr = plan(true);
+    with_group_long(grow(), Pr.thr != 0x7fffffff, [&](auto g, auto l) {
+      k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_r, kSpmvBlock, 0, stream>>>(
+          Pr, rowptr, colind, aval, GatherPlain{vg}, w, rpg_r);
+    });
+  }
+}
+void Context::power_cols(const double* wg, double* u, bool scaled) {
+  const double* atval = scaled ? sval_csc : val_csc;
+  const SpmvPlan Pc = plan(false);
+  with_group_long(gcol(), Pc.thr != 0x7fffffff, [&](auto g, auto l) {
+    k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(
+        Pc, colptr, rowind, atval, GatherPlain{wg}, u, rpg_c);
+  });
 }
 
 void Context::launch_rows_half(bool init) {
@@ -2778,7 +2884,7 @@ int cclp_cu_sharded_begin(cclp_cu_sharded* ctx, const cclp_cu_config* cfg, const
   return guarded([&] {
     auto& S = ctx->s;
     cclp_cu::ck(cudaSetDevice(S.device), "cudaSetDevice");
-    validate_inputs_eq(S.full->equality, *cfg, *tol, nullptr, 0);
+    validate_inputs_eq(S.equality, *cfg, *tol, nullptr, 0);
     S.begin(*cfg, *tol, nullptr, 0);
     for (auto& sh : S.shards) {  // measurement mode: never converge, never hit the limit
       sh->params.eps_rel = -1.0;
@@ -2823,7 +2929,7 @@ int cclp_cu_sharded_solve(cclp_cu_sharded* ctx, const cclp_cu_config* cfg_in, co
     auto& S = ctx->s;
     cclp_cu::ck(cudaSetDevice(S.device), "cudaSetDevice");
     const cclp_cu_config cfg = *cfg_in;
-    validate_inputs_eq(S.full->equality, cfg, *tol, thresholds, nthr);
+    validate_inputs_eq(S.equality, cfg, *tol, thresholds, nthr);
     const auto wall0 = std::chrono::steady_clock::now();
     S.launches = 0;
     S.abort_req.store(0);

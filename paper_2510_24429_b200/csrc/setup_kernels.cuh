@@ -264,6 +264,174 @@ __global__ void __launch_bounds__(kBlock) k_reduce(const double* __restrict__ a,
   }
 }
 
+// ---- partition-independent (reproducible) sums ------------------------------
+// The setup's scalars (||b||, ||c||, omega's norms, the power iteration's
+// ||u|| and v.u; pdhg.cpp:53-61, :253-265) are sums whose rounding depends on
+// the order of the terms. To make the sharded solve bit-identical to one
+// device, every such sum is computed by error-free pre-rounding: with
+// M = max |term| and N the global term count (both partition-free), level k
+// rounds each term's remainder to a multiple of a quantum u_k (the extraction
+// (T_k + v) - T_k with T_k = 1.5 * 2^E_k), chosen so that any partial sum of N
+// such multiples is exactly representable. Each level's sum is then EXACT in
+// any order and over any split into blocks, shards or ranks, and the result
+// (S_1 + S_2) + S_3 carries ~3(53 - log2 N) bits below 2^E_1: the same
+// double on one device and on P shards. (Terms with M = 0, inf or nan fall
+// back to a plain sum, still order-dependent only in the degenerate case.)
+struct ReproConsts {
+  double T[3];
+  int ok;
+};
+__host__ __device__ inline ReproConsts repro_consts(double M, long long N) {
+  ReproConsts c{{0.0, 0.0, 0.0}, 0};
+  if (!(M > 0.0) || !(M <= 1.7e308) || N <= 0) return c;
+  int k = 1;
+  while ((1LL << k) <= N) ++k;  // N < 2^k
+  int e;
+  (void)frexp(M, &e);  // M < 2^e
+  const int E1 = e + k;
+  const int E2 = E1 - 53 + k;
+  const int E3 = E2 - 53 + k;
+  if (E1 > 1020 || E3 < -1000) return c;
+  c.T[0] = ldexp(1.5, E1);
+  c.T[1] = ldexp(1.5, E2);
+  c.T[2] = ldexp(1.5, E3);
+  c.ok = 1;
+  return c;
+}
+__host__ __device__ inline double repro_final(const double* S) { return (S[0] + S[1]) + S[2]; }
+
+// Terms of the reductions: mode 0 a_i^2, 1 (a_i b_i)^2, 2 a_i b_i,
+// 3 (two sums, the power iteration) a_i^2 and b_i a_i (= u^2, v.u).
+template <int MODE>
+struct ReproTerms {
+  static constexpr int K = MODE == 3 ? 2 : 1;
+  __device__ __forceinline__ static void at(const double* __restrict__ a, const double* __restrict__ b,
+                                            long long i, double* t) {
+    if (MODE == 0) {
+      t[0] = a[i] * a[i];
+    } else if (MODE == 1) {
+      const double q = a[i] * b[i];
+      t[0] = q * q;
+    } else if (MODE == 2) {
+      t[0] = a[i] * b[i];
+    } else {
+      const double ui = a[i];
+      t[0] = ui * ui;
+      t[1] = b[i] * ui;
+    }
+  }
+};
+
+// Pass 1: out[k] = max |term_k| (exact, order-free); the last block writes it.
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_repro_max(const double* __restrict__ a, const double* __restrict__ b,
+                                                      long long n, double* part, unsigned* counter,
+                                                      double* out) {
+  using F = ReproTerms<MODE>;
+  constexpr int K = F::K;
+  constexpr unsigned MX = (1u << K) - 1u;
+  __shared__ double red[(kBlock / 32) * K];
+  __shared__ double o[K];
+  __shared__ bool last;
+  double acc[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) acc[q] = 0.0;
+  for (long long i = blockIdx.x * (long long)kBlock + threadIdx.x; i < n; i += (long long)gridDim.x * kBlock) {
+    double t[K];
+    F::at(a, b, i, t);
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      const double v = fabs(t[q]);
+      acc[q] = (v != v) ? v : amax(acc[q], v);  // nan wins
+    }
+  }
+  block_reduce<K, MX>(acc, red, o);
+  if (threadIdx.x < K) part[blockIdx.x * K + threadIdx.x] = o[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < K) {
+    double mx = 0.0;
+    for (int bl = 0; bl < static_cast<int>(gridDim.x); ++bl) {
+      const double v = __ldcg(part + bl * K + threadIdx.x);
+      mx = (v != v) ? v : amax(mx, v);
+    }
+    out[threadIdx.x] = mx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// Pass 2: out[3k + l] = the exact level-l sum of term k, given its global
+// max Mx[k] and global count N (repro_consts); plain sums when !ok.
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_repro_sum(const double* __restrict__ a, const double* __restrict__ b,
+                                                      long long n, const double* __restrict__ Mx, long long N,
+                                                      double* part, unsigned* counter, double* out) {
+  using F = ReproTerms<MODE>;
+  constexpr int K = F::K;
+  constexpr int K3 = 3 * K;
+  __shared__ double red[(kBlock / 32) * K3];
+  __shared__ double o[K3];
+  __shared__ bool last;
+  ReproConsts c[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) c[q] = repro_consts(Mx[q], N);
+  double acc[K3];
+#pragma unroll
+  for (int q = 0; q < K3; ++q) acc[q] = 0.0;
+  for (long long i = blockIdx.x * (long long)kBlock + threadIdx.x; i < n; i += (long long)gridDim.x * kBlock) {
+    double t[K];
+    F::at(a, b, i, t);
+#pragma unroll
+    for (int q = 0; q < K; ++q) {
+      if (!c[q].ok) {
+        acc[3 * q] += t[q];
+        continue;
+      }
+      double v = t[q];
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        const double T = c[q].T[l];
+        const double x = (T + v) - T;  // v rounded to the level's quantum (exact)
+        acc[3 * q + l] += x;           // exact
+        v = v - x;                     // exact remainder
+      }
+    }
+  }
+  block_reduce<K3, 0u>(acc, red, o);
+  if (threadIdx.x < K3) part[blockIdx.x * K3 + threadIdx.x] = o[threadIdx.x];
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < K3) {
+    double sm = 0.0;
+    for (int bl = 0; bl < static_cast<int>(gridDim.x); ++bl) sm += __ldcg(part + bl * K3 + threadIdx.x);
+    out[threadIdx.x] = sm;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// The power iteration's scalars from the level sums of mode 3 (pdhg.cpp:59-61):
+// nu = ||u||, lambda = v.u; a zero norm sets `zero` (the reference returns 0).
+__global__ void k_power_finish(const double* __restrict__ S, PowerCtrl* pc) {
+  if (pc->zero) return;
+  const double norm = sqrt(repro_final(S));
+  if (norm == 0.0) {
+    pc->zero = 1;
+  } else {
+    pc->lambda = repro_final(S + 3);
+    pc->nu = norm;
+  }
+}
+
 __global__ void k_div_scalar(const double* __restrict__ a, const double* den, double* __restrict__ out,
                              long long n) {
   const double d = *den;

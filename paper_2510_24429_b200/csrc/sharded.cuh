@@ -151,10 +151,60 @@ void nck(ncclResult_t r, const char* what) {
     throw Error(CCLP_CU_ENCCL, std::string(what) + ": " + nccl().GetErrorString(r));
 }
 
-// ---- shard slicing ------------------------------------------------------------
-void Context::shard_from(Context& F, int rank, int P, const std::vector<int>& rb,
-                         const std::vector<int>& cb, cudaStream_t shared) {
-  device = F.device;
+// ---- shard slicing (from the caller's host CSC: no device copy of the full LP)
+// idx -> owner * S + (idx - bounds[owner]) in place (the padded full-vector index)
+__global__ void k_remap_idx(int* __restrict__ idx, long long cnt, const int* __restrict__ bounds, int P, int S) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < cnt;
+       q += (long long)gridDim.x * blockDim.x) {
+    const int j = idx[q];
+    int o = 0;
+    while (o + 1 < P && bounds[o + 1] <= j) ++o;
+    idx[q] = o * S + (j - bounds[o]);
+  }
+}
+
+// Runs body(t, lo, hi) on T host threads over [0, len).
+template <class F>
+void host_parallel(long long len, F&& body) {
+  const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  const long long per = (len + T - 1) / T;
+  std::vector<std::thread> th;
+  for (int t = 1; t < T; ++t)
+    th.emplace_back([&, t] { body(t, std::min(len, t * per), std::min(len, (t + 1) * per)); });
+  body(0, 0, std::min(len, per));
+  for (auto& x : th) x.join();
+}
+
+// The entries of rows [rlo, rhi) of the host CSC, still column-major (rows
+// ascend within a column, so each column's part is one binary-searched run):
+// cptr[n + 1], local row indices, values.
+void host_row_slice(const cclp_cu_lp* lp, int rlo, int rhi, std::vector<int>& cptr, std::vector<int>& ridx,
+                    std::vector<double>& val) {
+  const int n = lp->n;
+  std::vector<int> lo(n), hi(n);
+  cptr.assign(static_cast<size_t>(n) + 1, 0);
+  host_parallel(n, [&](int, long long a, long long b) {
+    for (long long j = a; j < b; ++j) {
+      const int* first = lp->rowind + lp->colptr[j];
+      const int* last = lp->rowind + lp->colptr[j + 1];
+      lo[j] = static_cast<int>(std::lower_bound(first, last, rlo) - lp->rowind);
+      hi[j] = static_cast<int>(std::lower_bound(first, last, rhi) - lp->rowind);
+    }
+  });
+  for (int j = 0; j < n; ++j) cptr[j + 1] = cptr[j] + (hi[j] - lo[j]);
+  ridx.resize(cptr[n]);
+  val.resize(cptr[n]);
+  host_parallel(n, [&](int, long long a, long long b) {
+    for (long long j = a; j < b; ++j)
+      for (int q = lo[j], o = cptr[j]; q < hi[j]; ++q, ++o) {
+        ridx[o] = lp->rowind[q] - rlo;
+        val[o] = lp->val[q];
+      }
+  });
+}
+
+void Context::shard_from_host(const cclp_cu_lp* lp, int rank, int P, const std::vector<int>& rb,
+                              const std::vector<int>& cb, cudaStream_t shared, const std::vector<int>& panel_G) {
   stream = shared;
   own_stream = false;
   CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
@@ -173,57 +223,63 @@ void Context::shard_from(Context& F, int rank, int P, const std::vector<int>& rb
     Sm = std::max(Sm, rb[q + 1] - rb[q]);
     Sn = std::max(Sn, cb[q + 1] - cb[q]);
   }
-  // the full matrix's lanes-per-row (the per-row summation order)
-  Grow = F.Grow;
-  Gcol = F.Gcol;
-  exact = F.exact;
-  b_norm = F.b_norm;
-  c_norm = F.c_norm;
-  norm_est = F.norm_est;
-  omega = F.omega;
-  tau = F.tau;
-  sigma = F.sigma;
-  equality = F.equality;
+  // the full matrix's lanes-per-row (the per-row summation order), from the
+  // global shape alone
+  const long long gnnz = lp->colptr[lp->n];
+  Grow = pick_group(gnnz, lp->m);
+  Gcol = pick_group(gnnz, lp->n);
+  equality = true;
   int* d_rb = alloc<int>(P + 1);
   int* d_cb = alloc<int>(P + 1);
   CK(cudaMemcpyAsync(d_rb, rb.data(), sizeof(int) * (P + 1), cudaMemcpyHostToDevice, stream));
   CK(cudaMemcpyAsync(d_cb, cb.data(), sizeof(int) * (P + 1), cudaMemcpyHostToDevice, stream));
-  auto slice = [&](const int* fptr, const int* fidx, const double* fval, const double* fsval, int first,
-                   int rows, const int* d_bounds, int S, int*& ptr_out, int*& idx_out,
-                   double*& val_out, double*& sval_out) -> long long {
-    int pe[2];
-    CK(cudaMemcpyAsync(&pe[0], fptr + first, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CK(cudaMemcpyAsync(&pe[1], fptr + first + rows, sizeof(int), cudaMemcpyDeviceToHost, stream));
-    CK(cudaStreamSynchronize(stream));
-    const long long cnt = static_cast<long long>(pe[1]) - pe[0];
-    ptr_out = alloc<int>(rows + 1);
-    idx_out = alloc<int>(cnt);
-    val_out = alloc<double>(cnt);
-    sval_out = alloc<double>(cnt);
-    k_slice_ptr<<<blocks_for(rows + 1), kBlock, 0, stream>>>(fptr, first, rows, ptr_out);
-    if (cnt > 0)
-      k_slice_remap<<<blocks_for(cnt), kBlock, 0, stream>>>(fidx + pe[0], fval + pe[0], fsval + pe[0], cnt,
-                                                             d_bounds, P, S, idx_out, val_out, sval_out);
-    CKL("shard slice");
-    return cnt;
-  };
-  const long long nnz_a = slice(F.rowptr, F.colind, F.val_csr, F.sval_csr, r0, m, d_cb, Sn, rowptr, colind,
-                                val_csr, sval_csr);
-  const long long nnz_at = slice(F.colptr, F.rowind, F.val_csc, F.sval_csc, c0, n, d_rb, Sm, colptr, rowind,
-                                 val_csc, sval_csc);
+  // rows [r0, r0 + m) of A as CSR (global columns -> padded x space)
+  long long nnz_a = 0;
+  {
+    std::vector<int> cptr, ridx;
+    std::vector<double> v;
+    host_row_slice(lp, r0, r0 + m, cptr, ridx, v);
+    nnz_a = static_cast<long long>(ridx.size());
+    int* d_cptr = alloc<int>(cptr.size());
+    int* d_ridx = alloc<int>(ridx.size());
+    double* d_val = alloc<double>(v.size());
+    h2d(d_cptr, cptr.data(), sizeof(int) * cptr.size());
+    h2d(d_ridx, ridx.data(), sizeof(int) * ridx.size());
+    h2d(d_val, v.data(), sizeof(double) * v.size());
+    build_csr_from(d_cptr, d_ridx, d_val, lp->n, nnz_a);  // synchronizes
+    release(d_cptr);
+    release(d_ridx);
+    release(d_val);
+    if (nnz_a > 0) k_remap_idx<<<blocks_for(nnz_a), kBlock, 0, stream>>>(colind, nnz_a, d_cb, P, Sn);
+    CKL("shard rows");
+  }
+  // columns [c0, c0 + n) of A (the caller's CSC, global rows -> padded y space)
+  const long long b0 = lp->colptr[c0];
+  const long long nnz_at = static_cast<long long>(lp->colptr[c0 + n]) - b0;
+  {
+    std::vector<int> cp(static_cast<size_t>(n) + 1);
+    for (int j = 0; j <= n; ++j) cp[j] = static_cast<int>(lp->colptr[c0 + j] - b0);
+    colptr = alloc<int>(n + 1);
+    rowind = alloc<int>(nnz_at);
+    val_csc = alloc<double>(nnz_at);
+    h2d(colptr, cp.data(), sizeof(int) * (n + 1));
+    h2d(rowind, lp->rowind + b0, sizeof(int) * nnz_at);
+    h2d(val_csc, lp->val + b0, sizeof(double) * nnz_at);
+    if (nnz_at > 0) k_remap_idx<<<blocks_for(nnz_at), kBlock, 0, stream>>>(rowind, nnz_at, d_rb, P, Sm);
+    CKL("shard cols");
+  }
   nnz = std::max(nnz_a, nnz_at);
-  auto vec = [&](const double* src, int off, int len) {
+  auto vec = [&](const double* src, int len) {
     double* d = alloc<double>(len);
-    if (len > 0)
-      CK(cudaMemcpyAsync(d, src + off, sizeof(double) * len, cudaMemcpyDeviceToDevice, stream));
+    if (len > 0) h2d(d, src, sizeof(double) * len);
     return d;
   };
-  c = vec(F.c, c0, n);
-  l = vec(F.l, c0, n);
-  u = vec(F.u, c0, n);
-  s = vec(F.s, c0, n);
-  b = vec(F.b, r0, m);
-  r = vec(F.r, r0, m);
+  c = vec(lp->c + c0, n);
+  l = vec(lp->col_lower + c0, n);
+  u = vec(lp->col_upper + c0, n);
+  b = vec(lp->row_lower + r0, m);
+  s = alloc<double>(n);
+  r = alloc<double>(m);
   // the buffers peers write into: plain cudaMalloc when they are shared with
   // other processes over CUDA IPC (pool memory cannot be exported)
   auto xalloc = [&](size_t count) -> double* {
@@ -244,23 +300,43 @@ void Context::shard_from(Context& F, int rank, int P, const std::vector<int>& rb
   CK(cudaMemsetAsync(x_full, 0, sizeof(double) * std::max<size_t>(1, size_t(P) * Sn), stream));
   CK(cudaMemsetAsync(y_full, 0, sizeof(double) * std::max<size_t>(1, size_t(P) * Sm), stream));
   CK(cudaMemsetAsync(xpart, 0, sizeof(double) * P * (kRowParts + kColParts), stream));
+  CK(cudaStreamSynchronize(stream));
   release(d_rb);
   release(d_cb);
-  panel_gn = F.n;  // column panels on the full matrix's column space
+  panel_gn = lp->n;  // column panels on the full matrix's column space
   panel_cb = cb;
-  for (const auto& pn : F.panels) panel_G_hint.push_back(pn.G);
+  panel_G_hint = panel_G;
   partition();  // setup-kernel grids, the local SpMV plans and their tuned geometry
-  for (auto& pn : panels)  // the shard never runs setup(): its panels take the scaled values here
-    if (pn.nnz > 0)
-      k_gather_vals<<<blocks_for(pn.nnz), kBlock, 0, stream>>>(pn.perm, pn.nnz, sval_csr, pn.val);
-  CKL("shard panel values");
+}
+
+// Per-panel lanes-per-row of the full matrix from the host CSC (build_panels'
+// layout: K panels of W original columns), so a shard's panel sums equal the
+// single device's bit for bit.
+std::vector<int> host_panel_groups(const cclp_cu_lp* lp) {
+  long long pb = static_cast<long long>(Context::kPanelBytes);
+  if (const char* e = std::getenv("CCLP_CU_PANEL_BYTES")) pb = std::max(64LL, std::atoll(e));  // tests
+  const long long gn = lp->n;
+  const long long K = (gn * 8 + pb - 1) / pb;
+  std::vector<int> G;
+  if (K < 3) return G;
+  const long long W = (gn + K - 1) / K;
+  for (long long k = 0; k < K; ++k) {
+    const long long lo = std::min(k * W, gn), hi = std::min((k + 1) * W, gn);
+    G.push_back(pick_group(static_cast<long long>(lp->colptr[hi]) - lp->colptr[lo], lp->m));
+  }
+  return G;
 }
 
 // ---- the sharded solve ---------------------------------------------------------
 struct Sharded {
   int P = 1, rank = 0, nranks = 1, device = 0;
   int m = 0, n = 0;  // global
-  std::unique_ptr<Context> full;                 // full matrix: setup (replicated per rank)
+  std::unique_ptr<Context> full;                 // no matrix: stream + coordinator scratch
+  bool equality = true;                          // all rows equality (run_pdhg's precondition)
+  long long gnnz = 0;                            // nonzeros of the full matrix
+  std::vector<int> panel_G;                      // the full matrix's per-panel lanes-per-row
+  std::vector<double> h_v0;                      // power-iteration start vector (full n)
+  unsigned long long v0_seed = ~0ull;
   std::vector<std::unique_ptr<Context>> shards;  // this process's shards
   std::vector<int> rb, cb;
   ncclComm_t comm = nullptr;
@@ -294,39 +370,56 @@ struct Sharded {
     double* recvbuf = nullptr;
   } halo_x, halo_y;
 
-  void build_halo(Halo& h, bool x_side) {
-    // x side: rows of A owned by p (full CSR), columns owned by q; y side:
-    // rows of A' = columns of A owned by p (the CSC), rows of A owned by q
-    const int* ptr = x_side ? full->rowptr : full->colptr;
-    const int* idx = x_side ? full->colind : full->rowind;
-    const std::vector<int>& own = x_side ? rb : cb;     // rows of this side's matrix per shard
-    const std::vector<int>& tgt = x_side ? cb : rb;     // gathered vector's split
-    const int len = x_side ? n : m;
+  // The lists come from the caller's host CSC, which every rank holds: no
+  // device copy of the full matrix and no extra communication.
+  void build_halo(Halo& h, bool x_side, const cclp_cu_lp* lp) {
     const long long S = x_side ? s0().Sn : s0().Sm;
     const long long allgather = static_cast<long long>(P) * (P - 1) * S;
-    unsigned char* flags = full->alloc<unsigned char>(len);
-    std::vector<unsigned char> hf(static_cast<size_t>(len));
     h.need.assign(P, std::vector<int*>(P, nullptr));
     h.cnt.assign(P, std::vector<int>(P, 0));
-    std::vector<std::vector<std::vector<int>>> lists(P, std::vector<std::vector<int>>(P));
     h.volume = 0;
-    for (int p = 0; p < P; ++p) {
-      CK(cudaMemsetAsync(flags, 0, std::max(1, len), stream));
-      if (own[p + 1] > own[p])
-        k_mark_cols<<<blocks_for(1 << 20), kBlock, 0, stream>>>(ptr, idx, own[p], own[p + 1], flags);
-      CKL("halo mark");
-      CK(cudaMemcpyAsync(hf.data(), flags, len, cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
+    h.on = false;
+    if (P < 2 || P > 64) return;
+    std::vector<int> rown(static_cast<size_t>(m)), coln(static_cast<size_t>(n));
+    for (int q = 0; q < P; ++q) {
+      for (int i = rb[q]; i < rb[q + 1]; ++i) rown[i] = q;
+      for (int j = cb[q]; j < cb[q + 1]; ++j) coln[j] = q;
+    }
+    std::vector<std::vector<std::vector<int>>> lists(P, std::vector<std::vector<int>>(P));
+    if (x_side) {
+      // shard p's rows gather x_j (column j, owner q) when a row of p has an entry in column j
+      std::vector<unsigned long long> mask(static_cast<size_t>(n), 0ull);
+      host_parallel(n, [&](int, long long a, long long b) {
+        for (long long j = a; j < b; ++j)
+          for (int q = lp->colptr[j]; q < lp->colptr[j + 1]; ++q) mask[j] |= 1ull << rown[lp->rowind[q]];
+      });
+      for (int j = 0; j < n; ++j) {
+        const int q = coln[j];
+        for (unsigned long long mk = mask[j] & ~(1ull << q); mk; mk &= mk - 1)
+          lists[__builtin_ctzll(mk)][q].push_back(j - cb[q]);
+      }
+    } else {
+      // shard p's columns gather y_i (row i, owner q) when a column of p has an entry in row i
+      std::vector<unsigned long long> mask(static_cast<size_t>(m), 0ull);
+      host_parallel(n, [&](int, long long a, long long b) {
+        for (long long j = a; j < b; ++j) {
+          const unsigned long long bit = 1ull << coln[j];
+          for (int q = lp->colptr[j]; q < lp->colptr[j + 1]; ++q)
+            __atomic_fetch_or(&mask[lp->rowind[q]], bit, __ATOMIC_RELAXED);
+        }
+      });
+      for (int i = 0; i < m; ++i) {
+        const int q = rown[i];
+        for (unsigned long long mk = mask[i] & ~(1ull << q); mk; mk &= mk - 1)
+          lists[__builtin_ctzll(mk)][q].push_back(i - rb[q]);
+      }
+    }
+    for (int p = 0; p < P; ++p)
       for (int q = 0; q < P; ++q) {
-        if (q == p) continue;
-        for (int j = tgt[q]; j < tgt[q + 1]; ++j)
-          if (hf[j]) lists[p][q].push_back(j - tgt[q]);
         h.cnt[p][q] = static_cast<int>(lists[p][q].size());
         h.volume += h.cnt[p][q];
       }
-    }
-    full->release(flags);
-    h.on = P > 1 && h.volume * 2 < allgather;
+    h.on = h.volume * 2 < allgather;
     if (!h.on) return;
     for (int p = 0; p < P; ++p)
       for (int q = 0; q < P; ++q)
@@ -590,17 +683,29 @@ struct Sharded {
     if (nr > 1 && local_shards != 1)
       throw std::invalid_argument("sharded: one shard per process with NCCL");
     full = std::make_unique<Context>();
-    full->device = dev;
-    full->upload(lp);
+    full->init_aux(dev);
     stream = full->stream;
-    // nnz-balanced row blocks of A (CSR built on the device) and of A^T
-    // (the caller's CSC): the same split on every rank
-    std::vector<int> rowptr_h(static_cast<size_t>(m) + 1);
-    CK(cudaMemcpy(rowptr_h.data(), full->rowptr, sizeof(int) * (m + 1), cudaMemcpyDeviceToHost));
+    // equality form, checked on the host view (lp.hpp:66-70)
+    for (int i = 0; i < m && equality; ++i)
+      equality = lp->row_lower[i] == lp->row_upper[i] && std::isfinite(lp->row_lower[i]);
+    // nnz-balanced row blocks of A (row counts from the caller's CSC) and of
+    // A^T (its column pointers): the same split on every rank
+    std::vector<int> rowptr_h(static_cast<size_t>(m) + 1, 0);
+    {
+      const long long nz = lp->colptr[n];
+      std::vector<std::atomic<int>> cnt(static_cast<size_t>(m));
+      for (auto& c : cnt) c.store(0, std::memory_order_relaxed);
+      host_parallel(nz, [&](int, long long a, long long b) {
+        for (long long q = a; q < b; ++q) cnt[lp->rowind[q]].fetch_add(1, std::memory_order_relaxed);
+      });
+      for (int i = 0; i < m; ++i) rowptr_h[i + 1] = rowptr_h[i] + cnt[i].load(std::memory_order_relaxed);
+    }
     rb.assign(P + 1, 0);
     cb.assign(P + 1, 0);
     host_partition(rowptr_h.data(), m, P, 4, rb.data());
     host_partition(lp->colptr, n, P, 4, cb.data());
+    panel_G = host_panel_groups(lp);
+    gnnz = lp->colptr[n];
     {  // transport: push (P2P stores fused into the producers) or NCCL / device-copy gathers
       const char* e = std::getenv("CCLP_CU_TRANSPORT");
       const bool want_push = e == nullptr || std::string(e) != "gather";  // push unless asked
@@ -612,6 +717,209 @@ struct Sharded {
       if (!nccl().ok) throw Error(CCLP_CU_ENCCL, nccl().err);
       nck(nccl().CommInitRank(&comm, nr, *id, rk), "ncclCommInitRank");
     }
+    // this process's shards, each holding only its slices of A / A^T and
+    // of the vectors (device memory ~ 1/P of the LP per shard)
+    const int first = multi() ? rank : 0;
+    const int count = multi() ? 1 : P;
+    for (int q = first; q < first + count; ++q) {
+      auto sh = std::make_unique<Context>();
+      sh->device = dev;
+      sh->ipc_buffers = push && multi();
+      sh->shard_from_host(lp, q, P, rb, cb, stream, panel_G);
+      shards.push_back(std::move(sh));
+    }
+    const char* e = std::getenv("CCLP_CU_HALO");  // 0: always all-gather (A/B)
+    if (e == nullptr || std::atoi(e) != 0) {
+      build_halo(halo_x, true, lp);
+      build_halo(halo_y, false, lp);
+    }
+    halo_built = true;
+    // the start vector of the default seed (full length: a shard takes its slice)
+    v0_seed = 0;
+    h_v0.resize(static_cast<size_t>(n));
+    if (n > 0) gaussian_start(0, n, h_v0.data());
+  }
+
+  // ---- distributed setup (scaling.cpp:46-90, pdhg.cpp:46-65, :253-267) -----
+  // Every rank works on its own slices; the setup exchanges are in-place
+  // all-gathers of the padded full r / s / v / w (x_full, y_full) and small
+  // host gathers of per-shard scalars. The maxima are order-free and the
+  // sums are the partition-free reproducible sums (k_repro_*), so every
+  // scale factor, ||A||, tau and sigma equal the single device's bit for bit.
+  void allgather_any(double* Context::*buf, size_t count) {
+    if (have_hcomm) {
+      Context& me = s0();
+      std::vector<double> mine(count);
+      CK(cudaMemcpyAsync(mine.data(), me.*buf + static_cast<size_t>(rank) * count, sizeof(double) * count,
+                         cudaMemcpyDeviceToHost, stream));
+      CK(cudaStreamSynchronize(stream));
+      const std::vector<char> all = gather_bytes(mine.data(), sizeof(double) * count);
+      CK(cudaMemcpyAsync(me.*buf, all.data(), all.size(), cudaMemcpyHostToDevice, stream));
+      CK(cudaStreamSynchronize(stream));
+      return;
+    }
+    allgather(buf, count);
+  }
+  // Combine per-shard host values over all shards of all ranks.
+  std::vector<double> combine(const std::vector<double>& local, bool is_max) {
+    std::vector<double> out = local;
+    if (!multi()) return out;
+    const std::vector<char> all = gather_bytes(local.data(), sizeof(double) * local.size());
+    const size_t K = local.size();
+    for (size_t k = 0; k < K; ++k) out[k] = is_max ? 0.0 : 0.0;
+    for (int q = 0; q < P; ++q)
+      for (size_t k = 0; k < K; ++k) {
+        double v;
+        std::memcpy(&v, all.data() + (q * K + k) * sizeof(double), sizeof v);
+        if (is_max)
+          out[k] = (v != v || out[k] != out[k]) ? NAN : std::max(out[k], v);
+        else
+          out[k] = out[k] + v;  // exact level sums: any order
+      }
+    return out;
+  }
+  // Reproducible global sum(s) of a per-shard term vector (mode as k_repro_*).
+  template <class A, class B, class L>
+  std::vector<double> global_sum(int mode, A a, B b, L len, long long N) {
+    const int K = mode == 3 ? 2 : 1;
+    std::vector<double> M(K, 0.0);
+    for (auto& sp : shards) {
+      double Ms[2];
+      sp->repro_local_max(mode, a(*sp), b(*sp), len(*sp), Ms);
+      for (int k = 0; k < K; ++k) M[k] = (Ms[k] != Ms[k] || M[k] != M[k]) ? NAN : std::max(M[k], Ms[k]);
+    }
+    M = combine(M, true);
+    std::vector<double> S(3 * K, 0.0);
+    for (auto& sp : shards) {
+      double Ss[6];
+      sp->repro_local_sums(mode, a(*sp), b(*sp), len(*sp), M.data(), N, Ss);
+      for (int k = 0; k < 3 * K; ++k) S[k] += Ss[k];
+    }
+    S = combine(S, false);
+    std::vector<double> out(K);
+    for (int k = 0; k < K; ++k) out[k] = repro_final(S.data() + 3 * k);
+    return out;
+  }
+  bool any_true(bool local) {
+    std::vector<double> v{local ? 1.0 : 0.0};
+    return combine(v, true)[0] > 0.0;
+  }
+  // r into every shard's y_full and s into its x_full (padded, in full)
+  void publish(double* Context::*own_m, double* Context::*own_n) {
+    for (auto& sp : shards) {
+      if (own_m && sp->m > 0)
+        CK(cudaMemcpyAsync(sp->y_full + static_cast<size_t>(sp->shard_rank) * sp->Sm, (*sp).*own_m,
+                           sizeof(double) * sp->m, cudaMemcpyDeviceToDevice, stream));
+      if (own_n && sp->n > 0)
+        CK(cudaMemcpyAsync(sp->x_full + static_cast<size_t>(sp->shard_rank) * sp->Sn, (*sp).*own_n,
+                           sizeof(double) * sp->n, cudaMemcpyDeviceToDevice, stream));
+    }
+    if (own_m) allgather_any(&Context::y_full, static_cast<size_t>(s0().Sm));
+    if (own_n) allgather_any(&Context::x_full, static_cast<size_t>(s0().Sn));
+  }
+
+  void dist_setup(const cclp_cu_config& cfg) {
+    for (auto& sp : shards) sp->exact = cfg.exact_spmv != 0;
+    auto none = [](Context&) -> const double* { return nullptr; };
+    auto lm = [](Context& c) { return static_cast<long long>(c.m); };
+    auto ln = [](Context& c) { return static_cast<long long>(c.n); };
+    // norms on the unscaled model (pdhg.cpp:253-254)
+    const double bn = std::sqrt(global_sum(0, [](Context& c) -> const double* { return c.b; }, none, lm, m)[0]);
+    const double cn = std::sqrt(global_sum(0, [](Context& c) -> const double* { return c.c; }, none, ln, n)[0]);
+    // Ruiz (scaling.cpp:46-90): row maxima need the gathered s, column maxima the gathered r
+    for (auto& sp : shards) sp->ruiz_init();
+    for (int t = 0; t < cfg.scaling_iterations; ++t) {
+      publish(&Context::r, &Context::s);
+      bool notdone = false;
+      for (auto& sp : shards) notdone = sp->ruiz_maxima(sp->x_full, sp->y_full) || notdone;
+      if (!any_true(notdone)) break;
+      for (auto& sp : shards) sp->ruiz_update();
+    }
+    publish(&Context::r, &Context::s);
+    for (auto& sp : shards) {  // A' = R A S on both slices, the reference's exact products
+      Context& c = *sp;
+      if (!c.sval_csr) c.sval_csr = c.alloc<double>(c.nnz);
+      if (!c.sval_csc) c.sval_csc = c.alloc<double>(c.nnz);
+      k_scale_values<<<blocks_for(static_cast<long long>(c.m) * 32), kBlock, 0, stream>>>(
+          c.rowptr, c.m, c.colind, c.val_csr, c.r, c.x_full, 1, c.sval_csr);
+      k_scale_values<<<blocks_for(static_cast<long long>(c.n) * 32), kBlock, 0, stream>>>(
+          c.colptr, c.n, c.rowind, c.val_csc, c.s, c.y_full, 0, c.sval_csc);
+      for (auto& pn : c.panels)
+        if (pn.nnz > 0)
+          k_gather_vals<<<blocks_for(pn.nnz), kBlock, 0, stream>>>(pn.perm, pn.nnz, c.sval_csr, pn.val);
+      CKL("shard scale");
+    }
+    // ||A||_2 by the power iteration (pdhg.cpp:46-65) over the shards
+    double norm = 0.0;
+    if (m > 0 && n > 0 && gnnz > 0) {
+      if (v0_seed != cfg.seed) {
+        h_v0.resize(static_cast<size_t>(n));
+        gaussian_start(cfg.seed, n, h_v0.data());
+        v0_seed = cfg.seed;
+      }
+      for (auto& sp : shards) {
+        sp->ensure_tuned();
+        if (sp->n > 0)
+          CK(cudaMemcpyAsync(sp->wn, h_v0.data() + sp->c0, sizeof(double) * sp->n, cudaMemcpyHostToDevice,
+                             stream));
+      }
+      auto vv = [](Context& c) -> const double* { return c.wn; };
+      double nv = global_sum(0, vv, none, ln, n)[0];
+      if (std::sqrt(nv) == 0.0) {
+        for (auto& sp : shards) k_fill<<<blocks_for(sp->n), kBlock, 0, stream>>>(sp->wn, sp->n, 1.0);
+        nv = global_sum(0, vv, none, ln, n)[0];
+      }
+      auto set_nu = [&](double nu) {
+        for (auto& sp : shards) {
+          PowerCtrl pc{nu, 0.0, 0, 0};
+          CK(cudaMemcpyAsync(sp->pctrl, &pc, sizeof pc, cudaMemcpyHostToDevice, stream));
+        }
+      };
+      set_nu(std::sqrt(nv));
+      for (auto& sp : shards)
+        k_div_scalar<<<blocks_for(sp->n), kBlock, 0, stream>>>(sp->wn, &sp->pctrl->nu, sp->wn, sp->n);
+      double lambda = 0.0;
+      bool zero = false;
+      for (int t = 0; t < cfg.norm_iterations; ++t) {
+        publish(nullptr, &Context::wn);  // v in full
+        for (auto& sp : shards) sp->power_rows(sp->x_full, sp->wm, true);  // w = A v
+        publish(&Context::wm, nullptr);  // w in full
+        for (auto& sp : shards) sp->power_cols(sp->y_full, sp->wn2, true);  // u = A' w
+        const std::vector<double> r2 = global_sum(
+            3, [](Context& c) -> const double* { return c.wn2; }, vv, ln, n);
+        const double nu = std::sqrt(r2[0]);
+        if (nu == 0.0) {
+          zero = true;
+          break;
+        }
+        lambda = r2[1];
+        set_nu(nu);
+        for (auto& sp : shards)
+          k_div_scalar<<<blocks_for(sp->n), kBlock, 0, stream>>>(sp->wn2, &sp->pctrl->nu, sp->wn, sp->n);
+        CKL("shard power");
+      }
+      norm = zero ? 0.0 : std::sqrt(std::max(lambda, 0.0));
+    } else {
+      for (auto& sp : shards) sp->ensure_tuned();
+    }
+    const double a_norm = norm > 0.0 ? norm : 1.0;
+    double omega = cfg.primal_weight;
+    if (omega <= 0.0) {  // pdhg.cpp:260-265 on the scaled model
+      const double cs = std::sqrt(global_sum(1, [](Context& c) -> const double* { return c.c; },
+                                             [](Context& c) -> const double* { return c.s; }, ln, n)[0]);
+      const double bs = std::sqrt(global_sum(1, [](Context& c) -> const double* { return c.b; },
+                                             [](Context& c) -> const double* { return c.r; }, lm, m)[0]);
+      omega = (cs > 0.0 && bs > 0.0) ? cs / bs : 1.0;
+    }
+    for (auto& sp : shards) {
+      sp->b_norm = bn;
+      sp->c_norm = cn;
+      sp->norm_est = norm;
+      sp->omega = omega;
+      sp->tau = cfg.step_scale * omega / a_norm;
+      sp->sigma = cfg.step_scale / (omega * a_norm);
+    }
+    CK(cudaStreamSynchronize(stream));
   }
 
   void build_shards(const cclp_cu_config& cfg) {
@@ -619,28 +927,10 @@ struct Sharded {
       cudaGraphExecDestroy(graph);
       graph = nullptr;
     }
-    shards.clear();
-    full->exact = cfg.exact_spmv != 0;
-    k_stamp<<<1, 1, 0, stream>>>(full->t0);
-    CKL("stamp");
-    full->setup(cfg);
-    const int first = multi() ? rank : 0;
-    const int count = multi() ? 1 : P;
-    for (int q = first; q < first + count; ++q) {
-      auto sh = std::make_unique<Context>();
-      sh->ipc_buffers = push && multi();
-      sh->shard_from(*full, q, P, rb, cb, stream);
+    dist_setup(cfg);
+    for (auto& sh : shards) {
       k_stamp<<<1, 1, 0, stream>>>(sh->t0);
       CKL("stamp");
-      shards.push_back(std::move(sh));
-    }
-    if (!halo_built) {
-      const char* e = std::getenv("CCLP_CU_HALO");  // 0: always all-gather (A/B)
-      if (e == nullptr || std::atoi(e) != 0) {
-        build_halo(halo_x, true);
-        build_halo(halo_y, false);
-      }
-      halo_built = true;
     }
   }
 
