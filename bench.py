@@ -21,6 +21,11 @@ x and the report sums each iteration; iterates bit-identical to one GPU):
 value = iterations/s of that one solve (strong scaling), device time max
 over ranks.
 
+Every N > 1 replica line also carries `partitioned`: C4 (configs[3], 100M nnz)
+row-block sharded over the N ranks (5 x 50 iterations, device time max over
+ranks, per-GPU fraction of the HBM roofline); at N = 1 it is the single
+engine's C4 line (`per_config`).
+
 `--impl reference` times the reference's own run_pdhg (oracle/_ref, built
 from /root/reference's sources) on the host cores of rank 0.
 """
@@ -308,14 +313,18 @@ def _fresh_nccl_id(pg, rank, dev):
     return bytes(idt.cpu().numpy().tobytes())
 
 
-def run_sharded_arm(args, world, rank, local, pg):
-    """N ranks, one row-block shard each (cclp_cu_sharded over NCCL)."""
+def run_sharded_arm(args, world, rank, local, pg, emit=True, workload=None, steps=None, iters=None,
+                    e2e=True):
+    """N ranks, one row-block shard each (cclp_cu_sharded over NCCL). With
+    emit=False the line is returned (rank 0) instead of printed: the
+    `partitioned` record of a replica run."""
     import torch
     from paper_2510_24429_b200 import lpgen
     from paper_2510_24429_b200.pdhg import PdhgConfig, ShardedEngine, nccl_unique_id
 
     dev = torch.device("cuda", local)
-    lp = lpgen.make_config(args.workload)
+    workload = workload or args.workload
+    lp = lpgen.make_config(workload)
     if ONE_DEVICE:
         def host_allgather(blob: bytes):
             parts = [None] * world
@@ -331,9 +340,11 @@ def run_sharded_arm(args, world, rank, local, pg):
         nccl_id = bytes(idt.cpu().numpy().tobytes())
         make = lambda src: ShardedEngine(src, 1, device=local, rank=rank, nranks=world,  # noqa: E731
                                          nccl_id=nccl_id if src is lp else _fresh_nccl_id(pg, rank, dev))
+    t_setup = time.perf_counter()
     eng = make(lp)
     eng.begin(PdhgConfig())
-    K, W, I = args.steps, args.warmup, args.iters_per_step
+    t_setup = allreduce_max(pg, time.perf_counter() - t_setup, dev)
+    K, W, I = steps or args.steps, args.warmup, iters or args.iters_per_step
     for _ in range(W):
         eng.advance(I)
     torch.cuda.synchronize(dev)
@@ -345,6 +356,20 @@ def run_sharded_arm(args, world, rank, local, pg):
     d = eng.describe()
     eng.close()
     value = K * I / (t_max * 1e-3)
+    B = 24 * lp.nnz + 20 * (lp.m + lp.n) + 8
+    peak, peak_kind = measured_peak_gbs()
+    if not e2e:
+        if rank != 0:
+            return None
+        return {"workload": workload, "m": lp.m, "n": lp.n, "nnz": lp.nnz, "shards": world,
+                "iters_per_s": value, "us_per_iteration": t_max * 1e3 / (K * I), "iters_timed": K * I,
+                "setup_s_incl_create": t_setup,
+                "iteration_frac_per_gpu": B * value / 1e9 / world / peak,
+                "row_bounds": d["row_bounds"], "col_bounds": d["col_bounds"],
+                "halo_x": d["halo_x"], "halo_y": d["halo_y"],
+                "slice_nnz": [(s_["nnz_rows"], s_["nnz_cols"]) for s_ in d["local_shards"]],
+                "transport": "push (P2P stores over CUDA IPC)" if ONE_DEVICE else "NCCL / push",
+                "clocks": clk.summary()}
     # e2e: every rank builds its shard engine from the LP in pinned host
     # memory and solves `--e2e-iters` iterations, result gathered to every
     # rank (upload, slicing, setup, loop, download); max over ranks
@@ -356,15 +381,13 @@ def run_sharded_arm(args, world, rank, local, pg):
         res = e2.solve(cfg)
     e2e_t = allreduce_max(pg, time.perf_counter() - t, dev)
     e2e_value = res.iterations / e2e_t
-    B = 24 * lp.nnz + 20 * (lp.m + lp.n) + 8
-    peak, peak_kind = measured_peak_gbs()
     if rank == 0:
         line = {
-            "metric": metric_for(args.workload), "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": metric_for(workload), "value": value, "unit": UNIT, "n_gpus": world,
             "steps": K, "warmup": W, "ms_per_step": t_max / K, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded generator, paper_2510_24429_b200/lpgen.py)",
-            "config": {"workload": args.workload, "m": lp.m, "n": lp.n, "nnz": lp.nnz,
+            "config": {"workload": workload, "m": lp.m, "n": lp.n, "nnz": lp.nnz,
                        "iters_per_step": I, "check_interval": 1,
                        "parallelism": f"row-block sharded x{world} (NCCL all-gather)",
                        "row_bounds": d["row_bounds"], "col_bounds": d["col_bounds"],
@@ -443,6 +466,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--per-config", default="C3,C4",
                     help="extra configs timed in the same N=1 run ('' to skip)")
+    ap.add_argument("--partitioned", default="C4",
+                    help="config of the per-N partitioned record ('' to skip)")
     ap.add_argument("--no-ttt", action="store_true", help="skip the time-to-tolerance solves (profiling runs)")
     ap.add_argument("--workload", default=CONFIG_NAME,
                     help="C2 (default, configs[1]); C3/C4/C5/C5s: with N>1 the sharded solve")
@@ -548,6 +573,14 @@ def main():
         ttt = [ttt, {"eps_rel": 1e-6, "seconds": time.perf_counter() - t,
                      "iterations": r6.iterations, "stop": r6.stop.name, "restarts": r6.restarts}]
 
+    # the partitioned path (north_star (4)) at this N: C4 row-block sharded
+    # over the N ranks (N = 1: the single engine's C4 line below)
+    partitioned = None
+    if world > 1 and args.partitioned:
+        torch.cuda.synchronize(dev)
+        partitioned = run_sharded_arm(args, world, rank, local, pg, emit=False, workload=args.partitioned,
+                                      steps=5, iters=50, e2e=False)
+
     per_config = None
     if rank == 0 and world == 1 and args.per_config:
         per_config = {c: per_config_line(c, args, local) for c in args.per_config.split(",") if c}
@@ -598,6 +631,10 @@ def main():
         }
         if per_config:
             line["per_config"] = per_config
+            if args.partitioned in per_config:
+                partitioned = dict(per_config[args.partitioned], shards=1, workload=args.partitioned)
+        if partitioned:
+            line["partitioned"] = partitioned
         print(json.dumps(line), flush=True)
     if pg is not None:
         pg.destroy_process_group()

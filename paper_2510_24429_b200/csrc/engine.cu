@@ -514,6 +514,7 @@ struct Context {
   // `shard_count`, owning rows [r0, r0 + m) of A and columns [c0, c0 + n)
   bool own_stream = true;
   int shard_rank = 0, shard_count = 1, r0 = 0, c0 = 0, Sm = 0, Sn = 0;
+  long long nnz_rows_slice = 0, nnz_cols_slice = 0;  // this shard's part of A (rows) / A' (rows)
   double* x_full = nullptr;  // [P * Sn] padded full x (gather source of the row SpMV)
   double* y_full = nullptr;  // [P * Sm] padded full y (gather source of the column SpMV)
   double* xpart = nullptr;   // [P][kRowParts + kColParts] exchanged report sums
@@ -2876,6 +2877,12 @@ int cclp_cu_sharded_describe(cclp_cu_sharded* ctx, int64_t* out, int32_t nout) {
   v.push_back(S.halo_x.volume);
   v.push_back(S.halo_y.on ? 1 : 0);
   v.push_back(S.halo_y.volume);
+  v.push_back(static_cast<int64_t>(S.shards.size()));  // this process's shards:
+  for (const auto& sh : S.shards) {                   // rank, nnz of its A rows / A' rows
+    v.push_back(sh->shard_rank);
+    v.push_back(sh->nnz_rows_slice);
+    v.push_back(sh->nnz_cols_slice);
+  }
   for (int i = 0; i < nout && i < static_cast<int>(v.size()); ++i) out[i] = v[i];
   return CCLP_CU_OK;
 }

@@ -269,6 +269,8 @@ void Context::shard_from_host(const cclp_cu_lp* lp, int rank, int P, const std::
     CKL("shard cols");
   }
   nnz = std::max(nnz_a, nnz_at);
+  nnz_rows_slice = nnz_a;
+  nnz_cols_slice = nnz_at;
   auto vec = [&](const double* src, int len) {
     double* d = alloc<double>(len);
     if (len > 0) h2d(d, src, sizeof(double) * len);

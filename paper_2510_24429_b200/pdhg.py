@@ -593,15 +593,18 @@ class ShardedEngine:
         self.close()
 
     def describe(self) -> dict:
-        out = (C.c_int64 * 64)()
-        self.L.cclp_cu_sharded_describe(self.ctx, out, 64)
+        out = (C.c_int64 * 256)()
+        self.L.cclp_cu_sharded_describe(self.ctx, out, 256)
         P = int(out[0])
         rb = list(out[1:P + 2])
         cb = list(out[P + 2:2 * P + 3])
         o = 2 * P + 3
+        nloc = int(out[o + 5])
+        local = [dict(rank=int(out[o + 6 + 3 * k]), nnz_rows=int(out[o + 7 + 3 * k]),
+                      nnz_cols=int(out[o + 8 + 3 * k])) for k in range(nloc)]
         return dict(shards=P, row_bounds=rb, col_bounds=cb, launches=int(out[o]),
                     halo_x=bool(out[o + 1]), halo_x_volume=int(out[o + 2]),
-                    halo_y=bool(out[o + 3]), halo_y_volume=int(out[o + 4]))
+                    halo_y=bool(out[o + 3]), halo_y_volume=int(out[o + 4]), local_shards=local)
 
     def solve(self, config: Optional[PdhgConfig] = None, tol: Optional[Tolerances] = None,
               thresholds: Sequence[float] = (), sink=None, cancel=None) -> PdhgResult:

@@ -129,3 +129,28 @@ def test_sharded_column_panels_bit_identical(P, monkeypatch):
     sh = run_pdhg_sharded(lp, P, cfg)
     assert np.array_equal(sh.iterate.x, one.iterate.x)
     assert np.array_equal(sh.iterate.y, one.iterate.y)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_shards_hold_only_their_slices_and_setup_is_bit_identical(P):
+    """No device copy of the full LP: shard p holds only the nonzeros of its
+    row block of A and its column block of A' (sum = nnz, each ~ nnz/P), and
+    the distributed setup (Ruiz over all-gathered scales, the power iteration
+    over the shards, reproducible sums) gives the single device's
+    ||A||, omega, tau and sigma bit for bit."""
+    lp = lpgen.staircase_lp(stages=32, cols_per_stage=400, rows_per_stage=200, seed=6)[0]
+    cfg = PdhgConfig(max_iterations=50)
+    one = run_pdhg(lp, cfg)
+    with ShardedEngine(lp, P) as eng:
+        sh = eng.solve(cfg)
+        d = eng.describe()
+    loc = d["local_shards"]
+    assert [s["rank"] for s in loc] == list(range(P))
+    assert sum(s["nnz_rows"] for s in loc) == lp.nnz
+    assert sum(s["nnz_cols"] for s in loc) == lp.nnz
+    for s in loc:
+        assert s["nnz_rows"] <= 1.25 * lp.nnz / P and s["nnz_cols"] <= 1.25 * lp.nnz / P
+    for k in ("norm_estimate", "omega", "tau", "sigma"):
+        assert getattr(sh, k) == getattr(one, k), k
+    assert np.array_equal(sh.iterate.x, one.iterate.x)
+    assert np.array_equal(sh.iterate.y, one.iterate.y)
