@@ -39,6 +39,10 @@ def lib(kind: str):
                                          C.c_double, C.c_char_p, C.c_int]
         L.cclp_race_standard_form_check.argtypes = [C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp, _dp,
                                                     _dp, _dp, C.c_int, C.c_int, _dp]
+        L.cclp_race_set_crossover.argtypes = [C.c_int, C.c_int]
+        L.cclp_race_crossover.argtypes = [C.c_int, C.c_int, _ip, _ip, _dp, _dp, _dp, _dp, _dp, _dp, _dp, _dp,
+                                          C.c_double, C.c_double, C.c_int, C.c_int, C.c_char_p, C.c_int]
+        L.cclp_race_pricing_counts.argtypes = [C.POINTER(C.c_longlong)]
         _cache[kind] = L
     return _cache[kind]
 
@@ -64,10 +68,50 @@ def standard_form_check(lp, maximize: bool = False, named: bool = False, kind: s
     return out + ((float(t[0]), float(t[1])),) if timings else out
 
 
+CROSSOVER = {"reference": 0, "scalable": 1, "scalable-device": 2}
+
+
+def set_crossover(kind: str, crossover: str, device: int = 0) -> None:
+    """The race's crossover (race_capi.cpp cclp_race_set_crossover): the
+    reference's run_crossover, or crossover_scalable.cpp with host or B200
+    pricing. Library defaults: gpu -> scalable-device, cpu -> reference."""
+    L = lib(kind)
+    if L.cclp_race_set_crossover(CROSSOVER[crossover], device) != 0:
+        raise RuntimeError(L.cclp_race_last_error().decode())
+
+
+def crossover(std_lp, x, y, z, threshold: float, crossover: str = "scalable", eps_abs: float = 1e-6,
+              kind: str = "cpu", device: int = 0) -> dict:
+    """One run_crossover on an equality-form LP from the iterate (x, y, z):
+    status, sorted basic set, objective, pivots, seconds and the scalable
+    engine's statistics (race_capi.cpp cclp_race_crossover)."""
+    L = lib(kind)
+    k = [np.ascontiguousarray(std_lp.colptr, np.int32), np.ascontiguousarray(std_lp.rowind, np.int32)]
+    d = [np.ascontiguousarray(a, np.float64) for a in (std_lp.val, std_lp.c, std_lp.row_lower, std_lp.col_lower,
+                                                       std_lp.col_upper, x, y, z)]
+    cap = 64 * 1024 + 24 * std_lp.m
+    buf = C.create_string_buffer(cap)
+    rc = L.cclp_race_crossover(std_lp.m, std_lp.n, k[0].ctypes.data_as(_ip), k[1].ctypes.data_as(_ip),
+                               *[a.ctypes.data_as(_dp) for a in d], threshold, eps_abs, CROSSOVER[crossover],
+                               device, buf, cap)
+    if rc != 0:
+        raise RuntimeError(L.cclp_race_last_error().decode())
+    return json.loads(buf.value.decode())
+
+
+def pricing_counts(kind: str) -> tuple:
+    """(device, host) pricing calls made by scalable crossovers so far."""
+    out = (C.c_longlong * 2)()
+    lib(kind).cclp_race_pricing_counts(out)
+    return int(out[0]), int(out[1])
+
+
 def run_race(lp, kind: str = "gpu", mode: str = "concurrent", eps_rel: float = 1e-6,
              eps_cross: float = 1e-2, eps_abs: float = 1e-6, time_limit: float = 3600.0,
-             pool: int = 4, max_iterations: int = 2_000_000) -> dict:
+             pool: int = 4, max_iterations: int = 2_000_000, crossover: str = None) -> dict:
     L = lib(kind)
+    if crossover is not None:
+        set_crossover(kind, crossover)
     k = [np.ascontiguousarray(lp.colptr, np.int32), np.ascontiguousarray(lp.rowind, np.int32)]
     d = [np.ascontiguousarray(a, np.float64) for a in (lp.val, lp.c, lp.row_lower, lp.row_upper,
                                                        lp.col_lower, lp.col_upper)]

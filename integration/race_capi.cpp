@@ -5,6 +5,7 @@
 // reference's own CPU loop). Crossover is the reference's run_crossover in
 // both, compiled from /root/reference, so the two differ only in the PDHG.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -15,9 +16,11 @@
 #include <vector>
 
 #include <fstream>
+#include <memory>
 
 #include "cclp/mps.hpp"
 #include "cclp/race.hpp"
+#include "crossover_scalable.hpp"
 #include "json.hpp"
 
 namespace {
@@ -93,9 +96,99 @@ namespace cclp {
 StandardFormMap to_standard_form_direct(const LinearProgram& lp);
 }
 
+namespace cclp_race {
+extern std::atomic<int> g_crossover, g_device;
+extern std::atomic<long long> g_device_prices, g_host_prices;
+}  // namespace cclp_race
+
 extern "C" {
 
 const char* cclp_race_last_error() { return g_err.c_str(); }
+
+// The race's crossover: 0 the reference's run_crossover, 1 the scalable one
+// with host pricing, 2 the scalable one with pricing on the B200 (device).
+// Returns 0, or 1 when kind 2 is asked of a library without the engine.
+int cclp_race_set_crossover(int kind, int device) {
+#ifdef CCLP_XO_NO_DEVICE
+  if (kind == 2) {
+    g_err = "cclp_race_set_crossover: this library has no B200 engine (device pricing)";
+    return 1;
+  }
+#endif
+  cclp_race::g_crossover.store(kind);
+  cclp_race::g_device.store(device);
+  return 0;
+}
+int cclp_race_get_crossover() { return cclp_race::g_crossover.load(); }
+
+// One crossover (crossover.hpp:61-85) on an equality-form LP from a given
+// iterate (the snapshot x, y, z in that space), timed: kind as
+// cclp_race_set_crossover. `out` receives the result JSON (status, sorted
+// basic set, objective, pivots, seconds and the scalable engine's stats).
+int cclp_race_crossover(int m, int n, const int* colptr, const int* rowind, const double* val, const double* c,
+                        const double* b, const double* cl, const double* cu, const double* x, const double* y,
+                        const double* z, double threshold, double eps_abs, int kind, int device, char* out,
+                        int cap) {
+  try {
+    cclp::LinearProgram lp;
+    lp.A = cclp::SparseMat(Eigen::Map<cclp::SparseMat>(m, n, colptr[n], colptr, rowind, val));
+    lp.c = vec(c, n);
+    lp.row_lower = vec(b, m);
+    lp.row_upper = vec(b, m);
+    lp.col_lower = vec(cl, n);
+    lp.col_upper = vec(cu, n);
+    lp.sense.assign(static_cast<size_t>(m), cclp::RowSense::kEq);
+    cclp::CrossoverTask task;
+    task.std_lp = &lp;
+    task.snapshot.x = vec(x, n);
+    task.snapshot.y = vec(y, m);
+    task.snapshot.z = vec(z, n);
+    task.launch_threshold = threshold;
+    task.tol.eps_abs = eps_abs;
+    cclp_xo::ScalableStats st;
+    double pricer_s = 0.0;
+    const auto t0 = std::chrono::steady_clock::now();
+    cclp::CrossoverResult r;
+    if (kind == 0) {
+      r = cclp::run_crossover(task);
+    } else {
+      std::unique_ptr<cclp_xo::DevicePricer> pricer;
+      if (kind == 2) {
+        const auto tp = std::chrono::steady_clock::now();
+        pricer = std::make_unique<cclp_xo::DevicePricer>(lp, device);
+        pricer_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - tp).count();
+      }
+      r = cclp_xo::run_crossover(task, pricer.get(), &st);
+    }
+    const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::vector<long long> basic(r.basis.basic.begin(), r.basis.basic.end());
+    std::sort(basic.begin(), basic.end());
+    double obj = 0.0;
+    for (int j = 0; j < n && r.iterate.x.size() == n; ++j) obj += lp.c[j] * r.iterate.x[j];
+    nlohmann::json j{{"status", cclp::to_string(r.status)}, {"basic", basic}, {"objective", obj},
+                     {"pivots", r.cleanup_pivots}, {"seconds", r.seconds}, {"wall_s", wall},
+                     {"pricer_setup_s", pricer_s}, {"violation", r.abs_violation},
+                     {"crash_candidates", st.crash_candidates}, {"crash_accepted", st.crash_accepted},
+                     {"lu_nnz", st.lu_nnz}, {"device_prices", st.device_prices},
+                     {"host_prices", st.host_prices}, {"crash_s", st.crash_s}, {"simplex_s", st.simplex_s},
+                     {"verify_s", st.verify_s}};
+    const std::string s2 = j.dump();
+    if (static_cast<int>(s2.size()) + 1 > cap) {
+      g_err = "cclp_race_crossover: output buffer too small";
+      return 2;
+    }
+    std::memcpy(out, s2.c_str(), s2.size() + 1);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+// Pricing calls made by scalable crossovers since load: [0] device, [1] host.
+void cclp_race_pricing_counts(long long* out) {
+  out[0] = cclp_race::g_device_prices.load();
+  out[1] = cclp_race::g_host_prices.load();
+}
 
 // mode 0 = baseline, 1 = concurrent. Writes the RaceOutcome JSON plus the
 // sorted basic column set and the event log into `out` (NUL-terminated).

@@ -20,6 +20,7 @@
 #include <cstdlib>
 #include <deque>
 #include <limits>
+#include <memory>
 #include <mutex>
 #include <ostream>
 #include <stdexcept>
@@ -28,7 +29,22 @@
 #include <vector>
 
 #include "cclp/race.hpp"
+#include "crossover_scalable.hpp"
 #include "json.hpp"
+
+// Which crossover the race's workers and main thread run: the reference's
+// run_crossover (dense etas; m up to ~1e4) or the scalable one
+// (crossover_scalable.hpp: sparse LU crash and factors, pricing on the B200
+// when the library carries the engine). Set through cclp_race_set_crossover.
+namespace cclp_race {
+#ifdef CCLP_RACE_DEFAULT_SCALABLE
+std::atomic<int> g_crossover{2};  // 2: scalable + device pricing
+#else
+std::atomic<int> g_crossover{0};  // 0: reference
+#endif
+std::atomic<int> g_device{0};
+std::atomic<long long> g_device_prices{0}, g_host_prices{0};
+}  // namespace cclp_race
 
 namespace cclp {
 
@@ -166,6 +182,17 @@ struct RaceState {
     return true;
   }
 
+  std::unique_ptr<cclp_xo::DevicePricer> pricer;  // crossover kind 2 only
+  CrossoverResult crossover(const CrossoverTask& task) {
+    const int kind = cclp_race::g_crossover.load();
+    if (kind == 0) return run_crossover(task);
+    cclp_xo::ScalableStats st;
+    CrossoverResult r = cclp_xo::run_crossover(task, kind == 2 ? pricer.get() : nullptr, &st);
+    cclp_race::g_device_prices += st.device_prices;
+    cclp_race::g_host_prices += st.host_prices;
+    return r;
+  }
+
   CrossoverTask task_for(const Iterate& it, Scalar maxresid, const std::atomic<bool>* cancel) const {
     CrossoverTask task;
     task.std_lp = std_lp;
@@ -194,7 +221,7 @@ struct RaceState {
     event("launch", w.label);
     CrossoverTask task = task_for(snap.iterate, snap.maxresid, &w.cancel);
     w.th = std::thread([this, &w, task = std::move(task)]() {
-      CrossoverResult r = run_crossover(task);
+      CrossoverResult r = crossover(task);
       {
         std::lock_guard<std::mutex> g2(mu);
         w.rec.finish_s = now_s();
@@ -220,6 +247,8 @@ RaceOutcome run_race(const LinearProgram& lp, const RaceConfig& config) {
   S.t0 = Clock::now();
   const StandardFormMap sf = to_standard_form_direct(lp);
   S.std_lp = &sf.std_lp;
+  if (cclp_race::g_crossover.load() == 2)  // the device pricing context (LP upload, CSR)
+    S.pricer = std::make_unique<cclp_xo::DevicePricer>(sf.std_lp, cclp_race::g_device.load());
   const bool concurrent = config.mode == RaceMode::kConcurrent;
   out.thresholds = concurrent ? schedule_thresholds(config.tol) : std::vector<Scalar>{};
   const int pool = reserve_threads(config, static_cast<int>(std::thread::hardware_concurrency())).second;
@@ -250,7 +279,7 @@ RaceOutcome run_race(const LinearProgram& lp, const RaceConfig& config) {
     }
     if (!skip) {
       main_ran = true;
-      CrossoverResult r = run_crossover(S.task_for(pr.iterate, pr.report.maxresid_rel, &S.main_cancel));
+      CrossoverResult r = S.crossover(S.task_for(pr.iterate, pr.report.maxresid_rel, &S.main_cancel));
       {
         std::lock_guard<std::mutex> g(S.mu);
         S.event("finish", "main", to_string(r.status));

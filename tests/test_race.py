@@ -105,3 +105,54 @@ def test_direct_standard_form_rejects_free_row():
     lp.row_lower[4], lp.row_upper[4] = -INF, INF
     with pytest.raises(ValueError):
         race.standard_form_check(lp)
+
+
+# ---- the scalable crossover (integration/crossover_scalable.cpp) -----------
+@pytest.mark.parametrize("make", [lambda: lpgen.transportation_lp(20, 30, seed=3),
+                                  lambda: lpgen.transportation_lp(20, 30, seed=4),
+                                  lambda: lpgen.small_equality_lp(40, 90, 0.2, 7)[0],
+                                  lambda: lpgen.two_var_lp()])
+def test_scalable_crossover_race_matches_reference_crossover(make):
+    """The race with the scalable crossover (sparse LU crash and factors,
+    sparse etas, host pricing) ends on the reference crossover's basis."""
+    lp = make()
+    ref = race.run_race(lp, kind="cpu", mode="baseline", crossover="reference")
+    sc = race.run_race(lp, kind="cpu", mode="baseline", crossover="scalable")
+    race.set_crossover("cpu", "reference")
+    assert ref["status"] == sc["status"] == "solved"
+    assert sc["basic"] == ref["basic"]
+    assert sc["objective"] == pytest.approx(ref["objective"], rel=1e-9, abs=1e-9)
+
+
+@pytest.mark.parametrize("eps", [1e-2, 1e-4])
+def test_scalable_crossover_from_snapshots_matches_reference(eps):
+    """From the same PDHG iterate (the oracle's, at a ladder tolerance) both
+    crossovers verify the same basis; the scalable one is the faster."""
+    from oracle.pyoracle import Restatement
+    from paper_2510_24429_b200 import lp as lpm
+    std = lpm.to_standard_form(lpgen.transportation_lp(60, 150, seed=1))
+    r = Restatement().run_pdhg(std, tol=dict(eps_rel=eps))
+    a = race.crossover(std, r["x"], r["y"], r["z"], r["report"]["maxresid_rel"], crossover="reference")
+    b = race.crossover(std, r["x"], r["y"], r["z"], r["report"]["maxresid_rel"], crossover="scalable")
+    assert a["status"] == b["status"] == "success"
+    assert a["basic"] == b["basic"]
+    assert b["objective"] == pytest.approx(a["objective"], rel=1e-9)
+    assert b["crash_accepted"] <= std.m and b["host_prices"] >= 1
+
+
+def test_scalable_crossover_rejects_dependent_candidates_like_the_reference():
+    """Duplicate columns: the second copy is dependent on the first and is
+    rejected by the crash exactly as build_basis does (crossover.cpp:131-133)."""
+    import numpy as np
+    from paper_2510_24429_b200.lp import LinearProgram
+    # min x0 + x1 + 3 x2 s.t. x0 + x1 + x2 = 2, x0 + x1 - x2 = 0 ; x0 and x1 identical columns
+    colptr = np.array([0, 2, 4, 6], np.int32)
+    rowind = np.array([0, 1, 0, 1, 0, 1], np.int32)
+    val = np.array([1.0, 1.0, 1.0, 1.0, 1.0, -1.0])
+    lp = LinearProgram(2, 3, colptr, rowind, val, np.array([1.0, 1.0, 3.0]), np.array([2.0, 0.0]),
+                       np.array([2.0, 0.0]), np.zeros(3), np.full(3, np.inf), name="DUP")
+    x = np.array([0.5, 0.5, 1.0]); y = np.array([2.0, -1.0]); z = np.array([0.0, 0.0, 0.0])
+    a = race.crossover(lp, x, y, z, 1e-3, crossover="reference")
+    b = race.crossover(lp, x, y, z, 1e-3, crossover="scalable")
+    assert a["status"] == b["status"]
+    assert a["basic"] == b["basic"]
