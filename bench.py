@@ -104,7 +104,8 @@ class OneCore:
 
 
 CPU_NOTE = ("the reference's own sources (proj/src/*.cpp, unmodified) compiled against the "
-            "repo's Eigen-API subset (oracle/eigen_shim: Eigen 3.4 is not installed on the box)")
+            "repo's Eigen-API subset (third_party/eigen_subset, built by oracle/Makefile): Eigen 3.4 "
+            "is not installed on the box")
 
 
 def measured_peak_gbs():

@@ -125,11 +125,24 @@ int blocks_for(long long n, int per = kBlock, int cap = 148 * 8) {
   return static_cast<int>(std::max<long long>(1, std::min<long long>(b, cap)));
 }
 
+// Development knobs (A/B experiments and tests: lanes per row, panel width,
+// SELL layouts, launch geometry, PDL, halo): read only when
+// CCLP_CU_DEV_KNOBS=1, so a user's environment cannot change the engine's
+// summation order or layouts. (CCLP_CU_TRANSPORT, a bit-identical transport
+// choice of the sharded solve, is a documented user option.)
+const char* dev_knob(const char* name) {
+  static const bool on = [] {
+    const char* e = std::getenv("CCLP_CU_DEV_KNOBS");
+    return e != nullptr && std::atoi(e) == 1;
+  }();
+  return on ? std::getenv(name) : nullptr;
+}
+
 // Launch with programmatic stream serialization (PDL): the kernel may begin
 // launching while its predecessor drains; it synchronizes with griddepcontrol.
 bool pdl_enabled() {
   static const bool on = [] {
-    const char* e = std::getenv("CCLP_CU_PDL");
+    const char* e = dev_knob("CCLP_CU_PDL");
     return e == nullptr || std::atoi(e) != 0;
   }();
   return on;
@@ -697,8 +710,8 @@ void Context::build_csr_from(const int* cptr, const int* ridx, const double* cva
 void Context::partition() {
   if (Grow == 0) Grow = pick_group(nnz, m);
   if (Gcol == 0) Gcol = pick_group(nnz, n);
-  if (const char* e = std::getenv("CCLP_CU_G_ROWS")) Grow = std::atoi(e);  // A/B experiments only
-  if (const char* e = std::getenv("CCLP_CU_G_COLS")) Gcol = std::atoi(e);
+  if (const char* e = dev_knob("CCLP_CU_G_ROWS")) Grow = std::atoi(e);  // A/B experiments only
+  if (const char* e = dev_knob("CCLP_CU_G_COLS")) Gcol = std::atoi(e);
   // Setup kernels use nnz-balanced row ranges of `row_grid` / `col_grid`
   // blocks. The iteration's SpMV kernels run one full wave of resident
   // blocks (grid-stride over rows); the epilogues one wave of kEpiBlock-thread
@@ -835,7 +848,7 @@ SpmvPlan Context::plan(bool rows_side) const {
 
 void Context::build_panels(long long gather_len) {
   long long pb = static_cast<long long>(kPanelBytes);
-  if (const char* e = std::getenv("CCLP_CU_PANEL_BYTES")) pb = std::max(64LL, std::atoll(e));  // tests
+  if (const char* e = dev_knob("CCLP_CU_PANEL_BYTES")) pb = std::max(64LL, std::atoll(e));  // tests
   // Panels are defined on the ORIGINAL column space (a shard maps them into
   // its padded gather space), and a shard takes each panel's G from the full
   // matrix, so sharded sums equal the single-device sums bit for bit.
@@ -878,7 +891,7 @@ void Context::build_panels(long long gather_len) {
     k_panel_fill<<<blocks_for(m), kBlock, 0, stream>>>(rowptr, colind, m, lo, pn.ptr, pn.idx, pn.perm);
     CKL("panel fill");
     pn.G = k < static_cast<long long>(panel_G_hint.size()) ? panel_G_hint[k] : pick_group(pn.nnz, m);
-    if (const char* e = std::getenv("CCLP_CU_PANEL_G")) pn.G = std::atoi(e);  // A/B experiments only
+    if (const char* e = dev_knob("CCLP_CU_PANEL_G")) pn.G = std::atoi(e);  // A/B experiments only
     plan_side_ptr(pn.ptr, m, pn.G, pn.sp);
     pn.start = plan_starts_ptr(pn.ptr, m, pn.sp, panel_grid);
     pn.sp.wrow.clear();
@@ -940,7 +953,7 @@ void Context::tune_spmv() {
   tune_pending = true;
   // A device-wide context (not a shard) without column panels tunes inside
   // its first power iterations (power_norm); everything else now.
-  const bool defer = x_full == nullptr && !use_panels() && std::getenv("CCLP_CU_TUNE_EAGER") == nullptr;
+  const bool defer = x_full == nullptr && !use_panels() && dev_knob("CCLP_CU_TUNE_EAGER") == nullptr;
   if (!defer) explicit_tune();
 }
 
@@ -1007,7 +1020,7 @@ void Context::explicit_tune() {
     }
     CKL("tune spmv");
   };
-  const char* force = std::getenv("CCLP_CU_RPG");
+  const char* force = dev_knob("CCLP_CU_RPG");
   std::vector<float> ms[2][4];
   const int reps = (nnz > 30'000'000) ? 4 : 6;
   for (int side = 0; side < 2; ++side) {
@@ -1035,7 +1048,7 @@ void Context::explicit_tune() {
 // slice range of about equal slots + per-column overhead. CCLP_CU_SELL=0
 // keeps the G-lane CSR column kernel (A/B).
 void Context::build_sell_cols() {
-  const char* e = std::getenv("CCLP_CU_SELL");
+  const char* e = dev_knob("CCLP_CU_SELL");
   sell_on = false;
   if ((e != nullptr && std::atoi(e) == 0) || n == 0 || nnz == 0 || !sval_csc) return;
   // Measured (profiles/r1/history/r1_spmv_experiments.txt): SELL wins where
@@ -1152,7 +1165,7 @@ void Context::build_sell_cols() {
         std::sort(t.begin(), t.end());
         t_gs = t[t.size() / 2];
       }
-      const char* fm = std::getenv("CCLP_CU_SELL_MODE");  // A/B: contig | small | gs
+      const char* fm = dev_knob("CCLP_CU_SELL_MODE");  // A/B: contig | small | gs
       int mode = 0;  // 0 contiguous 1024, 1 contiguous 256, 2 grid-stride 1024
       if (fm != nullptr) {
         mode = std::string(fm) == "small" ? 1 : (std::string(fm) == "gs" ? 2 : 0);
@@ -1188,7 +1201,7 @@ void Context::build_sell_rows() { build_sellg(true); }
 
 void Context::build_sellg(bool rows_side) {
   SellG& S = rows_side ? sgr : sgc;
-  const char* e = std::getenv(rows_side ? "CCLP_CU_SELL_ROWS" : "CCLP_CU_SELLG_COLS");
+  const char* e = dev_knob(rows_side ? "CCLP_CU_SELL_ROWS" : "CCLP_CU_SELLG_COLS");
   const bool force = e != nullptr && std::atoi(e) == 2;
   const int cnt = rows_side ? m : n;
   const int* ptr = rows_side ? rowptr : colptr;
@@ -1712,7 +1725,7 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
   } else {
     ensure_tuned();
   }
-  const char* force = std::getenv("CCLP_CU_RPG");
+  const char* force = dev_knob("CCLP_CU_RPG");
   for (int t = 0; t < iterations; ++t) {
     const int cand = t % 4;
     if (t < K) {

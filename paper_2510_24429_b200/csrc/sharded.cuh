@@ -316,7 +316,7 @@ void Context::shard_from_host(const cclp_cu_lp* lp, int rank, int P, const std::
 // single device's bit for bit.
 std::vector<int> host_panel_groups(const cclp_cu_lp* lp) {
   long long pb = static_cast<long long>(Context::kPanelBytes);
-  if (const char* e = std::getenv("CCLP_CU_PANEL_BYTES")) pb = std::max(64LL, std::atoll(e));  // tests
+  if (const char* e = dev_knob("CCLP_CU_PANEL_BYTES")) pb = std::max(64LL, std::atoll(e));  // tests
   const long long gn = lp->n;
   const long long K = (gn * 8 + pb - 1) / pb;
   std::vector<int> G;
@@ -730,7 +730,7 @@ struct Sharded {
       sh->shard_from_host(lp, q, P, rb, cb, stream, panel_G);
       shards.push_back(std::move(sh));
     }
-    const char* e = std::getenv("CCLP_CU_HALO");  // 0: always all-gather (A/B)
+    const char* e = dev_knob("CCLP_CU_HALO");  // 0: always all-gather (A/B)
     if (e == nullptr || std::atoi(e) != 0) {
       build_halo(halo_x, true, lp);
       build_halo(halo_y, false, lp);

@@ -8,6 +8,11 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
+# the engine's development knobs (csrc/engine.cu dev_knob) are read only with
+# this switch; some tests force layouts through them
+os.environ.setdefault("CCLP_CU_DEV_KNOBS", "1")
+
+
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the sm_100a engine)")
 

@@ -13,6 +13,7 @@ t = time.time()
 lp = lpgen.make_config(cfg)
 print("gen", cfg, lp.m, lp.n, lp.nnz, f"{time.time() - t:.1f}s", flush=True)
 for mb in [int(a) for a in sys.argv[2:]] or [32, 48, 64, 80]:
+    os.environ["CCLP_CU_DEV_KNOBS"] = "1"
     os.environ["CCLP_CU_PANEL_BYTES"] = str(mb << 20)
     eng = Engine(lp)
     eng.begin(PdhgConfig())

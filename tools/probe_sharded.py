@@ -23,6 +23,7 @@ ms = eng.advance(its)
 print(f"{cfg} single: {ms/its*1e3:.1f} us/it ({B/(ms/its*1e-3)/1e9:.0f} GB/s)", flush=True)
 eng.close()
 for halo in ("1", "0"):
+    os.environ["CCLP_CU_DEV_KNOBS"] = "1"
     os.environ["CCLP_CU_HALO"] = halo
     for P in (2, 4, 8):
         with ShardedEngine(lp, P) as se:

@@ -15,6 +15,7 @@ from paper_2510_24429_b200.pdhg import Engine, PdhgConfig, run_pdhg, run_pdhg_sh
 from test_gpu_longrows import dense_rows_lp  # noqa: E402
 from test_gpu_sell import dense_cols_lp  # noqa: E402
 
+os.environ["CCLP_CU_DEV_KNOBS"] = "1"
 os.environ["CCLP_CU_SELL"] = "1"
 os.environ["CCLP_CU_SELL_ROWS"] = "2"
 lps = [lpgen.small_equality_lp(40, 90, 0.2, 7)[0], lpgen.random_equality_lp(2000, 10000, 8, seed=9)[0],
