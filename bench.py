@@ -59,6 +59,16 @@ def algorithmic_bytes(m: int, n: int, nnz: int) -> dict:
                 cols=12 * nnz + 4 * (n + 1) + 8 * m + 8 * n)
 
 
+def kernel_table(m: int, n: int, nnz: int, ph: dict, dsc: dict) -> list:
+    """(kernel, algorithmic bytes per launch, in-graph us, SpMV side) of the
+    four kernels one iteration launches (DESIGN.md §4 table)."""
+    ab = algorithmic_bytes(m, n, nnz)
+    return [("k_spmv_rows_sellg" if dsc.get("sell_rows_block") else "k_spmv_rows", ab["rows"], ph["spmv_rows"], "rows"),
+            ("k_dual", 80 * m, ph["dual"], None),
+            ("k_spmv_cols_sell" if dsc.get("sell_cols_block") else "k_spmv_cols", ab["cols"], ph["spmv_cols"], "cols"),
+            ("k_primal", 96 * n, ph["primal"], None)]
+
+
 def l2_roofline(lp, dom: str, dom_ms: float, clocks: dict, kernel: str = "") -> dict:
     rows = dom == "rows"
     out_len, vec_len = (lp.m, lp.n) if rows else (lp.n, lp.m)
@@ -435,11 +445,9 @@ def per_config_line(name: str, args, local: int) -> dict:
         dsc = eng.describe()
     ab = algorithmic_bytes(lp.m, lp.n, lp.nnz)
     iter_us = ms * 1e3 / (K * I)
-    dom = "rows" if ph["spmv_rows"] >= ph["spmv_cols"] else "cols"
-    dom_kernel = {"rows": "k_spmv_rows_sellg" if dsc.get("sell_rows_block") else
-                  ("k_spmv_rows_panel" if False else "k_spmv_rows"),
-                  "cols": "k_spmv_cols_sell" if dsc.get("sell_cols_block") else "k_spmv_cols"}[dom]
-    dom_gbs = ab[dom] / (ph["spmv_" + dom] * 1e-6) / 1e9
+    ks = kernel_table(lp.m, lp.n, lp.nnz, ph, dsc)
+    dom_kernel, dom_bytes, dom_us, _ = max(ks, key=lambda k: k[2])
+    dom_gbs = dom_bytes / (dom_us * 1e-6) / 1e9
     it_gbs = ab["iteration"] / (iter_us * 1e-6) / 1e9
     del lp
     return {"m": dsc.get("m"), "n": dsc.get("n"), "nnz": dsc.get("nnz"),
@@ -447,7 +455,9 @@ def per_config_line(name: str, args, local: int) -> dict:
             "iters_timed": K * I,
             "kernels_us": {k: ph[k] for k in ("spmv_rows", "dual", "spmv_cols", "primal")},
             "kernels_timing": f"in-graph stamps, median of {ph['steps']} steps",
-            "dominant": {"kernel": dom_kernel, "bytes_per_launch": ab[dom], "achieved": dom_gbs,
+            "kernels": {k: {"us": us, "bytes_per_launch": b, "frac": b / (us * 1e-6) / 1e9 / peak}
+                        for k, b, us, _ in ks if us > 0},
+            "dominant": {"kernel": dom_kernel, "bytes_per_launch": dom_bytes, "achieved": dom_gbs,
                          "frac": dom_gbs / peak},
             "iteration": {"bytes": ab["iteration"], "achieved": it_gbs, "frac": it_gbs / peak},
             "peak": peak, "peak_kind": peak_kind, "clocks": clk.summary()}
@@ -524,13 +534,12 @@ def main():
     pk_eager = eng.profile_kernels(100)
     pk = {k: ph[k] * 1e-3 for k in ("spmv_rows", "dual", "spmv_cols", "primal")}
     ab = algorithmic_bytes(lp.m, lp.n, lp.nnz)
-    dom = "rows" if pk["spmv_rows"] >= pk["spmv_cols"] else "cols"
-    dom_ms = pk["spmv_" + dom]
     dsc = eng.describe()
-    # the kernel that actually ran for that product (SELL layouts: engine.cu)
-    dom_kernel = {"rows": "k_spmv_rows_sellg" if dsc.get("sell_rows_block") else "k_spmv_rows",
-                  "cols": "k_spmv_cols_sell" if dsc.get("sell_cols_block") else "k_spmv_cols"}[dom]
-    achieved = ab[dom] / (dom_ms * 1e-3) / 1e9
+    # the kernels that actually ran (SELL layouts: engine.cu)
+    ks = kernel_table(lp.m, lp.n, lp.nnz, ph, dsc)
+    dom_kernel, dom_bytes, dom_us, dom = max(ks, key=lambda k: k[2])
+    dom_ms = dom_us * 1e-3
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
     peak, peak_kind = measured_peak_gbs()
     traffic = None
     try:
@@ -608,12 +617,15 @@ def main():
             "us_per_iteration": iter_us,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": dom_kernel,
-                         "kernel_us": dom_ms * 1e3, "bytes_per_launch": ab[dom],
+                         "kernel_us": dom_ms * 1e3, "bytes_per_launch": dom_bytes,
                          "peak_kind": peak_kind,
                          "iteration": {"bytes": ab["iteration"],
                                        "achieved": ab["iteration"] / (iter_us * 1e-6) / 1e9,
                                        "frac": ab["iteration"] / (iter_us * 1e-6) / 1e9 / peak},
                          "kernels_us": {k: v * 1e3 for k, v in pk.items()},
+                         "kernels": {k: {"us": us, "bytes_per_launch": b,
+                                         "frac": b / (us * 1e-6) / 1e9 / peak}
+                                     for k, b, us, _ in ks if us > 0},
                          "kernels_timing": f"in-graph: block-0 %globaltimer stamps after each "
                                            f"kernel's PDL wait, median of {ph['steps']} steps",
                          "kernels_us_eager": {k: v * 1e3 for k, v in pk_eager.items()}},
@@ -621,7 +633,8 @@ def main():
             # 12 B stream + one 32 B sector per gathered nonzero (+ the vectors),
             # against the LTS throughput cap (~6,300 B/clk, B300_MICROARCH.md) at
             # the sampled SM clock
-            "l2_roofline": l2_roofline(lp, dom, dom_ms, clk.summary(), dom_kernel),
+            "l2_roofline": (l2_roofline(lp, dom, dom_ms, clk.summary(), dom_kernel)
+                            if dom is not None else None),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "iters_per_step": args.e2e_iters,
                     "includes": "upload, CSR build, Ruiz, ||A|| power iteration, loop, download"},

@@ -149,11 +149,12 @@ bool pdl_enabled() {
 }
 
 template <class... KArgs, class... Args>
-void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t st, Args&&... args) {
+void launch_pdl_smem(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -161,6 +162,25 @@ void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t st, 
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
+template <class... KArgs, class... Args>
+void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t st, Args&&... args) {
+  launch_pdl_smem(kernel, grid, block, 0, st, std::forward<Args>(args)...);
+}
+// More than 48 KB of dynamic shared memory needs the kernel's opt-in
+// attribute, per device (set once each).
+void allow_smem(const void* kernel, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> set;
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = set[{kernel, dev}];
+  if (smem > have) {
+    ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
+       "cudaFuncSetAttribute");
+    have = smem;
+  }
 }
 
 // Calls f(std::integral_constant<int, G>) for the runtime group size G.
@@ -381,7 +401,9 @@ struct Context {
   template <class T>
   T* alloc(size_t count) {
     void* p = nullptr;
-    ck(cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), stream), "cudaMallocAsync");
+    // +4 elements of slack: the bulk copies of the epilogues move whole
+    // 16-byte units and may read one element past a vector's end (bulk_stream)
+    ck(cudaMallocAsync(&p, (std::max<size_t>(count, 1) + 4) * sizeof(T), stream), "cudaMallocAsync");
     return static_cast<T*>(p);
   }
   void release(void* p) {
@@ -507,7 +529,7 @@ struct Context {
   double reduce(const double* a, const double* bvec, long long len, int mode);  // reproducible
   void launch_repro_max(int mode, const double* a, const double* bvec, long long len);
   void launch_repro_sum(int mode, const double* a, const double* bvec, long long len, const double* Mdev,
-                        long long N);
+                        long long N, PowerCtrl* pc = nullptr);
   void repro_local_max(int mode, const double* a, const double* bvec, long long len, double* M);
   void repro_local_sums(int mode, const double* a, const double* bvec, long long len, const double* M,
                         long long N, double* S);
@@ -546,6 +568,8 @@ struct Context {
   void launch_iteration(bool init);
   void launch_rows_half(bool init);  // k_spmv_rows + k_dual
   void launch_cols_half(bool init);  // k_spmv_cols + k_primal
+  void launch_dual(int ii);
+  void launch_primal(int ii);
   void build_graph(int k);
   void fetch_ctrl(Ctrl* dst);
   void extract_view(int view, const Ctrl& st);
@@ -714,11 +738,11 @@ void Context::partition() {
   if (const char* e = dev_knob("CCLP_CU_G_COLS")) Gcol = std::atoi(e);
   // Setup kernels use nnz-balanced row ranges of `row_grid` / `col_grid`
   // blocks. The iteration's SpMV kernels run one full wave of resident
-  // blocks (grid-stride over rows); the epilogues one wave of kEpiBlock-thread
+  // blocks (grid-stride over rows); the epilogues one wave of kTile-thread
   // blocks, so finalize reduces only that many partials.
   int sms = 148;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  epi_grid = sms;  // one wave of kEpiBlock-thread epilogue blocks (register-limited to 1 per SM)
+  epi_grid = sms;  // one epilogue block per SM (its shared-memory tile ring: bulk_stream)
   const long long cap = 148 * 4;
   row_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (m + 31) / 32 + nnz / 1024)));
   col_grid = static_cast<int>(std::max<long long>(1, std::min<long long>(cap, (n + 31) / 32 + nnz / 1024)));
@@ -1472,14 +1496,16 @@ void Context::launch_repro_max(int mode, const double* a, const double* bvec, lo
   CKL("repro max");
 }
 void Context::launch_repro_sum(int mode, const double* a, const double* bvec, long long len, const double* Mdev,
-                               long long N) {
+                               long long N, PowerCtrl* pc) {
   const int grid = blocks_for(std::max(len, 1LL), kBlock, 148 * 4);
   double* out = scalars + 2;
   switch (mode) {
     case 0: k_repro_sum<0><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out); break;
     case 1: k_repro_sum<1><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out); break;
     case 2: k_repro_sum<2><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out); break;
-    default: k_repro_sum<3><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out); break;
+    default:
+      k_repro_sum<3><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out, pc);
+      break;
   }
   CKL("repro sum");
 }
@@ -1753,8 +1779,7 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
     // nu = ||u||, lambda = v.u with the partition-free sums (sharded setups
     // reproduce them bit for bit)
     launch_repro_max(3, u, v, n);
-    launch_repro_sum(3, u, v, n, scalars, n);
-    k_power_finish<<<1, 1, 0, stream>>>(scalars + 2, pctrl);
+    launch_repro_sum(3, u, v, n, scalars, n, pctrl);  // its last block finishes nu, lambda
     k_div_scalar<<<blocks_for(n), kBlock, 0, stream>>>(u, &pctrl->nu, v, n);  // v = u / norm
     CKL("power");
   }
@@ -1821,7 +1846,7 @@ void Context::launch_rows_half(bool init) {
                  ii);
     });
   }
-  launch_pdl(k_dual, epi_grid, kEpiBlock, stream, p, ii);
+  launch_dual(ii);
 }
 
 void Context::launch_cols_half(bool init) {
@@ -1847,7 +1872,18 @@ void Context::launch_cols_half(bool init) {
       launch_pdl(k_spmv_cols<decltype(g)::value, decltype(l)::value>, spmv_grid_c, kSpmvBlock, stream, p, ii);
     });
   }
-  launch_pdl(k_primal, epi_grid, kEpiBlock, stream, p, ii);
+  launch_primal(ii);
+}
+
+// The streaming epilogues: one block per SM with its shared-memory ring of
+// operand tiles (bulk_stream, iter_kernels.cuh).
+void Context::launch_dual(int ii) {
+  allow_smem(reinterpret_cast<const void*>(k_dual), bulk_smem<kDualStreams>());
+  launch_pdl_smem(k_dual, epi_grid, kTile, bulk_smem<kDualStreams>(), stream, params, ii);
+}
+void Context::launch_primal(int ii) {
+  allow_smem(reinterpret_cast<const void*>(k_primal), bulk_smem<kPrimalStreams>());
+  launch_pdl_smem(k_primal, epi_grid, kTile, bulk_smem<kPrimalStreams>(), stream, params, ii);
 }
 
 void Context::launch_iteration(bool init) {
@@ -2353,7 +2389,7 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
         });
       }
       CK(cudaEventRecord(e[1], C.stream));
-      cclp_cu::k_dual<<<C.epi_grid, cclp_cu::kEpiBlock, 0, C.stream>>>(p, 0);
+      C.launch_dual(0);
       CK(cudaEventRecord(e[2], C.stream));
       if (p.use_sell_cg) {
         cclp_cu::with_group_long(C.gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
@@ -2380,7 +2416,7 @@ int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
         });
       }
       CK(cudaEventRecord(e[3], C.stream));
-      cclp_cu::k_primal<<<C.epi_grid, cclp_cu::kEpiBlock, 0, C.stream>>>(p, 0);
+      C.launch_primal(0);
       CK(cudaEventRecord(e[4], C.stream));
       C.launches += K;
     }
@@ -2562,7 +2598,32 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
     hf[0] = 0u;
     hf[1] = 0u;
     mirror_cancel();
+    // three pinned staging sets of x | z (n) | y (m) for ladder snapshots:
+    // cudaHostAlloc costs ~1 ms per MB, so it runs on a helper thread while
+    // the setup works on the device, and is done before the loop's timer
+    const size_t stage_bytes = sizeof(double) * 3 * (2 * static_cast<size_t>(C.n) + C.m);
+    void* stage_p = nullptr;
+    std::exception_ptr stage_err;
+    std::thread stage_alloc;
+    if (nthr > 0 && !C.h_sx)
+      stage_alloc = std::thread([&] {
+        try {
+          stage_p = cclp_cu::pinned_alloc(stage_bytes);
+        } catch (...) {
+          stage_err = std::current_exception();
+        }
+      });
+    struct JoinStage {
+      std::thread& t;
+      ~JoinStage() { if (t.joinable()) t.join(); }
+    } stage_join{stage_alloc};
     C.begin(cfg, *tol, thresholds, nthr);
+    if (stage_alloc.joinable()) {
+      stage_alloc.join();
+      if (stage_err) std::rethrow_exception(stage_err);
+      C.pinned.emplace_back(stage_p, stage_bytes);
+      C.h_sx = static_cast<double*>(stage_p);
+    }
     const double setup_s =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
     C.build_graph(k);
@@ -2594,9 +2655,6 @@ int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_
       events.push_back(std::move(e));
       cv.notify_all();
     };
-    if (nthr > 0 && !C.h_sx) {  // three pinned staging sets of x | z (n) | y (m)
-      C.h_sx = C.host_alloc<double>(3 * (2 * static_cast<size_t>(C.n) + C.m));
-    }
     auto set_ptr = [&](int set) { return C.h_sx + static_cast<size_t>(set) * (2 * static_cast<size_t>(C.n) + C.m); };
     auto acquire_set = [&](int set) {  // launcher: wait until the sink released it
       std::unique_lock<std::mutex> g(mu);

@@ -689,71 +689,104 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_cols(const IterParams p, in
                       p.aty[si.s1], p.rpg_cols);
 }
 
-// k_dual's work on rows i0 + k*stride < end (k < kDualU), loads hoisted:
-// y_{t+1}, the sums, the push of y and the row-side report partials.
-constexpr int kDualU = 2;
-__device__ __forceinline__ void dual_span(const IterParams& p, const StepInfo& si, int i0, int stride,
-                                          int end, double* acc) {
-  const double* __restrict__ axn_v = p.ax[si.s1];
-  const double* __restrict__ y0 = p.y[si.s0];
-  const double* __restrict__ ax0 = p.ax[si.s0];
-  const double* __restrict__ ys0v = p.ysum[si.s0];
-  const double* __restrict__ axs0v = p.axsum[si.s0];
-  double* __restrict__ y1 = p.y[si.s1];
-  double* __restrict__ ys1 = p.ysum[si.s1];
-  double* __restrict__ axs1 = p.axsum[si.s1];
-  constexpr int U = kDualU;
-  double r[U], b[U], axn[U], yo[U], axo[U], ys[U], axs[U];
+// ---- the epilogues' operand streams, moved by the TMA engine -------------
+// 1-D bulk async copies (cp.async.bulk) of kTile-element tiles of every
+// operand stream into a kStages-deep shared-memory ring: one thread issues, an
+// mbarrier per stage counts the bytes in. An SM keeps up to kStages tiles of
+// all streams in flight (112-128 KB) without holding registers. Block b takes
+// tiles b, b + grid, ..., thread t element t of each: body(j, v) with
+// v[q * kTile] = stream q's element j (streams outside `mask` are not copied
+// and read as 0). The grid is fixed (one block per SM), so every thread's
+// partial sums cover the same elements on every run.
+constexpr int kTile = 512;
+constexpr int kStages = 4;
+template <int NS>
+__host__ __device__ constexpr size_t bulk_smem() {
+  return static_cast<size_t>(kStages) * NS * kTile * sizeof(double) + kStages * 8;
+}
+template <int NS, class Body>
+__device__ __forceinline__ void bulk_stream(int n, const double* const (&src)[NS], unsigned mask, Body&& body) {
+  extern __shared__ __align__(16) double sbuf[];  // [stage][stream][tile]
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(sbuf + kStages * NS * kTile);
+  const int ntiles = (n + kTile - 1) / kTile;
+  const int b = static_cast<int>(blockIdx.x), g = static_cast<int>(gridDim.x);
+  const int mine = b < ntiles ? (ntiles - 1 - b) / g + 1 : 0;
+  auto issue = [&](int k) {  // my k-th tile into stage k % kStages
+    const int j0 = (b + k * g) * kTile;
+    // whole 16-byte units: an odd tail reads one element past the end
+    // (every device vector is allocated with slack, Context::alloc)
+    const unsigned bytes = static_cast<unsigned>((min(kTile, n - j0) + 1) & ~1) * 8u;
+    const int st = k % kStages;
+    mbar_expect_tx(&full[st], bytes * static_cast<unsigned>(__popc(mask)));
 #pragma unroll
-  for (int k = 0; k < U; ++k) {
-    const int i = i0 + k * stride;
-    const bool ok = i < end;
-    r[k] = ok ? p.r[i] : 1.0;
-    b[k] = ok ? p.b[i] : 0.0;
-    axn[k] = ok ? axn_v[i] : 0.0;
-    yo[k] = ok ? y0[i] : 0.0;
-    axo[k] = ok && !si.init && !si.R ? ax0[i] : 0.0;
-    ys[k] = ok && !si.init ? ys0v[i] : 0.0;
-    axs[k] = ok && !si.init ? axs0v[i] : 0.0;
+    for (int q = 0; q < NS; ++q)
+      if ((mask >> q) & 1u) bulk_g2s(sbuf + (st * NS + q) * kTile, src[q] + j0, bytes, &full[st]);
+  };
+  if (threadIdx.x == 0) {
+    for (int st = 0; st < kStages; ++st) mbar_init(&full[st], 1);
+    mbar_init_fence();
+    for (int k = 0; k < min(kStages, mine); ++k) issue(k);
   }
+  __syncthreads();
+  double v[NS];
+  for (int k = 0; k < mine; ++k) {
+    const int st = k % kStages;
+    mbar_wait(&full[st], static_cast<unsigned>((k / kStages) & 1));
+    const int j = (b + k * g) * kTile + static_cast<int>(threadIdx.x);
+    if (j < n) {
 #pragma unroll
-  for (int k = 0; k < U; ++k) {
-    const int i = i0 + k * stride;
-    if (i >= end) break;
-    const double rinv = pow2_recip(r[k]);
-    if (si.init) {
-      row_report(axn[k], yo[k], r[k], rinv, b[k], acc);
-      continue;
+      for (int q = 0; q < NS; ++q) v[q] = ((mask >> q) & 1u) ? sbuf[(st * NS + q) * kTile + threadIdx.x] : 0.0;
+      body(j, v);
     }
-    double y_old = yo[k], ax_old = axo[k];
-    if (si.R) {
-      y_old = ys[k] * si.inv;
-      ax_old = axs[k] * si.inv;
+    __syncthreads();  // every thread is done with this stage
+    if (threadIdx.x == 0 && k + kStages < mine) {
+      fence_proxy_async();
+      issue(k + kStages);
     }
-    const double bs = b[k] * r[k];  // row_lower.cwiseProduct(r)
-    double t = 2.0 * axn[k];
-    t = t - ax_old;
-    t = bs - t;
-    t = p.sigma * t;
-    const double yn = y_old + t;
-    const double ysn = (si.R ? 0.0 : ys[k]) + yn;
-    const double axsn = (si.R ? 0.0 : axs[k]) + axn[k];
-    y1[i] = yn;
-    if (p.push.on) {  // fused push: into every shard that gathers this row
-      const unsigned mk = p.push.mask_y != nullptr ? p.push.mask_y[i] : 0xFFu;
-      const long long off = static_cast<long long>(p.push.rank) * p.push.Sm;
-      for (int q = 0; q < p.push.P; ++q)
-        if ((mk >> q) & 1u) p.push.y[q][off + i] = yn;
-    } else if (p.y_full_loc != nullptr) {
-      p.y_full_loc[i] = yn;
-    }
-    ys1[i] = ysn;
-    axs1[i] = axsn;
-    if (nonfinite(yn)) acc[6] += 1.0;
-    if (si.check) {
-      row_report(axn[k], yn, r[k], rinv, b[k], acc);
-      row_report(axsn * si.inv1, ysn * si.inv1, r[k], rinv, b[k], acc + 3);
-    }
+  }
+}
+
+// k_dual's operand streams: r, b, ax_{t+1}, then state t: y, ax, y_sum, ax_sum.
+enum DualStream : int { kDsR = 0, kDsB, kDsAxn, kDsY, kDsAx, kDsYs, kDsAxs, kDualStreams };
+
+// One row of k_dual's work (pdhg.cpp:125-126, :139-140, :179-189): y_{t+1},
+// the sums, the push of y_{t+1} (sharded) and the row-side report partials.
+__device__ __forceinline__ void dual_row(const IterParams& p, const StepInfo& si, int i, const double* v,
+                                         double* acc) {
+  const double r = v[kDsR], b = v[kDsB], axn = v[kDsAxn];
+  const double rinv = pow2_recip(r);
+  if (si.init) {
+    row_report(axn, v[kDsY], r, rinv, b, acc);
+    return;
+  }
+  double y_old = v[kDsY], ax_old = v[kDsAx];
+  if (si.R) {
+    y_old = v[kDsYs] * si.inv;
+    ax_old = v[kDsAxs] * si.inv;
+  }
+  const double bs = b * r;  // row_lower.cwiseProduct(r)
+  double t = 2.0 * axn;
+  t = t - ax_old;
+  t = bs - t;
+  t = p.sigma * t;
+  const double yn = y_old + t;
+  const double ysn = (si.R ? 0.0 : v[kDsYs]) + yn;
+  const double axsn = (si.R ? 0.0 : v[kDsAxs]) + axn;
+  p.y[si.s1][i] = yn;
+  if (p.push.on) {  // fused push: into every shard that gathers this row
+    const unsigned mk = p.push.mask_y != nullptr ? p.push.mask_y[i] : 0xFFu;
+    const long long off = static_cast<long long>(p.push.rank) * p.push.Sm;
+    for (int q = 0; q < p.push.P; ++q)
+      if ((mk >> q) & 1u) p.push.y[q][off + i] = yn;
+  } else if (p.y_full_loc != nullptr) {
+    p.y_full_loc[i] = yn;
+  }
+  p.ysum[si.s1][i] = ysn;
+  p.axsum[si.s1][i] = axsn;
+  if (nonfinite(yn)) acc[6] += 1.0;
+  if (si.check) {
+    row_report(axn, yn, r, rinv, b, acc);
+    row_report(axsn * si.inv1, ysn * si.inv1, r, rinv, b, acc + 3);
   }
 }
 
@@ -788,106 +821,87 @@ __device__ __forceinline__ void snap_cols(const IterParams& p, const StepInfo& s
   }
 }
 
-// Dual update + row-side report partials (one row per thread, coalesced).
-__global__ void __launch_bounds__(kEpiBlock) k_dual(const IterParams p, int init) {
+// Dual update + row-side report partials, the operand streams staged by the
+// TMA engine (bulk_stream).
+__global__ void __launch_bounds__(kTile, 1) k_dual(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si, 1)) return;
-  __shared__ double red[(kEpiBlock / 32) * kRowParts];
+  __shared__ double red[(kTile / 32) * kRowParts];
   __shared__ double out[kRowParts];
   double acc[kRowParts];
 #pragma unroll
   for (int k = 0; k < kRowParts; ++k) acc[k] = 0.0;
-  const int stride = gridDim.x * kEpiBlock;
-  for (int i0 = blockIdx.x * kEpiBlock + threadIdx.x; i0 < p.m; i0 += kDualU * stride)
-    dual_span(p, si, i0, stride, p.m, acc);
+  const double* const src[kDualStreams] = {p.r, p.b, p.ax[si.s1], p.y[si.s0], p.ax[si.s0], p.ysum[si.s0],
+                                           p.axsum[si.s0]};
+  // state t's ax is read when no restart is applied, the sums except at init
+  const unsigned mask = 0xFu | (si.init || si.R ? 0u : (1u << kDsAx)) |
+                        (si.init ? 0u : ((1u << kDsYs) | (1u << kDsAxs)));
+  bulk_stream<kDualStreams>(p.m, src, mask, [&](int i, const double* v) { dual_row(p, si, i, v, acc); });
   if (si.snap) snap_rows(p, si);
-  block_reduce<kRowParts, kRowMaxMask, kEpiBlock>(acc, red, out);
+  block_reduce<kRowParts, kRowMaxMask, kTile>(acc, red, out);
   if (threadIdx.x < kRowParts) p.rowp[threadIdx.x * gridDim.x + blockIdx.x] = out[threadIdx.x];  // field-major
   if (p.push.on) push_signal_grid(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1), p.push.counter);
 }
 
-// k_primal's work on columns j0 + k*stride < end (k < kPrimalU): the sums,
-// both next-x candidates and the column-side report partials.
-constexpr int kPrimalU = 2;
-__device__ __forceinline__ void primal_span(const IterParams& p, const StepInfo& si, int j0, int stride,
-                                            int end, double* acc) {
-  const double* __restrict__ atyn_v = p.aty[si.s1];
-  double* __restrict__ cand_c = p.xc[si.xs2][0];
-  double* __restrict__ cand_a = p.xc[si.xs2][1];
-  const double* __restrict__ xcur = p.xc[si.xs][si.R];
-  const double* __restrict__ xs0v = p.xsum[si.s0];
-  const double* __restrict__ as0v = p.atysum[si.s0];
-  double* __restrict__ xs1 = p.xsum[si.s1];
-  double* __restrict__ as1 = p.atysum[si.s1];
-  constexpr int U = kPrimalU;
-  double s[U], c[U], l[U], u[U], x1[U], atyn[U], xs0[U], as0[U];
-#pragma unroll
-  for (int k = 0; k < U; ++k) {
-    const int j = j0 + k * stride;
-    const bool ok = j < end;
-    s[k] = ok ? p.s[j] : 1.0;
-    c[k] = ok ? p.c[j] : 0.0;
-    l[k] = ok ? p.l[j] : 0.0;
-    u[k] = ok ? p.u[j] : 0.0;
-    x1[k] = ok ? xcur[j] : 0.0;
-    atyn[k] = ok ? atyn_v[j] : 0.0;
-    xs0[k] = ok && !si.init ? xs0v[j] : 0.0;
-    as0[k] = ok && !si.init ? as0v[j] : 0.0;
+// One column of k_primal's work: the sums, both next-x candidates and the
+// column-side report partials (pdhg.cpp:121-123, :138, :141, :190-210).
+__device__ __forceinline__ void primal_column(const IterParams& p, const StepInfo& si, int j, double s, double c,
+                                              double l, double u, double x1, double atyn, double xs0, double as0,
+                                              double* acc) {
+  const double sinv = pow2_recip(s);
+  // apply_scaling: c*s, l/s, u/s (l/s == l*(1/s) exactly)
+  const double cs = c * s, ls = l * sinv, us = u * sinv;
+  p.xc[si.xs2][0][j] = primal_update(x1, atyn, cs, ls, us, p.tau);
+  if (si.init) {
+    col_report(x1, atyn, s, sinv, c, l, u, acc);
+    return;
   }
-#pragma unroll
-  for (int k = 0; k < U; ++k) {
-    const int j = j0 + k * stride;
-    if (j >= end) break;
-    const double sinv = pow2_recip(s[k]);
-    // apply_scaling: c*s, l/s, u/s (l/s == l*(1/s) exactly)
-    const double cs = c[k] * s[k], ls = l[k] * sinv, us = u[k] * sinv;
-    cand_c[j] = primal_update(x1[k], atyn[k], cs, ls, us, p.tau);
-    if (si.init) {
-      col_report(x1[k], atyn[k], s[k], sinv, c[k], l[k], u[k], acc);
-      continue;
-    }
-    const double xsn = (si.R ? 0.0 : xs0[k]) + x1[k];
-    const double asn = (si.R ? 0.0 : as0[k]) + atyn[k];
-    xs1[j] = xsn;
-    as1[j] = asn;
-    if (nonfinite(x1[k])) acc[12] += 1.0;
-    if (si.check) {
-      col_report(x1[k], atyn[k], s[k], sinv, c[k], l[k], u[k], acc);
-      const double xa = xsn * si.inv1, aa = asn * si.inv1;
-      col_report(xa, aa, s[k], sinv, c[k], l[k], u[k], acc + 6);
-      cand_a[j] = primal_update(xa, aa, cs, ls, us, p.tau);
-    }
+  const double xsn = (si.R ? 0.0 : xs0) + x1;
+  const double asn = (si.R ? 0.0 : as0) + atyn;
+  p.xsum[si.s1][j] = xsn;
+  p.atysum[si.s1][j] = asn;
+  if (nonfinite(x1)) acc[12] += 1.0;
+  if (si.check) {
+    col_report(x1, atyn, s, sinv, c, l, u, acc);
+    const double xa = xsn * si.inv1, aa = asn * si.inv1;
+    col_report(xa, aa, s, sinv, c, l, u, acc + 6);
+    p.xc[si.xs2][1][j] = primal_update(xa, aa, cs, ls, us, p.tau);
   }
 }
 
-// Primal side: sums, column-side report partials, both next-x candidates;
-// the last block to finish runs finalize().
-__global__ void __launch_bounds__(kEpiBlock) k_primal(const IterParams p, int init) {
+// k_primal's operand streams: s, c, l, u, x_{t+1}, aty_{t+1}, x_sum, aty_sum.
+enum PrimalStream : int { kPsS = 0, kPsC, kPsL, kPsU, kPsX, kPsAty, kPsXs, kPsAs, kPrimalStreams };
+
+// Primal side: sums, column-side report partials, both next-x candidates,
+// the operand streams staged by the TMA engine (bulk_stream); the last block
+// to finish runs finalize().
+__global__ void __launch_bounds__(kTile, 1) k_primal(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si, 3)) return;
-  __shared__ double red[(kEpiBlock / 32) * kColParts];
+  __shared__ double red[(kTile / 32) * kColParts];
   __shared__ double out[kColParts];
   __shared__ bool last;
-  double acc[kColParts];
-#pragma unroll
-  for (int k = 0; k < kColParts; ++k) acc[k] = 0.0;
   // block 0 samples the host's cancel request early (a PCIe read that
   // completes behind the column stream) for this step's decide()
   const bool sampler = blockIdx.x == 0 && threadIdx.x == 0 && p.host_flags != nullptr;
   const unsigned cancel_req = sampler ? ld_relaxed_sys(p.host_flags) : 0u;
-  const int stride = gridDim.x * kEpiBlock;
-  for (int j0 = blockIdx.x * kEpiBlock + threadIdx.x; j0 < p.n; j0 += kPrimalU * stride)
-    primal_span(p, si, j0, stride, p.n, acc);
+  double acc[kColParts];
+#pragma unroll
+  for (int k = 0; k < kColParts; ++k) acc[k] = 0.0;
+  const double* const src[kPrimalStreams] = {p.s, p.c, p.l, p.u, p.xc[si.xs][si.R], p.aty[si.s1],
+                                             p.xsum[si.s0], p.atysum[si.s0]};
+  // the sums are read only when they carry on (not at init, not after a restart)
+  const unsigned mask = (si.init || si.R) ? 0x3Fu : 0xFFu;
+  bulk_stream<kPrimalStreams>(p.n, src, mask, [&](int j, const double* v) {
+    primal_column(p, si, j, v[kPsS], v[kPsC], v[kPsL], v[kPsU], v[kPsX], v[kPsAty], v[kPsXs], v[kPsAs], acc);
+  });
   if (si.snap) snap_cols(p, si);
-  block_reduce<kColParts, kColMaxMask, kEpiBlock>(acc, red, out);
+  block_reduce<kColParts, kColMaxMask, kTile>(acc, red, out);
   if (threadIdx.x < kColParts) p.colp[threadIdx.x * gridDim.x + blockIdx.x] = out[threadIdx.x];  // field-major
   if (sampler && p.cancel_dev != nullptr) *p.cancel_dev = cancel_req;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned prev = atomicAdd(p.counter, 1u);
-    last = (prev == gridDim.x - 1);
-  }
+  if (threadIdx.x == 0) last = atomicAdd(p.counter, 1u) == gridDim.x - 1;
   __syncthreads();
   // Every block fenced its partials before its counter increment, and the
   // last block reads them with L2 (.cg) loads, so no second fence is needed

@@ -322,14 +322,44 @@ struct ReproTerms {
   }
 };
 
-// Pass 1: out[k] = max |term_k| (exact, order-free); the last block writes it.
+// NaN-absorbing max (the reduction of k_repro_max: a nan term wins) and a
+// block-wide reduction of K such maxima or K exact sums. Both operations are
+// order-free (max; sums of the level quanta are exact), so the tree shape
+// never changes a bit of the result.
+__device__ __forceinline__ double nanmax(double a, double b) { return (b != b) ? b : amax(a, b); }
+template <int K, bool MAX>
+__device__ __forceinline__ void block_reduce_free(double (&v)[K], double* smem, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    double a = v[k];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+      const double o = __shfl_down_sync(0xffffffffu, a, off);
+      a = MAX ? nanmax(a, o) : a + o;
+    }
+    if (lane == 0) smem[warp * K + k] = a;
+  }
+  __syncthreads();
+  if (threadIdx.x < K) {
+    double a = smem[threadIdx.x];
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w) {
+      const double o = smem[w * K + threadIdx.x];
+      a = MAX ? nanmax(a, o) : a + o;
+    }
+    out[threadIdx.x] = a;
+  }
+  __syncthreads();
+}
+
+// Pass 1: out[k] = max |term_k| (exact, order-free); the last block to finish
+// reduces the per-block maxima with all its threads.
 template <int MODE>
 __global__ void __launch_bounds__(kBlock) k_repro_max(const double* __restrict__ a, const double* __restrict__ b,
                                                       long long n, double* part, unsigned* counter,
                                                       double* out) {
   using F = ReproTerms<MODE>;
   constexpr int K = F::K;
-  constexpr unsigned MX = (1u << K) - 1u;
   __shared__ double red[(kBlock / 32) * K];
   __shared__ double o[K];
   __shared__ bool last;
@@ -340,12 +370,9 @@ __global__ void __launch_bounds__(kBlock) k_repro_max(const double* __restrict__
     double t[K];
     F::at(a, b, i, t);
 #pragma unroll
-    for (int q = 0; q < K; ++q) {
-      const double v = fabs(t[q]);
-      acc[q] = (v != v) ? v : amax(acc[q], v);  // nan wins
-    }
+    for (int q = 0; q < K; ++q) acc[q] = nanmax(acc[q], fabs(t[q]));
   }
-  block_reduce<K, MX>(acc, red, o);
+  block_reduce_free<K, true>(acc, red, o);
   if (threadIdx.x < K) part[blockIdx.x * K + threadIdx.x] = o[threadIdx.x];
   __threadfence();
   __syncthreads();
@@ -353,24 +380,37 @@ __global__ void __launch_bounds__(kBlock) k_repro_max(const double* __restrict__
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < K) {
-    double mx = 0.0;
-    for (int bl = 0; bl < static_cast<int>(gridDim.x); ++bl) {
-      const double v = __ldcg(part + bl * K + threadIdx.x);
-      mx = (v != v) ? v : amax(mx, v);
-    }
-    out[threadIdx.x] = mx;
-  }
-  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < K; ++q) acc[q] = 0.0;
+  for (int bl = threadIdx.x; bl < static_cast<int>(gridDim.x); bl += kBlock)
+#pragma unroll
+    for (int q = 0; q < K; ++q) acc[q] = nanmax(acc[q], __ldcg(part + bl * K + q));
+  block_reduce_free<K, true>(acc, red, o);
+  if (threadIdx.x < K) out[threadIdx.x] = o[threadIdx.x];
   if (threadIdx.x == 0) *counter = 0u;
 }
+
+// The power iteration's scalars from the level sums of mode 3 (pdhg.cpp:59-61):
+// nu = ||u||, lambda = v.u; a zero norm sets `zero` (the reference returns 0).
+__device__ __forceinline__ void power_finish(const double* S, PowerCtrl* pc) {
+  if (pc->zero) return;
+  const double norm = sqrt(repro_final(S));
+  if (norm == 0.0) {
+    pc->zero = 1;
+  } else {
+    pc->lambda = repro_final(S + 3);
+    pc->nu = norm;
+  }
+}
+__global__ void k_power_finish(const double* __restrict__ S, PowerCtrl* pc) { power_finish(S, pc); }
 
 // Pass 2: out[3k + l] = the exact level-l sum of term k, given its global
 // max Mx[k] and global count N (repro_consts); plain sums when !ok.
 template <int MODE>
 __global__ void __launch_bounds__(kBlock) k_repro_sum(const double* __restrict__ a, const double* __restrict__ b,
                                                       long long n, const double* __restrict__ Mx, long long N,
-                                                      double* part, unsigned* counter, double* out) {
+                                                      double* part, unsigned* counter, double* out,
+                                                      PowerCtrl* pc = nullptr) {
   using F = ReproTerms<MODE>;
   constexpr int K = F::K;
   constexpr int K3 = 3 * K;
@@ -402,7 +442,7 @@ __global__ void __launch_bounds__(kBlock) k_repro_sum(const double* __restrict__
       }
     }
   }
-  block_reduce<K3, 0u>(acc, red, o);
+  block_reduce_free<K3, false>(acc, red, o);
   if (threadIdx.x < K3) part[blockIdx.x * K3 + threadIdx.x] = o[threadIdx.x];
   __threadfence();
   __syncthreads();
@@ -410,25 +450,16 @@ __global__ void __launch_bounds__(kBlock) k_repro_sum(const double* __restrict__
   __syncthreads();
   if (!last) return;
   __threadfence();
-  if (threadIdx.x < K3) {
-    double sm = 0.0;
-    for (int bl = 0; bl < static_cast<int>(gridDim.x); ++bl) sm += __ldcg(part + bl * K3 + threadIdx.x);
-    out[threadIdx.x] = sm;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) *counter = 0u;
-}
-
-// The power iteration's scalars from the level sums of mode 3 (pdhg.cpp:59-61):
-// nu = ||u||, lambda = v.u; a zero norm sets `zero` (the reference returns 0).
-__global__ void k_power_finish(const double* __restrict__ S, PowerCtrl* pc) {
-  if (pc->zero) return;
-  const double norm = sqrt(repro_final(S));
-  if (norm == 0.0) {
-    pc->zero = 1;
-  } else {
-    pc->lambda = repro_final(S + 3);
-    pc->nu = norm;
+#pragma unroll
+  for (int q = 0; q < K3; ++q) acc[q] = 0.0;
+  for (int bl = threadIdx.x; bl < static_cast<int>(gridDim.x); bl += kBlock)
+#pragma unroll
+    for (int q = 0; q < K3; ++q) acc[q] += __ldcg(part + bl * K3 + q);
+  block_reduce_free<K3, false>(acc, red, o);  // exact level sums: any order
+  if (threadIdx.x < K3) out[threadIdx.x] = o[threadIdx.x];
+  if (threadIdx.x == 0) {
+    *counter = 0u;
+    if (pc != nullptr) power_finish(o, pc);
   }
 }
 

@@ -36,6 +36,7 @@ CASES = {
     "T2000x5000": lambda: lpm.to_standard_form(lpgen.transportation_lp(2000, 5000, seed=1)),
     "MCF2000x4": lambda: lpgen.multicommodity_lp(nodes=2000, arcs_per_node=6, commodities=4, side_rows=2000,
                                                  side_per_var=2, seed=3),
+    "C2": lambda: lpgen.make_config("C2"),
     "MCF10000x8": lambda: lpgen.multicommodity_lp(nodes=10000, arcs_per_node=8, commodities=8, side_rows=8000,
                                                   side_per_var=3, seed=3),
 }
@@ -62,7 +63,7 @@ def emit(**kw):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--eps", type=float, default=1e-4)
-    ap.add_argument("--cases", default=",".join(CASES))
+    ap.add_argument("--cases", default=",".join(c for c in CASES if c != "C2"))
     ap.add_argument("--ref-timeout", type=float, default=300.0)
     ap.add_argument("--ref-max-m", type=int, default=12000)
     ap.add_argument("--no-race", action="store_true")
