@@ -24,10 +24,14 @@
 // kernels) or, for development and tests on one GPU, P shards in one process
 // exchanging by device copies - the same kernels and the same launch order.
 //
-// The one-time setup (Ruiz, ||A||, step sizes) runs redundantly on every
-// rank on the full matrix with the single-device kernels, so every rank
-// starts from identical scaled data; the iteration is what scales. The time
-// limit is checked on the host between batches so all shards stop together.
+// Each shard is built from the caller's host CSC and holds only its slices
+// (rows of A, columns of A^T). The one-time setup is distributed: Ruiz passes
+// all-gather the row/column maxima's scale factors, the power iteration runs
+// its two products over the shards, and every setup sum (||b||, ||c||, omega's
+// norms, ||u||, v.u) is a partition-free reproducible sum (repro_consts,
+// setup_kernels.cuh), so scale factors, ||A||, tau and sigma are the same
+// doubles as on one device. The time limit and cancel are agreed on the host
+// between batches so all shards stop together.
 #pragma once
 
 #include <dlfcn.h>
