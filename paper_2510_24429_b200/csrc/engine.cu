@@ -7,573 +7,11 @@
 // batch. Snapshots are extracted on the device and copied out on a side
 // stream into pinned memory; the sink is called on the caller's thread.
 // Reference: run_pdhg, proj/src/pdhg.cpp:230-378.
-#include <fcntl.h>
-#include <sys/mman.h>
-#include <sys/stat.h>
-#include <unistd.h>
-
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_scan.cuh>
-#include <cuda_runtime.h>
-
-#include <algorithm>
-#include <atomic>
-#include <climits>
-#include <condition_variable>
-#include <chrono>
-#include <cmath>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <deque>
-#include <map>
-#include <mutex>
-#include <type_traits>
-#include <random>
-#include <stdexcept>
-#include <memory>
-#include <thread>
-#include <string>
-#include <vector>
-
-#include "../../include/cclp_cu.h"
+#include "context.cuh"
 #include "iter_kernels.cuh"
 #include "setup_kernels.cuh"
 
 namespace cclp_cu {
-
-thread_local std::string g_err;
-
-struct Error : std::runtime_error {
-  int code;
-  Error(int c, const std::string& w) : std::runtime_error(w), code(c) {}
-};
-
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) {
-    const int code = (e == cudaErrorMemoryAllocation) ? CCLP_CU_ENOMEM : CCLP_CU_ECUDA;
-    cudaGetLastError();
-    throw Error(code, std::string(what) + ": " + cudaGetErrorString(e));
-  }
-}
-#define CK(x) ::cclp_cu::ck((x), #x)
-#define CKL(what) ::cclp_cu::ck(cudaGetLastError(), what)
-
-namespace {
-
-// Device memory comes from the device's default stream-ordered pool with an
-// unbounded release threshold: a solve's buffers return to the pool on
-// destroy and the next context reuses them, so create/destroy never touch
-// the driver's allocator (cudaMalloc/cudaFree synchronize the device and cost
-// milliseconds each at these sizes).
-void ensure_pool(int device) {
-  static std::mutex mu;
-  static std::vector<int> done;
-  std::lock_guard<std::mutex> g(mu);
-  if (std::find(done.begin(), done.end(), device) != done.end()) return;
-  cudaMemPool_t pool;
-  CK(cudaDeviceGetDefaultMemPool(&pool, device));
-  uint64_t thr = UINT64_MAX;
-  CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
-  done.push_back(device);
-}
-
-// Pinned host buffers (control block, log, snapshot staging) are recycled
-// process-wide for the same reason: cudaHostAlloc/cudaFreeHost pin and unpin
-// pages synchronously.
-std::mutex g_pinned_mu;
-std::multimap<size_t, void*> g_pinned_free;
-
-void* pinned_alloc(size_t bytes) {
-  {
-    std::lock_guard<std::mutex> g(g_pinned_mu);
-    auto it = g_pinned_free.lower_bound(bytes);
-    if (it != g_pinned_free.end() && it->first <= 2 * bytes + 4096) {
-      void* p = it->second;
-      g_pinned_free.erase(it);
-      return p;
-    }
-  }
-  void* p = nullptr;
-  CK(cudaHostAlloc(&p, std::max<size_t>(bytes, 1), cudaHostAllocDefault));
-  return p;
-}
-
-void pinned_release(void* p, size_t bytes) {
-  if (p == nullptr) return;
-  std::lock_guard<std::mutex> g(g_pinned_mu);
-  g_pinned_free.emplace(std::max<size_t>(bytes, 1), p);
-}
-
-// Lanes per row from the mean row length L. A fixed rule (never timing
-// based): G sets the per-row summation order, so it must not vary between
-// runs. Thresholds measured on B200 (profiles/r1/history/): L <= 8 -> 2
-// (C1 columns, C5 column panels at L ~ 5.5: G 1/2/4 = 4.40/4.22/4.69 ms),
-// L 9-24 -> 4 (C2/C4 columns, C4 rows), L ~ 50 -> 8, L ~ 100 -> 16,
-// L >= 160 -> 32.
-int pick_group(long long nnz, long long rows) {
-  const double L = rows > 0 ? static_cast<double>(nnz) / static_cast<double>(rows) : 0.0;
-  if (L <= 8.0) return 2;
-  if (L <= 24.0) return 4;
-  if (L <= 64.0) return 8;
-  if (L <= 160.0) return 16;
-  return 32;
-}
-
-int blocks_for(long long n, int per = kBlock, int cap = 148 * 8) {
-  long long b = (n + per - 1) / per;
-  return static_cast<int>(std::max<long long>(1, std::min<long long>(b, cap)));
-}
-
-// Development knobs (A/B experiments and tests: lanes per row, panel width,
-// SELL layouts, launch geometry, PDL, halo): read only when
-// CCLP_CU_DEV_KNOBS=1, so a user's environment cannot change the engine's
-// summation order or layouts. (CCLP_CU_TRANSPORT, a bit-identical transport
-// choice of the sharded solve, is a documented user option.)
-const char* dev_knob(const char* name) {
-  static const bool on = [] {
-    const char* e = std::getenv("CCLP_CU_DEV_KNOBS");
-    return e != nullptr && std::atoi(e) == 1;
-  }();
-  return on ? std::getenv(name) : nullptr;
-}
-
-// Launch with programmatic stream serialization (PDL): the kernel may begin
-// launching while its predecessor drains; it synchronizes with griddepcontrol.
-bool pdl_enabled() {
-  static const bool on = [] {
-    const char* e = dev_knob("CCLP_CU_PDL");
-    return e == nullptr || std::atoi(e) != 0;
-  }();
-  return on;
-}
-
-template <class... KArgs, class... Args>
-void launch_pdl_smem(void (*kernel)(KArgs...), int grid, int block, size_t smem, cudaStream_t st,
-                     Args&&... args) {
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(block);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
-}
-template <class... KArgs, class... Args>
-void launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t st, Args&&... args) {
-  launch_pdl_smem(kernel, grid, block, 0, st, std::forward<Args>(args)...);
-}
-// More than 48 KB of dynamic shared memory needs the kernel's opt-in
-// attribute, per device (set once each).
-void allow_smem(const void* kernel, size_t smem) {
-  static std::mutex mu;
-  static std::map<std::pair<const void*, int>, size_t> set;
-  int dev = 0;
-  ck(cudaGetDevice(&dev), "cudaGetDevice");
-  std::lock_guard<std::mutex> lock(mu);
-  size_t& have = set[{kernel, dev}];
-  if (smem > have) {
-    ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)),
-       "cudaFuncSetAttribute");
-    have = smem;
-  }
-}
-
-// Calls f(std::integral_constant<int, G>) for the runtime group size G.
-// Host <-> device copies of the caller's arrays (the LP in, the result out).
-// Pinned memory goes straight to the DMA engine; large pageable arrays are
-// staged through two pinned chunks filled (or drained) by several host
-// threads while the other chunk is in flight - the driver's own pageable path
-// is a single-threaded bounce (~8 GB/s).
-constexpr size_t kStageChunk = size_t(32) << 20;
-
-bool is_pinned(const void* p) {
-  cudaPointerAttributes a{};
-  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return a.type == cudaMemoryTypeHost;
-}
-
-void par_memcpy(void* dst, const void* src, size_t bytes) {
-  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-  if (bytes < (size_t(4) << 20) || hw == 1) {
-    std::memcpy(dst, src, bytes);
-    return;
-  }
-  const size_t per = (bytes + hw - 1) / hw;
-  std::vector<std::thread> th;
-  for (unsigned t = 1; t < hw && size_t(t) * per < bytes; ++t) {
-    const size_t a = size_t(t) * per;
-    th.emplace_back([=] {
-      std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, std::min(per, bytes - a));
-    });
-  }
-  std::memcpy(dst, src, std::min(per, bytes));
-  for (auto& t : th) t.join();
-}
-
-// The CSC checks of LinearProgram::validate (lp.cpp:71-83) that guard memory
-// safety: colptr[0] == 0, non-decreasing offsets, 0 <= row < m, rows strictly
-// ascending within a column. Same messages; host threads over column ranges.
-void validate_csc(const cclp_cu_lp* lp) {
-  const int m = lp->m, n = lp->n;
-  const int32_t* cp = lp->colptr;
-  const int32_t* ri = lp->rowind;
-  if (cp[0] != 0) throw std::invalid_argument("colptr[0] != 0");
-  for (int j = 0; j < n; ++j)
-    if (cp[j] > cp[j + 1]) throw std::invalid_argument("decreasing column offsets");
-  const long long nnz = cp[n];
-  if (nnz > 0 && ri == nullptr) throw std::invalid_argument("null row indices");
-  const unsigned hw = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
-  const unsigned T = nnz < (1LL << 20) ? 1u : hw;
-  std::vector<int> bad(T, 0);
-  auto work = [&](unsigned t) {
-    const int j0 = static_cast<int>(static_cast<long long>(n) * t / T);
-    const int j1 = static_cast<int>(static_cast<long long>(n) * (t + 1) / T);
-    for (int j = j0; j < j1 && !bad[t]; ++j)
-      for (int q = cp[j]; q < cp[j + 1]; ++q) {
-        const int i = ri[q];
-        if (i < 0 || i >= m) { bad[t] = 1; break; }
-        if (q > cp[j] && i <= ri[q - 1]) { bad[t] = 2; break; }
-      }
-  };
-  std::vector<std::thread> th;
-  for (unsigned t = 1; t < T; ++t) th.emplace_back(work, t);
-  work(0);
-  for (auto& x : th) x.join();
-  for (int b : bad) {
-    if (b == 1) throw std::invalid_argument("row index out of range");
-    if (b == 2) throw std::invalid_argument("unsorted or duplicate row indices");
-  }
-}
-
-template <class F>
-void with_group(int G, F&& f) {
-  switch (G) {
-    case 1: f(std::integral_constant<int, 1>{}); break;
-    case 2: f(std::integral_constant<int, 2>{}); break;
-    case 4: f(std::integral_constant<int, 4>{}); break;
-    case 8: f(std::integral_constant<int, 8>{}); break;
-    case 16: f(std::integral_constant<int, 16>{}); break;
-    default: f(std::integral_constant<int, 32>{}); break;
-  }
-}
-
-// Calls f(G constant, LONG constant): long-row segments compiled in only when
-// the matrix has rows past the threshold.
-template <class F>
-void with_group_long(int G, bool lng, F&& f) {
-  if (lng) {
-    with_group(G, [&](auto g) { f(g, std::true_type{}); });
-  } else {
-    with_group(G, [&](auto g) { f(g, std::false_type{}); });
-  }
-}
-
-}  // namespace
-
-void gaussian_start(uint64_t seed, long long n, double* v);
-
-struct Context {
-  int device = 0;
-  cudaStream_t stream = nullptr, side = nullptr;
-  int m = 0, n = 0;
-  long long nnz = 0;
-  // unscaled matrix: CSC (reference layout) and CSR
-  int *colptr = nullptr, *rowind = nullptr, *rowptr = nullptr, *colind = nullptr;
-  double *val_csc = nullptr, *val_csr = nullptr;
-  // scaled matrix values
-  double *sval_csc = nullptr, *sval_csr = nullptr;
-  double *c = nullptr, *l = nullptr, *u = nullptr, *b = nullptr;
-  double *r = nullptr, *s = nullptr;
-  bool equality = true;
-  // partitions
-  int Grow = 0, Gcol = 0, row_grid = 1, col_grid = 1;  // G = 0: pick from the mean row length
-  int spmv_grid_r = 1, spmv_grid_c = 1, epi_grid = 1;
-  int rpg_r = 1, rpg_c = 1;  // SpMV rows per lane group in flight (tuned)
-  struct SidePlan {  // long-row segments of one SpMV side (SpmvPlan)
-    int thr = 0x7fffffff, nseg = 0, nlong = 0;
-    bool has_long = false;
-    int4* seg = nullptr;
-    int* lr_first = nullptr;
-    double* part = nullptr;
-    unsigned* cnt = nullptr;
-    std::vector<long long> wrow, wseg;  // host weights while planning
-  } plan_rows, plan_cols;
-  void plan_side(bool rows_side, int G, SidePlan& sp);
-  void plan_side_ptr(const int* dptr, int rows, int G, SidePlan& sp);
-  int* plan_starts(bool rows_side, const SidePlan& sp, int grid);
-  int* plan_starts_ptr(const int* dptr, int rows, const SidePlan& sp, int grid);
-  // ---- column panels of the row SpMV: when the gathered x is larger than
-  // the L2 can keep (C5: 400 MB), A is split by columns into panels of
-  // kPanelBytes of x, stored panel-major (each panel a CSR over all rows with
-  // its rows' entries in column order), and A x = sum over panels in panel
-  // order, each panel's gathers L2-resident.
-  static constexpr size_t kPanelBytes = size_t(48) << 20;
-  struct Panel {
-    int* ptr = nullptr;    // [m + 1]
-    int* idx = nullptr;    // [nnz_k] global (gather-space) column indices
-    int* perm = nullptr;   // [nnz_k] position in CSR(A) (values are gathered per solve)
-    double* val = nullptr; // [nnz_k] scaled values
-    long long nnz = 0;
-    int G = 1;
-    SidePlan sp;
-    int* start = nullptr;
-  };
-  std::vector<Panel> panels;
-  int panel_grid = 0;
-  long long panel_gn = 0;          // shards: the full matrix's column count
-  std::vector<int> panel_cb;       // shards: every shard's column bounds
-  std::vector<int> panel_G_hint;   // shards: the full matrix's per-panel G
-  void build_panels(long long gather_len);
-  bool use_panels() const { return !panels.empty() && !exact; }
-  PanelArgs panel_args(int k) const;
-  SpmvPlan plan(bool rows_side) const;
-  int* spmv_row_start = nullptr;  // [spmv_grid_r + 1]
-  int* spmv_col_start = nullptr;  // [spmv_grid_c + 1]
-  int *row_start = nullptr, *col_start = nullptr;
-  bool exact = false;  // G = 1: reference-order (bit-identical) SpMV sums
-  // state
-  double* xc[3][2] = {};
-  double *aty[2] = {}, *xsum[2] = {}, *atysum[2] = {};
-  double *y[2] = {}, *ax[2] = {}, *ysum[2] = {}, *axsum[2] = {};
-  double *rowp = nullptr, *colp = nullptr, *work_part = nullptr;
-  unsigned* counter = nullptr;
-  Ctrl* ctrl = nullptr;
-  Ctrl* h_ctrl = nullptr;  // pinned, [4]
-  LogEntry* log = nullptr;
-  int log_cap = 4096;
-  LogEntry* h_log = nullptr;
-  double* thr = nullptr;
-  int thr_cap = 0;
-  unsigned long long* t0 = nullptr;
-  double* scalars = nullptr;  // device scratch [16]
-  double* h_scalars = nullptr;
-  PowerCtrl* pctrl = nullptr;
-  int* iflags = nullptr;    // [0] ruiz notdone, [1] amb row count, [2] amb col count
-  int* amb_idx = nullptr;   // [2][256]
-  double* wn = nullptr;     // n-vector scratch x2
-  double* wn2 = nullptr;
-  double* wm = nullptr;
-  // outputs (device views) + pinned staging for snapshots
-  double *vx = nullptr, *vy = nullptr, *vz = nullptr, *vrep = nullptr;
-  double *h_sx = nullptr, *h_sy = nullptr, *h_sz = nullptr;
-  // inline ladder snapshots: kSnapSlots device slots of x | z (n each) | y (m)
-  double* snap_buf[kSnapSlots] = {};
-  // host flags in pinned, device-mapped memory: [0] cancel request (mirrored
-  // from the caller's flag by the host loop, read by the kernels every
-  // iteration), [1] snapshots copied out by the host
-  unsigned* h_flags = nullptr;
-  const unsigned* d_flags = nullptr;
-  unsigned* cancel_dev = nullptr;
-  unsigned long long* stamps = nullptr;  // in-graph phase stamps (stamp_phase)
-  std::atomic<int> abort_req{0};  // cclp_cu_request_cancel (any thread)
-  void ensure_flags() {
-    if (h_flags) return;
-    h_flags = host_alloc<unsigned>(16);
-    std::memset(h_flags, 0, 16 * sizeof(unsigned));
-    void* dp = nullptr;
-    CK(cudaHostGetDevicePointer(&dp, h_flags, 0));
-    d_flags = static_cast<const unsigned*>(dp);
-  }
-  cudaEvent_t ev_snap = nullptr, ev_a = nullptr, ev_b = nullptr;
-  // graph
-  cudaGraphExec_t graph = nullptr;
-  int graph_k = 0;
-  IterParams params{};
-  bool begun = false;
-  long long launches = 0;
-  double b_norm = 0, c_norm = 0;
-  double norm_est = 0, omega = 0, tau = 0, sigma = 0;
-  // host-side phase timings (seconds; stream synchronized at each border):
-  // 0 upload, 1 csr build, 2 partition + spmv tuning, 3 norms, 4 ruiz,
-  // 5 scale values, 6 power iteration, 7 state init + check(0),
-  // 8 graph build, 9 loop, 10 result view + download
-  static constexpr int kPhases = 11;
-  double phase[kPhases] = {};
-  std::chrono::steady_clock::time_point phase_t0;
-  template <class T>
-  T* alloc(size_t count) {
-    void* p = nullptr;
-    // +4 elements of slack: the bulk copies of the epilogues move whole
-    // 16-byte units and may read one element past a vector's end (bulk_stream)
-    ck(cudaMallocAsync(&p, (std::max<size_t>(count, 1) + 4) * sizeof(T), stream), "cudaMallocAsync");
-    return static_cast<T*>(p);
-  }
-  void release(void* p) {
-    if (p) cudaFreeAsync(p, stream);
-  }
-  // pinned host buffers with their sizes (returned to the process cache)
-  std::vector<std::pair<void*, size_t>> pinned;
-  template <class T>
-  T* host_alloc(size_t count) {
-    const size_t bytes = std::max<size_t>(count, 1) * sizeof(T);
-    void* p = pinned_alloc(bytes);
-    pinned.emplace_back(p, bytes);
-    return static_cast<T*>(p);
-  }
-  double* stage[2] = {nullptr, nullptr};
-  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
-  void ensure_stage() {
-    for (int b = 0; b < 2; ++b)
-      if (!stage[b]) {
-        stage[b] = host_alloc<double>(kStageChunk / sizeof(double));
-        CK(cudaEventCreateWithFlags(&stage_ev[b], cudaEventDisableTiming));
-      }
-  }
-  void h2d(void* dst, const void* src, size_t bytes) {
-    if (bytes == 0) return;
-    if (bytes < 2 * kStageChunk || is_pinned(src)) {
-      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
-      return;
-    }
-    ensure_stage();
-    size_t k = 0;
-    for (size_t off = 0; off < bytes; off += kStageChunk, ++k) {
-      const int b = static_cast<int>(k & 1);
-      CK(cudaEventSynchronize(stage_ev[b]));  // the chunk's previous DMA (this or an earlier call)
-      const size_t len = std::min(kStageChunk, bytes - off);
-      par_memcpy(stage[b], static_cast<const char*>(src) + off, len);
-      CK(cudaMemcpyAsync(static_cast<char*>(dst) + off, stage[b], len, cudaMemcpyHostToDevice, stream));
-      CK(cudaEventRecord(stage_ev[b], stream));
-    }
-  }
-  void d2h(void* dst, const void* src, size_t bytes) {  // synchronous on return
-    if (bytes == 0) return;
-    if (bytes < 2 * kStageChunk || is_pinned(dst)) {
-      CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
-      CK(cudaStreamSynchronize(stream));
-      return;
-    }
-    ensure_stage();
-    const size_t nch = (bytes + kStageChunk - 1) / kStageChunk;
-    auto issue = [&](size_t k) {
-      const size_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
-      CK(cudaMemcpyAsync(stage[k & 1], static_cast<const char*>(src) + off, len, cudaMemcpyDeviceToHost,
-                         stream));
-      CK(cudaEventRecord(stage_ev[k & 1], stream));
-    };
-    issue(0);
-    for (size_t k = 0; k < nch; ++k) {
-      if (k + 1 < nch) issue(k + 1);
-      CK(cudaEventSynchronize(stage_ev[k & 1]));
-      const size_t off = k * kStageChunk, len = std::min(kStageChunk, bytes - off);
-      par_memcpy(static_cast<char*>(dst) + off, stage[k & 1], len);
-    }
-  }
-  void mark(int k) {
-    CK(cudaStreamSynchronize(stream));
-    const auto now = std::chrono::steady_clock::now();
-    phase[k] = std::chrono::duration<double>(now - phase_t0).count();
-    phase_t0 = now;
-  }
-
-  ~Context();
-  void upload(const cclp_cu_lp* lp);
-  void build_csr();
-  void build_csr_from(const int* cptr, const int* ridx, const double* cval, int ncols, long long cnt);
-  void init_aux(int dev);
-  void partition();
-  void tune_spmv();
-  bool rows_equality = false;
-  // SELL-32 copy of A' for the column product (k_spmv_cols_sell): structure
-  // per long-row threshold, block ranges per column grid, values per solve.
-  bool sell_on = false;
-  static constexpr double kSellMaxPad = 1.25;
-  int sell_thr = -1, sell_grid = 0, sell_nsl = 0, sell_bs = kSpmvBlock;
-  long long* sell_off = nullptr;
-  int* sell_start = nullptr;
-  int* sell_idx = nullptr;
-  double* sell_val = nullptr;
-  std::vector<long long> sell_cum;  // host: slots before each slice
-  void build_sell_cols();
-  // SELL-G copy of A for the row product (k_spmv_rows_sellg): the same sums
-  // as the CSR-G kernel, so it is chosen by timing (decided once).
-  struct SellG {
-    bool on = false, decided = false;
-    int thr = -1, G = 0, grid = 0, bs = kSpmvBlock, nsl = 0;
-    long long* off = nullptr;
-    int* start = nullptr;
-    int* idx = nullptr;
-    double* val = nullptr;
-  };
-  SellG sgr, sgc;  // rows (k_spmv_rows_sellg), columns (k_spmv_cols_sellg)
-  void build_sell_rows();
-  void build_sellg(bool rows_side);
-  void relative_report(const double* x, const double* y, const double* z, double* rep, double* abs_viol);
-  void price(const double* y, const char* status, const unsigned char* skip, int phase1, double dtol, int bland,
-             long long* entering, int* direction, double* violation);
-  // SpMV geometry tuning folded into the first power iterations (results are
-  // geometry-independent, so the candidates can do real work): both start
-  // tables stay alive until the choice is made.
-  bool tune_pending = false;
-  int* tune_rows_st[3] = {nullptr, nullptr, nullptr};
-  int* tune_cols_st[3] = {nullptr, nullptr, nullptr};
-  int tune_sms = 148;
-  cudaEvent_t tune_ev[96] = {};
-  void set_geometry(bool rows_side, int per_sm, int rpg);
-  void choose_geometry(const std::vector<float> (&ms)[2][4]);
-  void explicit_tune();
-  void ensure_tuned() {
-    if (tune_pending) explicit_tune();
-  }
-  int grow() const { return exact ? 1 : Grow; }
-  int gcol() const { return exact ? 1 : Gcol; }
-  void launch_spmv(bool transpose, const double* vec, double* out, bool scaled, const int* stop);
-  double reduce(const double* a, const double* bvec, long long len, int mode);  // reproducible
-  void launch_repro_max(int mode, const double* a, const double* bvec, long long len);
-  void launch_repro_sum(int mode, const double* a, const double* bvec, long long len, const double* Mdev,
-                        long long N, PowerCtrl* pc = nullptr);
-  void repro_local_max(int mode, const double* a, const double* bvec, long long len, double* M);
-  void repro_local_sums(int mode, const double* a, const double* bvec, long long len, const double* M,
-                        long long N, double* S);
-  void ruiz(int iterations);
-  void ruiz_init();
-  bool ruiz_maxima(const double* s_g, const double* r_g);
-  void ruiz_update();
-  void power_rows(const double* vg, double* w, bool scaled);
-  void power_cols(const double* wg, double* u, bool scaled);
-  double power_norm(int iterations, uint64_t seed, bool scaled, bool pregenerated = false);
-  double* h_v0 = nullptr;  // pinned start vector of the power iteration
-  // h_v0 holds the start vector of seed v0_seed (a pure function of (seed, n)):
-  // the default seed's is generated on a host thread during upload / CSR build
-  std::thread v0_thread;
-  unsigned long long v0_seed = ~0ull;
-  // ---- sharded mode (sharded.cuh): this context is shard `shard_rank` of
-  // `shard_count`, owning rows [r0, r0 + m) of A and columns [c0, c0 + n)
-  bool own_stream = true;
-  int shard_rank = 0, shard_count = 1, r0 = 0, c0 = 0, Sm = 0, Sn = 0;
-  long long nnz_rows_slice = 0, nnz_cols_slice = 0;  // this shard's part of A (rows) / A' (rows)
-  double* x_full = nullptr;  // [P * Sn] padded full x (gather source of the row SpMV)
-  double* y_full = nullptr;  // [P * Sm] padded full y (gather source of the column SpMV)
-  double* xpart = nullptr;   // [P][kRowParts + kColParts] exchanged report sums
-  double* vparts = nullptr;  // [kRowParts + kColParts] report sums of the last view
-  unsigned long long* push_flags = nullptr;  // [3][kMaxPushShards] peer epochs (push transport)
-  unsigned* push_counter = nullptr;          // [2]
-  bool ipc_buffers = false;                  // exchange buffers from cudaMalloc (CUDA IPC)
-  std::vector<void*> ipc_owned;
-  void setup(const cclp_cu_config& cfg);
-  void init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thresholds,
-                  int nthr, bool launch_init);
-  void shard_from_host(const cclp_cu_lp* lp, int rank, int P, const std::vector<int>& rb,
-                       const std::vector<int>& cb, cudaStream_t shared, const std::vector<int>& panel_G);
-  void begin(const cclp_cu_config& cfg, const cclp_cu_tolerances& tol, const double* thresholds,
-             int nthr);
-  void launch_iteration(bool init);
-  void launch_rows_half(bool init);  // k_spmv_rows + k_dual
-  void launch_cols_half(bool init);  // k_spmv_cols + k_primal
-  void launch_dual(int ii);
-  void launch_primal(int ii);
-  void build_graph(int k);
-  void fetch_ctrl(Ctrl* dst);
-  void extract_view(int view, const Ctrl& st);
-};
 
 Context::~Context() {
   if (v0_thread.joinable()) v0_thread.join();
@@ -2129,978 +1567,84 @@ void Context::extract_view(int view, const Ctrl& st) {
   CKL("view");
 }
 
-}  // namespace cclp_cu
 
-#include "sharded.cuh"
-
-using cclp_cu::Context;
-using cclp_cu::Ctrl;
-using cclp_cu::Error;
-using cclp_cu::g_err;
-
-struct cclp_cu_ctx {
-  Context c;
-};
-
-struct cclp_cu_sharded {
-  cclp_cu::Sharded s;
-};
-
-namespace {
-
-template <class F>
-int guarded(F&& f) {
-  try {
-    f();
-    return CCLP_CU_OK;
-  } catch (const Error& e) {
-    g_err = e.what();
-    return e.code;
-  } catch (const std::invalid_argument& e) {
-    g_err = e.what();
-    return CCLP_CU_EINVAL;
-  } catch (const std::bad_alloc& e) {
-    g_err = e.what();
-    return CCLP_CU_ENOMEM;
-  } catch (const std::exception& e) {
-    g_err = e.what();
-    return CCLP_CU_ECUDA;
-  }
-}
-
-void validate_inputs_eq(bool equality, const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
-                        const double* thr, int nthr) {
-  // run_pdhg preconditions (pdhg.cpp:235-244, kkt.cpp:26-37)
-  if (!equality) throw std::invalid_argument("run_pdhg: LP must be in equality form");
-  if (!(tol.decrement > 0.0 && tol.decrement < 1.0))
-    throw std::invalid_argument("tolerances: decrement must be in (0,1)");
-  if (!(tol.eps_rel > 0.0 && tol.eps_rel <= tol.eps_cross))
-    throw std::invalid_argument("tolerances: need 0 < eps_rel <= eps_cross");
-  if (!(tol.eps_abs > 0.0)) throw std::invalid_argument("tolerances: eps_abs must be positive");
-  for (int i = 1; i < nthr; ++i)
-    if (!(thr[i] < thr[i - 1]))
-      throw std::invalid_argument("run_pdhg: thresholds must be strictly decreasing");
-  if (cfg.check_interval <= 0)  // modulo by zero in the reference (pdhg.cpp:311)
-    throw std::invalid_argument("run_pdhg: check_interval must be positive");
-}
-
-void validate_inputs(const cclp_cu_ctx* ctx, const cclp_cu_config& cfg, const cclp_cu_tolerances& tol,
-                     const double* thr, int nthr) {
-  validate_inputs_eq(ctx->c.equality, cfg, tol, thr, nthr);
-}
-
-void copy_report(const double* src, cclp_cu_report* dst) {
-  std::memcpy(dst, src, sizeof(double) * cclp_cu::kRepN);
-}
-
-}  // namespace
-
-extern "C" {
-
-const char* cclp_cu_last_error(void) { return g_err.c_str(); }
-
-void cclp_cu_gaussian_start(uint64_t seed, int64_t n, double* out) {
-  cclp_cu::gaussian_start(seed, n, out);
-}
-
-const char* cclp_cu_stop_string(int32_t stop) {
-  switch (stop) {  // pdhg.cpp:28-44
-    case CCLP_CU_STOP_CONVERGED: return "converged";
-    case CCLP_CU_STOP_ITERATION_LIMIT: return "iteration-limit";
-    case CCLP_CU_STOP_TIME_LIMIT: return "time-limit";
-    case CCLP_CU_STOP_CANCELLED: return "cancelled";
-    case CCLP_CU_STOP_WON_BY_CROSSOVER: return "won-by-crossover";
-    case CCLP_CU_STOP_NUMERICAL_ERROR: return "numerical-error";
-  }
-  return "unknown";
-}
-
-void cclp_cu_default_config(cclp_cu_config* cfg) {
-  cfg->step_scale = 0.9;
-  cfg->primal_weight = 0.0;
-  cfg->restart_factor = 0.5;
-  cfg->time_limit = INFINITY;
-  cfg->norm_iterations = 100;
-  cfg->scaling_iterations = 10;
-  cfg->max_iterations = 2000000;
-  cfg->check_interval = 1;
-  cfg->seed = 0;
-  cfg->log_interval = 0;
-  cfg->deterministic = 1;
-  cfg->poll_interval = 0;
-  cfg->exact_spmv = 0;
-}
-
-void cclp_cu_default_tolerances(cclp_cu_tolerances* t) {
-  t->eps_rel = 1e-6;
-  t->eps_abs = 1e-6;
-  t->eps_cross = 1e-2;
-  t->decrement = 0.1;
-}
-
-int cclp_cu_create(const cclp_cu_lp* lp, int device, cclp_cu_ctx** out) {
-  *out = nullptr;
-  return guarded([&] {
-    if (lp == nullptr || lp->m < 0 || lp->n < 0 || lp->colptr == nullptr)
-      throw std::invalid_argument("cclp_cu_create: bad LP");
-    cclp_cu::validate_csc(lp);  // before any device work
-    cclp_cu::ck(cudaSetDevice(device), "cudaSetDevice");
-    auto* ctx = new cclp_cu_ctx();
-    ctx->c.device = device;
-    try {
-      ctx->c.upload(lp);
-    } catch (...) {
-      delete ctx;
-      throw;
-    }
-    *out = ctx;
-  });
-}
-
-int cclp_cu_create_from_file(const char* path, int device, cclp_cu_ctx** out, int32_t* m_out,
-                             int32_t* n_out) {
-  *out = nullptr;
-  int fd = -1;
-  void* map = MAP_FAILED;
-  size_t len = 0;
-  const int rc = guarded([&] {
-    fd = open(path, O_RDONLY);
-    if (fd < 0) throw std::invalid_argument(std::string("cclp_cu_create_from_file: cannot open ") + path);
-    struct stat st;
-    if (fstat(fd, &st) != 0 || st.st_size < 32) throw std::invalid_argument("cclp_cu_create_from_file: short file");
-    len = static_cast<size_t>(st.st_size);
-    map = mmap(nullptr, len, PROT_READ, MAP_SHARED, fd, 0);
-    if (map == MAP_FAILED) throw std::invalid_argument("cclp_cu_create_from_file: mmap failed");
-    const char* base = static_cast<const char*>(map);
-    if (std::memcmp(base, "CCLPCSC1", 8) != 0) throw std::invalid_argument("cclp_cu_create_from_file: bad magic");
-    int32_t mn[2];
-    int64_t nnz;
-    std::memcpy(mn, base + 8, sizeof mn);
-    std::memcpy(&nnz, base + 16, sizeof nnz);
-    const int32_t m = mn[0], n = mn[1];
-    if (m < 0 || n < 0 || nnz < 0) throw std::invalid_argument("cclp_cu_create_from_file: bad header");
-    size_t off = 32;
-    auto take = [&](size_t bytes) {  // exact bound: the array ends inside the file
-      const char* p = base + off;
-      if (off + bytes > len) throw std::invalid_argument("cclp_cu_create_from_file: truncated file");
-      off += bytes;
-      off = (off + 7) / 8 * 8;
-      return p;
-    };
-    cclp_cu_lp lp;
-    lp.m = m;
-    lp.n = n;
-    lp.colptr = reinterpret_cast<const int32_t*>(take(sizeof(int32_t) * (static_cast<size_t>(n) + 1)));
-    lp.rowind = reinterpret_cast<const int32_t*>(take(sizeof(int32_t) * static_cast<size_t>(nnz)));
-    lp.val = reinterpret_cast<const double*>(take(sizeof(double) * static_cast<size_t>(nnz)));
-    lp.c = reinterpret_cast<const double*>(take(sizeof(double) * n));
-    lp.row_lower = reinterpret_cast<const double*>(take(sizeof(double) * m));
-    lp.row_upper = reinterpret_cast<const double*>(take(sizeof(double) * m));
-    lp.col_lower = reinterpret_cast<const double*>(take(sizeof(double) * n));
-    lp.col_upper = reinterpret_cast<const double*>(take(sizeof(double) * n));
-    if (lp.colptr[n] != nnz) throw std::invalid_argument("cclp_cu_create_from_file: colptr[n] != nnz");
-    if (m_out) *m_out = m;
-    if (n_out) *n_out = n;
-    const int rc2 = cclp_cu_create(&lp, device, out);
-    if (rc2 != CCLP_CU_OK) throw Error(rc2, g_err);
-  });
-  if (map != MAP_FAILED) munmap(map, len);
-  if (fd >= 0) close(fd);
-  return rc;
-}
-
-int cclp_cu_destroy(cclp_cu_ctx* ctx) {
-  delete ctx;
-  return CCLP_CU_OK;
-}
-
-int cclp_cu_begin(cclp_cu_ctx* ctx, const cclp_cu_config* cfg, const cclp_cu_tolerances* tol) {
-  return guarded([&] {
-    cclp_cu::ck(cudaSetDevice(ctx->c.device), "cudaSetDevice");
-    validate_inputs(ctx, *cfg, *tol, nullptr, 0);
-    cclp_cu_tolerances t = *tol;
-    ctx->c.ensure_flags();
-    ctx->c.h_flags[0] = ctx->c.h_flags[1] = 0u;
-    ctx->c.begin(*cfg, t, nullptr, 0);
-    // measurement mode: never converge, never hit the limit
-    ctx->c.params.eps_rel = -1.0;
-    ctx->c.params.max_iter = (1LL << 62);
-    ctx->c.params.time_limit = INFINITY;
-  });
-}
-
-int cclp_cu_advance(cclp_cu_ctx* ctx, int64_t iters, double* device_ms) {
-  return guarded([&] {
-    Context& C = ctx->c;
-    if (!C.begun) throw std::invalid_argument("cclp_cu_advance: call cclp_cu_begin first");
-    const int k = 32;
-    C.build_graph(k);
-    CK(cudaEventRecord(C.ev_a, C.stream));
-    long long done = 0;
-    while (done + k <= iters) {
-      CK(cudaGraphLaunch(C.graph, C.stream));
-      C.launches += cclp_cu::kKernelsPerIteration * k;
-      done += k;
-    }
-    while (done < iters) {
-      C.launch_iteration(false);
-      ++done;
-    }
-    CK(cudaEventRecord(C.ev_b, C.stream));
-    CK(cudaEventSynchronize(C.ev_b));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, C.ev_a, C.ev_b));
-    if (device_ms) *device_ms = ms;
-  });
-}
-
-int cclp_cu_profile_kernels(cclp_cu_ctx* ctx, int64_t iters, double* out) {
-  return guarded([&] {
-    Context& C = ctx->c;
-    if (!C.begun) throw std::invalid_argument("cclp_cu_profile_kernels: call cclp_cu_begin first");
-    constexpr int K = cclp_cu::kKernelsPerIteration;
-    std::vector<cudaEvent_t> ev((K + 1) * iters);
-    for (auto& e : ev) CK(cudaEventCreate(&e));
-    const cclp_cu::IterParams& p = C.params;
-    for (long long i = 0; i < iters; ++i) {
-      cudaEvent_t* e = &ev[(K + 1) * i];
-      CK(cudaEventRecord(e[0], C.stream));
-      if (C.use_panels()) {
-        for (int k = 0; k < static_cast<int>(C.panels.size()); ++k) {
-          const cclp_cu::PanelArgs a = C.panel_args(k);
-          cclp_cu::with_group_long(C.panels[k].G, a.plan.thr != 0x7fffffff, [&](auto g, auto l) {
-            cclp_cu::k_spmv_rows_panel<decltype(g)::value, decltype(l)::value>
-                <<<C.panel_grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0, a);
-          });
-        }
-      } else if (p.use_sell_r) {
-        cclp_cu::with_group_long(C.grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
-          if (C.sgr.bs == 256)
-            cclp_cu::k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, 256>
-                <<<C.sgr.grid, 256, 0, C.stream>>>(p, 0);
-          else
-            cclp_cu::k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, cclp_cu::kSpmvBlock>
-                <<<C.sgr.grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
-        });
-      } else {
-        cclp_cu::with_group_long(C.grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
-          cclp_cu::k_spmv_rows<decltype(g)::value, decltype(l)::value>
-              <<<C.spmv_grid_r, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
+// cclp_cu_profile_kernels: average device time per launch of the four
+// iteration kernels, launched eagerly (no PDL, no graph) with events between
+// them (the bench keeps it beside the in-graph split).
+void Context::profile_kernels(long long iters, double* out) {
+  if (!begun) throw std::invalid_argument("cclp_cu_profile_kernels: call cclp_cu_begin first");
+  constexpr int K = kKernelsPerIteration;
+  std::vector<cudaEvent_t> ev((K + 1) * iters);
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  const IterParams& p = params;
+  for (long long i = 0; i < iters; ++i) {
+    cudaEvent_t* e = &ev[(K + 1) * i];
+    CK(cudaEventRecord(e[0], stream));
+    if (use_panels()) {
+      for (int k = 0; k < static_cast<int>(panels.size()); ++k) {
+        const PanelArgs a = panel_args(k);
+        with_group_long(panels[k].G, a.plan.thr != 0x7fffffff, [&](auto g, auto l) {
+          k_spmv_rows_panel<decltype(g)::value, decltype(l)::value>
+              <<<panel_grid, kSpmvBlock, 0, stream>>>(p, 0, a);
         });
       }
-      CK(cudaEventRecord(e[1], C.stream));
-      C.launch_dual(0);
-      CK(cudaEventRecord(e[2], C.stream));
-      if (p.use_sell_cg) {
-        cclp_cu::with_group_long(C.gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
-          if (C.sgc.bs == 256)
-            cclp_cu::k_spmv_cols_sellg<decltype(g)::value, decltype(l)::value, 256>
-                <<<C.sgc.grid, 256, 0, C.stream>>>(p, 0);
-          else
-            cclp_cu::k_spmv_cols_sellg<decltype(g)::value, decltype(l)::value, cclp_cu::kSpmvBlock>
-                <<<C.sgc.grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
-        });
-      } else if (p.use_sell_c) {
-        if (p.plan_c.thr != 0x7fffffff)
-          cclp_cu::k_spmv_cols_sell<true, cclp_cu::kSpmvBlock>
-              <<<C.spmv_grid_c, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
-        else if (C.sell_bs == 256)
-          cclp_cu::k_spmv_cols_sell<false, 256><<<C.sell_grid, 256, 0, C.stream>>>(p, 0);
+    } else if (p.use_sell_r) {
+      with_group_long(grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
+        if (sgr.bs == 256)
+          k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, 256>
+              <<<sgr.grid, 256, 0, stream>>>(p, 0);
         else
-          cclp_cu::k_spmv_cols_sell<false, cclp_cu::kSpmvBlock>
-              <<<C.sell_grid, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
-      } else {
-        cclp_cu::with_group_long(C.gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
-          cclp_cu::k_spmv_cols<decltype(g)::value, decltype(l)::value>
-              <<<C.spmv_grid_c, cclp_cu::kSpmvBlock, 0, C.stream>>>(p, 0);
-        });
-      }
-      CK(cudaEventRecord(e[3], C.stream));
-      C.launch_primal(0);
-      CK(cudaEventRecord(e[4], C.stream));
-      C.launches += K;
-    }
-    CK(cudaStreamSynchronize(C.stream));
-    double acc[K] = {0, 0, 0, 0};
-    for (long long i = 0; i < iters; ++i)
-      for (int k = 0; k < K; ++k) {
-        float ms;
-        CK(cudaEventElapsedTime(&ms, ev[(K + 1) * i + k], ev[(K + 1) * i + k + 1]));
-        acc[k] += ms;
-      }
-    for (auto& e : ev) cudaEventDestroy(e);
-    for (int k = 0; k < K; ++k) out[k] = iters ? acc[k] / iters : 0.0;
-  });
-}
-
-int cclp_cu_phase_profile(cclp_cu_ctx* ctx, double* out, int64_t* steps) {
-  return guarded([&] {
-    Context& C = ctx->c;
-    if (!C.begun || C.stamps == nullptr)
-      throw std::invalid_argument("cclp_cu_phase_profile: call cclp_cu_begin/advance first (single device)");
-    constexpr int R = cclp_cu::kStampRing;
-    std::vector<unsigned long long> st(R * 4);
-    Ctrl ctl;
-    CK(cudaStreamSynchronize(C.stream));
-    CK(cudaMemcpy(st.data(), C.stamps, sizeof(unsigned long long) * R * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(&ctl, C.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost));
-    // steps t and t+1 both still in the ring: t in [it - R + 1, it - 2]
-    std::vector<double> d[4];
-    const long long it = ctl.iteration;
-    for (long long t = std::max<long long>(1, it - R + 1); t + 1 < it; ++t) {
-      const unsigned long long* a = &st[(t % R) * 4];
-      const unsigned long long nxt = st[((t + 1) % R) * 4];
-      const unsigned long long e[5] = {a[0], a[1], a[2], a[3], nxt};
-      bool ok = true;
-      for (int k = 0; k < 4; ++k) ok = ok && e[k] != 0 && e[k + 1] > e[k];
-      if (!ok) continue;
-      for (int k = 0; k < 4; ++k) d[k].push_back(1e-3 * static_cast<double>(e[k + 1] - e[k]));
-    }
-    for (int k = 0; k < 4; ++k) {
-      if (d[k].empty()) { out[k] = 0.0; continue; }
-      std::nth_element(d[k].begin(), d[k].begin() + d[k].size() / 2, d[k].end());
-      out[k] = d[k][d[k].size() / 2];
-    }
-    if (steps) *steps = static_cast<int64_t>(d[0].size());
-  });
-}
-
-void* cclp_cu_stream(cclp_cu_ctx* ctx) { return ctx ? static_cast<void*>(ctx->c.stream) : nullptr; }
-
-int cclp_cu_describe(cclp_cu_ctx* ctx, int64_t* out, int32_t nout) {
-  const Context& C = ctx->c;
-  Ctrl st;
-  std::memset(&st, 0, sizeof st);
-  if (C.ctrl != nullptr && cudaMemcpy(&st, C.ctrl, sizeof st, cudaMemcpyDeviceToHost) != cudaSuccess)
-    cudaGetLastError();
-  const int64_t v[] = {C.m, C.n, C.nnz, C.grow(), C.gcol(), C.spmv_grid_r * 10 + C.rpg_r,
-                       C.spmv_grid_c * 10 + C.rpg_c, C.launches,
-                       static_cast<int64_t>(st.t_fin_start - st.t_cols_start),
-                       static_cast<int64_t>(st.t_fin_end - st.t_fin_start),
-                       // 10..20: phase timings in ns (Context::phase)
-                       static_cast<int64_t>(1e9 * C.phase[0]), static_cast<int64_t>(1e9 * C.phase[1]),
-                       static_cast<int64_t>(1e9 * C.phase[2]), static_cast<int64_t>(1e9 * C.phase[3]),
-                       static_cast<int64_t>(1e9 * C.phase[4]), static_cast<int64_t>(1e9 * C.phase[5]),
-                       static_cast<int64_t>(1e9 * C.phase[6]), static_cast<int64_t>(1e9 * C.phase[7]),
-                       static_cast<int64_t>(1e9 * C.phase[8]), static_cast<int64_t>(1e9 * C.phase[9]),
-                       static_cast<int64_t>(1e9 * C.phase[10]),
-                       // 21, 22: block size of the SELL row / column product (0: CSR-G kernel)
-                       C.sgr.on ? C.sgr.bs : 0, C.sell_on ? C.sell_bs : (C.sgc.on ? C.sgc.bs : 0)};
-  for (int i = 0; i < nout && i < static_cast<int>(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
-  return CCLP_CU_OK;
-}
-
-int cclp_cu_matvec(cclp_cu_ctx* ctx, const double* x, double* out) {
-  return guarded([&] {
-    Context& C = ctx->c;
-    CK(cudaSetDevice(C.device));
-    CK(cudaMemcpyAsync(C.wn, x, sizeof(double) * C.n, cudaMemcpyHostToDevice, C.stream));
-    C.launch_spmv(false, C.wn, C.wm, false, nullptr);
-    CK(cudaMemcpyAsync(out, C.wm, sizeof(double) * C.m, cudaMemcpyDeviceToHost, C.stream));
-    CK(cudaStreamSynchronize(C.stream));
-  });
-}
-
-int cclp_cu_relative_report(cclp_cu_ctx* ctx, const double* x, const double* y, const double* z,
-                            cclp_cu_report* out, double* abs_violation) {
-  return guarded([&] {
-    Context& C = ctx->c;
-    CK(cudaSetDevice(C.device));
-    double rep[cclp_cu::kRepN];
-    C.relative_report(x, y, z, rep, abs_violation);
-    copy_report(rep, out);
-  });
-}
-
-int cclp_cu_price(cclp_cu_ctx* ctx, const double* y, const char* status, const uint8_t* skip, int32_t phase1,
-                  double dtol, int32_t bland, int64_t* entering, int32_t* direction, double* violation) {
-  return guarded([&] {
-    Context& C = ctx->c;
-    CK(cudaSetDevice(C.device));
-    long long e = -1;
-    int d = 0;
-    C.price(y, status, skip, phase1, dtol, bland, &e, &d, violation);
-    *entering = e;
-    *direction = d;
-  });
-}
-
-int cclp_cu_matvec_transpose(cclp_cu_ctx* ctx, const double* y, double* out) {
-  return guarded([&] {
-    Context& C = ctx->c;
-    CK(cudaSetDevice(C.device));
-    CK(cudaMemcpyAsync(C.wm, y, sizeof(double) * C.m, cudaMemcpyHostToDevice, C.stream));
-    C.launch_spmv(true, C.wm, C.wn, false, nullptr);
-    CK(cudaMemcpyAsync(out, C.wn, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.stream));
-    CK(cudaStreamSynchronize(C.stream));
-  });
-}
-
-int cclp_cu_ruiz(cclp_cu_ctx* ctx, int32_t iterations, double* row_scale, double* col_scale) {
-  return guarded([&] {
-    Context& C = ctx->c;
-    CK(cudaSetDevice(C.device));
-    C.ruiz(iterations);
-    CK(cudaMemcpyAsync(row_scale, C.r, sizeof(double) * C.m, cudaMemcpyDeviceToHost, C.stream));
-    CK(cudaMemcpyAsync(col_scale, C.s, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.stream));
-    CK(cudaStreamSynchronize(C.stream));
-  });
-}
-
-int cclp_cu_estimate_norm(cclp_cu_ctx* ctx, int32_t iterations, uint64_t seed, double* out) {
-  return guarded([&] {
-    Context& C = ctx->c;
-    CK(cudaSetDevice(C.device));
-    *out = C.power_norm(iterations, seed, false);
-  });
-}
-
-int cclp_cu_solve(cclp_cu_ctx* ctx, const cclp_cu_config* cfg_in, const cclp_cu_tolerances* tol,
-                  const double* thresholds, int32_t nthr, cclp_cu_sink_fn sink, void* sink_user,
-                  const volatile uint8_t* cancel, cclp_cu_log_fn logfn, void* log_user,
-                  double* x_out, double* y_out, double* z_out, cclp_cu_result* res) {
-  return guarded([&] {
-    Context& C = ctx->c;
-    CK(cudaSetDevice(C.device));
-    const cclp_cu_config cfg = *cfg_in;
-    validate_inputs(ctx, cfg, *tol, thresholds, nthr);
-    const auto wall0 = std::chrono::steady_clock::now();
-    C.launches = 0;
-    // First-touch the caller's result arrays on a host thread while the
-    // device works, so the final device-to-host copies do not take page
-    // faults (fresh pageable arrays cost ~4 ms on C2 otherwise).
-    std::thread prefault([=, &C] {
-      if (x_out) std::memset(x_out, 0, sizeof(double) * C.n);
-      if (y_out) std::memset(y_out, 0, sizeof(double) * C.m);
-      if (z_out) std::memset(z_out, 0, sizeof(double) * C.n);
-    });
-    struct JoinOnExit {
-      std::thread& t;
-      ~JoinOnExit() { if (t.joinable()) t.join(); }
-    } prefault_join{prefault};
-    const int k = cfg.poll_interval > 0 ? cfg.poll_interval : 64;
-    // the log ring holds two batches in flight (at most one line per iteration)
-    if (cfg.log_interval > 0 && C.log_cap < 4 * k) {
-      C.release(C.log);
-      C.log = nullptr;
-      C.log_cap = 4 * k;
-      C.h_log = C.host_alloc<cclp_cu::LogEntry>(C.log_cap);
-      C.log = C.alloc<cclp_cu::LogEntry>(C.log_cap);
-    }
-    // cancel: the caller's flag (and cclp_cu_request_cancel) mirrored into
-    // mapped memory that k_primal reads every iteration (pdhg.cpp:301)
-    C.ensure_flags();
-    C.abort_req.store(0);
-    volatile unsigned* hf = C.h_flags;
-    auto mirror_cancel = [&]() {
-      if ((cancel != nullptr && *cancel) || C.abort_req.load(std::memory_order_relaxed)) hf[0] = 1u;
-    };
-    hf[0] = 0u;
-    hf[1] = 0u;
-    mirror_cancel();
-    // three pinned staging sets of x | z (n) | y (m) for ladder snapshots:
-    // cudaHostAlloc costs ~1 ms per MB, so it runs on a helper thread while
-    // the setup works on the device, and is done before the loop's timer
-    const size_t stage_bytes = sizeof(double) * 3 * (2 * static_cast<size_t>(C.n) + C.m);
-    void* stage_p = nullptr;
-    std::exception_ptr stage_err;
-    std::thread stage_alloc;
-    if (nthr > 0 && !C.h_sx)
-      stage_alloc = std::thread([&] {
-        try {
-          stage_p = cclp_cu::pinned_alloc(stage_bytes);
-        } catch (...) {
-          stage_err = std::current_exception();
-        }
+          k_spmv_rows_sellg<decltype(g)::value, decltype(l)::value, kSpmvBlock>
+              <<<sgr.grid, kSpmvBlock, 0, stream>>>(p, 0);
       });
-    struct JoinStage {
-      std::thread& t;
-      ~JoinStage() { if (t.joinable()) t.join(); }
-    } stage_join{stage_alloc};
-    C.begin(cfg, *tol, thresholds, nthr);
-    if (stage_alloc.joinable()) {
-      stage_alloc.join();
-      if (stage_err) std::rethrow_exception(stage_err);
-      C.pinned.emplace_back(stage_p, stage_bytes);
-      C.h_sx = static_cast<double*>(stage_p);
+    } else {
+      with_group_long(grow(), p.plan_r.thr != 0x7fffffff, [&](auto g, auto l) {
+        k_spmv_rows<decltype(g)::value, decltype(l)::value>
+            <<<spmv_grid_r, kSpmvBlock, 0, stream>>>(p, 0);
+      });
     }
-    const double setup_s =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
-    C.build_graph(k);
-    C.mark(8);
-    CK(cudaEventRecord(C.ev_a, C.stream));
-
-    // ---- host side of the loop ------------------------------------------
-    // A launcher thread keeps two graph batches in flight (the device never
-    // waits for the host between batches), mirrors the cancel flag, and
-    // copies ladder snapshots out of their device slots on the side stream;
-    // the calling thread receives log lines and snapshots through a queue, in
-    // iteration order, and runs the caller's log and sink callbacks
-    // (pdhg.cpp:332-358) while the device keeps iterating.
-    struct Event {
-      int kind;  // 0 log line, 1 snapshot (staging set `set`), 2 end of loop
-      long long iteration;
-      std::string line;
-      int set = 0, thr_idx = 0, use_avg = 0;
-      double maxresid = 0.0;
-    };
-    std::mutex mu;
-    std::condition_variable cv;
-    std::deque<Event> events;
-    bool staging_busy[3] = {false, false, false};  // 0,1: slot snapshots; 2: host-extracted
-    std::exception_ptr launcher_error;
-    Ctrl st;
-    auto push = [&](Event e) {
-      std::lock_guard<std::mutex> g(mu);
-      events.push_back(std::move(e));
-      cv.notify_all();
-    };
-    auto set_ptr = [&](int set) { return C.h_sx + static_cast<size_t>(set) * (2 * static_cast<size_t>(C.n) + C.m); };
-    auto acquire_set = [&](int set) {  // launcher: wait until the sink released it
-      std::unique_lock<std::mutex> g(mu);
-      cv.wait(g, [&] { return !staging_busy[set]; });
-      staging_busy[set] = true;
-    };
-
-    std::thread launcher([&] {
-      try {
-        CK(cudaSetDevice(C.device));
-        long long log_seen = 0;
-        int snaps_copied = 0;
-        auto emit_logs_upto = [&](const Ctrl& q, long long upto) {
-          if (!logfn || cfg.log_interval <= 0) {
-            log_seen = q.log_count;
-            return;
-          }
-          for (long long i = std::max(log_seen, q.log_count - C.log_cap); i < q.log_count; ++i) {
-            const auto& e = C.h_log[i % C.log_cap];
-            if (e.iteration > upto) return;
-            char line[160];
-            std::snprintf(line, sizeof line, "%lld\t%.6e\t%.6e\t%.6e\t%.3f\n", e.iteration, e.rel_primal,
-                          e.rel_dual, e.rel_gap, e.elapsed);
-            push(Event{0, e.iteration, line});
-            log_seen = i + 1;
-          }
-        };
-        auto fetch_log = [&](const Ctrl& q) {
-          if (!logfn || cfg.log_interval <= 0 || q.log_count == log_seen) return;
-          CK(cudaMemcpyAsync(C.h_log, C.log, sizeof(cclp_cu::LogEntry) * C.log_cap, cudaMemcpyDeviceToHost,
-                             C.side));
-          CK(cudaStreamSynchronize(C.side));
-        };
-        // snapshot `idx`, extracted by the kernels into slot idx % kSnapSlots
-        auto copy_inline = [&](const Ctrl& q, int idx) {
-          const cclp_cu::SnapMeta& mt = q.snap_meta[idx % cclp_cu::kSnapSlots];
-          const int set = idx % cclp_cu::kSnapSlots;
-          acquire_set(set);
-          CK(cudaMemcpyAsync(set_ptr(set), C.snap_buf[set], sizeof(double) * (2 * static_cast<size_t>(C.n) + C.m),
-                             cudaMemcpyDeviceToHost, C.side));
-          CK(cudaStreamSynchronize(C.side));
-          hf[1] = static_cast<unsigned>(idx + 1);  // the device slot is free again
-          emit_logs_upto(q, mt.iteration);
-          push(Event{1, mt.iteration, {}, set, mt.thr_idx, mt.use_avg, mt.maxresid});
-        };
-        // a snapshot the loop halted for, or one requested at the final check
-        auto copy_extracted = [&](const Ctrl& q) {
-          acquire_set(2);
-          C.extract_view(q.snap_use_avg ? cclp_cu::kViewAvg : cclp_cu::kViewCur, q);
-          double* h = set_ptr(2);
-          CK(cudaEventRecord(C.ev_snap, C.stream));
-          CK(cudaStreamWaitEvent(C.side, C.ev_snap, 0));
-          CK(cudaMemcpyAsync(h, C.vx, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.side));
-          CK(cudaMemcpyAsync(h + C.n, C.vz, sizeof(double) * C.n, cudaMemcpyDeviceToHost, C.side));
-          CK(cudaMemcpyAsync(h + 2 * static_cast<size_t>(C.n), C.vy, sizeof(double) * C.m, cudaMemcpyDeviceToHost,
-                             C.side));
-          CK(cudaStreamSynchronize(C.side));
-          emit_logs_upto(q, q.snap_iteration);
-          push(Event{1, q.snap_iteration, {}, 2, q.snap_thr_idx, q.snap_use_avg, q.snap_maxresid});
-        };
-        auto clear_halt = [&]() {
-          const int zero[2] = {0, 0};
-          CK(cudaMemcpyAsync(&C.ctrl->halt, &zero[0], sizeof(int), cudaMemcpyHostToDevice, C.stream));
-          CK(cudaMemcpyAsync(&C.ctrl->snap_pending, &zero[1], sizeof(int), cudaMemcpyHostToDevice, C.stream));
-          CK(cudaStreamSynchronize(C.stream));
-        };
-        auto process = [&](const Ctrl& q) {  // everything a finished batch reported
-          fetch_log(q);
-          while (snaps_copied < q.snaps_done) copy_inline(q, snaps_copied++);
-          if (q.halt && q.snap_pending) {
-            copy_extracted(q);
-            clear_halt();
-          }
-          emit_logs_upto(q, LLONG_MAX);
-        };
-        cudaEvent_t evb[2];
-        for (auto& e : evb) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        struct EvGuard {
-          cudaEvent_t* e;
-          ~EvGuard() { for (int i = 0; i < 2; ++i) cudaEventDestroy(e[i]); }
-        } evguard{evb};
-        auto launch_batch = [&](int slot) {
-          CK(cudaGraphLaunch(C.graph, C.stream));
-          C.launches += cclp_cu::kKernelsPerIteration * k;
-          CK(cudaMemcpyAsync(&C.h_ctrl[slot], C.ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, C.stream));
-          CK(cudaEventRecord(evb[slot], C.stream));
-        };
-        auto wait_batch = [&](int slot) {  // polls, mirroring the cancel flag meanwhile
-          while (true) {
-            const cudaError_t e = cudaEventQuery(evb[slot]);
-            if (e == cudaSuccess) return;
-            if (e != cudaErrorNotReady) CK(e);
-            mirror_cancel();
-            std::this_thread::sleep_for(std::chrono::microseconds(20));
-          }
-        };
-        Ctrl q;
-        C.fetch_ctrl(&q);  // after the initial check
-        process(q);
-        if (q.stop < 0) {
-          int cur = 0;
-          launch_batch(cur);
-          bool ahead = false;
-          while (true) {
-            if (!ahead) launch_batch(cur ^ 1);  // one batch ahead of the one waited for
-            ahead = false;
-            wait_batch(cur);
-            q = C.h_ctrl[cur];
-            const bool drained = q.stop >= 0 || q.halt;
-            if (drained) wait_batch(cur ^ 1);  // exits at once: the device state is q
-            process(q);
-            if (q.stop >= 0) break;
-            if (drained) {  // the halt was served: restart the pipeline
-              launch_batch(cur);
-              continue;
-            }
-            cur ^= 1;
-          }
-        }
-        if (q.snap_pending && !q.halt) copy_extracted(q);  // the step that would extract it never ran
-        emit_logs_upto(q, LLONG_MAX);
-        st = q;
-      } catch (...) {
-        launcher_error = std::current_exception();
-      }
-      push(Event{2, 0, {}});
-    });
-    struct JoinLauncher {
-      std::thread& t;
-      ~JoinLauncher() { if (t.joinable()) t.join(); }
-    } launcher_join{launcher};
-
-    // calling thread: callbacks in order
-    while (true) {
-      Event e;
-      {
-        std::unique_lock<std::mutex> g(mu);
-        cv.wait(g, [&] { return !events.empty(); });
-        e = std::move(events.front());
-        events.pop_front();
-      }
-      if (e.kind == 2) break;
-      if (e.kind == 0) {
-        logfn(e.line.c_str(), log_user);
-        continue;
-      }
-      if (sink) {
-        const double* h = set_ptr(e.set);
-        cclp_cu_snapshot sp;
-        sp.x = h;
-        sp.z = h + C.n;
-        sp.y = h + 2 * static_cast<size_t>(C.n);
-        sp.m = C.m;
-        sp.n = C.n;
-        sp.threshold = thresholds[e.thr_idx];
-        sp.maxresid = e.maxresid;
-        sp.from_average = e.use_avg;
-        sp.iteration = e.iteration;
-        sink(&sp, sink_user);
-      }
-      std::lock_guard<std::mutex> g(mu);
-      staging_busy[e.set] = false;
-      cv.notify_all();
+    CK(cudaEventRecord(e[1], stream));
+    launch_dual(0);
+    CK(cudaEventRecord(e[2], stream));
+    if (p.use_sell_cg) {
+      with_group_long(gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
+        if (sgc.bs == 256)
+          k_spmv_cols_sellg<decltype(g)::value, decltype(l)::value, 256>
+              <<<sgc.grid, 256, 0, stream>>>(p, 0);
+        else
+          k_spmv_cols_sellg<decltype(g)::value, decltype(l)::value, kSpmvBlock>
+              <<<sgc.grid, kSpmvBlock, 0, stream>>>(p, 0);
+      });
+    } else if (p.use_sell_c) {
+      if (p.plan_c.thr != 0x7fffffff)
+        k_spmv_cols_sell<true, kSpmvBlock>
+            <<<spmv_grid_c, kSpmvBlock, 0, stream>>>(p, 0);
+      else if (sell_bs == 256)
+        k_spmv_cols_sell<false, 256><<<sell_grid, 256, 0, stream>>>(p, 0);
+      else
+        k_spmv_cols_sell<false, kSpmvBlock>
+            <<<sell_grid, kSpmvBlock, 0, stream>>>(p, 0);
+    } else {
+      with_group_long(gcol(), p.plan_c.thr != 0x7fffffff, [&](auto g, auto l) {
+        k_spmv_cols<decltype(g)::value, decltype(l)::value>
+            <<<spmv_grid_c, kSpmvBlock, 0, stream>>>(p, 0);
+      });
     }
-    launcher.join();
-    if (launcher_error) std::rethrow_exception(launcher_error);
-    CK(cudaEventRecord(C.ev_b, C.stream));
-    CK(cudaEventSynchronize(C.ev_b));
-    float loop_ms = 0;
-    CK(cudaEventElapsedTime(&loop_ms, C.ev_a, C.ev_b));
-    C.mark(9);
-
-    const int view = st.result_view;
-    const int stop = st.stop;
-    const bool rep_valid = st.result_report_valid != 0;
-    C.extract_view(view, st);
-    if (prefault.joinable()) prefault.join();
-    C.d2h(x_out, C.vx, sizeof(double) * C.n);
-    C.d2h(y_out, C.vy, sizeof(double) * C.m);
-    C.d2h(z_out, C.vz, sizeof(double) * C.n);
-    double rep[cclp_cu::kRepN];
-    CK(cudaMemcpyAsync(rep, C.vrep, sizeof(rep), cudaMemcpyDeviceToHost, C.stream));
-    CK(cudaStreamSynchronize(C.stream));
-    C.mark(10);
-    res->stop = stop;
-    res->iterations = st.iteration;
-    res->restarts = st.restarts;
-    res->error_iteration = stop == CCLP_CU_STOP_NUMERICAL_ERROR ? st.error_iteration : -1;
-    copy_report(rep_valid ? st.result_report : rep, &res->report);
-    res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
-    res->norm_estimate = C.norm_est;
-    res->omega = C.omega;
-    res->tau = C.tau;
-    res->sigma = C.sigma;
-    res->setup_seconds = setup_s;
-    res->loop_seconds = loop_ms * 1e-3;
-    res->kernel_launches = C.launches;
-    C.begun = false;
-  });
-}
-
-int cclp_cu_sharded_request_cancel(cclp_cu_sharded* ctx) {
-  if (ctx == nullptr) return CCLP_CU_EINVAL;
-  ctx->s.abort_req.store(1);
-  return CCLP_CU_OK;
-}
-
-int cclp_cu_request_cancel(cclp_cu_ctx* ctx) {
-  if (ctx == nullptr) return CCLP_CU_EINVAL;
-  ctx->c.abort_req.store(1);
-  return CCLP_CU_OK;
-}
-
-int cclp_cu_partition(const int32_t* ptr, int32_t rows, int32_t parts, int32_t* bounds) {
-  return guarded([&] {
-    if (ptr == nullptr || bounds == nullptr || rows < 0 || parts < 1)
-      throw std::invalid_argument("cclp_cu_partition: bad arguments");
-    cclp_cu::host_partition(ptr, rows, parts, 4, bounds);
-  });
-}
-
-int cclp_cu_nccl_unique_id(uint8_t* out128) {
-  return guarded([&] {
-    auto& api = cclp_cu::nccl();
-    if (!api.ok) throw Error(CCLP_CU_ENCCL, api.err);
-    ncclUniqueId id;
-    cclp_cu::nck(api.GetUniqueId(&id), "ncclGetUniqueId");
-    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
-    std::memcpy(out128, &id, sizeof(id));
-  });
-}
-
-int cclp_cu_sharded_create(const cclp_cu_lp* lp, int device, int32_t nshards, int32_t rank,
-                           int32_t nranks, const uint8_t* nccl_id, cclp_cu_sharded** out) {
-  *out = nullptr;
-  return guarded([&] {
-    if (lp == nullptr || lp->m < 0 || lp->n < 0 || lp->colptr == nullptr)
-      throw std::invalid_argument("cclp_cu_sharded_create: bad LP");
-    if (nranks < 1 || rank < 0 || rank >= nranks || nshards < 1)
-      throw std::invalid_argument("cclp_cu_sharded_create: bad rank / shard counts");
-    if (nranks > 1 && nccl_id == nullptr)
-      throw std::invalid_argument("cclp_cu_sharded_create: NCCL needs the unique id");
-    cclp_cu::ck(cudaSetDevice(device), "cudaSetDevice");
-    auto* ctx = new cclp_cu_sharded();
-    try {
-      ncclUniqueId id;
-      if (nccl_id) std::memcpy(&id, nccl_id, sizeof(id));
-      ctx->s.create(lp, device, nshards, rank, nranks, nccl_id ? &id : nullptr);
-    } catch (...) {
-      delete ctx;
-      throw;
-    }
-    *out = ctx;
-  });
-}
-
-int cclp_cu_sharded_create_hostcomm(const cclp_cu_lp* lp, int device, int32_t rank, int32_t nranks,
-                                    const cclp_cu_host_comm* comm, cclp_cu_sharded** out) {
-  *out = nullptr;
-  return guarded([&] {
-    if (lp == nullptr || lp->m < 0 || lp->n < 0 || lp->colptr == nullptr || comm == nullptr)
-      throw std::invalid_argument("cclp_cu_sharded_create_hostcomm: bad arguments");
-    if (nranks < 1 || rank < 0 || rank >= nranks)
-      throw std::invalid_argument("cclp_cu_sharded_create_hostcomm: bad rank");
-    cclp_cu::ck(cudaSetDevice(device), "cudaSetDevice");
-    auto* ctx = new cclp_cu_sharded();
-    try {
-      ctx->s.create(lp, device, 1, rank, nranks, nullptr, comm);
-    } catch (...) {
-      delete ctx;
-      throw;
-    }
-    *out = ctx;
-  });
-}
-
-int cclp_cu_sharded_destroy(cclp_cu_sharded* ctx) {
-  if (ctx) cudaSetDevice(ctx->s.device);
-  delete ctx;
-  return CCLP_CU_OK;
-}
-
-int cclp_cu_sharded_describe(cclp_cu_sharded* ctx, int64_t* out, int32_t nout) {
-  const auto& S = ctx->s;
-  std::vector<int64_t> v;
-  v.push_back(S.P);
-  for (int b : S.rb) v.push_back(b);
-  for (int b : S.cb) v.push_back(b);
-  v.push_back(S.launches);
-  v.push_back(S.halo_x.on ? 1 : 0);
-  v.push_back(S.halo_x.volume);
-  v.push_back(S.halo_y.on ? 1 : 0);
-  v.push_back(S.halo_y.volume);
-  v.push_back(static_cast<int64_t>(S.shards.size()));  // this process's shards:
-  for (const auto& sh : S.shards) {                   // rank, nnz of its A rows / A' rows
-    v.push_back(sh->shard_rank);
-    v.push_back(sh->nnz_rows_slice);
-    v.push_back(sh->nnz_cols_slice);
+    CK(cudaEventRecord(e[3], stream));
+    launch_primal(0);
+    CK(cudaEventRecord(e[4], stream));
+    launches += K;
   }
-  for (int i = 0; i < nout && i < static_cast<int>(v.size()); ++i) out[i] = v[i];
-  return CCLP_CU_OK;
+  CK(cudaStreamSynchronize(stream));
+  double acc[K] = {0, 0, 0, 0};
+  for (long long i = 0; i < iters; ++i)
+    for (int k = 0; k < K; ++k) {
+      float ms;
+      CK(cudaEventElapsedTime(&ms, ev[(K + 1) * i + k], ev[(K + 1) * i + k + 1]));
+      acc[k] += ms;
+    }
+  for (auto& e : ev) cudaEventDestroy(e);
+  for (int k = 0; k < K; ++k) out[k] = iters ? acc[k] / iters : 0.0;
 }
 
-int cclp_cu_sharded_begin(cclp_cu_sharded* ctx, const cclp_cu_config* cfg, const cclp_cu_tolerances* tol) {
-  return guarded([&] {
-    auto& S = ctx->s;
-    cclp_cu::ck(cudaSetDevice(S.device), "cudaSetDevice");
-    validate_inputs_eq(S.equality, *cfg, *tol, nullptr, 0);
-    S.begin(*cfg, *tol, nullptr, 0);
-    for (auto& sh : S.shards) {  // measurement mode: never converge, never hit the limit
-      sh->params.eps_rel = -1.0;
-      sh->params.max_iter = (1LL << 62);
-    }
-    if (S.graph) {
-      cudaGraphExecDestroy(S.graph);
-      S.graph = nullptr;
-    }
-  });
-}
-
-int cclp_cu_sharded_advance(cclp_cu_sharded* ctx, int64_t iters, double* device_ms) {
-  return guarded([&] {
-    auto& S = ctx->s;
-    if (!S.begun) throw std::invalid_argument("cclp_cu_sharded_advance: call begin first");
-    Context& C = S.s0();
-    const int k = 16;
-    CK(cudaEventRecord(C.ev_a, S.stream));
-    long long done = 0;
-    while (done + k <= iters) {
-      S.run_batch(k);
-      done += k;
-    }
-    while (done < iters) {
-      S.launch_round(false);
-      ++done;
-    }
-    CK(cudaEventRecord(C.ev_b, S.stream));
-    CK(cudaEventSynchronize(C.ev_b));
-    float ms = 0;
-    CK(cudaEventElapsedTime(&ms, C.ev_a, C.ev_b));
-    if (device_ms) *device_ms = ms;
-  });
-}
-
-int cclp_cu_sharded_solve(cclp_cu_sharded* ctx, const cclp_cu_config* cfg_in, const cclp_cu_tolerances* tol,
-                          const double* thresholds, int32_t nthr, cclp_cu_sink_fn sink, void* sink_user,
-                          const volatile uint8_t* cancel, double* x_out, double* y_out, double* z_out,
-                          cclp_cu_result* res) {
-  return guarded([&] {
-    auto& S = ctx->s;
-    cclp_cu::ck(cudaSetDevice(S.device), "cudaSetDevice");
-    const cclp_cu_config cfg = *cfg_in;
-    validate_inputs_eq(S.equality, cfg, *tol, thresholds, nthr);
-    const auto wall0 = std::chrono::steady_clock::now();
-    S.launches = 0;
-    S.abort_req.store(0);
-    S.begin(cfg, *tol, thresholds, nthr);
-    const double setup_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
-    const int k = cfg.poll_interval > 0 ? cfg.poll_interval : 32;
-    S.build_graph(k);
-    Context& C0 = S.s0();
-    CK(cudaEventRecord(C0.ev_a, S.stream));
-    Ctrl st;
-    S.fetch_ctrl(&st);
-    std::vector<double> hx(S.n), hy(S.m), hz(S.n);
-    double sums[cclp_cu::kRowParts + cclp_cu::kColParts];
-    bool cancelled = false, timed_out = false;
-    while (true) {
-      if (st.halt && st.snap_pending) {  // PdhgSnapshot of the better view (pdhg.cpp:346-358)
-        S.assemble_view(st.snap_use_avg ? cclp_cu::kViewAvg : cclp_cu::kViewCur, st, hx.data(), hy.data(),
-                        hz.data(), sums);
-        if (sink) {
-          cclp_cu_snapshot sp;
-          sp.x = hx.data();
-          sp.y = hy.data();
-          sp.z = hz.data();
-          sp.m = S.m;
-          sp.n = S.n;
-          sp.threshold = thresholds[st.snap_thr_idx];
-          sp.maxresid = st.snap_maxresid;
-          sp.from_average = st.snap_use_avg;
-          sp.iteration = st.snap_iteration;
-          sink(&sp, sink_user);
-        }
-        S.clear_halt();
-        st.halt = 0;
-      }
-      if (st.stop >= 0) break;
-      const bool want_cancel = (cancel != nullptr && *cancel) || S.abort_req.load(std::memory_order_relaxed);
-      const bool want_time =
-          std::isfinite(cfg.time_limit) &&
-          std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count() > cfg.time_limit;
-      using Req = cclp_cu::Sharded::StopReq;
-      const Req req = S.agree(want_cancel ? Req::kStopCancel : want_time ? Req::kStopTime : Req::kStopNone);
-      if (req != Req::kStopNone) {  // all ranks stop together, with the same reason
-        cancelled = req == Req::kStopCancel;
-        timed_out = req == Req::kStopTime;
-        break;
-      }
-      S.run_batch(k);
-      S.fetch_ctrl(&st);
-    }
-    CK(cudaEventRecord(C0.ev_b, S.stream));
-    CK(cudaEventSynchronize(C0.ev_b));
-    float loop_ms = 0;
-    CK(cudaEventElapsedTime(&loop_ms, C0.ev_a, C0.ev_b));
-    int view = st.result_view;
-    int stop = st.stop;
-    bool rep_valid = st.result_report_valid != 0;
-    if (cancelled || timed_out) {
-      stop = cancelled ? CCLP_CU_STOP_CANCELLED : CCLP_CU_STOP_TIME_LIMIT;
-      view = cclp_cu::kViewCurEff;
-      rep_valid = st.checked != 0;
-      if (rep_valid) std::memcpy(st.result_report, st.R ? st.avg : st.cur, sizeof(st.result_report));
-    }
-    S.assemble_view(view, st, x_out, y_out, z_out, sums);
-    double rep[cclp_cu::kRepN];
-    cclp_cu::host_make_report(sums, sums + cclp_cu::kRowParts, C0.b_norm, C0.c_norm, rep);
-    res->stop = stop;
-    res->iterations = st.iteration;
-    res->restarts = st.restarts;
-    res->error_iteration = stop == CCLP_CU_STOP_NUMERICAL_ERROR ? st.error_iteration : -1;
-    copy_report(rep_valid ? st.result_report : rep, &res->report);
-    res->seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall0).count();
-    res->norm_estimate = C0.norm_est;
-    res->omega = C0.omega;
-    res->tau = C0.tau;
-    res->sigma = C0.sigma;
-    res->setup_seconds = setup_s;
-    res->loop_seconds = loop_ms * 1e-3;
-    res->kernel_launches = S.launches;
-    S.begun = false;
-  });
-}
-
-int cclp_cu_run_pdhg(const cclp_cu_lp* lp, const cclp_cu_config* cfg, const cclp_cu_tolerances* tol,
-                     const double* thresholds, int32_t nthr, cclp_cu_sink_fn sink, void* sink_user,
-                     const volatile uint8_t* cancel, double* x_out, double* y_out, double* z_out,
-                     cclp_cu_result* res, int device) {
-  cclp_cu_ctx* ctx = nullptr;
-  int rc = cclp_cu_create(lp, device, &ctx);
-  if (rc != CCLP_CU_OK) return rc;
-  rc = cclp_cu_solve(ctx, cfg, tol, thresholds, nthr, sink, sink_user, cancel, nullptr, nullptr,
-                     x_out, y_out, z_out, res);
-  cclp_cu_destroy(ctx);
-  return rc;
-}
-
-}  // extern "C"
+}  // namespace cclp_cu

@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 
 namespace cclp_cu {
+namespace {  // internal linkage: compiled into engine.cu and sharded.cu
 
 constexpr unsigned kRowMaxMask = (1u << 1) | (1u << 4);
 constexpr unsigned kColMaxMask = (1u << 1) | (1u << 2) | (1u << 3) | (1u << 7) | (1u << 8) | (1u << 9);
@@ -1021,4 +1022,5 @@ __global__ void __launch_bounds__(kBlock) k_view_cols(const ViewParams v, int ro
   }
 }
 
+}  // namespace
 }  // namespace cclp_cu

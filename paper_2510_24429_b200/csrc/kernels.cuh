@@ -215,6 +215,14 @@ struct IterParams {
   unsigned long long* stamps;
 };
 
+// Power-iteration scalars on the device (Context::power_norm, setup_kernels.cuh).
+struct PowerCtrl {
+  double nu;      // ||u_prev|| (v = u_prev / nu)
+  double lambda;  // Rayleigh quotient v.u
+  int zero;       // ||u|| == 0 -> result 0
+  int pad;
+};
+
 // ---------------------------------------------------------------------------
 // Block reductions (deterministic: fixed shuffle tree, fixed warp order).
 // ---------------------------------------------------------------------------

@@ -6,6 +6,7 @@
 #include "kernels.cuh"
 
 namespace cclp_cu {
+namespace {  // internal linkage: compiled into engine.cu and sharded.cu
 
 __global__ void k_expand_major(const int* __restrict__ ptr, int outer, int* __restrict__ major) {
   // major[p] = outer index owning nonzero p
@@ -124,12 +125,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv(const int* __restrict__ ptr, co
 }
 
 // ---- power iteration (estimate_matrix_norm, pdhg.cpp:46-65) ---------------
-struct PowerCtrl {
-  double nu;      // ||u_prev|| (v = u_prev / nu)
-  double lambda;  // Rayleigh quotient v.u
-  int zero;       // ||u|| == 0 -> result 0
-  int pad;
-};
+
 
 // u = A' w, partial sums of u.u and v.u with v = u_prev / nu; the last block
 // finalizes nu and lambda.
@@ -584,6 +580,7 @@ __global__ void k_init_x(const double* __restrict__ l, const double* __restrict_
 
 __global__ void k_stamp(unsigned long long* t) { *t = globaltimer(); }
 
+}  // namespace
 }  // namespace cclp_cu
 
 // ---------------------------------------------------------------------------
@@ -594,6 +591,7 @@ __global__ void k_stamp(unsigned long long* t) { *t = globaltimer(); }
 // each field over the blocks in block order (deterministic).
 // ---------------------------------------------------------------------------
 namespace cclp_cu {
+namespace {  // internal linkage: compiled into engine.cu and sharded.cu
 
 constexpr int kKktRowF = 4;   // 0 sum r^2, 1 max |r|, 2 b.y, 3 sum b^2   (r = b - ax, kkt.cpp:37-52)
 constexpr int kKktColF = 7;   // 0 sum rd^2, 1 max |rd|, 2 max bound violation, 3 complementarity,
@@ -671,10 +669,12 @@ __global__ void k_kkt_finish(const double* __restrict__ rpart, int rblocks, cons
   }
 }
 
+}  // namespace
 }  // namespace cclp_cu
 
 // SELL-32 build (Context::build_sell_cols): slice widths, then the slots.
 namespace cclp_cu {
+namespace {  // internal linkage: compiled into engine.cu and sharded.cu
 
 __global__ void k_sell_width(const int* __restrict__ ptr, int n, int thr, int nsl, int* __restrict__ width) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nsl; s += gridDim.x * blockDim.x) {
@@ -715,11 +715,13 @@ __global__ void k_sell_fill(const int* __restrict__ ptr, const int* __restrict__
   }
 }
 
+}  // namespace
 }  // namespace cclp_cu
 
 // SELL-G build (Context::build_sell_rows): 32/G rows per slice, G lanes per
 // row; slot k of lane (r, gl) holds row s*R + r's element k*G + gl.
 namespace cclp_cu {
+namespace {  // internal linkage: compiled into engine.cu and sharded.cu
 
 __global__ void k_sellg_width(const int* __restrict__ ptr, int n, int thr, int nsl, int G,
                               int* __restrict__ width) {
@@ -761,6 +763,7 @@ __global__ void k_sellg_fill(const int* __restrict__ ptr, const int* __restrict_
   }
 }
 
+}  // namespace
 }  // namespace cclp_cu
 
 // ---------------------------------------------------------------------------
@@ -774,6 +777,7 @@ __global__ void k_sellg_fill(const int* __restrict__ ptr, const int* __restrict_
 // the pick is the reference's.
 // ---------------------------------------------------------------------------
 namespace cclp_cu {
+namespace {  // internal linkage: compiled into engine.cu and sharded.cu
 
 struct PriceCand {
   double viol;
@@ -852,4 +856,5 @@ __global__ void k_price_finish(const PriceCand* __restrict__ part, int nblocks, 
   *out = b;
 }
 
+}  // namespace
 }  // namespace cclp_cu

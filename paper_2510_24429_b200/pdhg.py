@@ -165,7 +165,7 @@ EXPORTED_SYMBOLS = [
 ]
 
 
-# Host phase timings reported by cclp_cu_describe (engine.cu, Context::phase).
+# Host phase timings reported by cclp_cu_describe (context.cuh, Context::phase).
 PHASES = ["upload", "csr_build", "partition_tune", "norms", "ruiz", "scale_values", "power_norm",
           "init_check0", "graph_build", "loop", "result_download"]
 

@@ -8,7 +8,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 
-# the engine's development knobs (csrc/engine.cu dev_knob) are read only with
+# the engine's development knobs (csrc/host_util.cuh dev_knob) are read only with
 # this switch; some tests force layouts through them
 os.environ.setdefault("CCLP_CU_DEV_KNOBS", "1")
 

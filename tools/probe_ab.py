@@ -1,4 +1,4 @@
-"""A/B of one development knob (csrc/engine.cu dev_knob) on the device loop:
+"""A/B of one development knob (csrc/host_util.cuh dev_knob) on the device loop:
 us per iteration (CUDA graph, best of 3) and the in-graph phase split, per
 config and knob value. Knobs read at begin() share one engine per config;
 `--fresh` builds an engine per value (knobs read at create, e.g. the G).

@@ -9,6 +9,9 @@ from paper_2510_24429_b200.pdhg import Engine, PdhgConfig  # noqa: E402
 cfgname = sys.argv[1] if len(sys.argv) > 1 else "C2"
 iters = int(sys.argv[2]) if len(sys.argv) > 2 else 2000
 lp = lpgen.make_config(cfgname)
+if "--pinned" in sys.argv:  # the bench's e2e input: the LP in pinned host buffers
+    import bench
+    lp, _keep = bench.pinned_copy(lp)
 for rep in range(3):
     t = time.perf_counter()
     eng = Engine(lp)
