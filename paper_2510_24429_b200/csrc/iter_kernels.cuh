@@ -144,11 +144,33 @@ __device__ __forceinline__ void push_signal_grid(const PushArgs& ps, int kind, u
   *counter = 0u;
 }
 
+// The global values decide() reads, loaded into shared memory by a thread the
+// partial reduction leaves idle, so their latency overlaps it: the cancel
+// request block 0 of the column kernel mirrored, the loop's start time and
+// the next ladder threshold.
+constexpr int kPrefetchThread = 480;  // reduce_partials uses threads 0..351
+struct DecidePrefetch {
+  unsigned cancel;
+  unsigned long long t0;
+  double thr;
+};
+__device__ __forceinline__ DecidePrefetch decide_prefetch(const IterParams& p) {
+  DecidePrefetch f{0u, 0ull, 0.0};
+  if (p.cancel_dev != nullptr) f.cancel = *reinterpret_cast<volatile unsigned*>(p.cancel_dev);
+  f.t0 = *p.t0_ns;
+  const int nt = __ldcg(&p.ctrl->next_threshold);
+  if (nt < p.nthr) f.thr = __ldcg(p.thr + nt);
+  return f;
+}
+
 // check(t+1) and everything after the step in the reference pass
 // (pdhg.cpp:128-130 error, 301-368 next pass: time, check, limit), taken by
-// thread 0 on a shared-memory copy of the control block.
+// thread 0 on a shared-memory copy of the control block. `rep` holds the two
+// reports of check(t+1) (current, average), assembled beforehand by two
+// other threads.
 __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, Ctrl* C,
-                                       const double* rowv, const double* colv, bool write_log = true) {
+                                       const double* rowv, const double* colv, const double (*rep)[kRepN],
+                                       const DecidePrefetch& pf, bool write_log = true) {
   if (!si.init && p.snap_inline && C->snap_pending) {  // this step extracted the pending snapshot
     SnapMeta& mt = C->snap_meta[C->snaps_done % kSnapSlots];
     mt.iteration = C->snap_iteration;
@@ -179,12 +201,13 @@ __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, 
   const long long win = C->window;
   C->checked = si.check ? 1 : 0;
   if (si.check) {
-    make_report(rowv, colv, p.b_norm, p.c_norm, C->cur);
-    if (win > 0) make_report(rowv + 3, colv + 6, p.b_norm, p.c_norm, C->avg);
+    for (int k = 0; k < kRepN; ++k) C->cur[k] = rep[0][k];
+    if (win > 0)
+      for (int k = 0; k < kRepN; ++k) C->avg[k] = rep[1][k];
   }
   // cancel poll at the top of the pass (pdhg.cpp:301-305): the request the
   // host mirrored into mapped memory, read by k_primal's block 0 this step
-  if (p.cancel_dev != nullptr && *reinterpret_cast<volatile unsigned*>(p.cancel_dev) != 0u) {
+  if (pf.cancel != 0u) {
     C->stop = 3;
     C->result_view = kViewCur;
     C->result_report_valid = C->checked;
@@ -193,7 +216,7 @@ __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, 
     return;
   }
   if (isfin(p.time_limit)) {  // pdhg.cpp:306-310
-    const double el = 1e-9 * static_cast<double>(globaltimer() - *p.t0_ns);
+    const double el = 1e-9 * static_cast<double>(globaltimer() - pf.t0);
     if (el > p.time_limit) {
       C->stop = 2;
       C->result_view = kViewCur;
@@ -219,7 +242,7 @@ __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, 
         e.rel_primal = better[kRelP];
         e.rel_dual = better[kRelD];
         e.rel_gap = better[kRelGap];
-        e.elapsed = 1e-9 * static_cast<double>(globaltimer() - *p.t0_ns);
+        e.elapsed = 1e-9 * static_cast<double>(globaltimer() - pf.t0);
       }
       C->log_count++;
     }
@@ -230,7 +253,7 @@ __device__ __forceinline__ void decide(const IterParams& p, const StepInfo& si, 
       for (int k = 0; k < kRepN; ++k) C->result_report[k] = better[k];
       return;
     }
-    if (C->next_threshold < p.nthr && better[kMaxResid] <= p.thr[C->next_threshold]) {
+    if (C->next_threshold < p.nthr && better[kMaxResid] <= pf.thr) {
       // a free slot: the next step extracts the view and the loop runs on;
       // else halt and let the host extract it (pdhg.cpp:346-358)
       const int copied = p.host_flags != nullptr ? static_cast<int>(ld_relaxed_sys(p.host_flags + 1)) : 0;
@@ -317,15 +340,22 @@ __device__ __forceinline__ void load_ctrl(const IterParams& p) {
   for (int w = threadIdx.x; w < kWords; w += blockDim.x) csw[w] = __ldcg(gw + w);
 }
 
-// Expects load_ctrl() and a block barrier before it.
+// Expects load_ctrl() and a block barrier before it, and `pf` in shared memory.
 __device__ void decide_and_store(const IterParams& p, const StepInfo& si, const double* rowv,
-                                 const double* colv) {
+                                 const double* colv, const DecidePrefetch& pf) {
   Ctrl& cs = ctrl_smem();
   constexpr int kWords = sizeof(Ctrl) / 8;
   long long* csw = reinterpret_cast<long long*>(&cs);
+  __shared__ double rep[2][kRepN];
+  // the two reports of check(t+1) in parallel (make_report: sqrt and divisions)
+  if (si.check) {
+    if (threadIdx.x == 32) make_report(rowv, colv, p.b_norm, p.c_norm, rep[0]);
+    if (threadIdx.x == 64) make_report(rowv + 3, colv + 6, p.b_norm, p.c_norm, rep[1]);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     cs.t_cols_start = globaltimer();  // debug: reuse as "partials reduced" stamp
-    decide(p, si, &cs, rowv, colv);
+    decide(p, si, &cs, rowv, colv, rep, pf);
     cs.t_fin_end = globaltimer();
   }
   __syncthreads();
@@ -339,7 +369,10 @@ __device__ void decide_and_store(const IterParams& p, const StepInfo& si, const 
 __device__ void finalize(const IterParams& p, const StepInfo& si) {
   __shared__ double rowv[kRowParts];
   __shared__ double colv[kColParts];
-  if (p.xpart_loc == nullptr && !p.push.on) load_ctrl(p);
+  const bool deciding = p.xpart_loc == nullptr && !p.push.on;
+  __shared__ DecidePrefetch pf;
+  if (deciding && threadIdx.x == kPrefetchThread % blockDim.x) pf = decide_prefetch(p);
+  if (deciding) load_ctrl(p);
   reduce_partials(p.rowp, p.row_grid, p.colp, p.col_grid, rowv, colv);  // ends with a barrier
   if (p.push.on) {  // this shard's sums into every shard's [P][22], then release
     constexpr int W = kRowParts + kColParts;
@@ -360,7 +393,7 @@ __device__ void finalize(const IterParams& p, const StepInfo& si) {
     if (threadIdx.x < kColParts) p.xpart_loc[kRowParts + threadIdx.x] = colv[threadIdx.x];
     return;
   }
-  decide_and_store(p, si, rowv, colv);
+  decide_and_store(p, si, rowv, colv, pf);
 }
 
 // Sharded mode: every shard reduces the exchanged per-shard sums
@@ -373,6 +406,8 @@ __global__ void __launch_bounds__(kEpiBlock) k_finalize_shard(const IterParams p
   __shared__ double rowv[kRowParts];
   __shared__ double colv[kColParts];
   if (p.push.on) push_wait(p.push, kPushPart, static_cast<unsigned long long>(si.t1 + 1));
+  __shared__ DecidePrefetch pf;
+  if (threadIdx.x == kPrefetchThread % blockDim.x) pf = decide_prefetch(p);
   load_ctrl(p);
   constexpr int W = kRowParts + kColParts;
   if (threadIdx.x < W) {
@@ -388,7 +423,7 @@ __global__ void __launch_bounds__(kEpiBlock) k_finalize_shard(const IterParams p
     (is_row ? rowv : colv)[k] = a;
   }
   __syncthreads();
-  decide_and_store(p, si, rowv, colv);
+  decide_and_store(p, si, rowv, colv, pf);
 }
 
 // Sharded mode: this shard's slice of the next iterate, x_{t+2} =
