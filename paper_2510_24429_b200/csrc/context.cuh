@@ -300,6 +300,9 @@ struct Context {
   void launch_cols_half(bool init);  // k_spmv_cols + k_primal
   void launch_dual(int ii);
   void launch_primal(int ii);
+  static constexpr int kBulkMinRows = 256 * 1024;   // k_dual: bulk-copy ring from this many rows
+  static constexpr int kBulkMinCols = 1024 * 1024;  // k_primal: from this many columns
+  bool bulk_epilogue(bool rows_side) const;
   void build_graph(int k);
   void profile_kernels(long long iters, double* out);  // cclp_cu_profile_kernels
   void fetch_ctrl(Ctrl* dst);

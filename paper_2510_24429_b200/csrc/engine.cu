@@ -1313,15 +1313,36 @@ void Context::launch_cols_half(bool init) {
   launch_primal(ii);
 }
 
-// The streaming epilogues: one block per SM with its shared-memory ring of
-// operand tiles (bulk_stream, iter_kernels.cuh).
+// The streaming epilogues: one block per SM, the operand streams through the
+// shared-memory ring of bulk copies (bulk_stream, iter_kernels.cuh) on long
+// vectors, loaded by the threads on short ones (reg_stream: the same elements
+// in the same order, so the results do not depend on the choice). Measured
+// crossovers (profiles/r2/history/r2_epilogue_bulk_vs_reg.txt): k_dual's 7
+// streams at 100k rows (C2) 3.8 vs 4.3 us, at 400k (C3) 8.9 vs 7.8 us;
+// k_primal's 8 at 500k columns (C2) 14.8 vs 15.9 us, at 2.2M (C3) 45.9 vs
+// 40.8 us.
+bool Context::bulk_epilogue(bool rows_side) const {
+  if (const char* e = dev_knob("CCLP_CU_EPI")) {  // tests: reg | bulk
+    if (std::string(e) == "reg") return false;
+    if (std::string(e) == "bulk") return true;
+  }
+  return rows_side ? m >= kBulkMinRows : n >= kBulkMinCols;
+}
 void Context::launch_dual(int ii) {
-  allow_smem(reinterpret_cast<const void*>(k_dual), bulk_smem<kDualStreams>());
-  launch_pdl_smem(k_dual, epi_grid, kTile, bulk_smem<kDualStreams>(), stream, params, ii);
+  if (bulk_epilogue(true)) {
+    allow_smem(reinterpret_cast<const void*>(k_dual<true>), bulk_smem<kDualStreams>());
+    launch_pdl_smem(k_dual<true>, epi_grid, kTile, bulk_smem<kDualStreams>(), stream, params, ii);
+  } else {
+    launch_pdl(k_dual<false>, epi_grid, kTile, stream, params, ii);
+  }
 }
 void Context::launch_primal(int ii) {
-  allow_smem(reinterpret_cast<const void*>(k_primal), bulk_smem<kPrimalStreams>());
-  launch_pdl_smem(k_primal, epi_grid, kTile, bulk_smem<kPrimalStreams>(), stream, params, ii);
+  if (bulk_epilogue(false)) {
+    allow_smem(reinterpret_cast<const void*>(k_primal<true>), bulk_smem<kPrimalStreams>());
+    launch_pdl_smem(k_primal<true>, epi_grid, kTile, bulk_smem<kPrimalStreams>(), stream, params, ii);
+  } else {
+    launch_pdl(k_primal<false>, epi_grid, kTile, stream, params, ii);
+  }
 }
 
 void Context::launch_iteration(bool init) {

@@ -782,6 +782,29 @@ __device__ __forceinline__ void bulk_stream(int n, const double* const (&src)[NS
   }
 }
 
+// The same walk without the shared-memory ring, for short vectors (a block
+// gets only a few tiles, so the ring's first-tile latency is not amortized):
+// thread t of block b takes elements b * kTile + t + k * grid * kTile,
+// k = 0, 1, ... in order — the elements and order of bulk_stream, so every
+// thread's partial sums, the block partials and all results are identical —
+// with two elements' loads in flight.
+template <int NS, class Body>
+__device__ __forceinline__ void reg_stream(int n, const double* const (&src)[NS], unsigned mask, Body&& body) {
+  const int stride = static_cast<int>(gridDim.x) * kTile;
+  for (int j0 = static_cast<int>(blockIdx.x) * kTile + static_cast<int>(threadIdx.x); j0 < n; j0 += 2 * stride) {
+    const int j1 = j0 + stride;
+    double v0[NS], v1[NS];
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      const bool on = (mask >> q) & 1u;
+      v0[q] = on ? src[q][j0] : 0.0;
+      v1[q] = on && j1 < n ? src[q][j1] : 0.0;
+    }
+    body(j0, v0);
+    if (j1 < n) body(j1, v1);
+  }
+}
+
 // k_dual's operand streams: r, b, ax_{t+1}, then state t: y, ax, y_sum, ax_sum.
 enum DualStream : int { kDsR = 0, kDsB, kDsAxn, kDsY, kDsAx, kDsYs, kDsAxs, kDualStreams };
 
@@ -858,7 +881,9 @@ __device__ __forceinline__ void snap_cols(const IterParams& p, const StepInfo& s
 }
 
 // Dual update + row-side report partials, the operand streams staged by the
-// TMA engine (bulk_stream).
+// TMA engine (bulk_stream) or, on short vectors, loaded by the threads
+// (reg_stream): the same results either way.
+template <bool BULK>
 __global__ void __launch_bounds__(kTile, 1) k_dual(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si, 1)) return;
@@ -872,7 +897,11 @@ __global__ void __launch_bounds__(kTile, 1) k_dual(const IterParams p, int init)
   // state t's ax is read when no restart is applied, the sums except at init
   const unsigned mask = 0xFu | (si.init || si.R ? 0u : (1u << kDsAx)) |
                         (si.init ? 0u : ((1u << kDsYs) | (1u << kDsAxs)));
-  bulk_stream<kDualStreams>(p.m, src, mask, [&](int i, const double* v) { dual_row(p, si, i, v, acc); });
+  auto body = [&](int i, const double* v) { dual_row(p, si, i, v, acc); };
+  if constexpr (BULK)
+    bulk_stream<kDualStreams>(p.m, src, mask, body);
+  else
+    reg_stream<kDualStreams>(p.m, src, mask, body);
   if (si.snap) snap_rows(p, si);
   block_reduce<kRowParts, kRowMaxMask, kTile>(acc, red, out);
   if (threadIdx.x < kRowParts) p.rowp[threadIdx.x * gridDim.x + blockIdx.x] = out[threadIdx.x];  // field-major
@@ -909,8 +938,10 @@ __device__ __forceinline__ void primal_column(const IterParams& p, const StepInf
 enum PrimalStream : int { kPsS = 0, kPsC, kPsL, kPsU, kPsX, kPsAty, kPsXs, kPsAs, kPrimalStreams };
 
 // Primal side: sums, column-side report partials, both next-x candidates,
-// the operand streams staged by the TMA engine (bulk_stream); the last block
-// to finish runs finalize().
+// the operand streams staged by the TMA engine (bulk_stream) or, on short
+// vectors, loaded by the threads (reg_stream); the last block to finish runs
+// finalize().
+template <bool BULK>
 __global__ void __launch_bounds__(kTile, 1) k_primal(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si, 3)) return;
@@ -928,9 +959,13 @@ __global__ void __launch_bounds__(kTile, 1) k_primal(const IterParams p, int ini
                                              p.xsum[si.s0], p.atysum[si.s0]};
   // the sums are read only when they carry on (not at init, not after a restart)
   const unsigned mask = (si.init || si.R) ? 0x3Fu : 0xFFu;
-  bulk_stream<kPrimalStreams>(p.n, src, mask, [&](int j, const double* v) {
+  auto body = [&](int j, const double* v) {
     primal_column(p, si, j, v[kPsS], v[kPsC], v[kPsL], v[kPsU], v[kPsX], v[kPsAty], v[kPsXs], v[kPsAs], acc);
-  });
+  };
+  if constexpr (BULK)
+    bulk_stream<kPrimalStreams>(p.n, src, mask, body);
+  else
+    reg_stream<kPrimalStreams>(p.n, src, mask, body);
   if (si.snap) snap_cols(p, si);
   block_reduce<kColParts, kColMaxMask, kTile>(acc, red, out);
   if (threadIdx.x < kColParts) p.colp[threadIdx.x * gridDim.x + blockIdx.x] = out[threadIdx.x];  // field-major
