@@ -52,7 +52,9 @@ def raw_rows(rep):
 
 
 def short(name):
-    name = name.replace("cclp_cu::", "").replace("void ", "")
+    name = name.replace("void ", "")
+    for ns in ("cclp_cu::", "(anonymous namespace)::", "<unnamed>::", "unnamed>::"):
+        name = name.replace(ns, "")
     return name.split("(")[0]
 
 
