@@ -70,6 +70,11 @@ if b.get("time_to_tolerance"):
                f"{t6['seconds']:.1f} s ({t6['iterations']:,} it) |")
 out.append(f"| clocks during the timed region | {b['clocks']['sm_mhz']:.0f} MHz of {b['clocks']['sm_max_mhz']:.0f}, "
            f"reasons {b['clocks']['reasons']} |")
+ttt = [json.loads(x) for x in text("time_to_tol_c3_c4.jsonl").splitlines() if x.strip()]
+if ttt:
+    out += ["", "Time to 1e-4 end to end (`tools/time_to_tol.py`, `time_to_tol_c3_c4.jsonl`): "
+            + "; ".join(f"{t['config']} {t['seconds']:.1f} s ({t['iterations']:,} iterations, {t['restarts']} restarts)"
+                        for t in ttt) + "."]
 out += ["", "## Per configuration (same bench run, `per_config`; in-graph kernel split)", "",
         "| config | nnz | us / iteration | B_iter fraction | rows | dual | cols | primal | dominant (fraction) |",
         "|---|---|---|---|---|---|---|---|---|"]
