@@ -731,8 +731,8 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_cols(const IterParams p, in
 // mbarrier per stage counts the bytes in. An SM keeps up to kStages tiles of
 // all streams in flight (112-128 KB) without holding registers. Block b takes
 // tiles b, b + grid, ..., thread t element t of each: body(j, v) with
-// v[q * kTile] = stream q's element j (streams outside `mask` are not copied
-// and read as 0). The grid is fixed (one block per SM), so every thread's
+// v[q] = stream q's element j (streams outside `mask` are not copied and
+// read as 0). The grid is fixed (one block per SM), so every thread's
 // partial sums cover the same elements on every run.
 constexpr int kTile = 512;
 constexpr int kStages = 4;
