@@ -50,3 +50,25 @@ def test_epilogues_identical_to_convergence(monkeypatch):
     b, _ = solve(lp, monkeypatch, "reg", max_iterations=100_000)
     assert a.iterations == b.iterations and a.stop == b.stop
     assert np.array_equal(a.iterate.x, b.iterate.x)
+
+
+def _degenerate_lps():
+    from paper_2510_24429_b200.lp import LinearProgram
+    inf = np.inf
+    c = np.array([1.0, -1.0, 0.0])
+    return [("no_nonzeros", LinearProgram(2, 3, np.zeros(4, np.int32), np.zeros(0, np.int32), np.zeros(0), c,
+                                          np.zeros(2), np.zeros(2), np.array([0.0, -inf, 0.0]),
+                                          np.array([inf, 2.0, 1.0]))),
+            ("no_rows", LinearProgram(0, 3, np.zeros(4, np.int32), np.zeros(0, np.int32), np.zeros(0), c,
+                                      np.zeros(0), np.zeros(0), np.array([0.0, -5.0, 0.0]),
+                                      np.array([inf, 2.0, 1.0])))]
+
+
+@pytest.mark.parametrize("name,lp", _degenerate_lps())
+@pytest.mark.parametrize("form", ["reg", "bulk"])
+def test_degenerate_shapes_match_oracle(name, lp, form, monkeypatch, oracle):
+    """No nonzeros / no rows: empty tiles in both epilogue forms, ||A|| = 0."""
+    res, _ = solve(lp, monkeypatch, form, max_iterations=50)
+    ref = oracle.run_pdhg(lp, config=dict(max_iterations=50))
+    assert res.iterations == ref["iterations"] and res.stop.name == "kConverged" and ref["stop"] == "converged"
+    assert np.allclose(res.iterate.x, ref["x"], rtol=0, atol=1e-12)
