@@ -2,7 +2,9 @@
 that do not need a full CPU solve (the CPU oracle would take minutes to
 hours there), plus the loop's control paths on small LPs:
 
-* C2: equal-iteration parity against the CPU oracle itself (20 iterations);
+* C2: equal-iteration parity against the CPU oracle itself (20 iterations),
+  and the first ladder snapshot (1e-2, iteration 681) against its synchronous
+  snapshot;
   C3 (20), C4 (5) and C5s (20) the same, against the plain-C restatement of the
   reference (bit-exact to the reference's own build, tests/test_oracle.py).
 * Convergence against fixtures made by the reference's own run_pdhg
@@ -55,6 +57,25 @@ def test_c2_full_size_equal_iteration_parity(lps, oracle):
     assert rel(res.iterate.x, ref["x"]) <= 1e-6
     assert rel(res.iterate.y, ref["y"]) <= 1e-6
     assert rel(res.iterate.z, ref["z"]) <= 1e-6
+
+
+def test_c2_full_size_snapshot_parity(lps, oracle):
+    """The ladder's first snapshot at full C2 size (iteration 681 at 1e-2),
+    extracted by the iteration kernels into a device slot while the loop runs
+    on: the same iteration, threshold and iterate as the restatement's
+    synchronous snapshot (pdhg.cpp:346-358)."""
+    lp = lps("C2")
+    snaps = []
+    res = run_pdhg(lp, PdhgConfig(max_iterations=700), thresholds=[1e-2], sink=snaps.append)
+    ref = oracle.run_pdhg(lp, config=dict(max_iterations=700), thresholds=[1e-2])
+    assert res.iterations == ref["iterations"] == 700
+    assert len(snaps) == len(ref["snapshots"]) == 1
+    s, r = snaps[0], ref["snapshots"][0]
+    assert s.iteration == r["iteration"] and s.threshold == r["threshold"]
+    assert s.from_average == bool(r["from_average"])
+    for a, b in ((s.iterate.x, r["x"]), (s.iterate.y, r["y"]), (s.iterate.z, r["z"])):
+        assert rel(a, b) <= 1e-6
+    assert rel(res.iterate.x, ref["x"]) <= 1e-6
 
 
 @pytest.mark.parametrize("name,iters", [("C3", 20), ("C4", 5), ("C5s", 20)])
