@@ -16,18 +16,23 @@ are all inside the timed region. The working set (~180 MB) exceeds the
 Multi-GPU (torchrun, N>1): C2 fits one GPU, so ranks run independent
 replicas ("replicas only" for C1-C3); value sums iterations over
 ranks, time is the max over ranks. `--workload C4|C5|C5s` with N>1 runs the
-row-block sharded solve instead (one shard per rank, NCCL all-gathers of y,
-x and the report sums each iteration; iterates bit-identical to one GPU):
-value = iterations/s of that one solve (strong scaling), device time max
-over ranks.
+row-block sharded solve instead (one shard per rank; each iteration the
+producing kernels store y, x and the report sums straight into the peers'
+buffers over NVLink (CUDA IPC), or NCCL all-gathers / halo exchanges with
+CCLP_CU_TRANSPORT=gather; iterates bit-identical to one GPU): value =
+iterations/s of that one solve (strong scaling), device time max over ranks.
 
 Every N > 1 replica line also carries `partitioned`: C4 (configs[3], 100M nnz)
 row-block sharded over the N ranks (5 x 50 iterations, device time max over
 ranks, per-GPU fraction of the HBM roofline); at N = 1 it is the single
 engine's C4 line (`per_config`).
 
+The roofline's per-kernel times are the kernels' durations inside the CUDA
+graph (in-kernel %globaltimer stamps, cclp_cu_phase_profile), with the eager
+per-launch event timing reported beside them.
+
 `--impl reference` times the reference's own run_pdhg (oracle/_ref, built
-from /root/reference's sources) on the host cores of rank 0.
+from /root/reference's sources) on one pinned host core of rank 0.
 """
 from __future__ import annotations
 
