@@ -1,11 +1,9 @@
-// cclp_cu host engine + C ABI (include/cclp_cu.h).
-//
-// Host side of the B200 PDHG path: it owns the device copy of the LP, builds
-// CSR(A) next to the reference's CSC, runs the one-time setup on the device
-// (Ruiz scaling, ||A|| power iteration) and drives the fused iteration
-// kernels in CUDA-graph batches, reading back a small control block per
-// batch. Snapshots are extracted on the device and copied out on a side
-// stream into pinned memory; the sink is called on the caller's thread.
+// The engine's context (context.cuh): the device copy of the LP, CSR(A) built
+// next to the reference's CSC, the SELL layouts and column panels, the SpMV
+// plans and their tuning, the one-time setup on the device (Ruiz scaling,
+// ||A|| power iteration, step sizes), the iteration's kernel launches and
+// CUDA graphs, and the view extraction for results and snapshots. The C ABI
+// over it is capi.cu (one device) and sharded.cu (row-block shards).
 // Reference: run_pdhg, proj/src/pdhg.cpp:230-378.
 #include "context.cuh"
 #include "iter_kernels.cuh"
