@@ -247,6 +247,8 @@ struct Context {
   int* tune_cols_st[3] = {nullptr, nullptr, nullptr};
   int tune_sms = 148;
   cudaEvent_t tune_ev[96] = {};
+  static constexpr int kSellTuneEvents = 64;
+  cudaEvent_t sell_ev[kSellTuneEvents] = {};  // SELL-G geometry timing (build_sellg)
   void set_geometry(bool rows_side, int per_sm, int rpg);
   void choose_geometry(const std::vector<float> (&ms)[2][4]);
   void explicit_tune();

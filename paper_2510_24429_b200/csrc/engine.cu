@@ -58,6 +58,8 @@ Context::~Context() {
   if (ev_snap) cudaEventDestroy(ev_snap);
   for (auto& e : tune_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : sell_ev)
+    if (e) cudaEventDestroy(e);
   if (ev_a) cudaEventDestroy(ev_a);
   if (ev_b) cudaEventDestroy(ev_b);
   if (stream && own_stream) cudaStreamDestroy(stream);
@@ -756,61 +758,77 @@ void Context::build_sellg(bool rows_side) {
         });
       }
     };
-    auto timed = [&](auto launch) {
-      std::vector<float> t;
-      for (int rep = 0; rep < 5; ++rep) {
-        other_side();
-        CK(cudaEventRecord(ev_a, stream));
-        launch();
-        CK(cudaEventRecord(ev_b, stream));
-        CK(cudaEventSynchronize(ev_b));
-        float ms = 0;
-        CK(cudaEventElapsedTime(&ms, ev_a, ev_b));
-        if (rep > 0) t.push_back(ms);
-      }
-      std::sort(t.begin(), t.end());
-      return t[t.size() / 2];
-    };
-    const float t_csr = timed([&] {
-      with_group_long(G, lng, [&](auto g, auto l) {
-        k_spmv_range<decltype(g)::value, decltype(l)::value><<<side_grid, kSpmvBlock, 0, stream>>>(
-            P, ptr, idx, uval, GatherPlain{gv}, outv, side_rpg);
-      });
-    });
     struct Cand { int bs, grid; };
     std::vector<Cand> cands{{kSpmvBlock, side_grid}};
     if (!lng) {
       cands.push_back({kSpmvBlock, 2 * tune_sms});
       cands.push_back({256, 8 * tune_sms});
     }
+    std::vector<int*> cand_start(cands.size());
+    for (size_t ci = 0; ci < cands.size(); ++ci) cand_start[ci] = starts(cands[ci].grid);
+    // variant 0: the CSR-G kernel in its tuned geometry; 1..: SELL-G candidates
+    auto launch_variant = [&](size_t v) {
+      with_group_long(G, lng, [&](auto g, auto l) {
+        constexpr int GG = decltype(g)::value;
+        constexpr bool LL = decltype(l)::value;
+        if (v == 0) {
+          k_spmv_range<GG, LL><<<side_grid, kSpmvBlock, 0, stream>>>(P, ptr, idx, uval, GatherPlain{gv}, outv,
+                                                                   side_rpg);
+          return;
+        }
+        const Cand& c = cands[v - 1];
+        const SellPlan SP{S.off, cand_start[v - 1], ptr, S.idx, S.val, cnt, thr};
+        if (c.bs == 256)
+          k_sellg_range<GG, LL, 256><<<c.grid, 256, 0, stream>>>(SP, P, idx, uval, GatherPlain{gv}, outv);
+        else
+          k_sellg_range<GG, LL, kSpmvBlock><<<c.grid, kSpmvBlock, 0, stream>>>(SP, P, idx, uval, GatherPlain{gv},
+                                                                               outv);
+      });
+    };
+    // interleaved rounds (each variant once per round, the other side's
+    // product before each sample, as in the iteration), so clock ramps and
+    // drift weigh on every variant alike; round 0 is a warm-up; medians
+    const size_t V = cands.size() + 1;
+    constexpr int kRounds = 8;
+    static_assert(2 * kRounds * 4 <= kSellTuneEvents, "event pool");
+    for (size_t e = 0; e < 2 * kRounds * V; ++e)
+      if (!sell_ev[e]) CK(cudaEventCreate(&sell_ev[e]));
+    for (int round = 0; round < kRounds; ++round)
+      for (size_t v = 0; v < V; ++v) {
+        other_side();
+        CK(cudaEventRecord(sell_ev[2 * (round * V + v)], stream));
+        launch_variant(v);
+        CK(cudaEventRecord(sell_ev[2 * (round * V + v) + 1], stream));
+      }
+    CK(cudaEventSynchronize(sell_ev[2 * (kRounds * V - 1) + 1]));  // one host wait
+    std::vector<std::vector<float>> samples(V);
+    for (int round = 1; round < kRounds; ++round)
+      for (size_t v = 0; v < V; ++v) {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, sell_ev[2 * (round * V + v)], sell_ev[2 * (round * V + v) + 1]));
+        samples[v].push_back(ms);
+      }
+    auto median = [](std::vector<float> t) {
+      std::sort(t.begin(), t.end());
+      return t[t.size() / 2];
+    };
+    const float t_csr = median(samples[0]);
     // rows: SELL-G unless the timing finds it clearly (10%) slower — inside
     // the iteration it won on every matrix that passes the padding rule, and
     // a tighter margin let sample noise flip C2 back to CSR-G (+1 us)
     float best = force ? 1e30f : (rows_side ? 1.10f : 0.97f) * t_csr;
     int* best_start = nullptr;
-    for (const Cand& c : cands) {
-      int* st = starts(c.grid);
-      SellPlan SP{S.off, st, ptr, S.idx, S.val, cnt, thr};
-      const float t = timed([&] {
-        with_group_long(G, lng, [&](auto g, auto l) {
-          if (c.bs == 256)
-            k_sellg_range<decltype(g)::value, decltype(l)::value, 256><<<c.grid, 256, 0, stream>>>(
-                SP, P, idx, uval, GatherPlain{gv}, outv);
-          else
-            k_sellg_range<decltype(g)::value, decltype(l)::value, kSpmvBlock><<<c.grid, kSpmvBlock, 0, stream>>>(
-                SP, P, idx, uval, GatherPlain{gv}, outv);
-        });
-      });
+    for (size_t ci = 0; ci < cands.size(); ++ci) {
+      const float t = median(samples[ci + 1]);
       if (t < best) {
         best = t;
-        release(best_start);
-        best_start = st;
-        S.bs = c.bs;
-        S.grid = c.grid;
-      } else {
-        release(st);
+        best_start = cand_start[ci];
+        S.bs = cands[ci].bs;
+        S.grid = cands[ci].grid;
       }
     }
+    for (int* st : cand_start)
+      if (st != best_start) release(st);
     CKL("sellg tune");
     S.decided = true;
     S.on = best_start != nullptr;
