@@ -761,7 +761,7 @@ void Context::build_sellg(bool rows_side) {
     struct Cand { int bs, grid; };
     std::vector<Cand> cands{{kSpmvBlock, side_grid}};
     if (!lng) {
-      cands.push_back({kSpmvBlock, 2 * tune_sms});
+      if (side_grid != 2 * tune_sms) cands.push_back({kSpmvBlock, 2 * tune_sms});
       cands.push_back({256, 8 * tune_sms});
     }
     std::vector<int*> cand_start(cands.size());
@@ -819,7 +819,12 @@ void Context::build_sellg(bool rows_side) {
     float best = force ? 1e30f : (rows_side ? 1.10f : 0.97f) * t_csr;
     int* best_start = nullptr;
     for (size_t ci = 0; ci < cands.size(); ++ci) {
-      const float t = median(samples[ci + 1]);
+      // 256-thread blocks must win by 5 %: launched after the epilogue with
+      // PDL inside the iteration they run ~5 % slower than stand-alone
+      // against 1024-thread blocks (C2: 28.0 vs 26.6 us in the graph at equal
+      // stand-alone times), while where they win they win by far (C3: 86 vs
+      // 106 us)
+      const float t = median(samples[ci + 1]) * (cands[ci].bs == 256 ? 1.05f : 1.0f);
       if (t < best) {
         best = t;
         best_start = cand_start[ci];
