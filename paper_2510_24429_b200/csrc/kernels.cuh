@@ -128,6 +128,7 @@ constexpr int kMaxPushShards = 8;
 enum PushKind : int { kPushY = 0, kPushX = 1, kPushPart = 2 };
 struct PushArgs {
   int on, P, rank;
+  int gpu_scope;                 // every shard on this device in this process: GPU-scope fences/flags
   long long Sm, Sn;
   double* y[kMaxPushShards];     // every shard's padded full y
   double* x[kMaxPushShards];     // every shard's padded full x

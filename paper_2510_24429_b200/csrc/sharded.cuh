@@ -632,6 +632,7 @@ struct Sharded {
     for (auto& s : shards) {
       PushArgs a{};
       a.on = 1;
+      a.gpu_scope = multi() ? 0 : 1;  // one process, one device: GPU scope suffices
       a.P = P;
       a.rank = s->shard_rank;
       a.Sm = s->Sm;
