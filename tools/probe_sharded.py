@@ -14,6 +14,9 @@ from paper_2510_24429_b200.pdhg import (Engine, PdhgConfig, ShardedEngine,  # no
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C4"
 its = int(sys.argv[2]) if len(sys.argv) > 2 else 100
+shard_counts = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [2, 4, 8]
+halos = sys.argv[4].split(",") if len(sys.argv) > 4 else ["1", "0"]
+with_nccl = len(sys.argv) <= 5 or sys.argv[5] != "no-nccl"
 lp = lpgen.make_config(cfg)
 B = 24 * lp.nnz + 20 * (lp.m + lp.n) + 8
 eng = Engine(lp)
@@ -22,10 +25,10 @@ eng.advance(20)
 ms = eng.advance(its)
 print(f"{cfg} single: {ms/its*1e3:.1f} us/it ({B/(ms/its*1e-3)/1e9:.0f} GB/s)", flush=True)
 eng.close()
-for halo in ("1", "0"):
+for halo in halos:
     os.environ["CCLP_CU_DEV_KNOBS"] = "1"
     os.environ["CCLP_CU_HALO"] = halo
-    for P in (2, 4, 8):
+    for P in shard_counts:
         with ShardedEngine(lp, P) as se:
             se.begin(PdhgConfig())
             se.advance(20)
@@ -34,6 +37,8 @@ for halo in ("1", "0"):
             print(f"{cfg} local shards P={P} halo={'on' if d['halo_x'] else 'off'}: {ms/its*1e3:.1f} us/it, "
                   f"x/y exchange {d['halo_x_volume']}/{d['halo_y_volume']} doubles "
                   f"(all-gather {(P-1)*(lp.n)}/{(P-1)*lp.m})", flush=True)
+if not with_nccl:
+    sys.exit(0)
 with ShardedEngine(lp, 1, rank=0, nranks=1, nccl_id=nccl_unique_id()) as se:
     se.begin(PdhgConfig())
     se.advance(20)
