@@ -259,9 +259,9 @@ struct Context {
   int gcol() const { return exact ? 1 : Gcol; }
   void launch_spmv(bool transpose, const double* vec, double* out, bool scaled, const int* stop);
   double reduce(const double* a, const double* bvec, long long len, int mode);  // reproducible
-  void launch_repro_max(int mode, const double* a, const double* bvec, long long len);
+  void launch_repro_max(int mode, const double* a, const double* bvec, long long len, bool pdl = false);
   void launch_repro_sum(int mode, const double* a, const double* bvec, long long len, const double* Mdev,
-                        long long N, PowerCtrl* pc = nullptr);
+                        long long N, PowerCtrl* pc = nullptr, bool pdl = false);
   void repro_local_max(int mode, const double* a, const double* bvec, long long len, double* M);
   void repro_local_sums(int mode, const double* a, const double* bvec, long long len, const double* M,
                         long long N, double* S);
@@ -269,8 +269,12 @@ struct Context {
   void ruiz_init();
   bool ruiz_maxima(const double* s_g, const double* r_g);
   void ruiz_update();
-  void power_rows(const double* vg, double* w, bool scaled);
-  void power_cols(const double* wg, double* u, bool scaled);
+  void power_rows(const double* vg, double* w, bool scaled, bool pdl = false);
+  void power_cols(const double* wg, double* u, bool scaled, bool pdl = false);
+  // One k_spmv_range launch, programmatic when pdl (engine.cu).
+  template <int G, bool LONG>
+  void range_launch(bool pdl, int grid, const SpmvPlan& P, const int* ptr, const int* idx, const double* val,
+                    const double* vec, double* out, int rpg, int accumulate);
   double power_norm(int iterations, uint64_t seed, bool scaled, bool pregenerated = false);
   double* h_v0 = nullptr;  // pinned start vector of the power iteration
   // h_v0 holds the start vector of seed v0_seed (a pure function of (seed, n)):

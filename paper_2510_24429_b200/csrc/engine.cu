@@ -944,8 +944,12 @@ void Context::launch_spmv(bool transpose, const double* vec, double* out, bool s
 // per-term maxima into scalars[0..K), pass 2 the exact level sums into
 // scalars[2..2 + 3K), both on the stream. `N` is the GLOBAL term count (a
 // shard passes the full length), `Mdev` the global maxima on the device.
-void Context::launch_repro_max(int mode, const double* a, const double* bvec, long long len) {
+void Context::launch_repro_max(int mode, const double* a, const double* bvec, long long len, bool pdl) {
   const int grid = blocks_for(std::max(len, 1LL), kBlock, 148 * 4);
+  if (pdl && mode == 3) {  // the power iteration's
+    launch_pdl(k_repro_max<3>, grid, kBlock, stream, a, bvec, len, work_part, counter + 1, scalars);
+    return;
+  }
   switch (mode) {
     case 0: k_repro_max<0><<<grid, kBlock, 0, stream>>>(a, bvec, len, work_part, counter + 1, scalars); break;
     case 1: k_repro_max<1><<<grid, kBlock, 0, stream>>>(a, bvec, len, work_part, counter + 1, scalars); break;
@@ -955,9 +959,13 @@ void Context::launch_repro_max(int mode, const double* a, const double* bvec, lo
   CKL("repro max");
 }
 void Context::launch_repro_sum(int mode, const double* a, const double* bvec, long long len, const double* Mdev,
-                               long long N, PowerCtrl* pc) {
+                               long long N, PowerCtrl* pc, bool pdl) {
   const int grid = blocks_for(std::max(len, 1LL), kBlock, 148 * 4);
   double* out = scalars + 2;
+  if (pdl && mode == 3) {
+    launch_pdl(k_repro_sum<3>, grid, kBlock, stream, a, bvec, len, Mdev, N, work_part, counter + 1, out, pc);
+    return;
+  }
   switch (mode) {
     case 0: k_repro_sum<0><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out); break;
     case 1: k_repro_sum<1><<<grid, kBlock, 0, stream>>>(a, bvec, len, Mdev, N, work_part, counter + 1, out); break;
@@ -1231,15 +1239,23 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
       }
       choose_geometry(ms);
     }
-    power_rows(v, wm, scaled);  // w = A v (:57)
+    // Past the timed tuning rounds the five launches are programmatic (PDL):
+    // each kernel's launch overlaps its predecessor's tail and waits for it
+    // (griddepcontrol.wait) before reading anything.
+    const bool pdl = t >= K;
+    power_rows(v, wm, scaled, pdl);  // w = A v (:57)
     if (t < K) CK(cudaEventRecord(tune_ev[3 * t + 1], stream));
-    power_cols(wm, u, scaled);  // u = A' w (:58)
+    power_cols(wm, u, scaled, pdl);  // u = A' w (:58)
     if (t < K) CK(cudaEventRecord(tune_ev[3 * t + 2], stream));
     // nu = ||u||, lambda = v.u with the partition-free sums (sharded setups
     // reproduce them bit for bit)
-    launch_repro_max(3, u, v, n);
-    launch_repro_sum(3, u, v, n, scalars, n, pctrl);  // its last block finishes nu, lambda
-    k_div_scalar<<<blocks_for(n), kBlock, 0, stream>>>(u, &pctrl->nu, v, n);  // v = u / norm
+    launch_repro_max(3, u, v, n, pdl);
+    launch_repro_sum(3, u, v, n, scalars, n, pctrl, pdl);  // its last block finishes nu, lambda
+    if (pdl)  // v = u / norm
+      launch_pdl(k_div_scalar, blocks_for(n), kBlock, stream, static_cast<const double*>(u),
+                 static_cast<const double*>(&pctrl->nu), v, static_cast<long long>(n));
+    else
+      k_div_scalar<<<blocks_for(n), kBlock, 0, stream>>>(u, &pctrl->nu, v, n);
     CKL("power");
   }
   if (tune_pending) ensure_tuned();  // fewer iterations than the tuning rounds
@@ -1251,30 +1267,39 @@ double Context::power_norm(int iterations, uint64_t seed, bool scaled, bool preg
 
 // The power iteration's products on the tuned SpMV plans (sharded: the
 // gathered vector is the padded full one).
-void Context::power_rows(const double* vg, double* w, bool scaled) {
+template <int G, bool LONG>
+void Context::range_launch(bool pdl, int grid, const SpmvPlan& P, const int* ptr, const int* idx, const double* val,
+                           const double* vec, double* out, int rpg, int accumulate) {
+  if (pdl)
+    launch_pdl(k_spmv_range<G, LONG, GatherPlain>, grid, kSpmvBlock, stream, P, ptr, idx, val, GatherPlain{vec}, out,
+               rpg, accumulate);
+  else
+    k_spmv_range<G, LONG><<<grid, kSpmvBlock, 0, stream>>>(P, ptr, idx, val, GatherPlain{vec}, out, rpg, accumulate);
+}
+
+void Context::power_rows(const double* vg, double* w, bool scaled, bool pdl) {
   const double* aval = scaled ? sval_csr : val_csr;
   if (scaled && use_panels()) {  // panel by panel
     for (int k = 0; k < static_cast<int>(panels.size()); ++k) {
       const PanelArgs a = panel_args(k);
       with_group_long(panels[k].G, a.plan.thr != 0x7fffffff, [&](auto g, auto l) {
-        k_spmv_range<decltype(g)::value, decltype(l)::value><<<panel_grid, kSpmvBlock, 0, stream>>>(
-            a.plan, a.ptr, a.idx, a.val, GatherPlain{vg}, w, 1, a.accumulate);
+        range_launch<decltype(g)::value, decltype(l)::value>(pdl, panel_grid, a.plan, a.ptr, a.idx, a.val, vg, w, 1,
+                                                             a.accumulate);
       });
     }
   } else {
     const SpmvPlan Pr = plan(true);
     with_group_long(grow(), Pr.thr != 0x7fffffff, [&](auto g, auto l) {
-      k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_r, kSpmvBlock, 0, stream>>>(
-          Pr, rowptr, colind, aval, GatherPlain{vg}, w, rpg_r);
+      range_launch<decltype(g)::value, decltype(l)::value>(pdl, spmv_grid_r, Pr, rowptr, colind, aval, vg, w, rpg_r,
+                                                           0);
     });
   }
 }
-void Context::power_cols(const double* wg, double* u, bool scaled) {
+void Context::power_cols(const double* wg, double* u, bool scaled, bool pdl) {
   const double* atval = scaled ? sval_csc : val_csc;
   const SpmvPlan Pc = plan(false);
   with_group_long(gcol(), Pc.thr != 0x7fffffff, [&](auto g, auto l) {
-    k_spmv_range<decltype(g)::value, decltype(l)::value><<<spmv_grid_c, kSpmvBlock, 0, stream>>>(
-        Pc, colptr, rowind, atval, GatherPlain{wg}, u, rpg_c);
+    range_launch<decltype(g)::value, decltype(l)::value>(pdl, spmv_grid_c, Pc, colptr, rowind, atval, wg, u, rpg_c, 0);
   });
 }
 

@@ -555,6 +555,7 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_range(const SpmvPlan P, con
                                                            const double* __restrict__ val, Gather g,
                                                            double* __restrict__ out, int rpg = 1,
                                                            int accumulate = 0) {
+  pdl_wait();  // a no-op unless launched programmatically (the power iteration)
   spmv_block_range<G, LONG>(P, ptr, idx, val, g, out, rpg, accumulate);
 }
 

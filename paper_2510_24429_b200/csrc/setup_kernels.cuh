@@ -359,6 +359,7 @@ __global__ void __launch_bounds__(kBlock) k_repro_max(const double* __restrict__
   __shared__ double red[(kBlock / 32) * K];
   __shared__ double o[K];
   __shared__ bool last;
+  pdl_wait();  // no-op unless launched programmatically (the power iteration)
   double acc[K];
 #pragma unroll
   for (int q = 0; q < K; ++q) acc[q] = 0.0;
@@ -413,6 +414,7 @@ __global__ void __launch_bounds__(kBlock) k_repro_sum(const double* __restrict__
   __shared__ double red[(kBlock / 32) * K3];
   __shared__ double o[K3];
   __shared__ bool last;
+  pdl_wait();
   ReproConsts c[K];
 #pragma unroll
   for (int q = 0; q < K; ++q) c[q] = repro_consts(Mx[q], N);
@@ -461,6 +463,7 @@ __global__ void __launch_bounds__(kBlock) k_repro_sum(const double* __restrict__
 
 __global__ void k_div_scalar(const double* __restrict__ a, const double* den, double* __restrict__ out,
                              long long n) {
+  pdl_wait();
   const double d = *den;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x)
