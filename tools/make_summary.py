@@ -111,6 +111,8 @@ out += ["## Crossover scalability and time to basic", "",
         "* `r2_smem_panel_spmv_c2.txt` — x staged in shared memory by TMA, column panels: slower than the L1 gathers.",
         "* `r2_sellg_pipe_and_g.txt` — pipelined SELL-G loop, G = 2 on C4 rows, length-sorted SELL-G windows, adaptive",
         "  bulk tiles, k_select_x grid, parallel bulk issue: none faster; the cancel poll costs nothing.",
+        "* `r2_staged_rows.txt` — the CSR-G row product's matrix stream through a bulk-copy shared-memory ring",
+        "  (bit-identical; block-synchronous ring much slower on C4/C5s), and 8 loads in flight per lane (slower).",
         "* `r2_epilogue_bulk_vs_reg.txt`, `r2_ab_primal_bulk.txt` — the bulk-copy epilogues (adopted on long vectors).", ""]
 open(os.path.join(D, "SUMMARY.md"), "w").write("\n".join(out) + "\n")
 print("\n".join(out[:40]))
