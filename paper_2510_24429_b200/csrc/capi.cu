@@ -220,7 +220,9 @@ int cclp_cu_describe(cclp_cu_ctx* ctx, int64_t* out, int32_t nout) {
                        static_cast<int64_t>(1e9 * C.phase[8]), static_cast<int64_t>(1e9 * C.phase[9]),
                        static_cast<int64_t>(1e9 * C.phase[10]),
                        // 21, 22: block size of the SELL row / column product (0: CSR-G kernel)
-                       C.sgr.on ? C.sgr.bs : 0, C.sell_on ? C.sell_bs : (C.sgc.on ? C.sgc.bs : 0)};
+                       C.sgr.on ? C.sgr.bs : 0, C.sell_on ? C.sell_bs : (C.sgc.on ? C.sgc.bs : 0),
+                       // 23: the row product starts during the decision tail (row_step)
+                       C.params.spec != nullptr ? 1 : 0};
   for (int i = 0; i < nout && i < static_cast<int>(sizeof(v) / sizeof(v[0])); ++i) out[i] = v[i];
   return CCLP_CU_OK;
 }

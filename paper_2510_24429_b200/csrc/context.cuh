@@ -72,7 +72,7 @@ struct Context {
   // state
   double* xc[3][2] = {};
   double *aty[2] = {}, *xsum[2] = {}, *atysum[2] = {};
-  double *y[2] = {}, *ax[2] = {}, *ysum[2] = {}, *axsum[2] = {};
+  double *y[2] = {}, *ax[3] = {}, *ysum[2] = {}, *axsum[2] = {};
   double *rowp = nullptr, *colp = nullptr, *work_part = nullptr;
   unsigned* counter = nullptr;
   Ctrl* ctrl = nullptr;
@@ -103,6 +103,7 @@ struct Context {
   const unsigned* d_flags = nullptr;
   unsigned* cancel_dev = nullptr;
   unsigned long long* stamps = nullptr;  // in-graph phase stamps (stamp_phase)
+  unsigned long long* spec_sync = nullptr;  // speculative row products (IterParams::spec)
   std::atomic<int> abort_req{0};  // cclp_cu_request_cancel (any thread)
   void ensure_flags() {
     if (h_flags) return;
@@ -246,6 +247,7 @@ struct Context {
   int* tune_rows_st[3] = {nullptr, nullptr, nullptr};
   int* tune_cols_st[3] = {nullptr, nullptr, nullptr};
   int tune_sms = 148;
+  int row_sms = 148;  // SMs the row product's grid is planned on (tune_spmv)
   cudaEvent_t tune_ev[96] = {};
   static constexpr int kSellTuneEvents = 64;
   cudaEvent_t sell_ev[kSellTuneEvents] = {};  // SELL-G geometry timing (build_sellg)

@@ -29,7 +29,7 @@ Context::~Context() {
                     plan_cols.seg, plan_cols.lr_first, plan_cols.part, plan_cols.cnt, x_full, y_full,
                     xpart, vparts, push_flags, push_counter, sell_off, sell_start, sell_idx, sell_val,
                     sgr.off, sgr.start, sgr.idx, sgr.val, sgc.off, sgc.start, sgc.idx, sgc.val,
-                    cancel_dev, stamps, snap_buf[0], snap_buf[1]};
+                    cancel_dev, stamps, spec_sync, ax[2], snap_buf[0], snap_buf[1]};
     static_assert(kSnapSlots == 2, "release list");
     for (void* p : ptrs) release(p);
     for (int k = 0; k < 3; ++k)
@@ -402,6 +402,11 @@ void Context::tune_spmv() {
   tune_cols_st[1] = plan_starts(false, plan_cols, sms);
   tune_cols_st[2] = plan_starts(false, plan_cols, 2 * sms);
   build_panels(x_full ? static_cast<long long>(shard_count) * Sn : n);
+  // The single-device SELL-G row product starts while the last block of
+  // k_primal still runs the decision tail on one SM (row_step): its grids
+  // are multiples of the other SMs, so no block waits for that SM.
+  row_sms = (x_full == nullptr && !use_panels() && sms > 1) ? sms - 1 : sms;
+  if (const char* e = dev_knob("CCLP_CU_ROW_SMS")) row_sms = std::atoi(e);  // A/B experiments only
   plan_rows.wrow.clear();
   plan_rows.wrow.shrink_to_fit();
   plan_rows.wseg.clear();
@@ -759,10 +764,11 @@ void Context::build_sellg(bool rows_side) {
       }
     };
     struct Cand { int bs, grid; };
-    std::vector<Cand> cands{{kSpmvBlock, side_grid}};
+    const int side_sms = rows_side && !lng ? row_sms : tune_sms;
+    std::vector<Cand> cands{{kSpmvBlock, side_grid / tune_sms * side_sms}};
     if (!lng) {
-      if (side_grid != 2 * tune_sms) cands.push_back({kSpmvBlock, 2 * tune_sms});
-      cands.push_back({256, 8 * tune_sms});
+      if (cands[0].grid != 2 * side_sms) cands.push_back({kSpmvBlock, 2 * side_sms});
+      cands.push_back({256, 8 * side_sms});
     }
     std::vector<int*> cand_start(cands.size());
     for (size_t ci = 0; ci < cands.size(); ++ci) cand_start[ci] = starts(cands[ci].grid);
@@ -1491,6 +1497,7 @@ void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& to
     alloc_n(aty[q]); alloc_n(xsum[q]); alloc_n(atysum[q]);
     alloc_m(y[q]); alloc_m(ax[q]); alloc_m(ysum[q]); alloc_m(axsum[q]);
   }
+  alloc_m(ax[2]);
   for (int q = 0; q < 2; ++q) {
     CK(cudaMemsetAsync(y[q], 0, sizeof(double) * std::max(m, 1), stream));
     CK(cudaMemsetAsync(ysum[q], 0, sizeof(double) * std::max(m, 1), stream));
@@ -1543,6 +1550,7 @@ void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& to
     p.aty[q] = aty[q]; p.xsum[q] = xsum[q]; p.atysum[q] = atysum[q];
     p.y[q] = y[q]; p.ax[q] = ax[q]; p.ysum[q] = ysum[q]; p.axsum[q] = axsum[q];
   }
+  p.ax[2] = ax[2];
   p.rowp = rowp; p.colp = colp; p.counter = counter; p.ctrl = ctrl;
   p.log = log; p.log_cap = log_cap; p.log_interval = cfg.log_interval;
   p.tau = tau; p.sigma = sigma; p.eps_rel = tol.eps_rel; p.restart_factor = cfg.restart_factor;
@@ -1565,6 +1573,7 @@ void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& to
   const bool single = !(shard_count > 1 || x_full != nullptr);
   p.snap_inline = 0;
   p.stamps = nullptr;
+  p.spec = nullptr;
   p.host_flags = nullptr;
   p.cancel_dev = nullptr;
   for (int k = 0; k < kSnapSlots; ++k) p.snap_x[k] = p.snap_y[k] = p.snap_z[k] = nullptr;
@@ -1577,6 +1586,14 @@ void Context::init_state(const cclp_cu_config& cfg, const cclp_cu_tolerances& to
     if (!stamps) stamps = alloc<unsigned long long>(cclp_cu::kStampRing * 4);
     CK(cudaMemsetAsync(stamps, 0, sizeof(unsigned long long) * cclp_cu::kStampRing * 4, stream));
     p.stamps = stamps;
+    // speculative row products (row_step) where one kernel computes the whole
+    // row product of a step (not the column panels) and PDL is on
+    const char* ek = dev_knob("CCLP_CU_SPEC");  // A/B experiments only
+    if (p.use_sell_r && sgr.grid % row_sms == 0 && pdl_enabled() && (ek == nullptr || std::atoi(ek) != 0)) {
+      if (!spec_sync) spec_sync = alloc<unsigned long long>(4);
+      CK(cudaMemsetAsync(spec_sync, 0, sizeof(unsigned long long) * 4, stream));
+      p.spec = spec_sync;
+    }
     if (nthr > 0) {
       for (int k = 0; k < kSnapSlots; ++k) {
         if (!snap_buf[k]) snap_buf[k] = alloc<double>(2 * static_cast<size_t>(n) + m);

@@ -32,6 +32,7 @@ struct StepInfo {
   long long t1;  // t + 1
   int R;         // restart applied by this step
   int s0, s1;    // ping-pong slots of states t and t+1
+  int a0, a1;    // ax slots of states t and t+1 (index mod 3)
   int xs;        // candidate slot holding x_{t+1}
   int xs2;       // candidate slot receiving x_{t+2}
   double inv;    // 1/window_t (restart average)
@@ -52,6 +53,8 @@ __device__ __forceinline__ bool step_from(const Ctrl* C, const IterParams& p, bo
     si.R = 0;
     si.s0 = 0;
     si.s1 = 0;
+    si.a0 = 0;
+    si.a1 = 0;
     si.xs = 0;
     si.xs2 = 1;
     si.inv = 0.0;
@@ -70,6 +73,8 @@ __device__ __forceinline__ bool step_from(const Ctrl* C, const IterParams& p, bo
   si.inv1 = 1.0 / static_cast<double>(win1);
   si.s0 = static_cast<int>(si.t & 1);
   si.s1 = si.s0 ^ 1;
+  si.a0 = static_cast<int>(si.t % 3);
+  si.a1 = static_cast<int>(si.t1 % 3);
   si.xs = static_cast<int>(si.t1 % 3);
   si.xs2 = static_cast<int>((si.t1 + 1) % 3);
   si.check = (si.t1 % p.check_interval) == 0;
@@ -568,18 +573,65 @@ __global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows_panel(const IterParams
   if (!read_step(p, init != 0, si, a.accumulate ? -1 : 0)) return;
   if (p.push.on) push_wait(p.push, kPushX, static_cast<unsigned long long>(si.t1 + 1));
   spmv_block_range<G, LONG>(a.plan, a.ptr, a.idx, a.val,
-                            GatherPlain{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]}, p.ax[si.s1], 1,
+                            GatherPlain{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]}, p.ax[si.a1], 1,
                             a.accumulate);
 }
 
-template <int G, bool LONG>
-__global__ void __launch_bounds__(kSpmvBlock) k_spmv_rows(const IterParams p, int init) {
+// Row product ax_{t+1} = A x_{t+1} of step t, `rows(x, ax)`. On the
+// single-device loop (p.spec) it does not wait for k_primal(t-1)'s decision
+// tail: that kernel's last block publishes t and the candidates-ready epoch,
+// then triggers this launch while it reduces the partials and runs decide().
+// The product runs on the no-restart candidate xc[(t+1) % 3][0]; each block
+// then waits for the decided epoch and, in the rare step that restarts,
+// recomputes its rows from the restart candidate (stop / halt: the result is
+// never read; ax has three slots, so states t and t-1 stay intact). Per-row
+// order is unchanged, so ax is bit-identical to the waiting form. Without a
+// pending decision (PDL off, init, k_primal exited early) it takes the
+// waiting form.
+template <class Rows>
+__device__ __forceinline__ void row_step(const IterParams& p, int init, const Rows& rows) {
+  if (p.spec != nullptr && !init) {
+    __shared__ long long sp_t;
+    __shared__ unsigned long long sp_d;
+    __shared__ int sp_go, sp_r;
+    if (threadIdx.x == 0) {
+      const unsigned long long S = ld_acquire_gpu(p.spec);
+      const unsigned long long D = ld_relaxed_gpu(p.spec + 1);
+      sp_go = S != D ? 1 : 0;
+      sp_d = D;
+      sp_t = static_cast<long long>(ld_relaxed_gpu(p.spec + 2));
+    }
+    __syncthreads();
+    if (sp_go) {
+      const long long t = sp_t;
+      if (p.stamps != nullptr && blockIdx.x == 0 && threadIdx.x == 0)
+        p.stamps[(t % kStampRing) * 4] = globaltimer();
+      const int xs = static_cast<int>((t + 1) % 3);
+      double* out = p.ax[xs];
+      rows(p.xc[xs][0], out);
+      if (threadIdx.x == 0) {
+        while (ld_relaxed_gpu(p.spec + 1) == sp_d) __nanosleep(32);
+        ld_acquire_gpu(p.spec + 1);  // one acquire orders the control-block reads
+        const volatile Ctrl* C = p.ctrl;
+        sp_r = (C->stop >= 0 || C->halt) ? 0 : C->R;
+      }
+      __syncthreads();
+      if (sp_r) rows(p.xc[xs][1], out);
+      pdl_wait();
+      return;
+    }
+  }
   StepInfo si;
   if (!read_step(p, init != 0, si, 0)) return;
   if (p.push.on) push_wait(p.push, kPushX, static_cast<unsigned long long>(si.t1 + 1));
-  spmv_block_range<G, LONG>(p.plan_r, p.rowptr, p.colind, p.aval,
-                            GatherPlain{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]},
-                      p.ax[si.s1], p.rpg_rows);
+  rows(p.xg != nullptr ? p.xg : p.xc[si.xs][si.R], p.ax[si.a1]);
+}
+
+template <int G, bool LONG>
+__global__ void __launch_bounds__(kSpmvBlock, 2048 / kSpmvBlock) k_spmv_rows(const IterParams p, int init) {
+  row_step(p, init, [&](const double* x, double* out) {
+    spmv_block_range<G, LONG>(p.plan_r, p.rowptr, p.colind, p.aval, GatherPlain{x}, out, p.rpg_rows);
+  });
 }
 
 // SELL-32 column product of block blockIdx.x's slices: lane = column, its
@@ -617,8 +669,8 @@ __device__ __forceinline__ void sell_block(const SellPlan& S, const Gather& g, d
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const bool ok = u < len;
-      ii[u] = ok ? __ldcs(ib + 32 * u) : 0;
-      vv[u] = ok ? __ldcs(vb + 32 * u) : 0.0;
+      ii[u] = ok ? ld_stream(ib + 32 * u) : 0;
+      vv[u] = ok ? ld_stream(vb + 32 * u) : 0.0;
     }
     double acc = 0.0;
     for (int k = 0; k < w; k += U) {
@@ -630,8 +682,8 @@ __device__ __forceinline__ void sell_block(const SellPlan& S, const Gather& g, d
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool ok = k + U + u < len;
-        in[u] = ok ? __ldcs(ib + 32 * (k + U + u)) : 0;
-        vn[u] = ok ? __ldcs(vb + 32 * (k + U + u)) : 0.0;
+        in[u] = ok ? ld_stream(ib + 32 * (k + U + u)) : 0;
+        vn[u] = ok ? ld_stream(vb + 32 * (k + U + u)) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -674,8 +726,8 @@ __device__ __forceinline__ void sellg_block(const SellPlan& S, const Gather& g, 
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const bool ok = (k + u) * G + gl < len;
-        ii[u] = ok ? __ldcs(ib + 32 * (k + u)) : -1;
-        vv[u] = ok ? __ldcs(vb + 32 * (k + u)) : 0.0;
+        ii[u] = ok ? ld_line(ib + 32 * (k + u)) : -1;
+        vv[u] = ok ? ld_line(vb + 32 * (k + u)) : 0.0;
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) xx[u] = ii[u] >= 0 ? g(ii[u]) : 0.0;
@@ -698,13 +750,12 @@ __global__ void __launch_bounds__(BS) k_sellg_range(const SellPlan S, const Spmv
 }
 
 template <int G, bool LONG, int BS>
-__global__ void __launch_bounds__(BS) k_spmv_rows_sellg(const IterParams p, int init) {
-  StepInfo si;
-  if (!read_step(p, init != 0, si, 0)) return;
-  if (p.push.on) push_wait(p.push, kPushX, static_cast<unsigned long long>(si.t1 + 1));
-  const GatherPlain g{p.xg != nullptr ? p.xg : p.xc[si.xs][si.R]};
-  sellg_block<G>(p.sell_r, g, p.ax[si.s1]);
-  if (LONG) spmv_long_segments(p.plan_r, p.colind, p.aval, g, p.ax[si.s1], 0);
+__global__ void __launch_bounds__(BS, 2048 / BS) k_spmv_rows_sellg(const IterParams p, int init) {
+  row_step(p, init, [&](const double* x, double* out) {
+    const GatherPlain g{x};
+    sellg_block<G>(p.sell_r, g, out);
+    if (LONG) spmv_long_segments(p.plan_r, p.colind, p.aval, g, out, 0);
+  });
 }
 
 template <int G, bool LONG, int BS>
@@ -910,7 +961,7 @@ __global__ void __launch_bounds__(kTile, 1) k_dual(const IterParams p, int init)
   double acc[kRowParts];
 #pragma unroll
   for (int k = 0; k < kRowParts; ++k) acc[k] = 0.0;
-  const double* const src[kDualStreams] = {p.r, p.b, p.ax[si.s1], p.y[si.s0], p.ax[si.s0], p.ysum[si.s0],
+  const double* const src[kDualStreams] = {p.r, p.b, p.ax[si.a1], p.y[si.s0], p.ax[si.a0], p.ysum[si.s0],
                                            p.axsum[si.s0]};
   // state t's ax is read when no restart is applied, the sums except at init
   const unsigned mask = 0xFu | (si.init || si.R ? 0u : (1u << kDsAx)) |
@@ -996,9 +1047,23 @@ __global__ void __launch_bounds__(kTile, 1) k_primal(const IterParams p, int ini
   // last block reads them with L2 (.cg) loads, so no second fence is needed
   // here (the classic last-block reduction; 0.45 us off the decision tail).
   if (!last) return;
+  if (p.spec != nullptr) {  // every candidate of x_{t+1} is written: let row_step start
+    if (threadIdx.x == 0) {
+      p.spec[2] = static_cast<unsigned long long>(si.t1);
+      __threadfence();
+      st_release_gpu(p.spec, ld_acquire_gpu(p.spec) + 1);
+    }
+    __syncthreads();
+    pdl_trigger();
+  }
   if (threadIdx.x == 0) p.ctrl->t_fin_start = globaltimer();
   finalize(p, si);
   if (threadIdx.x == 0) *p.counter = 0u;
+  if (p.spec != nullptr) {  // the decisions (the whole control block) are stored
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) st_release_gpu(p.spec + 1, ld_acquire_gpu(p.spec));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1037,7 +1102,7 @@ __global__ void __launch_bounds__(kBlock) k_view_rows(const ViewParams v) {
       axs = p.axsum[sl][i] * v.inv;
     } else {
       ys = p.y[sl][i];
-      axs = p.ax[sl][i];
+      axs = p.ax[v.t % 3][i];
     }
     const double r = p.r[i];
     v.y_out[i] = ys * r;

@@ -13,6 +13,26 @@
 
 namespace cclp_cu {
 
+// Loads of the matrix streams (index/value arrays read once per product):
+// evict-first. ld_line is for the SELL-G row slices, where every load of a
+// warp is one whole 128-byte line: no L1 allocation (the x lines gathered
+// next stay in L1) and a 256-byte L2 prefetch of the slice's next line
+// (C3 row product 85.8 -> 83.8 us; on CSR rows, whose lanes re-read a line
+// over several loads, and on the SELL-32 columns it costs:
+// profiles/r2/history/r2_stream_hints.txt).
+__device__ __forceinline__ int ld_stream(const int* p) { return __ldcs(p); }
+__device__ __forceinline__ double ld_stream(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ int ld_line(const int* p) {
+  int v;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.s32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ld_line(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
 #define CCLP_INF (__longlong_as_double(0x7ff0000000000000LL))
 
 // std::max / std::min argument semantics (pdhg.cpp uses both).
@@ -31,6 +51,26 @@ __device__ __forceinline__ bool nonfinite(double v) { return isnan(v - v); }
 // measured on C4, successor blocks launched early squat on SMs the draining
 // grid still needs (+300 us/iteration); without it PDL is neutral-to-positive.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// The one early trigger: the last block of k_primal, once every candidate of
+// x_{t+1} is written (the other blocks have exited), lets the next step's row
+// product start on the no-restart candidate while it runs the decision tail
+// (row_step, iter_kernels.cuh).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+// Polling without the acquire's L1 invalidation (an ld.acquire.gpu drops the
+// SM's whole L1, which the other block on the SM may be gathering from).
+__device__ __forceinline__ unsigned long long ld_relaxed_gpu(const unsigned long long* a) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned long long* a, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a), "l"(v) : "memory");
+}
 
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
@@ -176,7 +216,8 @@ struct IterParams {
   double* xsum[2];
   double* atysum[2];
   double* y[2];
-  double* ax[2];
+  double* ax[3];  // by state index mod 3: the speculative row product of step t
+                  // writes state t+1's slot while states t and t-1 stay intact
   double* ysum[2];
   double* axsum[2];
   // partials and control
@@ -214,6 +255,9 @@ struct IterParams {
   unsigned* cancel_dev;
   // in-graph phase stamps (stamp_phase): u64[kStampRing * 4] or null
   unsigned long long* stamps;
+  // speculative row products (row_step): u64[3] = {candidates-ready epoch,
+  // decided epoch, t of the next row product}; null: off (sharded, panels)
+  unsigned long long* spec;
 };
 
 // Power-iteration scalars on the device (Context::power_norm, setup_kernels.cuh).
@@ -282,8 +326,8 @@ __device__ __forceinline__ double group_dot(int beg, int end, int lane, const in
     for (int k = 0; k < U; ++k) {
       const int q = p + k * G;
       const bool ok = q < end;
-      ii[k] = ok ? __ldcs(idx + q) : -1;
-      vv[k] = ok ? __ldcs(val + q) : 0.0;
+      ii[k] = ok ? ld_stream(idx + q) : -1;
+      vv[k] = ok ? ld_stream(val + q) : 0.0;
     }
     double xx[U];
 #pragma unroll
@@ -313,10 +357,10 @@ __device__ __forceinline__ void group_dot2(int b0, int e0, int b1, int e1, int l
     for (int k = 0; k < U; ++k) {
       const int q0 = p0 + k * G, q1 = p1 + k * G;
       const bool ok0 = q0 < e0, ok1 = q1 < e1;
-      i0[k] = ok0 ? __ldcs(idx + q0) : -1;
-      v0[k] = ok0 ? __ldcs(val + q0) : 0.0;
-      i1[k] = ok1 ? __ldcs(idx + q1) : -1;
-      v1[k] = ok1 ? __ldcs(val + q1) : 0.0;
+      i0[k] = ok0 ? ld_stream(idx + q0) : -1;
+      v0[k] = ok0 ? ld_stream(val + q0) : 0.0;
+      i1[k] = ok1 ? ld_stream(idx + q1) : -1;
+      v1[k] = ok1 ? ld_stream(val + q1) : 0.0;
     }
     double x0[U], x1[U];
 #pragma unroll

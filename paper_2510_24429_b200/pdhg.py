@@ -492,12 +492,13 @@ class Engine:
         keys = ["m", "n", "nnz", "group_rows", "group_cols", "spmv_rows_grid_x10_rpg",
                 "spmv_cols_grid_x10_rpg", "launches",
                 "last_cols_body_ns", "last_finalize_ns"]
-        out = (C.c_int64 * (len(keys) + len(PHASES) + 2))()
+        out = (C.c_int64 * (len(keys) + len(PHASES) + 3))()
         self.L.cclp_cu_describe(self.ctx, out, len(out))
         d = dict(zip(keys, list(out)))
         d["phase_seconds"] = {k: out[len(keys) + i] * 1e-9 for i, k in enumerate(PHASES)}
         d["sell_rows_block"] = int(out[len(keys) + len(PHASES)])  # 0: CSR-G row kernel
         d["sell_cols_block"] = int(out[len(keys) + len(PHASES) + 1])
+        d["speculative_rows"] = bool(out[len(keys) + len(PHASES) + 2])  # row_step after begin()
         return d
 
 
