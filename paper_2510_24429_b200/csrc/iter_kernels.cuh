@@ -636,9 +636,8 @@ __global__ void __launch_bounds__(kSpmvBlock, 2048 / kSpmvBlock) k_spmv_rows(con
 
 // SELL-32 column product of block blockIdx.x's slices: lane = column, its
 // elements in ascending position with one accumulator (the reference's
-// sequential order, as the G = 1 path), 4 gathers in flight and the next 4
-// idx/val already loading. Columns longer than S.thr are written by the
-// long-row segments instead.
+// sequential order, as the G = 1 path), 4 gathers in flight. Columns longer
+// than S.thr are written by the long-row segments instead.
 template <class Gather>
 __device__ __forceinline__ void sell_block(const SellPlan& S, const Gather& g, double* __restrict__ out) {
   constexpr int U = 4;
@@ -664,35 +663,25 @@ __device__ __forceinline__ void sell_block(const SellPlan& S, const Gather& g, d
     if (seg) len = 0;
     const int* __restrict__ ib = S.idx + off + lane;
     const double* __restrict__ vb = S.val + off + lane;
-    int ii[U];
-    double vv[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const bool ok = u < len;
-      ii[u] = ok ? ld_stream(ib + 32 * u) : 0;
-      vv[u] = ok ? ld_stream(vb + 32 * u) : 0.0;
-    }
+    // U index/value loads, then U gathers, then U multiply-adds in order:
+    // 32 registers, two 1024-thread blocks per SM (C3 columns 77.7 -> 69.6
+    // us against the software-pipelined loop's 44 registers and one block;
+    // profiles/r2/history/r2_sell_cols_occupancy.txt)
     double acc = 0.0;
     for (int k = 0; k < w; k += U) {
-      double xx[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) xx[u] = k + u < len ? g(ii[u]) : 0.0;
-      int in[U];
-      double vn[U];
+      int ii[U];
+      double vv[U], xx[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const bool ok = k + U + u < len;
-        in[u] = ok ? ld_stream(ib + 32 * (k + U + u)) : 0;
-        vn[u] = ok ? ld_stream(vb + 32 * (k + U + u)) : 0.0;
+        const bool ok = k + u < len;
+        ii[u] = ok ? ld_stream(ib + 32 * (k + u)) : -1;
+        vv[u] = ok ? ld_stream(vb + 32 * (k + u)) : 0.0;
       }
+#pragma unroll
+      for (int u = 0; u < U; ++u) xx[u] = ii[u] >= 0 ? g(ii[u]) : 0.0;
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (k + u < len) acc = acc + vv[u] * xx[u];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        ii[u] = in[u];
-        vv[u] = vn[u];
-      }
+        if (ii[u] >= 0) acc = acc + vv[u] * xx[u];
     }
     if (j < S.n && !seg) out[j] = acc;
   }
@@ -770,12 +759,12 @@ __global__ void __launch_bounds__(BS) k_spmv_cols_sellg(const IterParams p, int 
 
 // Stand-alone SELL product (geometry tuning in Context::build_sell_cols).
 template <int BS>
-__global__ void __launch_bounds__(BS) k_sell_range(const SellPlan S, GatherPlain g, double* __restrict__ out) {
+__global__ void __launch_bounds__(BS, 2048 / BS) k_sell_range(const SellPlan S, GatherPlain g, double* __restrict__ out) {
   sell_block(S, g, out);
 }
 
 template <bool LONG, int BS>
-__global__ void __launch_bounds__(BS) k_spmv_cols_sell(const IterParams p, int init) {
+__global__ void __launch_bounds__(BS, 2048 / BS) k_spmv_cols_sell(const IterParams p, int init) {
   StepInfo si;
   if (!read_step(p, init != 0, si, 2)) return;
   if (p.push.on) push_wait(p.push, kPushY, static_cast<unsigned long long>(si.t1 + 1));
