@@ -518,12 +518,13 @@ void Context::build_sell_cols() {
   const char* e = dev_knob("CCLP_CU_SELL");
   sell_on = false;
   if ((e != nullptr && std::atoi(e) == 0) || n == 0 || nnz == 0 || !sval_csc) return;
-  // Measured (profiles/r1/history/r1_spmv_experiments.txt): SELL wins where
-  // the gathered y is large (C3 m = 0.4M: -12 us, C4 m = 5M: -40 us per
-  // column product) and loses slightly when y is cache-resident (C2 m = 0.1M:
-  // +0.5 us); the threshold depends on the matrix only (CCLP_CU_SELL=1 forces).
-  const bool force = e != nullptr && std::atoi(e) == 1;
-  if (!force && static_cast<long long>(m) * 8 < (2LL << 20)) return;
+  // Measured: SELL wins where the gathered y is large (round 1,
+  // profiles/r1/history/r1_spmv_experiments.txt: C3 m = 0.4M -12 us, C4
+  // m = 5M -40 us per column product) and, since its loop runs at 32
+  // registers with two blocks per SM, also where y is cache-resident (round
+  // 2, profiles/r2/history/r2_sell_cols_occupancy.txt: C2 m = 0.1M 25.4 ->
+  // 22.8 us; round 1's pipelined loop lost 0.5 us there). The padding rule
+  // below is the only condition (CCLP_CU_SELL=0 keeps the CSR-G kernel).
   const SpmvPlan P = plan(false);
   const int thr = P.thr;
   const int nsl = (n + 31) / 32;

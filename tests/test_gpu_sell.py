@@ -1,7 +1,6 @@
 """GPU: the SELL-32 column product (k_spmv_cols_sell; engine.cu
-build_sell_cols), forced on with CCLP_CU_SELL=1 so small LPs take it (in
-production it is chosen by the matrix: near-uniform column lengths and a
-gathered y of at least 2 MB). Each column is summed by one lane in ascending
+build_sell_cols), chosen by the matrix (near-uniform column lengths: slices
+padded to at most 1.25x the nonzeros); CCLP_CU_SELL=1 is the default. Each column is summed by one lane in ascending
 position — the reference's own order — so: equal-iteration parity with the
 oracle, sharded solves bit-identical to one device, long columns (left to the
 segment path) handled, and the result within rounding of the CSR column
