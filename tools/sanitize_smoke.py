@@ -32,4 +32,9 @@ for lp in lps:
     with Engine.from_file(p) as e:
         f = e.solve(PdhgConfig(max_iterations=100))
     assert np.array_equal(f.iterate.x, r.iterate.x)
+# round 2: the speculative row product (three ax slots) with a ladder and restarts
+with Engine(lpgen.random_equality_lp(2000, 10000, 8, seed=9)[0]) as e:
+    snaps = []
+    from paper_2510_24429_b200.pdhg import Tolerances  # noqa: E402
+    e.solve(PdhgConfig(max_iterations=1500), Tolerances(), thresholds=[1e-1, 1e-2], sink=snaps.append)
 print("sanitize smoke ok")
