@@ -1,6 +1,5 @@
-# sanitizer smoke + C2 ncu (launch list and one --set full capture of the iteration kernels)
+# C2 ncu (launch list and one --set full capture of the iteration kernels)
 mkdir -p gpurun_out
-timeout 900 compute-sanitizer --tool memcheck python tools/sanitize_smoke.py > gpurun_out/sanitize_memcheck.txt 2>&1; echo "san_rc=$?"; tail -3 gpurun_out/sanitize_memcheck.txt
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_c2.csv python tools/ncu_target.py C2 20 > /dev/null 2>&1; echo "launch_rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on \
