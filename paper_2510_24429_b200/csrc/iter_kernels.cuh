@@ -610,7 +610,11 @@ __device__ __forceinline__ void row_step(const IterParams& p, int init, const Ro
       double* out = p.ax[xs];
       rows(p.xc[xs][0], out);
       if (threadIdx.x == 0) {
-        while (ld_relaxed_gpu(p.spec + 1) == sp_d) __nanosleep(32);
+        long long spins = 0;  // bounded: a lost decision traps instead of hanging
+        while (ld_relaxed_gpu(p.spec + 1) == sp_d) {
+          __nanosleep(32);
+          if (++spins > (1LL << 30)) __trap();
+        }
         ld_acquire_gpu(p.spec + 1);  // one acquire orders the control-block reads
         const volatile Ctrl* C = p.ctrl;
         sp_r = (C->stop >= 0 || C->halt) ? 0 : C->R;
