@@ -17,6 +17,9 @@ pytestmark = pytest.mark.gpu
 
 def solve(lp, monkeypatch, spec, thresholds=(), tol=None, **kw):
     monkeypatch.setenv("CCLP_CU_SPEC", "1" if spec else "0")
+    # the SELL-G row product (chosen by timing in production): pinned here so
+    # the speculative form is the one under test on every box
+    monkeypatch.setenv("CCLP_CU_SELL_ROWS", "2")
     snaps = []
     with Engine(lp) as eng:
         res = eng.solve(PdhgConfig(**kw), tol or Tolerances(), thresholds=thresholds, sink=snaps.append)
