@@ -36,7 +36,7 @@ out = [f"# {rnd} evidence (B200, 1 GPU)", "",
        "    python bench.py                                        -> bench_c2.json",
        "    python bench.py --impl reference --steps 2 --warmup 3  -> bench_ref_c2.json",
        "    ncu --metrics gpu__time_duration.sum --clock-control none --csv \\",
-       "        --log-file launches_c2.csv python tools/ncu_target.py C2 20   -> launches_c2.md",
+       "        --log-file launches_c2.csv python tools/ncu_target.py C2 200  -> launches_c2.md",
        "    ncu --set full --clock-control none --import-source on \\",
        "        -k regex:\"k_spmv_rows|k_spmv_cols|k_dual|k_primal\" -s 8 -c 4 python tools/ncu_target.py C2|C3|C4 5",
        "                                                           -> ncu_full_C*.md, ../ncu_traffic.json",

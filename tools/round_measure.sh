@@ -21,7 +21,7 @@ if want bench; then
 fi
 if want ncu; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-    --log-file gpurun_out/launches_c2.csv python tools/ncu_target.py C2 20 > /dev/null 2>&1
+    --log-file gpurun_out/launches_c2.csv python tools/ncu_target.py C2 200 > /dev/null 2>&1
   for c in C2 C3 C4; do
     timeout 900 ncu --set full --clock-control none --import-source on \
       -k regex:"k_spmv_rows|k_spmv_cols|k_dual|k_primal" -s 8 -c 4 \
