@@ -92,7 +92,7 @@ for c in ("C2", "C3", "C4"):
         out += [t, ""]
 out += ["`k_dual<1>`/`k_primal<1>` are the bulk-copy forms (512 threads, one block per SM, a 112-128 KB shared-memory",
         "ring; SASS `UBLKCP` bulk copies and `SYNCS` mbarrier waits); `<0>` the thread-load forms C2 takes.", "",
-        "## Launch list, C2 (`tools/ncu_target.py C2 20`: setup + 20 eager iterations; cold, serialized — compare shares)",
+        "## Launch list, C2 (`tools/ncu_target.py C2 200`: setup + 200 eager iterations; cold, serialized — compare shares; under ncu the geometry tuning picks the 256-thread SELL variants)",
         ""] + lines + ["",
         "The setup's power iteration (100 x: two SpMVs, `k_repro_max`, `k_repro_sum`, `k_div_scalar`) dominates the list.", ""]
 if c2snap:
