@@ -97,3 +97,14 @@ def test_speculative_numerical_error_returns_pre_step_state(monkeypatch):
         assert np.array_equal(u, v, equal_nan=True)
     assert np.array_equal(np.array([a.report.maxresid_rel, a.report.rel_gap]),
                           np.array([b.report.maxresid_rel, b.report.rel_gap]), equal_nan=True)
+
+
+def test_bench_config_takes_the_fast_paths():
+    """C2 (the bench workload): SELL-G rows with the speculative row product
+    and SELL-32 columns — the layouts the measured numbers come from."""
+    lp = lpgen.make_config("C2")
+    with Engine(lp) as eng:
+        eng.begin(PdhgConfig())
+        eng.advance(10)
+        d = eng.describe()
+    assert d["sell_rows_block"] > 0 and d["sell_cols_block"] > 0 and d["speculative_rows"]
